@@ -1,0 +1,215 @@
+/*
+ * ranc.h -- C ABI of the B200-native tick-accurate RANC core-update library
+ * (libranc.so, built from paper_2404_16208_b200/csrc).
+ *
+ * The library simulates the method of GPU-RANC (Hassan et al., arXiv
+ * 2404.16208): a 2-D mesh of neuromorphic cores (section II), each with
+ * axons, a binary synaptic crossbar, LIF neurons whose weight is selected by
+ * the axon type ("sets of four weights per neuron"), a scheduler ring
+ * of future input spikes (section III-E) and a router that writes
+ * each spike into the destination core's scheduler at (tick offset, axon)
+ * (section III-D).  One call to ranc_run_ticks advances every core
+ * of every sample by whole ticks of Algorithm 1.
+ *
+ * Citations: "P:NN" = line NN of the paper text, "S:NN" = line NN
+ * of SPEC.md; G-numbers are the readings listed in DESIGN.md section 3.
+ *
+ * Conventions (all entry points):
+ *   - every call returns ranc_status; RANC_OK == 0.  On failure a located,
+ *     human-readable message is available from ranc_last_error(ctx) (or
+ *     ranc_last_error(NULL) for a failed ranc_load_network).
+ *   - host arrays passed in are BORROWED for the duration of the call only
+ *     (the library copies what it needs); output buffers are caller-allocated
+ *     with an explicit element count, a wrong count returns RANC_E_SIZE.
+ *   - the library owns the context and all device memory (cudaMallocAsync on
+ *     the context stream, or the allocator installed by ranc_set_allocator).
+ *   - work is stream-ordered on the context stream; calls that return data
+ *     to the host synchronise that stream.  Asynchronous kernel failures are
+ *     reported (RANC_E_CUDA) by the next synchronising call.
+ *   - results are bit-identical regardless of sample tiling, GPU count, or
+ *     splitting ranc_run_ticks into pieces ("RANC contains no
+ *     stochastic effects").
+ *   - one context per host thread at a time; distinct contexts are
+ *     independent.  There is no CPU fallback: without a usable CUDA device
+ *     ranc_load_network fails with RANC_E_CUDA.
+ */
+#ifndef RANC_H
+#define RANC_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RANC_ABI_VERSION 1
+
+typedef struct ranc_ctx ranc_ctx;
+
+typedef enum {
+  RANC_OK = 0,
+  RANC_E_ARG = 1,       /* NULL pointer / bad argument                          */
+  RANC_E_CONFIG = 2,    /* unsupported configuration (counts out of range, G20) */
+  RANC_E_BITWIDTH = 3,  /* a value does not fit its signed bitwidth    */
+  RANC_E_RANGE = 4,     /* type >= K, axon >= A, delay not in [1,D], class >= C,
+                           line >= I, reset_mode/dest_kind invalid, padding bit */
+  RANC_E_OFFGRID = 5,   /* route destination outside the grid (G17)      */
+  RANC_E_BOUND = 6,     /* the int32 accumulator could overflow (G3)           */
+  RANC_E_STATE = 7,     /* wrong call order (e.g. run before inputs)           */
+  RANC_E_SIZE = 8,      /* caller buffer element count mismatch                */
+  RANC_E_CUDA = 9,      /* CUDA error (message carries cudaGetErrorString)     */
+  RANC_E_OOM = 10,      /* device allocation failed                            */
+  RANC_E_NCCL = 11      /* NCCL error / comm not initialised                   */
+} ranc_status;
+
+/* Network description.  All arrays: host, caller-owned,
+ * row-major, read during ranc_load_network only.  G = grid_w*grid_h; core
+ * c = y*grid_w + x (P:61, 2-D mesh).  Ranges are validated; every violation
+ * is reported with its location, e.g.
+ *   "core (3,1) neuron 17: weight[2]=300 exceeds weight_bits=9".           */
+typedef struct {
+  int32_t abi_version;           /* RANC_ABI_VERSION                                  */
+  int32_t grid_w, grid_h;        /* >= 1, G <= 65536                                  */
+  int32_t axons, neurons;        /* A, N in [1, 1024] (configurable)     */
+  int32_t num_types;             /* K in [1, 4] ("sets of four weights")        */
+  int32_t max_delay;             /* D in [1, 15]: packet tick offsets 1..D (G6, G7)   */
+  int32_t num_classes;           /* C >= 0 output-bus classes (G13)                   */
+  int32_t num_lines;             /* I >= 0 external input lines (G8)                  */
+  int32_t potential_bits, weight_bits, leak_bits, threshold_bits, reset_bits;
+                                 /* each in [2, 16] (P:42 configurable bitwidths; G20) */
+  const uint8_t*  axon_type;     /* [G][A]  < K (axon type per core, G12)       */
+  const int32_t*  input_line;    /* [G][A]  -1 or [0, I): line feeding this axon      */
+  const uint32_t* crossbar;      /* [G][N][ceil(A/32)]: bit (a&31) of word a>>5 is the
+                                    synaptic connection axon a -> neuron n;
+                                    bits >= A must be 0                               */
+  const int16_t*  weight;        /* [G][N][K]   fits weight_bits                      */
+  const int16_t*  leak;          /* [G][N]      fits leak_bits                        */
+  const int16_t*  pos_threshold; /* [G][N]      fits threshold_bits (fire iff v >= it, G1) */
+  const int16_t*  neg_threshold; /* [G][N]      fits threshold_bits (v < it: negative reset, G4) */
+  const int16_t*  reset_potential;   /* [G][N]  fits reset_bits (R; -R on the negative side) */
+  const int16_t*  initial_potential; /* [G][N]  fits potential_bits (G15)             */
+  const uint8_t*  reset_mode;    /* [G][N] 0 absolute (R / -R), 1 linear (v - threshold) */
+  const uint8_t*  dest_kind;     /* [G][N] 0 none, 1 route, 2 output bus (G13, G16)   */
+  const int16_t*  dest_dx;       /* [G][N] route only: destination core (x+dx, y+dy)  */
+  const int16_t*  dest_dy;       /*        must be on the grid (G17)                  */
+  const int16_t*  dest_axon;     /* [G][N] route only: [0, A)                         */
+  const uint8_t*  dest_delay;    /* [G][N] route only: [1, D] ticks (P:154 tick offset) */
+  const uint16_t* out_class;     /* [G][N] output only: [0, C)                        */
+} ranc_network_desc;
+
+/* Input stream of S_local independent samples (G14). */
+typedef struct {
+  int32_t  num_samples;          /* S_local >= 1                                      */
+  int64_t  first_sample;         /* global index of local sample 0 (sharding, traces) */
+  int32_t  num_input_ticks;      /* T_in >= 0; ticks >= T_in receive no input         */
+  const uint32_t* line_bits;     /* [S_local][T_in][ceil(I/32)]: bit i of row (s,t) =
+                                    line i spikes ARRIVE at tick t (G8; Alg. 1 l.5-9,
+                                    P:82-90).  May be NULL when I == 0 or T_in == 0.  */
+} ranc_inputs_desc;
+
+/* Validate and compile the network (per-core axon type-sort, route words,
+ * bound check) and upload it once to `cuda_device` ("allocated and
+ * copied to the GPU global memory once").  *out receives the new context.
+ * Errors: RANC_E_ARG/CONFIG/BITWIDTH/RANGE/OFFGRID/BOUND/CUDA/OOM. */
+ranc_status ranc_load_network(const ranc_network_desc* net, int cuda_device, ranc_ctx** out);
+
+/* Copy the input stream to the device and reset the simulation state:
+ * potentials = initial_potential, scheduler rings empty, class counts 0,
+ * tick = 0 (Alg. 1 l.1).  Stream-ordered; the host array is staged
+ * before the call returns.  Errors: RANC_E_ARG/RANGE/SIZE/CUDA/OOM. */
+ranc_status ranc_load_inputs(ranc_ctx* ctx, const ranc_inputs_desc* in);
+
+/* Reset the state exactly as ranc_load_inputs does, keeping the inputs
+ * already on the device.  Errors: RANC_E_STATE (no inputs loaded). */
+ranc_status ranc_reset_state(ranc_ctx* ctx);
+
+/* Advance every core of every sample by num_ticks >= 0 ticks of Alg. 1
+ * (P:77-113): scheduler read (l.3-5), input injection (l.6-9), synaptic
+ * integration + leak/threshold/reset (l.10-14), routing of fired spikes into
+ * destination scheduler rows or the output bus (l.15-20).  Stream-ordered and
+ * asynchronous; resumable (run(a); run(b) == run(a+b)).
+ * Errors: RANC_E_STATE (no inputs), RANC_E_ARG (num_ticks < 0), RANC_E_CUDA. */
+ranc_status ranc_run_ticks(ranc_ctx* ctx, int64_t num_ticks);
+
+/* Current tick (number of ticks executed since the last reset). */
+ranc_status ranc_now(const ranc_ctx* ctx, int64_t* tick);
+
+/* Output-bus spike counts per (sample, class) (P:250 output file; G13):
+ * counts[S_local][C] int32.  n must equal S_local*C.  Synchronises. */
+ranc_status ranc_read_outputs(ranc_ctx* ctx, int32_t* counts, size_t n);
+
+/* Parity / debug readers, in the ORIGINAL axon and neuron order.
+ * Potentials: [S_local][G][N] int32.  Pending: [S_local][G][D][ceil(A/32)]
+ * u32 bitmaps, row j = spikes due at tick now+j (j = 0..D-1).  Synchronise. */
+ranc_status ranc_read_potentials(ranc_ctx* ctx, int32_t* pot, size_t n);
+ranc_status ranc_read_pending(ranc_ctx* ctx, uint32_t* bits, size_t n);
+
+/* Tracing.  flags: RANC_TRACE_SPIKE_RASTER records, for every tick of each
+ * subsequent ranc_run_ticks call, the fired bit of every neuron:
+ * raster [ticks][S_local][G][ceil(N/32)] u32 (bit n&31 of word n>>5).
+ * RANC_TRACE_OUTPUT_EVENTS is derived from the raster: records of 5 int64
+ * (sample, tick, x, y, neuron) of output-bus spikes, canonical order
+ * (sample, tick, y, x, neuron).  Reading refers to the most recent
+ * ranc_run_ticks call.  *written receives the bytes required/written;
+ * a too-small buffer returns RANC_E_SIZE with *written = bytes required. */
+#define RANC_TRACE_SPIKE_RASTER 1u
+#define RANC_TRACE_OUTPUT_EVENTS 2u
+ranc_status ranc_set_trace(ranc_ctx* ctx, uint32_t flags);
+ranc_status ranc_read_trace(ranc_ctx* ctx, uint32_t kind, void* buf, size_t bytes, size_t* written);
+
+/* Runtime plumbing.  ranc_set_stream: use this cudaStream_t for all work
+ * (e.g. torch.cuda.current_stream().cuda_stream); NULL restores the context's
+ * own stream.  ranc_set_allocator: device allocations made from now on use
+ * alloc(bytes, user) / dealloc(ptr, user) (e.g. the torch caching allocator);
+ * must be called before ranc_load_inputs. */
+ranc_status ranc_set_stream(ranc_ctx* ctx, void* cuda_stream);
+ranc_status ranc_set_allocator(ranc_ctx* ctx, void* (*alloc)(size_t, void*),
+                               void (*dealloc)(void*, void*), void* user);
+
+/* Tuning knobs (no effect on results).  RANC_OPT_SAMPLE_TILE: samples per CTA
+ * of the tick kernel (default chosen from S).  RANC_OPT_USE_GRAPH: capture the
+ * tick loop in a CUDA graph (1) or launch directly (0, default 1). */
+#define RANC_OPT_SAMPLE_TILE 1
+#define RANC_OPT_USE_GRAPH 2
+#define RANC_OPT_KERNEL 3
+ranc_status ranc_set_option(ranc_ctx* ctx, int option, int64_t value);
+
+/* Introspection of the compiled network and of the last run. */
+typedef struct {
+  int32_t grid_w, grid_h, axons, neurons, num_types, max_delay, num_classes, num_lines;
+  int32_t ring_rows;          /* physical ring rows Rp = next_pow2(D+1)                 */
+  int32_t ring_words;         /* u32 words per ring row, ceil(A/32)                     */
+  int32_t pieces;             /* popcount pieces per neuron after the type-sort         */
+  int32_t sample_tile;        /* samples per CTA in use                                 */
+  int64_t num_samples;        /* S_local                                                */
+  int64_t device_bytes;       /* device memory held by the context                      */
+  int64_t kernel_launches;    /* kernels launched by the library since load             */
+  int32_t kernel;             /* kernel variant in use                                  */
+  int32_t reserved[7];
+} ranc_info;
+ranc_status ranc_get_info(const ranc_ctx* ctx, ranc_info* info);
+
+/* Multi-GPU (one process per GPU).  ranc_comm_init joins an NCCL
+ * communicator from a 128-byte ncclUniqueId (distributed by the caller, e.g.
+ * over torch.distributed), `world` ranks, this `rank`.  mode: 0 = sample
+ * sharded (each rank simulates its own samples of a replicated network).
+ * ranc_gather_outputs: every rank calls it; `root` receives the class counts
+ * of all ranks concatenated in rank order ([sum S_local][C] int32, n must be
+ * that size on root, ignored elsewhere).  Synchronises. */
+#define RANC_SHARD_SAMPLES 0
+ranc_status ranc_comm_init(ranc_ctx* ctx, const void* nccl_unique_id, int world, int rank, int mode);
+ranc_status ranc_gather_outputs(ranc_ctx* ctx, int32_t* counts_global, size_t n, int root);
+/* Fill a 128-byte buffer with a fresh ncclUniqueId (call on one rank). */
+ranc_status ranc_comm_unique_id(void* out128);
+
+/* Last error message of ctx, or (ctx == NULL) of the calling thread's last
+ * failed ranc_load_network.  Never NULL. */
+const char* ranc_last_error(const ranc_ctx* ctx);
+
+/* Release the context and all its device memory.  NULL is a no-op. */
+void ranc_destroy(ranc_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RANC_H */

@@ -1,0 +1,455 @@
+// api.cpp -- the extern "C" entry points of include/ranc.h: context lifetime,
+// device memory, call-order checks, readback (permutations undone) and
+// tracing.  Every step of the simulation itself runs in tick.cu kernels.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+namespace {
+thread_local std::string g_load_err;
+}
+
+namespace ranc {
+
+ranc_status set_cuda_error(ranc_ctx* ctx, cudaError_t e, const char* where) {
+  std::string m = std::string(where) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
+  if (ctx) ctx->err = m;
+  else g_load_err = m;
+  return (e == cudaErrorMemoryAllocation) ? RANC_E_OOM : RANC_E_CUDA;
+}
+
+ranc_status dev_alloc(ranc_ctx* ctx, DevBuf* b, size_t bytes) {
+  dev_free(ctx, b);
+  if (bytes == 0) return RANC_OK;
+  void* p = nullptr;
+  if (ctx->user_alloc) {
+    p = ctx->user_alloc(bytes, ctx->user);
+    if (!p) {
+      ctx->err = "user allocator returned NULL for " + std::to_string(bytes) + " bytes";
+      return RANC_E_OOM;
+    }
+  } else {
+    cudaError_t e = cudaMallocAsync(&p, bytes, ctx->stream);
+    if (e != cudaSuccess) return set_cuda_error(ctx, e, "cudaMallocAsync");
+  }
+  b->p = p;
+  b->bytes = bytes;
+  ctx->device_bytes += (int64_t)bytes;
+  return RANC_OK;
+}
+
+void dev_free(ranc_ctx* ctx, DevBuf* b) {
+  if (!b->p) return;
+  if (ctx->user_free) ctx->user_free(b->p, ctx->user);
+  else cudaFreeAsync(b->p, ctx->stream);
+  ctx->device_bytes -= (int64_t)b->bytes;
+  b->p = nullptr;
+  b->bytes = 0;
+}
+
+}  // namespace ranc
+
+using namespace ranc;
+
+#define CK(call, where)                                         \
+  do {                                                          \
+    cudaError_t _e = (call);                                    \
+    if (_e != cudaSuccess) return set_cuda_error(ctx, _e, where); \
+  } while (0)
+
+#define TRY(call)                      \
+  do {                                 \
+    ranc_status _s = (call);           \
+    if (_s != RANC_OK) return _s;      \
+  } while (0)
+
+namespace {
+
+template <class T>
+ranc_status upload(ranc_ctx* ctx, DevBuf* b, const std::vector<T>& v) {
+  TRY(dev_alloc(ctx, b, v.size() * sizeof(T)));
+  if (!v.empty()) CK(cudaMemcpyAsync(b->p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, ctx->stream),
+                     "upload");
+  return RANC_OK;
+}
+
+ranc_status check_ctx(const ranc_ctx* ctx) { return ctx ? RANC_OK : RANC_E_ARG; }
+
+ranc_status sync(ranc_ctx* ctx, const char* where) {
+  cudaError_t e = cudaStreamSynchronize(ctx->stream);
+  if (e != cudaSuccess) return set_cuda_error(ctx, e, where);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return set_cuda_error(ctx, e, where);
+  return RANC_OK;
+}
+
+void free_all(ranc_ctx* ctx) {
+  DevBuf* bufs[] = {&ctx->d_xp, &ctx->d_wp, &ctx->d_pword, &ctx->d_prm, &ctx->d_route, &ctx->d_inl,
+                    &ctx->d_has_in, &ctx->d_init, &ctx->d_pot, &ctx->d_ring, &ctx->d_counts, &ctx->d_lines,
+                    &ctx->d_raster};
+  for (DevBuf* b : bufs) dev_free(ctx, b);
+}
+
+}  // namespace
+
+extern "C" {
+
+ranc_status ranc_load_network(const ranc_network_desc* net, int cuda_device, ranc_ctx** out) {
+  g_load_err.clear();
+  if (!out) {
+    g_load_err = "out pointer is NULL";
+    return RANC_E_ARG;
+  }
+  *out = nullptr;
+  ranc_ctx* ctx = new (std::nothrow) ranc_ctx();
+  if (!ctx) return RANC_E_OOM;
+  // host-side validation first (located errors do not need a GPU)
+  ranc_status s = validate_and_compile(net, &ctx->net, &g_load_err);
+  if (s != RANC_OK) {
+    delete ctx;
+    return s;
+  }
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0) {
+    g_load_err = std::string("no CUDA device available (") + (e != cudaSuccess ? cudaGetErrorString(e) : "0 devices") +
+                 "); libranc has no CPU fallback";
+    delete ctx;
+    return RANC_E_CUDA;
+  }
+  if (cuda_device < 0 || cuda_device >= ndev) {
+    g_load_err = "cuda_device " + std::to_string(cuda_device) + " out of range (" + std::to_string(ndev) + " devices)";
+    delete ctx;
+    return RANC_E_ARG;
+  }
+  ctx->device = cuda_device;
+  e = cudaSetDevice(cuda_device);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    set_cuda_error(nullptr, e, "ranc_load_network");
+    delete ctx;
+    return RANC_E_CUDA;
+  }
+  ctx->stream = ctx->own_stream;
+  const Compiled& c = ctx->net;
+  s = upload(ctx, &ctx->d_xp, c.xp);
+  if (!s) s = upload(ctx, &ctx->d_wp, c.wp);
+  if (!s) s = upload(ctx, &ctx->d_pword, c.pword);
+  if (!s) s = upload(ctx, &ctx->d_prm, c.prm);
+  if (!s) s = upload(ctx, &ctx->d_route, c.route);
+  if (!s) s = upload(ctx, &ctx->d_inl, c.inl);
+  if (!s) s = upload(ctx, &ctx->d_has_in, c.has_in);
+  if (!s) s = upload(ctx, &ctx->d_init, c.init);
+  if (!s) s = sync(ctx, "ranc_load_network");
+  if (s) {
+    g_load_err = ctx->err;
+    free_all(ctx);
+    cudaStreamDestroy(ctx->own_stream);
+    delete ctx;
+    return s;
+  }
+  *out = ctx;
+  return RANC_OK;
+}
+
+ranc_status ranc_load_inputs(ranc_ctx* ctx, const ranc_inputs_desc* in) {
+  TRY(check_ctx(ctx));
+  if (!in) {
+    ctx->err = "inputs descriptor is NULL";
+    return RANC_E_ARG;
+  }
+  if (in->num_samples < 1 || in->num_input_ticks < 0) {
+    ctx->err = "num_samples=" + std::to_string(in->num_samples) + " num_input_ticks=" +
+               std::to_string(in->num_input_ticks) + ": need num_samples >= 1, num_input_ticks >= 0";
+    return RANC_E_RANGE;
+  }
+  const Compiled& c = ctx->net;
+  const size_t line_words = (size_t)in->num_samples * in->num_input_ticks * c.WI;
+  if (line_words && !in->line_bits) {
+    ctx->err = "line_bits is NULL but num_lines*num_input_ticks > 0";
+    return RANC_E_ARG;
+  }
+  CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+  const int64_t S = in->num_samples;
+  if (S != ctx->S || !ctx->d_pot.p) {
+    TRY(dev_alloc(ctx, &ctx->d_pot, (size_t)c.G * S * c.Npad * sizeof(int16_t)));
+    TRY(dev_alloc(ctx, &ctx->d_ring, (size_t)c.Rp * c.G * S * c.W * sizeof(uint32_t)));
+    TRY(dev_alloc(ctx, &ctx->d_counts, (size_t)S * c.C * sizeof(int32_t)));
+  }
+  if (ctx->d_lines.bytes != line_words * sizeof(uint32_t)) TRY(dev_alloc(ctx, &ctx->d_lines, line_words * 4));
+  if (line_words) {
+    // from pageable memory the copy is staged before the call returns, so the
+    // caller may reuse its buffer immediately (header contract)
+    CK(cudaMemcpyAsync(ctx->d_lines.p, in->line_bits, line_words * 4, cudaMemcpyHostToDevice, ctx->stream),
+       "ranc_load_inputs H2D");
+  }
+  ctx->S = S;
+  ctx->first_sample = in->first_sample;
+  ctx->T_in = in->num_input_ticks;
+  ctx->have_inputs = true;
+  return ranc_reset_state(ctx);
+}
+
+ranc_status ranc_reset_state(ranc_ctx* ctx) {
+  TRY(check_ctx(ctx));
+  if (!ctx->have_inputs) {
+    ctx->err = "ranc_reset_state before ranc_load_inputs";
+    return RANC_E_STATE;
+  }
+  CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+  CK(launch_reset(ctx), "reset kernel");
+  ctx->now = 0;
+  ctx->raster_ticks = 0;
+  return RANC_OK;
+}
+
+ranc_status ranc_run_ticks(ranc_ctx* ctx, int64_t num_ticks) {
+  TRY(check_ctx(ctx));
+  if (num_ticks < 0) {
+    ctx->err = "num_ticks < 0";
+    return RANC_E_ARG;
+  }
+  if (!ctx->have_inputs) {
+    ctx->err = "ranc_run_ticks before ranc_load_inputs";
+    return RANC_E_STATE;
+  }
+  CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+  ctx->sample_tile = ctx->sample_tile_opt > 0 ? ctx->sample_tile_opt : choose_sample_tile(ctx->net, ctx->S);
+  if (ctx->sample_tile > ctx->S) ctx->sample_tile = (int)ctx->S;
+  if (ctx->trace_flags) {
+    const size_t bytes = (size_t)num_ticks * ctx->S * ctx->net.G * ctx->net.Wn * 4;
+    if (ctx->d_raster.bytes < bytes) TRY(dev_alloc(ctx, &ctx->d_raster, bytes));
+    if (bytes) CK(cudaMemsetAsync(ctx->d_raster.p, 0, bytes, ctx->stream), "raster clear");
+    ctx->raster_t0 = ctx->now;
+    ctx->raster_ticks = num_ticks;
+  } else if (ctx->d_raster.p) {
+    dev_free(ctx, &ctx->d_raster);
+    ctx->raster_ticks = 0;
+  }
+  CK(launch_ticks(ctx, num_ticks), "tick kernel launch");
+  ctx->now += num_ticks;
+  return RANC_OK;
+}
+
+ranc_status ranc_now(const ranc_ctx* ctx, int64_t* tick) {
+  if (!ctx || !tick) return RANC_E_ARG;
+  *tick = ctx->now;
+  return RANC_OK;
+}
+
+ranc_status ranc_read_outputs(ranc_ctx* ctx, int32_t* counts, size_t n) {
+  TRY(check_ctx(ctx));
+  if (!ctx->have_inputs) {
+    ctx->err = "ranc_read_outputs before ranc_load_inputs";
+    return RANC_E_STATE;
+  }
+  const size_t want = (size_t)ctx->S * ctx->net.C;
+  if (n != want) {
+    ctx->err = "counts buffer has " + std::to_string(n) + " elements, need S*C = " + std::to_string(want);
+    return RANC_E_SIZE;
+  }
+  if (want && !counts) return RANC_E_ARG;
+  CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+  if (want) CK(cudaMemcpyAsync(counts, ctx->d_counts.p, want * 4, cudaMemcpyDeviceToHost, ctx->stream), "D2H counts");
+  return sync(ctx, "ranc_read_outputs");
+}
+
+ranc_status ranc_read_potentials(ranc_ctx* ctx, int32_t* pot, size_t n) {
+  TRY(check_ctx(ctx));
+  if (!ctx->have_inputs) {
+    ctx->err = "ranc_read_potentials before ranc_load_inputs";
+    return RANC_E_STATE;
+  }
+  const Compiled& c = ctx->net;
+  const size_t want = (size_t)ctx->S * c.G * c.N;
+  if (n != want || !pot) {
+    ctx->err = "potentials buffer has " + std::to_string(n) + " elements, need S*G*N = " + std::to_string(want);
+    return RANC_E_SIZE;
+  }
+  CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+  std::vector<int16_t> h((size_t)c.G * ctx->S * c.Npad);
+  CK(cudaMemcpyAsync(h.data(), ctx->d_pot.p, h.size() * 2, cudaMemcpyDeviceToHost, ctx->stream), "D2H pot");
+  TRY(sync(ctx, "ranc_read_potentials"));
+  for (int64_t s = 0; s < ctx->S; ++s)
+    for (int g = 0; g < c.G; ++g)
+      for (int j = 0; j < c.N; ++j) pot[((size_t)s * c.G + g) * c.N + j] = h[((size_t)g * ctx->S + s) * c.Npad + j];
+  return RANC_OK;
+}
+
+ranc_status ranc_read_pending(ranc_ctx* ctx, uint32_t* bits, size_t n) {
+  TRY(check_ctx(ctx));
+  if (!ctx->have_inputs) {
+    ctx->err = "ranc_read_pending before ranc_load_inputs";
+    return RANC_E_STATE;
+  }
+  const Compiled& c = ctx->net;
+  const size_t want = (size_t)ctx->S * c.G * c.D * c.W;
+  if (n != want || !bits) {
+    ctx->err = "pending buffer has " + std::to_string(n) + " elements, need S*G*D*ceil(A/32) = " +
+               std::to_string(want);
+    return RANC_E_SIZE;
+  }
+  CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+  std::vector<uint32_t> h((size_t)c.Rp * c.G * ctx->S * c.W);
+  CK(cudaMemcpyAsync(h.data(), ctx->d_ring.p, h.size() * 4, cudaMemcpyDeviceToHost, ctx->stream), "D2H ring");
+  TRY(sync(ctx, "ranc_read_pending"));
+  std::memset(bits, 0, want * 4);
+  for (int j = 0; j < c.D; ++j) {
+    const int slot = (int)((ctx->now + j) & (c.Rp - 1));
+    for (int64_t s = 0; s < ctx->S; ++s)
+      for (int g = 0; g < c.G; ++g) {
+        const uint32_t* src = &h[(((size_t)slot * c.G + g) * ctx->S + s) * c.W];
+        uint32_t* dst = bits + (((size_t)s * c.G + g) * c.D + j) * c.W;
+        const int32_t* perm = &c.perm[(size_t)g * c.A];
+        for (int ap = 0; ap < c.A; ++ap)
+          if ((src[ap >> 5] >> (ap & 31)) & 1u) {
+            const int a = perm[ap];
+            dst[a >> 5] |= 1u << (a & 31);
+          }
+      }
+  }
+  return RANC_OK;
+}
+
+ranc_status ranc_set_trace(ranc_ctx* ctx, uint32_t flags) {
+  TRY(check_ctx(ctx));
+  if (flags & ~(RANC_TRACE_SPIKE_RASTER | RANC_TRACE_OUTPUT_EVENTS)) {
+    ctx->err = "unknown trace flags";
+    return RANC_E_ARG;
+  }
+  ctx->trace_flags = flags;
+  return RANC_OK;
+}
+
+ranc_status ranc_read_trace(ranc_ctx* ctx, uint32_t kind, void* buf, size_t bytes, size_t* written) {
+  TRY(check_ctx(ctx));
+  if (!written) return RANC_E_ARG;
+  *written = 0;
+  if (!(ctx->trace_flags & kind) || (kind != RANC_TRACE_SPIKE_RASTER && kind != RANC_TRACE_OUTPUT_EVENTS)) {
+    ctx->err = "trace kind not enabled (ranc_set_trace) or unknown";
+    return RANC_E_STATE;
+  }
+  const Compiled& c = ctx->net;
+  const size_t rbytes = (size_t)ctx->raster_ticks * ctx->S * c.G * c.Wn * 4;
+  CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+  if (kind == RANC_TRACE_SPIKE_RASTER) {
+    *written = rbytes;
+    if (bytes < rbytes || (!buf && rbytes)) {
+      ctx->err = "raster buffer too small";
+      return RANC_E_SIZE;
+    }
+    if (rbytes) CK(cudaMemcpyAsync(buf, ctx->d_raster.p, rbytes, cudaMemcpyDeviceToHost, ctx->stream), "D2H raster");
+    return sync(ctx, "ranc_read_trace");
+  }
+  std::vector<uint32_t> r(rbytes / 4);
+  if (rbytes) CK(cudaMemcpyAsync(r.data(), ctx->d_raster.p, rbytes, cudaMemcpyDeviceToHost, ctx->stream), "D2H raster");
+  TRY(sync(ctx, "ranc_read_trace"));
+  // canonical order (sample, tick, y, x, neuron)
+  std::vector<int64_t> ev;
+  for (int64_t s = 0; s < ctx->S; ++s)
+    for (int64_t t = 0; t < ctx->raster_ticks; ++t)
+      for (int g = 0; g < c.G; ++g) {
+        const uint32_t* w = &r[(((size_t)t * ctx->S + s) * c.G + g) * c.Wn];
+        for (int j = 0; j < c.N; ++j)
+          if (((w[j >> 5] >> (j & 31)) & 1u) && c.kind[(size_t)g * c.N + j] == RK_OUTPUT) {
+            ev.push_back(ctx->first_sample + s);
+            ev.push_back(ctx->raster_t0 + t);
+            ev.push_back(g % c.grid_w);
+            ev.push_back(g / c.grid_w);
+            ev.push_back(j);
+          }
+      }
+  *written = ev.size() * sizeof(int64_t);
+  if (bytes < *written || (!buf && *written)) {
+    ctx->err = "events buffer too small";
+    return RANC_E_SIZE;
+  }
+  if (!ev.empty()) std::memcpy(buf, ev.data(), *written);
+  return RANC_OK;
+}
+
+ranc_status ranc_set_stream(ranc_ctx* ctx, void* cuda_stream) {
+  TRY(check_ctx(ctx));
+  ctx->stream = cuda_stream ? (cudaStream_t)cuda_stream : ctx->own_stream;
+  return RANC_OK;
+}
+
+ranc_status ranc_set_allocator(ranc_ctx* ctx, void* (*alloc)(size_t, void*), void (*dealloc)(void*, void*),
+                               void* user) {
+  TRY(check_ctx(ctx));
+  if ((alloc == nullptr) != (dealloc == nullptr)) {
+    ctx->err = "alloc and dealloc must both be set or both be NULL";
+    return RANC_E_ARG;
+  }
+  if (ctx->have_inputs) {
+    ctx->err = "ranc_set_allocator must be called before ranc_load_inputs";
+    return RANC_E_STATE;
+  }
+  ctx->user_alloc = alloc;
+  ctx->user_free = dealloc;
+  ctx->user = user;
+  return RANC_OK;
+}
+
+ranc_status ranc_set_option(ranc_ctx* ctx, int option, int64_t value) {
+  TRY(check_ctx(ctx));
+  switch (option) {
+    case RANC_OPT_SAMPLE_TILE:
+      if (value < 0 || value > 256) {
+        ctx->err = "sample tile must be in [0,256] (0 = automatic)";
+        return RANC_E_ARG;
+      }
+      ctx->sample_tile_opt = (int32_t)value;
+      return RANC_OK;
+    case RANC_OPT_USE_GRAPH:
+      ctx->use_graph = value ? 1 : 0;
+      return RANC_OK;
+    case RANC_OPT_KERNEL:
+      if (value != 0) {
+        ctx->err = "unknown kernel variant";
+        return RANC_E_ARG;
+      }
+      ctx->kernel = (int32_t)value;
+      return RANC_OK;
+    default:
+      ctx->err = "unknown option";
+      return RANC_E_ARG;
+  }
+}
+
+ranc_status ranc_get_info(const ranc_ctx* ctx, ranc_info* info) {
+  if (!ctx || !info) return RANC_E_ARG;
+  std::memset(info, 0, sizeof *info);
+  const Compiled& c = ctx->net;
+  info->grid_w = c.grid_w; info->grid_h = c.grid_h; info->axons = c.A; info->neurons = c.N;
+  info->num_types = c.K; info->max_delay = c.D; info->num_classes = c.C; info->num_lines = c.I;
+  info->ring_rows = c.Rp; info->ring_words = c.W; info->pieces = c.E;
+  info->sample_tile = ctx->sample_tile; info->num_samples = ctx->S;
+  info->device_bytes = ctx->device_bytes; info->kernel_launches = ctx->launches;
+  info->kernel = ctx->kernel;
+  return RANC_OK;
+}
+
+const char* ranc_last_error(const ranc_ctx* ctx) { return ctx ? ctx->err.c_str() : g_load_err.c_str(); }
+
+void ranc_comm_destroy_internal(ranc_ctx* ctx);
+
+void ranc_destroy(ranc_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  ranc_comm_destroy_internal(ctx);
+  cudaStreamSynchronize(ctx->stream);
+  free_all(ctx);
+  cudaStreamSynchronize(ctx->stream);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+  delete ctx;
+}
+
+}  // extern "C"

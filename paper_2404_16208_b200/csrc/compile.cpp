@@ -1,0 +1,262 @@
+// compile.cpp -- validation and network compiler (host side of
+// ranc_load_network).
+//
+// Validation follows SPEC load_network ("fully validated in-memory
+// tables; any violation reported with record coordinates") with the ranges
+// of include/ranc.h.  The compiler lays the network out for the popcount
+// tick kernel:
+//   * per-core axon type-sort: axons are renumbered a' so that each axon type
+//     occupies a contiguous range.  Integration (Alg. 1 l.12-13) is
+//     then sum_k w[n][k] * popcount(column & spikes & segment_k), evaluated
+//     over "pieces" = (32-axon word, type present in it): at most
+//     ceil(A/32) + K - 1 pieces per neuron instead of K*ceil(A/32).
+//     Relabeling axons does not change the result (pinned, P9).
+//   * route words with the destination core and the PERMUTED destination axon,
+//     so the router writes straight into the destination's sorted ring row
+//     ("a spike bit is written directly into the scheduler SRAM array").
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "internal.h"
+
+namespace ranc {
+
+namespace {
+
+std::string core_str(const ranc_network_desc* d, int c) {
+  char b[64];
+  snprintf(b, sizeof b, "core (%d,%d)", c % d->grid_w, c / d->grid_w);
+  return b;
+}
+
+bool fits(int64_t v, int bits) {
+  int64_t hi = (int64_t(1) << (bits - 1)) - 1, lo = -(int64_t(1) << (bits - 1));
+  return v >= lo && v <= hi;
+}
+
+ranc_status fail(std::string* err, ranc_status s, const std::string& m) {
+  *err = m;
+  return s;
+}
+
+}  // namespace
+
+ranc_status validate_and_compile(const ranc_network_desc* d, Compiled* out, std::string* err) {
+  char b[256];
+  if (!d) return fail(err, RANC_E_ARG, "network descriptor is NULL");
+  if (d->abi_version != RANC_ABI_VERSION) {
+    snprintf(b, sizeof b, "abi_version=%d, library expects %d", d->abi_version, RANC_ABI_VERSION);
+    return fail(err, RANC_E_CONFIG, b);
+  }
+  if (d->grid_w < 1 || d->grid_h < 1 || (int64_t)d->grid_w * d->grid_h > 65536) {
+    snprintf(b, sizeof b, "grid %dx%d: need grid_w, grid_h >= 1 and G <= 65536", d->grid_w, d->grid_h);
+    return fail(err, RANC_E_CONFIG, b);
+  }
+  if (d->axons < 1 || d->axons > 1024 || d->neurons < 1 || d->neurons > 1024) {
+    snprintf(b, sizeof b, "axons=%d neurons=%d: each must be in [1,1024]", d->axons, d->neurons);
+    return fail(err, RANC_E_CONFIG, b);
+  }
+  if (d->num_types < 1 || d->num_types > 4) {
+    snprintf(b, sizeof b, "num_types=%d: must be in [1,4]", d->num_types);
+    return fail(err, RANC_E_CONFIG, b);
+  }
+  if (d->max_delay < 1 || d->max_delay > 15) {
+    snprintf(b, sizeof b, "max_delay=%d: must be in [1,15]", d->max_delay);
+    return fail(err, RANC_E_CONFIG, b);
+  }
+  if (d->num_classes < 0 || d->num_lines < 0 || d->num_classes > 65536) {
+    snprintf(b, sizeof b, "num_classes=%d num_lines=%d: must be >= 0", d->num_classes, d->num_lines);
+    return fail(err, RANC_E_CONFIG, b);
+  }
+  const int bits[5] = {d->potential_bits, d->weight_bits, d->leak_bits, d->threshold_bits, d->reset_bits};
+  const char* bname[5] = {"potential_bits", "weight_bits", "leak_bits", "threshold_bits", "reset_bits"};
+  for (int i = 0; i < 5; ++i)
+    if (bits[i] < 2 || bits[i] > 16) {
+      snprintf(b, sizeof b, "%s=%d: supported range is [2,16] (int16 storage)", bname[i], bits[i]);
+      return fail(err, RANC_E_CONFIG, b);
+    }
+  if (!d->axon_type || !d->input_line || !d->crossbar || !d->weight || !d->leak || !d->pos_threshold ||
+      !d->neg_threshold || !d->reset_potential || !d->initial_potential || !d->reset_mode ||
+      !d->dest_kind || !d->dest_dx || !d->dest_dy || !d->dest_axon || !d->dest_delay || !d->out_class)
+    return fail(err, RANC_E_ARG, "a network array pointer is NULL");
+
+  const int G = d->grid_w * d->grid_h, A = d->axons, N = d->neurons, K = d->num_types;
+  const int D = d->max_delay, C = d->num_classes, I = d->num_lines;
+  const int W = (A + 31) / 32;
+  // G3: int32 accumulator bound  A*2^(wb-1) + 2^(pb-1) + 2^(lb-1) + 2^(tb-1) + 2^(rb-1) < 2^31
+  {
+    int64_t bound = (int64_t)A * (int64_t(1) << (d->weight_bits - 1)) + (int64_t(1) << (d->potential_bits - 1)) +
+                    (int64_t(1) << (d->leak_bits - 1)) + (int64_t(1) << (d->threshold_bits - 1)) +
+                    (int64_t(1) << (d->reset_bits - 1));
+    if (bound >= (int64_t(1) << 31)) return fail(err, RANC_E_BOUND, "int32 accumulator could overflow");
+  }
+
+  for (int c = 0; c < G; ++c) {
+    for (int a = 0; a < A; ++a) {
+      int ty = d->axon_type[(size_t)c * A + a];
+      if (ty >= K) {
+        snprintf(b, sizeof b, "%s axon %d: axon_type=%d >= num_types=%d", core_str(d, c).c_str(), a, ty, K);
+        return fail(err, RANC_E_RANGE, b);
+      }
+      int32_t ln = d->input_line[(size_t)c * A + a];
+      if (ln < -1 || ln >= I) {
+        snprintf(b, sizeof b, "%s axon %d: input_line=%d not in [-1,%d)", core_str(d, c).c_str(), a, ln, I);
+        return fail(err, RANC_E_RANGE, b);
+      }
+    }
+    for (int n = 0; n < N; ++n) {
+      size_t cn = (size_t)c * N + n;
+      std::string where = core_str(d, c) + " neuron " + std::to_string(n);
+      if (A % 32) {
+        uint32_t pad = d->crossbar[cn * W + W - 1] >> (A % 32);
+        if (pad) return fail(err, RANC_E_RANGE, where + ": crossbar bits beyond axons are set");
+      }
+      for (int k = 0; k < K; ++k) {
+        int v = d->weight[cn * K + k];
+        if (!fits(v, d->weight_bits)) {
+          snprintf(b, sizeof b, "%s: weight[%d]=%d exceeds weight_bits=%d", where.c_str(), k, v, d->weight_bits);
+          return fail(err, RANC_E_BITWIDTH, b);
+        }
+      }
+      struct { const char* nm; int v; int bits; } chk[5] = {
+          {"leak", d->leak[cn], d->leak_bits},
+          {"pos_threshold", d->pos_threshold[cn], d->threshold_bits},
+          {"neg_threshold", d->neg_threshold[cn], d->threshold_bits},
+          {"reset_potential", d->reset_potential[cn], d->reset_bits},
+          {"initial_potential", d->initial_potential[cn], d->potential_bits}};
+      for (auto& q : chk)
+        if (!fits(q.v, q.bits)) {
+          snprintf(b, sizeof b, "%s: %s=%d exceeds %d bits", where.c_str(), q.nm, q.v, q.bits);
+          return fail(err, RANC_E_BITWIDTH, b);
+        }
+      if (d->reset_mode[cn] > 1) {
+        snprintf(b, sizeof b, "%s: reset_mode=%d not in {0,1}", where.c_str(), d->reset_mode[cn]);
+        return fail(err, RANC_E_RANGE, b);
+      }
+      int kind = d->dest_kind[cn];
+      if (kind > 2) {
+        snprintf(b, sizeof b, "%s: dest_kind=%d not in {0,1,2}", where.c_str(), kind);
+        return fail(err, RANC_E_RANGE, b);
+      }
+      if (kind == 1) {
+        int x = c % d->grid_w + d->dest_dx[cn], y = c / d->grid_w + d->dest_dy[cn];
+        if (x < 0 || y < 0 || x >= d->grid_w || y >= d->grid_h) {
+          snprintf(b, sizeof b, "%s: route (dx=%d,dy=%d) leaves the %dx%d grid", where.c_str(), d->dest_dx[cn],
+                   d->dest_dy[cn], d->grid_w, d->grid_h);
+          return fail(err, RANC_E_OFFGRID, b);
+        }
+        if (d->dest_axon[cn] < 0 || d->dest_axon[cn] >= A) {
+          snprintf(b, sizeof b, "%s: dest_axon=%d not in [0,%d)", where.c_str(), d->dest_axon[cn], A);
+          return fail(err, RANC_E_RANGE, b);
+        }
+        if (d->dest_delay[cn] < 1 || d->dest_delay[cn] > D) {
+          snprintf(b, sizeof b, "%s: dest_delay=%d not in [1,%d]", where.c_str(), d->dest_delay[cn], D);
+          return fail(err, RANC_E_RANGE, b);
+        }
+      } else if (kind == 2) {
+        if (d->out_class[cn] >= C) {
+          snprintf(b, sizeof b, "%s: out_class=%d >= num_classes=%d", where.c_str(), d->out_class[cn], C);
+          return fail(err, RANC_E_RANGE, b);
+        }
+      }
+    }
+  }
+
+  // ---------------------------------------------------------------- compile
+  Compiled& o = *out;
+  o.G = G; o.A = A; o.N = N; o.K = K; o.D = D; o.C = C; o.I = I; o.W = W;
+  o.grid_w = d->grid_w; o.grid_h = d->grid_h; o.pb = d->potential_bits;
+  o.Npad = (N + 31) / 32 * 32;
+  o.Wn = (N + 31) / 32;
+  o.WI = (I + 31) / 32;
+  o.Rp = 1;
+  while (o.Rp < D + 1) o.Rp <<= 1;
+  o.perm.assign((size_t)G * A, 0);
+  o.inv.assign((size_t)G * A, 0);
+  // per-core stable type-sort
+  std::vector<std::vector<uint8_t>> piece_word(G), piece_type(G);
+  std::vector<std::vector<uint32_t>> piece_mask(G);
+  int E = 1;
+  for (int c = 0; c < G; ++c) {
+    const uint8_t* ty = d->axon_type + (size_t)c * A;
+    int32_t* perm = &o.perm[(size_t)c * A];
+    for (int a = 0; a < A; ++a) perm[a] = a;
+    std::stable_sort(perm, perm + A, [&](int x, int y) { return ty[x] < ty[y]; });
+    for (int ap = 0; ap < A; ++ap) o.inv[(size_t)c * A + perm[ap]] = ap;
+    for (int w = 0; w < W; ++w) {
+      for (int k = 0; k < K; ++k) {
+        uint32_t m = 0;
+        for (int j = 0; j < 32; ++j) {
+          int ap = w * 32 + j;
+          if (ap < A && ty[perm[ap]] == k) m |= 1u << j;
+        }
+        if (m) {
+          piece_word[c].push_back((uint8_t)w);
+          piece_type[c].push_back((uint8_t)k);
+          piece_mask[c].push_back(m);
+        }
+      }
+    }
+    E = std::max<int>(E, (int)piece_word[c].size());
+  }
+  o.E = pieces_template(E);
+  const int Np = o.Npad, Ep = o.E;
+  o.xp.assign((size_t)G * Ep * Np, 0u);
+  o.wp.assign((size_t)G * Ep * Np, 0);
+  o.pword.assign((size_t)G * Ep, 0);
+  o.prm.assign((size_t)G * Np, short4{0, 0x7FFF, (short)-0x8000, 0});
+  o.route.assign((size_t)G * Np, uint2{0u, 0u});
+  o.inl.assign((size_t)G * A, -1);
+  o.has_in.assign(G, 0);
+  o.init.assign((size_t)G * Np, 0);
+  o.kind.assign((size_t)G * N, 0);
+  std::vector<uint32_t> col(W);
+  for (int c = 0; c < G; ++c) {
+    const int32_t* perm = &o.perm[(size_t)c * A];
+    const int32_t* inv = &o.inv[(size_t)c * A];
+    const int ne = (int)piece_word[c].size();
+    for (int e = 0; e < ne; ++e) o.pword[(size_t)c * Ep + e] = piece_word[c][e];
+    for (int ap = 0; ap < A; ++ap) {
+      int32_t ln = d->input_line[(size_t)c * A + perm[ap]];
+      o.inl[(size_t)c * A + ap] = ln;
+      if (ln >= 0) o.has_in[c] = 1;
+    }
+    for (int n = 0; n < N; ++n) {
+      size_t cn = (size_t)c * N + n;
+      // permuted crossbar column
+      std::fill(col.begin(), col.end(), 0u);
+      const uint32_t* src = d->crossbar + cn * W;
+      for (int a = 0; a < A; ++a)
+        if ((src[a >> 5] >> (a & 31)) & 1u) {
+          int ap = inv[a];
+          col[ap >> 5] |= 1u << (ap & 31);
+        }
+      for (int e = 0; e < ne; ++e) {
+        o.xp[((size_t)c * Ep + e) * Np + n] = col[piece_word[c][e]] & piece_mask[c][e];
+        o.wp[((size_t)c * Ep + e) * Np + n] = d->weight[cn * K + piece_type[c][e]];
+      }
+      size_t cp = (size_t)c * Np + n;
+      o.prm[cp] = short4{d->leak[cn], d->pos_threshold[cn], d->neg_threshold[cn], d->reset_potential[cn]};
+      o.init[cp] = d->initial_potential[cn];
+      uint32_t kind = d->dest_kind[cn];
+      o.kind[cn] = (uint8_t)kind;
+      uint32_t x = kind | ((uint32_t)d->reset_mode[cn] << 2);
+      uint32_t y = 0;
+      if (kind == RK_ROUTE) {
+        int dx = c % d->grid_w + d->dest_dx[cn], dy = c / d->grid_w + d->dest_dy[cn];
+        int dc = dy * d->grid_w + dx;
+        int dap = o.inv[(size_t)dc * A + d->dest_axon[cn]];
+        x |= ((uint32_t)d->dest_delay[cn] << 3) | ((uint32_t)dap << 8);
+        y = (uint32_t)dc;
+      } else if (kind == RK_OUTPUT) {
+        y = d->out_class[cn];
+      }
+      o.route[cp] = uint2{x, y};
+    }
+  }
+  return RANC_OK;
+}
+
+}  // namespace ranc

@@ -1,0 +1,124 @@
+// internal.h -- context, compiled-network layout and kernel parameter block of
+// libranc.so.  Not part of the ABI (include/ranc.h is).
+//
+// Device layout, per context:
+//   compiled network (uploaded once), L2-resident at the paper's sizes:
+//     xp    u32 [G][E][Npad]   popcount piece words: crossbar column of neuron n
+//                              restricted to one axon-type segment of one
+//                              32-axon word, after the per-core axon type-sort
+//     wp    i16 [G][E][Npad]   weight of that piece's axon type for neuron n
+//     pword u8  [G][E]         ring word index of piece e
+//     prm   short4 [G][Npad]   {leak, pos_threshold, neg_threshold, reset}
+//     route uint2  [G][Npad]   x: kind | lin<<2 | delay<<3 | axon'<<8 ; y: dest core or class
+//     inl   i32 [G][A]         input line of permuted axon a' (-1 none)
+//   state (streamed every tick):
+//     pot   i16 [G][S][Npad]   membrane potentials (pb <= 16)
+//     ring  u32 [Rp][G][S][W]  scheduler rings, W = ceil(A/32) words per row,
+//                              slot of tick t = t & (Rp-1), Rp = next_pow2(D+1)
+//     counts i32 [S][C]        output-bus class counts
+//     lines u32 [S][T_in][WI]  external input line bits
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/ranc.h"
+
+namespace ranc {
+
+// route word fields
+enum : uint32_t { RK_NONE = 0, RK_ROUTE = 1, RK_OUTPUT = 2 };
+__host__ __device__ inline uint32_t route_kind(uint32_t x) { return x & 3u; }
+__host__ __device__ inline uint32_t route_lin(uint32_t x) { return (x >> 2) & 1u; }
+__host__ __device__ inline uint32_t route_delay(uint32_t x) { return (x >> 3) & 31u; }
+__host__ __device__ inline uint32_t route_axon(uint32_t x) { return (x >> 8) & 0x7FFu; }
+
+struct TickParams {
+  int32_t G, S, N, Npad, A, W, E, Wn, C, T_in, WI, ST;
+  int32_t rp_mask;          // Rp - 1
+  int32_t pot_lo, pot_hi;   // saturation range of pb bits
+  int64_t t;                // tick being executed
+  int64_t raster_t0;        // first tick of the raster buffer
+  const uint32_t* xp;
+  const int16_t* wp;
+  const uint8_t* pword;
+  const short4* prm;
+  const uint2* route;
+  const int32_t* inl;
+  const uint8_t* has_in;
+  const uint32_t* lines;
+  int16_t* pot;
+  uint32_t* ring;
+  int32_t* counts;
+  uint32_t* raster;         // [T][S][G][Wn] or nullptr
+};
+
+// Host copy of the compiled network.
+struct Compiled {
+  int32_t G = 0, A = 0, N = 0, Npad = 0, K = 0, D = 0, C = 0, I = 0, W = 0, E = 0, Wn = 0, WI = 0;
+  int32_t grid_w = 0, grid_h = 0, pb = 16, Rp = 2;
+  std::vector<uint32_t> xp;     // [G][E][Npad]
+  std::vector<int16_t> wp;      // [G][E][Npad]
+  std::vector<uint8_t> pword;   // [G][E]
+  std::vector<short4> prm;      // [G][Npad]
+  std::vector<uint2> route;     // [G][Npad]
+  std::vector<int32_t> inl;     // [G][A]
+  std::vector<uint8_t> has_in;  // [G]
+  std::vector<int16_t> init;    // [G][Npad]
+  std::vector<int32_t> perm;    // [G][A]  a' -> a
+  std::vector<int32_t> inv;     // [G][A]  a -> a'
+  std::vector<uint8_t> kind;    // [G][N]
+};
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+}  // namespace ranc
+
+struct ranc_ctx {
+  int device = 0;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  void* (*user_alloc)(size_t, void*) = nullptr;
+  void (*user_free)(void*, void*) = nullptr;
+  void* user = nullptr;
+  std::string err;
+  ranc::Compiled net;
+  // device: compiled network
+  ranc::DevBuf d_xp, d_wp, d_pword, d_prm, d_route, d_inl, d_has_in, d_init;
+  // device: state
+  ranc::DevBuf d_pot, d_ring, d_counts, d_lines, d_raster;
+  int64_t S = 0, first_sample = 0;
+  int32_t T_in = 0;
+  bool have_inputs = false;
+  int64_t now = 0;
+  int32_t sample_tile = 0;       // in use (set by ranc_run_ticks)
+  int32_t sample_tile_opt = 0;   // RANC_OPT_SAMPLE_TILE, 0 = automatic
+  int32_t use_graph = 1;
+  int32_t kernel = 0;
+  int64_t launches = 0;
+  int64_t device_bytes = 0;
+  uint32_t trace_flags = 0;
+  int64_t raster_t0 = 0, raster_ticks = 0;
+  // multi-GPU
+  void* nccl_comm = nullptr;
+  int world = 1, rank = 0;
+};
+
+namespace ranc {
+// compile.cpp
+ranc_status validate_and_compile(const ranc_network_desc* d, Compiled* out, std::string* err);
+// tick.cu
+cudaError_t launch_reset(ranc_ctx* ctx);
+cudaError_t launch_ticks(ranc_ctx* ctx, int64_t num_ticks);
+int choose_sample_tile(const Compiled& n, int64_t S);
+int pieces_template(int E);
+// api.cpp
+ranc_status dev_alloc(ranc_ctx* ctx, DevBuf* b, size_t bytes);
+void dev_free(ranc_ctx* ctx, DevBuf* b);
+ranc_status set_cuda_error(ranc_ctx* ctx, cudaError_t e, const char* where);
+}  // namespace ranc

@@ -1,0 +1,180 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle, bit-exact
+for every potential, pending spike, fired bit, output event and class count
+("a one-to-one match between output files")."""
+import numpy as np
+import pytest
+
+from workloads.gen import (config1, config2, config3, config5, corpus_case, tiny_case, vmm)
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ranc():
+    from paper_2404_16208_b200 import build
+    build.build()
+    import paper_2404_16208_b200 as m
+    return m
+
+
+def per_tick(ranc, oracle_mod, net, inp, T, tile=None):
+    sim = ranc.Simulator(net)
+    if tile:
+        sim.set_option(ranc.OPT_SAMPLE_TILE, tile)
+    sim.set_trace(ranc.TRACE_SPIKE_RASTER | ranc.TRACE_OUTPUT_EVENTS)
+    sim.load_inputs(inp)
+    o = oracle_mod.Oracle(net, inp)
+    for t in range(T):
+        sim.run(1)
+        o.run(1)
+        where = f"{net.name} tick {t}"
+        assert np.array_equal(sim.potentials(), o.potentials()), where + " potentials"
+        assert np.array_equal(sim.raster()[0], o.fired()), where + " fired"
+        assert np.array_equal(sim.pending(), o.pending()), where + " pending"
+        assert np.array_equal(sim.outputs(), o.counts()), where + " counts"
+    sim.close()
+    return o
+
+
+def final_state(ranc, oracle_mod, net, inp, T, tile=None, events=True):
+    sim = ranc.Simulator(net)
+    if tile:
+        sim.set_option(ranc.OPT_SAMPLE_TILE, tile)
+    if events:
+        sim.set_trace(ranc.TRACE_OUTPUT_EVENTS)
+    sim.load_inputs(inp).run(T)
+    o = oracle_mod.Oracle(net, inp).run(T)
+    assert np.array_equal(sim.outputs(), o.counts())
+    assert np.array_equal(sim.potentials(), o.potentials())
+    assert np.array_equal(sim.pending(), o.pending())
+    if events:
+        assert np.array_equal(sim.events(), o.events())
+    sim.close()
+    return o
+
+
+def test_config1_every_tick(ranc, oracle_mod):
+    net, inp = config1()
+    o = per_tick(ranc, oracle_mod, net, inp, 64)
+    assert o.counts().sum() > 0 and o.pending().sum() > 0
+
+
+@pytest.mark.parametrize("seed", range(0, 200))
+def test_tiny_every_tick(ranc, oracle_mod, seed):
+    net, inp = tiny_case(seed)
+    per_tick(ranc, oracle_mod, net, inp, 20)
+
+
+@pytest.mark.parametrize("seed", range(0, 40))
+def test_corpus_every_tick(ranc, oracle_mod, seed):
+    net, inp = corpus_case(seed)
+    per_tick(ranc, oracle_mod, net, inp, 12)
+
+
+@pytest.mark.parametrize("tile", [1, 3, 64])
+def test_config2_full(ranc, oracle_mod, tile):
+    net, inp = config2(S=300)
+    o = final_state(ranc, oracle_mod, net, inp, 17, tile=tile)
+    assert o.counts().sum() > 0
+
+
+def test_config2_1000_samples(ranc, oracle_mod):
+    net, inp = config2(S=1000)
+    final_state(ranc, oracle_mod, net, inp, 17)
+
+
+def test_config5_small_mesh(ranc, oracle_mod):
+    net, inp = config5(S=5, T=40, grid=8)
+    o = final_state(ranc, oracle_mod, net, inp, 40)
+    assert o.pending().sum() > 0
+
+
+def test_config5_global_every_tick(ranc, oracle_mod):
+    net, inp = config5(S=3, T=20, grid=6, variant="global")
+    per_tick(ranc, oracle_mod, net, inp, 20)
+
+
+def test_config3_full_size_sampled(ranc, oracle_mod):
+    """Config 3 at BASELINE size (10000 samples, 19 ticks, bench launch
+    configuration) on the GPU; the oracle recomputes a spread of samples one
+    by one (samples are independent, pinned by batch composition)."""
+    net, inp = config3(S=10000)
+    T = net.meta["T"]
+    sim = ranc.Simulator(net)
+    sim.load_inputs(inp).run(T)
+    cnt = sim.outputs()
+    pot = sim.potentials()
+    pick = [0, 1, 2, 4097, 5000, 7777, 9998, 9999]
+    o = oracle_mod.Oracle(net, inp.subset(pick)).run(T)
+    assert np.array_equal(cnt[pick], o.counts())
+    assert np.array_equal(pot[pick], o.potentials())
+    assert cnt.sum() > 0
+    sim.close()
+
+
+@pytest.mark.parametrize("variant", ["vmm32", "vmm60", "vmm256"])
+def test_vmm_closed_form_on_gpu(ranc, variant):
+    """P6: the GPU's class counts equal M+ x and M- x (numpy), independent of
+    the oracle."""
+    from workloads.gen import VMM_VARIANTS
+    net, inp = vmm(S=200, seed=1004, **VMM_VARIANTS[variant])
+    M, X = net.meta["M"], net.meta["X"]
+    sim = ranc.Simulator(net)
+    sim.load_inputs(inp).run(net.meta["T"])
+    cnt = sim.outputs()
+    assert np.array_equal(cnt[:, 0::2], X @ np.maximum(M, 0).T)
+    assert np.array_equal(cnt[:, 1::2], X @ np.maximum(-M, 0).T)
+    sim.close()
+
+
+def test_vmm_small_vs_oracle(ranc, oracle_mod):
+    net, inp = vmm(16, 10, 7, 5, S=20, seed=5, block_in=8)
+    final_state(ranc, oracle_mod, net, inp, net.meta["T"])
+
+
+def test_resumable_and_reload(ranc, oracle_mod):
+    net, inp = config1(T=40)
+    sim = ranc.Simulator(net)
+    sim.load_inputs(inp).run(7).run(0).run(33)
+    p1, c1 = sim.potentials(), sim.outputs()
+    sim.load_inputs(inp).run(40)
+    assert np.array_equal(sim.potentials(), p1) and np.array_equal(sim.outputs(), c1)
+    sim.reset().run(40)
+    assert np.array_equal(sim.potentials(), p1) and np.array_equal(sim.outputs(), c1)
+    o = oracle_mod.Oracle(net, inp).run(40)
+    assert np.array_equal(p1, o.potentials())
+    assert sim.now == 40
+    sim.close()
+
+
+def test_ticks_beyond_inputs_and_zero_ticks(ranc, oracle_mod):
+    net, inp = config2(S=5)
+    final_state(ranc, oracle_mod, net, inp, 30)
+    sim = ranc.Simulator(net)
+    sim.load_inputs(inp).run(0)
+    assert np.array_equal(sim.potentials(), np.broadcast_to(net.initial_potential, (5, 5, 256)))
+    sim.close()
+
+
+def test_torch_stream_and_allocator(ranc, oracle_mod):
+    import torch
+    net, inp = config2(S=17)
+    s = torch.cuda.Stream()
+    sim = ranc.Simulator(net, stream=s, torch_allocator=True)
+    sim.load_inputs(inp).run(17)
+    o = oracle_mod.Oracle(net, inp).run(17)
+    assert np.array_equal(sim.outputs(), o.counts())
+    sim.close()
+
+
+def test_call_order_errors(ranc):
+    net, inp = config1(T=4)
+    sim = ranc.Simulator(net)
+    with pytest.raises(ranc.RancError) as ei:
+        sim.run(1)
+    assert ei.value.code == "RANC_E_STATE"
+    sim.load_inputs(inp)
+    with pytest.raises(ranc.RancError) as ei:
+        sim._ck(sim.lib.ranc_read_outputs(sim.h, None, 3))
+    assert ei.value.code == "RANC_E_SIZE"
+    sim.close()
