@@ -93,7 +93,7 @@ ranc_status sync(ranc_ctx* ctx, const char* where) {
 void free_all(ranc_ctx* ctx) {
   DevBuf* bufs[] = {&ctx->d_xp, &ctx->d_wp, &ctx->d_pword, &ctx->d_prm, &ctx->d_route, &ctx->d_inl,
                     &ctx->d_has_in, &ctx->d_init, &ctx->d_pot, &ctx->d_ring, &ctx->d_counts, &ctx->d_lines,
-                    &ctx->d_raster};
+                    &ctx->d_stage, &ctx->d_raster};
   for (DevBuf* b : bufs) dev_free(ctx, b);
 }
 
@@ -183,16 +183,22 @@ ranc_status ranc_load_inputs(ranc_ctx* ctx, const ranc_inputs_desc* in) {
     TRY(dev_alloc(ctx, &ctx->d_ring, (size_t)c.Rp * c.G * S * c.W * sizeof(uint32_t)));
     TRY(dev_alloc(ctx, &ctx->d_counts, (size_t)S * c.C * sizeof(int32_t)));
   }
-  if (ctx->d_lines.bytes != line_words * sizeof(uint32_t)) TRY(dev_alloc(ctx, &ctx->d_lines, line_words * 4));
-  if (line_words) {
-    // from pageable memory the copy is staged before the call returns, so the
-    // caller may reuse its buffer immediately (header contract)
-    CK(cudaMemcpyAsync(ctx->d_lines.p, in->line_bits, line_words * 4, cudaMemcpyHostToDevice, ctx->stream),
-       "ranc_load_inputs H2D");
+  if (ctx->d_lines.bytes != line_words * sizeof(uint32_t)) {
+    TRY(dev_alloc(ctx, &ctx->d_lines, line_words * 4));
+    TRY(dev_alloc(ctx, &ctx->d_stage, line_words * 4));
   }
   ctx->S = S;
   ctx->first_sample = in->first_sample;
   ctx->T_in = in->num_input_ticks;
+  if (line_words) {
+    // H2D into a staging buffer, then a device transpose to [T_in][S][WI].
+    // The host buffer must stay valid until the call returns: from pageable
+    // memory the copy is staged before return; from pinned memory we wait.
+    CK(cudaMemcpyAsync(ctx->d_stage.p, in->line_bits, line_words * 4, cudaMemcpyHostToDevice, ctx->stream),
+       "ranc_load_inputs H2D");
+    CK(transpose_lines(ctx, (const uint32_t*)ctx->d_stage.p), "transpose_lines");
+    CK(cudaStreamSynchronize(ctx->stream), "ranc_load_inputs sync");
+  }
   ctx->have_inputs = true;
   return ranc_reset_state(ctx);
 }
@@ -274,6 +280,13 @@ ranc_status ranc_read_potentials(ranc_ctx* ctx, int32_t* pot, size_t n) {
     return RANC_E_SIZE;
   }
   CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+  if (ctx->fresh) {  // no tick since the reset: potentials are the initial ones
+    TRY(sync(ctx, "ranc_read_potentials"));
+    for (int64_t s = 0; s < ctx->S; ++s)
+      for (int g = 0; g < c.G; ++g)
+        for (int j = 0; j < c.N; ++j) pot[((size_t)s * c.G + g) * c.N + j] = c.init[(size_t)g * c.Npad + j];
+    return RANC_OK;
+  }
   std::vector<int16_t> h((size_t)c.G * ctx->S * c.Npad);
   CK(cudaMemcpyAsync(h.data(), ctx->d_pot.p, h.size() * 2, cudaMemcpyDeviceToHost, ctx->stream), "D2H pot");
   TRY(sync(ctx, "ranc_read_potentials"));

@@ -16,7 +16,8 @@
 //     ring  u32 [Rp][G][S][W]  scheduler rings, W = ceil(A/32) words per row,
 //                              slot of tick t = t & (Rp-1), Rp = next_pow2(D+1)
 //     counts i32 [S][C]        output-bus class counts
-//     lines u32 [S][T_in][WI]  external input line bits
+//     lines u32 [T_in][S][WI]  external input line bits (transposed at load so a
+//                              tile's rows of one tick are contiguous)
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -39,6 +40,7 @@ struct TickParams {
   int32_t G, S, N, Npad, A, W, E, Wn, C, T_in, WI, ST;
   int32_t rp_mask;          // Rp - 1
   int32_t pot_lo, pot_hi;   // saturation range of pb bits
+  int32_t fresh;            // first tick after a reset: potentials start at init
   int64_t t;                // tick being executed
   int64_t raster_t0;        // first tick of the raster buffer
   const uint32_t* xp;
@@ -48,7 +50,8 @@ struct TickParams {
   const uint2* route;
   const int32_t* inl;
   const uint8_t* has_in;
-  const uint32_t* lines;
+  const int16_t* init;      // [G][Npad] initial potentials
+  const uint32_t* lines;    // [T_in][S][WI]
   int16_t* pot;
   uint32_t* ring;
   int32_t* counts;
@@ -91,7 +94,8 @@ struct ranc_ctx {
   // device: compiled network
   ranc::DevBuf d_xp, d_wp, d_pword, d_prm, d_route, d_inl, d_has_in, d_init;
   // device: state
-  ranc::DevBuf d_pot, d_ring, d_counts, d_lines, d_raster;
+  ranc::DevBuf d_pot, d_ring, d_counts, d_lines, d_stage, d_raster;
+  bool fresh = false;            // no tick since the last reset: d_pot is stale, potentials = init
   int64_t S = 0, first_sample = 0;
   int32_t T_in = 0;
   bool have_inputs = false;
@@ -114,6 +118,7 @@ namespace ranc {
 ranc_status validate_and_compile(const ranc_network_desc* d, Compiled* out, std::string* err);
 // tick.cu
 cudaError_t launch_reset(ranc_ctx* ctx);
+cudaError_t transpose_lines(ranc_ctx* ctx, const uint32_t* staging);
 cudaError_t launch_ticks(ranc_ctx* ctx, int64_t num_ticks);
 int choose_sample_tile(const Compiled& n, int64_t S);
 int pieces_template(int E);

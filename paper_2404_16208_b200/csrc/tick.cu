@@ -10,11 +10,13 @@
 //   a7 tick barrier: the kernel boundary.
 //
 // Mapping (B200-first, not the paper's V100 mapping): CTA = (core c, tile of
-// ST samples); thread = neuron.  Each thread keeps its neuron's crossbar
-// pieces and weights in registers for the whole sample tile, so the
-// (L2-resident) network is read once per tile while potentials stream from
-// HBM once per tick.  Integration is sum_e w_e * popc(xbar_e & spikes_e) over
-// the <= ceil(A/32)+K-1 type-sorted pieces (compile.cpp).
+// ST samples); thread = neuron.  The tile's potentials ([ST][Npad] int16,
+// contiguous in the [G][S][Npad] layout) move HBM <-> shared memory with one
+// TMA bulk copy each way (cp.async.bulk, UBLKCP); each thread keeps its
+// neuron's crossbar pieces and weights in registers for the whole tile, so
+// the (L2-resident) network is read once per tile.  Integration is
+// sum_e w_e * popc(xbar_e & spikes_e) over the <= ceil(A/32)+K-1 type-sorted
+// pieces (compile.cpp).
 //
 // Why no intra-tick barrier is needed: every route delay is in [1, D] and the
 // ring has Rp >= D+1 physical rows, so no spike written during tick t lands in
@@ -26,26 +28,61 @@
 #include <algorithm>
 
 #include "internal.h"
+#include "ptx.h"
 
 namespace ranc {
 
 namespace {
 
 constexpr int kThreads = 256;
+constexpr int kPotTileBytes = 48 * 1024;  // shared-memory budget for the potential tile
+
+struct SmemLayout {
+  uint32_t pot, raw, pk, lines, total;
+};
+
+__host__ __device__ inline SmemLayout smem_layout(int ST, int Npad, int W, int E, int WI) {
+  SmemLayout L;
+  uint32_t o = 16;                                // mbarrier
+  L.pot = o;   o += (uint32_t)ST * Npad * 2;      // int16 [ST][Npad]
+  o = (o + 15) & ~15u;
+  L.pk = o;    o += (uint32_t)ST * E * 4;         // u32 [ST][E]
+  L.raw = o;   o += (uint32_t)ST * W * 4;         // u32 [ST][W]
+  o = (o + 15) & ~15u;
+  L.lines = o; o += (uint32_t)ST * WI * 4;        // u32 [ST][WI]
+  L.total = (o + 15) & ~15u;
+  return L;
+}
 
 template <int E>
-__global__ void __launch_bounds__(kThreads) tick_popc_kernel(const TickParams p) {
-  extern __shared__ uint32_t smem[];
+__global__ void __launch_bounds__(kThreads, (E <= 12 ? 4 : (E <= 16 ? 3 : 2))) tick_popc_kernel(const TickParams p) {
+  extern __shared__ __align__(16) uint8_t smem[];
   const int c = blockIdx.x;
   const int s0 = blockIdx.y * p.ST;
   const int ns = min(p.ST, p.S - s0);
   const int tid = threadIdx.x;
-  const int lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  const int lane = tid & 31;
   const int W = p.W;
-  uint32_t* raw = smem;                       // [ST][W]   ring rows of this tile
-  uint32_t* pk = smem + p.ST * W;             // [ST][E]   spike word of each piece
+  const SmemLayout L = smem_layout(p.ST, p.Npad, W, E, p.WI);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
+  int16_t* pot_s = reinterpret_cast<int16_t*>(smem + L.pot);
+  uint32_t* pk = reinterpret_cast<uint32_t*>(smem + L.pk);
+  uint32_t* raw = reinterpret_cast<uint32_t*>(smem + L.raw);
+  uint32_t* lines_s = reinterpret_cast<uint32_t*>(smem + L.lines);
   const int cur = (int)(p.t & p.rp_mask);
+  const uint32_t tile_bytes = (uint32_t)ns * p.Npad * 2;
+  int16_t* pot_g = p.pot + ((size_t)c * p.S + s0) * p.Npad;
 
+  if (tid == 0) {
+    ptx::mbar_init(bar, 1);
+    ptx::fence_mbar_init();
+  }
+  __syncthreads();
+  // stream the tile's potentials in (TMA bulk copy) while the spikes are staged
+  if (!p.fresh && tid == 0) {
+    ptx::mbar_arrive_expect_tx(bar, tile_bytes);
+    ptx::bulk_g2s(pot_s, pot_g, tile_bytes, bar);
+  }
   // a1: stage the current scheduler rows of (core c, samples s0..) and clear
   // them (the row is free again for spikes due at t + Rp).
   uint32_t* row = p.ring + (((size_t)cur * p.G + c) * p.S + s0) * W;
@@ -53,23 +90,25 @@ __global__ void __launch_bounds__(kThreads) tick_popc_kernel(const TickParams p)
     raw[i] = row[i];
     row[i] = 0u;
   }
+  const bool inject = p.t < p.T_in && p.has_in[c];
+  if (inject) {
+    const uint32_t* lg = p.lines + ((size_t)p.t * p.S + s0) * p.WI;   // [T_in][S][WI]
+    for (int i = tid; i < ns * p.WI; i += blockDim.x) lines_s[i] = lg[i];
+  }
   __syncthreads();
-  // a2: external input lines arriving at tick t (G8): one ballot per 32-axon word.
-  if (p.t < p.T_in && p.has_in[c]) {
-    const int32_t* inl = p.inl + (size_t)c * p.A;
-    for (int idx = warp; idx < ns * W; idx += nwarps) {
-      const int s = idx / W, w = idx - s * W;
-      const int ap = w * 32 + lane;
-      bool bit = false;
-      if (ap < p.A) {
-        const int32_t ln = inl[ap];
-        if (ln >= 0) {
-          const uint32_t* lb = p.lines + ((size_t)(s0 + s) * p.T_in + p.t) * p.WI;
-          bit = (lb[ln >> 5] >> (ln & 31)) & 1u;
-        }
+  // a2: external input lines arriving at tick t (G8).  Thread <-> permuted
+  // axon a'; one warp ballot builds one 32-axon ring word, so the OR into the
+  // staged row needs no atomics.
+  if (inject) {
+    for (int ap0 = tid - lane; ap0 < W * 32; ap0 += blockDim.x) {
+      const int ap = ap0 + lane;
+      const int32_t ln = ap < p.A ? p.inl[(size_t)c * p.A + ap] : -1;
+      const int lw = ln >> 5, lb = ln & 31;
+      for (int s = 0; s < ns; ++s) {
+        const bool bit = ln >= 0 && ((lines_s[s * p.WI + lw] >> lb) & 1u);
+        const uint32_t m = __ballot_sync(0xFFFFFFFFu, bit);
+        if (lane == 0) raw[s * W + (ap0 >> 5)] |= m;
       }
-      const uint32_t m = __ballot_sync(0xFFFFFFFFu, bit);
-      if (lane == 0) raw[idx] |= m;
     }
     __syncthreads();
   }
@@ -80,6 +119,7 @@ __global__ void __launch_bounds__(kThreads) tick_popc_kernel(const TickParams p)
     pk[i] = raw[s * W + pword[e]];
   }
   __syncthreads();
+  if (!p.fresh) ptx::mbar_wait(bar, 0);
 
   for (int n = tid; n < p.Npad; n += blockDim.x) {
     uint32_t xp[E];
@@ -91,32 +131,40 @@ __global__ void __launch_bounds__(kThreads) tick_popc_kernel(const TickParams p)
     }
     const short4 prm = p.prm[(size_t)c * p.Npad + n];
     const uint2 rt = p.route[(size_t)c * p.Npad + n];
+    const int init = p.init[(size_t)c * p.Npad + n];
     const uint32_t kind = route_kind(rt.x);
     const bool lin = route_lin(rt.x);
     const bool valid = n < p.N;
-    int16_t* pot = p.pot + ((size_t)c * p.S + s0) * p.Npad + n;
+    const int leak = prm.x, pth = prm.y, nth = prm.z, rst = prm.w;
+#pragma unroll 2
     for (int s = 0; s < ns; ++s) {
       // a3: integration
-      const uint32_t* sw = pk + s * E;
+      const uint4* sw = reinterpret_cast<const uint4*>(pk + s * E);
       int acc = 0;
 #pragma unroll
-      for (int e = 0; e < E; ++e) acc += wp[e] * __popc(xp[e] & sw[e]);
+      for (int q = 0; q < E / 4; ++q) {
+        const uint4 v4 = sw[q];
+        acc += wp[4 * q + 0] * __popc(xp[4 * q + 0] & v4.x);
+        acc += wp[4 * q + 1] * __popc(xp[4 * q + 1] & v4.y);
+        acc += wp[4 * q + 2] * __popc(xp[4 * q + 2] & v4.z);
+        acc += wp[4 * q + 3] * __popc(xp[4 * q + 3] & v4.w);
+      }
       // a4: leak, thresholds, reset, saturate once (G1-G5)
-      const int v = (int)pot[(size_t)s * p.Npad] + acc + prm.x;
-      const bool fire = v >= prm.y;
-      int nv;
-      if (fire) nv = lin ? v - prm.y : prm.w;
-      else if (v < prm.z) nv = lin ? v - prm.z : -prm.w;
-      else nv = v;
+      const int pot = p.fresh ? init : (int)pot_s[s * p.Npad + n];
+      const int v = pot + acc + leak;
+      const bool fire = v >= pth;
+      const bool neg = v < nth;
+      const int rv = lin ? v - (fire ? pth : nth) : (fire ? rst : -rst);
+      int nv = (fire || neg) ? rv : v;
       nv = min(max(nv, p.pot_lo), p.pot_hi);
-      pot[(size_t)s * p.Npad] = (int16_t)nv;
+      pot_s[s * p.Npad + n] = (int16_t)nv;
       // a5 / a6: route into the destination ring row of tick t+delay, or count
-      if (fire && valid) {
+      if (fire && valid && kind != RK_NONE) {
         if (kind == RK_ROUTE) {
           const uint32_t ax = route_axon(rt.x);
           const int slot = (int)((p.t + route_delay(rt.x)) & p.rp_mask);
           atomicOr(p.ring + (((size_t)slot * p.G + rt.y) * p.S + s0 + s) * W + (ax >> 5), 1u << (ax & 31));
-        } else if (kind == RK_OUTPUT) {
+        } else {
           atomicAdd(p.counts + (size_t)(s0 + s) * p.C + rt.y, 1);
         }
       }
@@ -127,20 +175,34 @@ __global__ void __launch_bounds__(kThreads) tick_popc_kernel(const TickParams p)
       }
     }
   }
+  // stream the updated tile back (TMA bulk store)
+  ptx::fence_proxy_async_smem();
+  __syncthreads();
+  if (tid == 0) {
+    ptx::bulk_s2g(pot_g, pot_s, tile_bytes);
+    ptx::bulk_commit();
+    ptx::bulk_wait_read0();
+  }
 }
 
-__global__ void reset_pot_kernel(int16_t* __restrict__ pot, const int16_t* __restrict__ init, int G, int S,
-                                 int Npad) {
-  const size_t total = (size_t)G * S * Npad;
+// [S][T_in][WI] -> [T_in][S][WI]
+__global__ void transpose_lines_kernel(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, int S, int T,
+                                       int WI) {
+  const size_t total = (size_t)S * T * WI;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
-    const size_t n = i % Npad;
-    const size_t c = i / ((size_t)S * Npad);
-    pot[i] = init[c * Npad + n];
+    const size_t w = i % WI, st = i / WI;
+    const size_t t = st % T, s = st / T;
+    out[(t * S + s) * WI + w] = in[i];
   }
 }
 
 template <int E>
 cudaError_t launch_one(const TickParams& p, dim3 grid, size_t smem, cudaStream_t st) {
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(tick_popc_kernel<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    configured = true;
+  }
   tick_popc_kernel<E><<<grid, kThreads, smem, st>>>(p);
   return cudaGetLastError();
 }
@@ -155,27 +217,33 @@ int pieces_template(int E) {
 }
 
 int choose_sample_tile(const Compiled& n, int64_t S) {
-  // enough CTAs to fill 148 SMs several times over, at most 64 samples per CTA
+  // as many samples per CTA as the potential tile budget allows (<= 64), but
+  // enough CTAs to fill the 148 SMs several times over
+  int64_t cap = std::max<int64_t>(1, kPotTileBytes / (n.Npad * 2));
   int64_t want = (int64_t)n.G * S / (4 * 148);
-  if (want < 1) want = 1;
-  if (want > 64) want = 64;
-  if (want > S) want = S;
+  want = std::max<int64_t>(1, std::min<int64_t>({want, 64, cap, S}));
   return (int)want;
 }
 
-cudaError_t launch_reset(ranc_ctx* ctx) {
+cudaError_t transpose_lines(ranc_ctx* ctx, const uint32_t* staging) {
   const Compiled& n = ctx->net;
-  cudaError_t e;
-  const size_t total = (size_t)n.G * ctx->S * n.Npad;
-  int blocks = (int)std::min<size_t>((total + 255) / 256, 148 * 16);
-  if (blocks < 1) blocks = 1;
-  reset_pot_kernel<<<blocks, 256, 0, ctx->stream>>>((int16_t*)ctx->d_pot.p, (const int16_t*)ctx->d_init.p, n.G,
-                                                    (int)ctx->S, n.Npad);
+  const size_t total = (size_t)ctx->S * ctx->T_in * n.WI;
+  if (!total) return cudaSuccess;
+  int blocks = (int)std::min<size_t>((total + 255) / 256, 148 * 8);
+  transpose_lines_kernel<<<blocks, 256, 0, ctx->stream>>>(staging, (uint32_t*)ctx->d_lines.p, (int)ctx->S,
+                                                          ctx->T_in, n.WI);
   ctx->launches++;
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_reset(ranc_ctx* ctx) {
+  // potentials are re-initialised by the first tick (p.fresh), so a reset only
+  // empties the rings and the class counts
+  cudaError_t e;
   if ((e = cudaMemsetAsync(ctx->d_ring.p, 0, ctx->d_ring.bytes, ctx->stream)) != cudaSuccess) return e;
   if (ctx->d_counts.bytes)
     if ((e = cudaMemsetAsync(ctx->d_counts.p, 0, ctx->d_counts.bytes, ctx->stream)) != cudaSuccess) return e;
+  ctx->fresh = true;
   return cudaSuccess;
 }
 
@@ -194,6 +262,7 @@ cudaError_t launch_ticks(ranc_ctx* ctx, int64_t num_ticks) {
   p.route = (const uint2*)ctx->d_route.p;
   p.inl = (const int32_t*)ctx->d_inl.p;
   p.has_in = (const uint8_t*)ctx->d_has_in.p;
+  p.init = (const int16_t*)ctx->d_init.p;
   p.lines = (const uint32_t*)ctx->d_lines.p;
   p.pot = (int16_t*)ctx->d_pot.p;
   p.ring = (uint32_t*)ctx->d_ring.p;
@@ -201,9 +270,10 @@ cudaError_t launch_ticks(ranc_ctx* ctx, int64_t num_ticks) {
   p.raster = (uint32_t*)ctx->d_raster.p;
   p.raster_t0 = ctx->raster_t0;
   const dim3 grid(n.G, (unsigned)((ctx->S + p.ST - 1) / p.ST));
-  const size_t smem = (size_t)p.ST * (n.W + n.E) * sizeof(uint32_t);
+  const size_t smem = smem_layout(p.ST, n.Npad, n.W, n.E, n.WI).total;
   for (int64_t i = 0; i < num_ticks; ++i) {
     p.t = ctx->now + i;
+    p.fresh = ctx->fresh ? 1 : 0;
     cudaError_t e;
     switch (n.E) {
       case 4: e = launch_one<4>(p, grid, smem, ctx->stream); break;
@@ -215,6 +285,7 @@ cudaError_t launch_ticks(ranc_ctx* ctx, int64_t num_ticks) {
     }
     ctx->launches++;
     if (e != cudaSuccess) return e;
+    ctx->fresh = false;
   }
   return cudaSuccess;
 }

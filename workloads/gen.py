@@ -245,7 +245,7 @@ def vmm(n, m, Mmax, Xmax, S=1000, seed=1004, A=256, block_in=None, block_out=Non
     gh = -(-G // gw)
     N = 256
     assert 2 * bout <= N and 4 * bin_ <= A
-    net = _blank(gw, gh, A, N, 4, 1, 2 * m, n, name=f"vmm-{n}x{m}")
+    net = _blank(gw, gh, A, N, 4, 1, 2 * m, n, tb=16, name=f"vmm-{n}x{m}")
     net.neg_threshold[:] = -(1 << 15)
     net.pos_threshold[:] = 1
     net.reset_mode[:] = MODE_LIN
