@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--samples", type=int, default=10000)
     ap.add_argument("--tile", type=int, default=0)
+    ap.add_argument("--kernel", default="auto", choices=["auto", "popc", "tc"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-samples", type=int, default=0, help="oracle sample size (0 = auto)")
     return ap.parse_args()
@@ -200,7 +201,7 @@ def run_reference(args, rank, world):
 def run_ours(args, rank, world, local):
     import torch
     import torch.distributed as dist
-    from paper_2404_16208_b200 import OPT_SAMPLE_TILE, Simulator
+    from paper_2404_16208_b200 import OPT_KERNEL, OPT_SAMPLE_TILE, Simulator
     from paper_2404_16208_b200 import build as pbuild
     if rank == 0:
         pbuild.build()
@@ -217,6 +218,7 @@ def run_ours(args, rank, world, local):
     sim = Simulator(net, device=local, stream=stream)
     if args.tile:
         sim.set_option(OPT_SAMPLE_TILE, args.tile)
+    sim.set_option(OPT_KERNEL, {"auto": 0, "popc": 1, "tc": 2}[args.kernel])
     if world > 1:
         uid = [Simulator.unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
@@ -297,13 +299,14 @@ def run_ours(args, rank, world, local):
             "config": {"workload": "config3-mnist-512c", "samples": args.samples, "ticks": T, "cores": net.G,
                        "axons": net.axons, "neurons": net.neurons, "parallelism": f"sample-sharded dp{world}",
                        "l2": "state (potentials 2.6 GB + rings 0.33 GB) exceeds the 126 MB L2; no flush needed",
-                       "sample_tile": info["sample_tile"], "pieces": info["pieces"]},
+                       "sample_tile": info["sample_tile"], "pieces": info["pieces"],
+                       "kernel": "tcgen05 kind::i8" if info["kernel"] == 2 else "popcount"},
             "core_ticks_per_s": core_ticks_s,
             "tick_kernel_ms": tick_ms,
             "gpu_launches": launches,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": None,
-                         "kernel": "tick_popc_kernel",
+                         "kernel": "tick_tc_kernel" if info["kernel"] == 2 else "tick_popc_kernel",
                          "note": f"{ALG_BYTES_PER_CORE_TICK} B/core-tick x {net.G} cores x {S_local} samples per "
                                  "launch / mean launch time (CUDA events on the launch stream); peak = "
                                  "MEASURED_PEAKS.json hbm_gbs"},

@@ -92,7 +92,7 @@ ranc_status sync(ranc_ctx* ctx, const char* where) {
 
 void free_all(ranc_ctx* ctx) {
   DevBuf* bufs[] = {&ctx->d_xp, &ctx->d_wp, &ctx->d_pword, &ctx->d_prm, &ctx->d_route, &ctx->d_inl,
-                    &ctx->d_has_in, &ctx->d_init, &ctx->d_pot, &ctx->d_ring, &ctx->d_counts, &ctx->d_lines,
+                    &ctx->d_has_in, &ctx->d_init, &ctx->d_wfold, &ctx->d_pot, &ctx->d_ring, &ctx->d_counts, &ctx->d_lines,
                     &ctx->d_stage, &ctx->d_raster};
   for (DevBuf* b : bufs) dev_free(ctx, b);
 }
@@ -147,6 +147,7 @@ ranc_status ranc_load_network(const ranc_network_desc* net, int cuda_device, ran
   if (!s) s = upload(ctx, &ctx->d_inl, c.inl);
   if (!s) s = upload(ctx, &ctx->d_has_in, c.has_in);
   if (!s) s = upload(ctx, &ctx->d_init, c.init);
+  if (!s && c.tc_ok) s = upload(ctx, &ctx->d_wfold, c.wfold);
   if (!s) s = sync(ctx, "ranc_load_network");
   if (s) {
     g_load_err = ctx->err;
@@ -179,7 +180,9 @@ ranc_status ranc_load_inputs(ranc_ctx* ctx, const ranc_inputs_desc* in) {
   CK(cudaSetDevice(ctx->device), "cudaSetDevice");
   const int64_t S = in->num_samples;
   if (S != ctx->S || !ctx->d_pot.p) {
-    TRY(dev_alloc(ctx, &ctx->d_pot, (size_t)c.G * S * c.Npad * sizeof(int16_t)));
+    // room for either potential layout: [G][S][Npad] or [G][nT][Npad][NT]
+    const int64_t nT = (S + tc_tile() - 1) / tc_tile();
+    TRY(dev_alloc(ctx, &ctx->d_pot, (size_t)c.G * std::max<int64_t>(S, nT * tc_tile()) * c.Npad * sizeof(int16_t)));
     TRY(dev_alloc(ctx, &ctx->d_ring, (size_t)c.Rp * c.G * S * c.W * sizeof(uint32_t)));
     TRY(dev_alloc(ctx, &ctx->d_counts, (size_t)S * c.C * sizeof(int32_t)));
   }
@@ -211,6 +214,8 @@ ranc_status ranc_reset_state(ranc_ctx* ctx) {
   }
   CK(cudaSetDevice(ctx->device), "cudaSetDevice");
   CK(launch_reset(ctx), "reset kernel");
+  // latch the kernel variant (the potential layout is re-initialised here)
+  ctx->kernel_active = (ctx->kernel == RANC_KERNEL_POPC || !ctx->net.tc_ok) ? RANC_KERNEL_POPC : RANC_KERNEL_TC;
   ctx->now = 0;
   ctx->raster_ticks = 0;
   return RANC_OK;
@@ -287,12 +292,16 @@ ranc_status ranc_read_potentials(ranc_ctx* ctx, int32_t* pot, size_t n) {
         for (int j = 0; j < c.N; ++j) pot[((size_t)s * c.G + g) * c.N + j] = c.init[(size_t)g * c.Npad + j];
     return RANC_OK;
   }
-  std::vector<int16_t> h((size_t)c.G * ctx->S * c.Npad);
+  std::vector<int16_t> h(ctx->d_pot.bytes / 2);
   CK(cudaMemcpyAsync(h.data(), ctx->d_pot.p, h.size() * 2, cudaMemcpyDeviceToHost, ctx->stream), "D2H pot");
   TRY(sync(ctx, "ranc_read_potentials"));
+  const int64_t NT = tc_tile(), nT = (ctx->S + NT - 1) / NT;
   for (int64_t s = 0; s < ctx->S; ++s)
     for (int g = 0; g < c.G; ++g)
-      for (int j = 0; j < c.N; ++j) pot[((size_t)s * c.G + g) * c.N + j] = h[((size_t)g * ctx->S + s) * c.Npad + j];
+      for (int j = 0; j < c.N; ++j)
+        pot[((size_t)s * c.G + g) * c.N + j] =
+            ctx->kernel_active == RANC_KERNEL_TC ? h[(((size_t)g * nT + s / NT) * c.Npad + j) * NT + s % NT]
+                                                 : h[((size_t)g * ctx->S + s) * c.Npad + j];
   return RANC_OK;
 }
 
@@ -425,11 +434,15 @@ ranc_status ranc_set_option(ranc_ctx* ctx, int option, int64_t value) {
       ctx->use_graph = value ? 1 : 0;
       return RANC_OK;
     case RANC_OPT_KERNEL:
-      if (value != 0) {
-        ctx->err = "unknown kernel variant";
+      if (value < 0 || value > 2) {
+        ctx->err = "kernel variant must be 0 (auto), 1 (popcount) or 2 (tensor core)";
         return RANC_E_ARG;
       }
-      ctx->kernel = (int32_t)value;
+      if (value == RANC_KERNEL_TC && !ctx->net.tc_ok) {
+        ctx->err = "network is outside the tensor-core envelope (|w| <= 127, Npad*32*ceil(A/32) <= 64 KB)";
+        return RANC_E_CONFIG;
+      }
+      ctx->kernel = (int32_t)value;  // takes effect at the next ranc_load_inputs / ranc_reset_state
       return RANC_OK;
     default:
       ctx->err = "unknown option";
@@ -446,7 +459,7 @@ ranc_status ranc_get_info(const ranc_ctx* ctx, ranc_info* info) {
   info->ring_rows = c.Rp; info->ring_words = c.W; info->pieces = c.E;
   info->sample_tile = ctx->sample_tile; info->num_samples = ctx->S;
   info->device_bytes = ctx->device_bytes; info->kernel_launches = ctx->launches;
-  info->kernel = ctx->kernel;
+  info->kernel = ctx->kernel_active;
   return RANC_OK;
 }
 

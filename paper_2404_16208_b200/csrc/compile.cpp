@@ -36,6 +36,11 @@ bool fits(int64_t v, int bits) {
   return v >= lo && v <= hi;
 }
 
+// canonical K-major core-matrix layout of a tensor-core operand (tc.h)
+inline uint32_t tc_operand_offset(uint32_t r, uint32_t k, uint32_t Kp) {
+  return (r >> 3) * (Kp * 8) + (k >> 4) * 128 + (r & 7) * 16 + (k & 15);
+}
+
 ranc_status fail(std::string* err, ranc_status s, const std::string& m) {
   *err = m;
   return s;
@@ -168,7 +173,8 @@ ranc_status validate_and_compile(const ranc_network_desc* d, Compiled* out, std:
   Compiled& o = *out;
   o.G = G; o.A = A; o.N = N; o.K = K; o.D = D; o.C = C; o.I = I; o.W = W;
   o.grid_w = d->grid_w; o.grid_h = d->grid_h; o.pb = d->potential_bits;
-  o.Npad = (N + 31) / 32 * 32;
+  o.Npad = (N + 127) / 128 * 128;   // whole 128-lane TMEM halves for the tensor-core path
+  o.Kp = W * 32;
   o.Wn = (N + 31) / 32;
   o.WI = (I + 31) / 32;
   o.Rp = 1;
@@ -254,6 +260,31 @@ ranc_status validate_and_compile(const ranc_network_desc* d, Compiled* out, std:
         y = d->out_class[cn];
       }
       o.route[cp] = uint2{x, y};
+    }
+  }
+  // tensor-core eligibility: folded weights fit int8 and Wfold of one core fits
+  // the 64 KB shared-memory operand budget (<= 256 neurons)
+  {
+    bool ok = o.Npad <= 256 && (size_t)o.Npad * o.Kp <= 65536;
+    for (size_t i = 0; ok && i < (size_t)G * N * K; ++i)
+      if (d->weight[i] < -127 || d->weight[i] > 127) ok = false;
+    o.tc_ok = ok;
+    if (ok) {
+      const size_t per = (size_t)o.Npad * o.Kp;
+      o.wfold.assign((size_t)G * per, 0);
+      for (int c = 0; c < G; ++c) {
+        const int32_t* inv = &o.inv[(size_t)c * A];
+        const uint8_t* ty = d->axon_type + (size_t)c * A;
+        int8_t* dst = &o.wfold[(size_t)c * per];
+        for (int n = 0; n < N; ++n) {
+          const size_t cn = (size_t)c * N + n;
+          const uint32_t* src = d->crossbar + cn * W;
+          for (int a = 0; a < A; ++a)
+            if ((src[a >> 5] >> (a & 31)) & 1u)
+              dst[tc_operand_offset((uint32_t)n, (uint32_t)inv[a], (uint32_t)o.Kp)] =
+                  (int8_t)d->weight[cn * K + ty[a]];
+        }
+      }
     }
   }
   return RANC_OK;

@@ -12,7 +12,8 @@
 //     route uint2  [G][Npad]   x: kind | lin<<2 | delay<<3 | axon'<<8 ; y: dest core or class
 //     inl   i32 [G][A]         input line of permuted axon a' (-1 none)
 //   state (streamed every tick):
-//     pot   i16 [G][S][Npad]   membrane potentials (pb <= 16)
+//     pot   i16 [G][S][Npad]   membrane potentials (pb <= 16), popcount kernel;
+//           i16 [G][nT][Npad][NT] tile-blocked, tensor-core kernel (NT = 64)
 //     ring  u32 [Rp][G][S][W]  scheduler rings, W = ceil(A/32) words per row,
 //                              slot of tick t = t & (Rp-1), Rp = next_pow2(D+1)
 //     counts i32 [S][C]        output-bus class counts
@@ -41,8 +42,10 @@ struct TickParams {
   int32_t rp_mask;          // Rp - 1
   int32_t pot_lo, pot_hi;   // saturation range of pb bits
   int32_t fresh;            // first tick after a reset: potentials start at init
+  int32_t Kp;               // tensor-core path: K bytes per operand row (= 32*W)
   int64_t t;                // tick being executed
   int64_t raster_t0;        // first tick of the raster buffer
+  const uint8_t* wfold;     // tensor-core path: [G][Npad*Kp] canonical-layout int8
   const uint32_t* xp;
   const int16_t* wp;
   const uint8_t* pword;
@@ -62,6 +65,9 @@ struct TickParams {
 struct Compiled {
   int32_t G = 0, A = 0, N = 0, Npad = 0, K = 0, D = 0, C = 0, I = 0, W = 0, E = 0, Wn = 0, WI = 0;
   int32_t grid_w = 0, grid_h = 0, pb = 16, Rp = 2;
+  int32_t Kp = 0;               // 32 * W
+  bool tc_ok = false;           // eligible for the tcgen05 kind::i8 path
+  std::vector<int8_t> wfold;    // [G][Npad*Kp] (empty unless tc_ok)
   std::vector<uint32_t> xp;     // [G][E][Npad]
   std::vector<int16_t> wp;      // [G][E][Npad]
   std::vector<uint8_t> pword;   // [G][E]
@@ -92,7 +98,7 @@ struct ranc_ctx {
   std::string err;
   ranc::Compiled net;
   // device: compiled network
-  ranc::DevBuf d_xp, d_wp, d_pword, d_prm, d_route, d_inl, d_has_in, d_init;
+  ranc::DevBuf d_xp, d_wp, d_pword, d_prm, d_route, d_inl, d_has_in, d_init, d_wfold;
   // device: state
   ranc::DevBuf d_pot, d_ring, d_counts, d_lines, d_stage, d_raster;
   bool fresh = false;            // no tick since the last reset: d_pot is stale, potentials = init
@@ -103,7 +109,8 @@ struct ranc_ctx {
   int32_t sample_tile = 0;       // in use (set by ranc_run_ticks)
   int32_t sample_tile_opt = 0;   // RANC_OPT_SAMPLE_TILE, 0 = automatic
   int32_t use_graph = 1;
-  int32_t kernel = 0;
+  int32_t kernel = 0;            // RANC_OPT_KERNEL request: 0 auto, 1 popcount, 2 tensor core
+  int32_t kernel_active = 1;     // latched at every reset (the potential layout depends on it)
   int64_t launches = 0;
   int64_t device_bytes = 0;
   uint32_t trace_flags = 0;
@@ -114,6 +121,7 @@ struct ranc_ctx {
 };
 
 namespace ranc {
+enum { RANC_KERNEL_AUTO = 0, RANC_KERNEL_POPC = 1, RANC_KERNEL_TC = 2 };
 // compile.cpp
 ranc_status validate_and_compile(const ranc_network_desc* d, Compiled* out, std::string* err);
 // tick.cu
@@ -122,6 +130,9 @@ cudaError_t transpose_lines(ranc_ctx* ctx, const uint32_t* staging);
 cudaError_t launch_ticks(ranc_ctx* ctx, int64_t num_ticks);
 int choose_sample_tile(const Compiled& n, int64_t S);
 int pieces_template(int E);
+// tick_tc.cu
+int tc_tile();
+cudaError_t launch_ticks_tc(ranc_ctx* ctx, TickParams p, int64_t num_ticks);
 // api.cpp
 ranc_status dev_alloc(ranc_ctx* ctx, DevBuf* b, size_t bytes);
 void dev_free(ranc_ctx* ctx, DevBuf* b);

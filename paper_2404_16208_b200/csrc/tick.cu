@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(kThreads, (E <= 12 ? 4 : (E <= 16 ? 3 : 2))) t
       }
       if (p.raster) {
         const uint32_t m = __ballot_sync(0xFFFFFFFFu, fire && valid);
-        if (lane == 0)
+        if (lane == 0 && (n >> 5) < p.Wn)
           p.raster[(((size_t)(p.t - p.raster_t0) * p.S + s0 + s) * p.G + c) * p.Wn + (n >> 5)] = m;
       }
     }
@@ -269,6 +269,9 @@ cudaError_t launch_ticks(ranc_ctx* ctx, int64_t num_ticks) {
   p.counts = (int32_t*)ctx->d_counts.p;
   p.raster = (uint32_t*)ctx->d_raster.p;
   p.raster_t0 = ctx->raster_t0;
+  p.Kp = n.Kp;
+  p.wfold = (const uint8_t*)ctx->d_wfold.p;
+  if (ctx->kernel_active == RANC_KERNEL_TC) return launch_ticks_tc(ctx, p, num_ticks);
   const dim3 grid(n.G, (unsigned)((ctx->S + p.ST - 1) / p.ST));
   const size_t smem = smem_layout(p.ST, n.Npad, n.W, n.E, n.WI).total;
   for (int64_t i = 0; i < num_ticks; ++i) {

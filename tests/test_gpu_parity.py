@@ -17,12 +17,36 @@ def ranc():
     return m
 
 
-def per_tick(ranc, oracle_mod, net, inp, T, tile=None):
-    sim = ranc.Simulator(net)
+KERNELS = {"popc": 1, "tc": 2}
+
+
+def make_sim(ranc, net, kernel, **kw):
+    sim = ranc.Simulator(net, **kw)
+    if kernel == "tc":
+        try:
+            sim.set_option(ranc.OPT_KERNEL, KERNELS[kernel])
+        except ranc.RancError as e:
+            sim.close()
+            assert e.code == "RANC_E_CONFIG"
+            pytest.skip("outside the tensor-core envelope")
+    elif kernel:
+        sim.set_option(ranc.OPT_KERNEL, KERNELS[kernel])
+    return sim
+
+
+@pytest.fixture(params=["popc", "tc"])
+def kernel(request):
+    return request.param
+
+
+def per_tick(ranc, oracle_mod, net, inp, T, tile=None, kernel=None):
+    sim = make_sim(ranc, net, kernel)
     if tile:
         sim.set_option(ranc.OPT_SAMPLE_TILE, tile)
     sim.set_trace(ranc.TRACE_SPIKE_RASTER | ranc.TRACE_OUTPUT_EVENTS)
     sim.load_inputs(inp)
+    if kernel:
+        assert sim.info()["kernel"] == KERNELS[kernel]
     o = oracle_mod.Oracle(net, inp)
     for t in range(T):
         sim.run(1)
@@ -36,8 +60,8 @@ def per_tick(ranc, oracle_mod, net, inp, T, tile=None):
     return o
 
 
-def final_state(ranc, oracle_mod, net, inp, T, tile=None, events=True):
-    sim = ranc.Simulator(net)
+def final_state(ranc, oracle_mod, net, inp, T, tile=None, events=True, kernel=None):
+    sim = make_sim(ranc, net, kernel)
     if tile:
         sim.set_option(ranc.OPT_SAMPLE_TILE, tile)
     if events:
@@ -53,54 +77,54 @@ def final_state(ranc, oracle_mod, net, inp, T, tile=None, events=True):
     return o
 
 
-def test_config1_every_tick(ranc, oracle_mod):
+def test_config1_every_tick(ranc, oracle_mod, kernel):
     net, inp = config1()
-    o = per_tick(ranc, oracle_mod, net, inp, 64)
+    o = per_tick(ranc, oracle_mod, net, inp, 64, kernel=kernel)
     assert o.counts().sum() > 0 and o.pending().sum() > 0
 
 
 @pytest.mark.parametrize("seed", range(0, 200))
-def test_tiny_every_tick(ranc, oracle_mod, seed):
+def test_tiny_every_tick(ranc, oracle_mod, seed, kernel):
     net, inp = tiny_case(seed)
-    per_tick(ranc, oracle_mod, net, inp, 20)
+    per_tick(ranc, oracle_mod, net, inp, 20, kernel=kernel)
 
 
 @pytest.mark.parametrize("seed", range(0, 40))
-def test_corpus_every_tick(ranc, oracle_mod, seed):
+def test_corpus_every_tick(ranc, oracle_mod, seed, kernel):
     net, inp = corpus_case(seed)
-    per_tick(ranc, oracle_mod, net, inp, 12)
+    per_tick(ranc, oracle_mod, net, inp, 12, kernel=kernel)
 
 
 @pytest.mark.parametrize("tile", [1, 3, 64])
-def test_config2_full(ranc, oracle_mod, tile):
+def test_config2_full(ranc, oracle_mod, tile, kernel):
     net, inp = config2(S=300)
-    o = final_state(ranc, oracle_mod, net, inp, 17, tile=tile)
+    o = final_state(ranc, oracle_mod, net, inp, 17, tile=tile, kernel=kernel)
     assert o.counts().sum() > 0
 
 
-def test_config2_1000_samples(ranc, oracle_mod):
+def test_config2_1000_samples(ranc, oracle_mod, kernel):
     net, inp = config2(S=1000)
-    final_state(ranc, oracle_mod, net, inp, 17)
+    final_state(ranc, oracle_mod, net, inp, 17, kernel=kernel)
 
 
-def test_config5_small_mesh(ranc, oracle_mod):
+def test_config5_small_mesh(ranc, oracle_mod, kernel):
     net, inp = config5(S=5, T=40, grid=8)
-    o = final_state(ranc, oracle_mod, net, inp, 40)
+    o = final_state(ranc, oracle_mod, net, inp, 40, kernel=kernel)
     assert o.pending().sum() > 0
 
 
-def test_config5_global_every_tick(ranc, oracle_mod):
+def test_config5_global_every_tick(ranc, oracle_mod, kernel):
     net, inp = config5(S=3, T=20, grid=6, variant="global")
-    per_tick(ranc, oracle_mod, net, inp, 20)
+    per_tick(ranc, oracle_mod, net, inp, 20, kernel=kernel)
 
 
-def test_config3_full_size_sampled(ranc, oracle_mod):
+def test_config3_full_size_sampled(ranc, oracle_mod, kernel):
     """Config 3 at BASELINE size (10000 samples, 19 ticks, bench launch
     configuration) on the GPU; the oracle recomputes a spread of samples one
     by one (samples are independent, pinned by batch composition)."""
     net, inp = config3(S=10000)
     T = net.meta["T"]
-    sim = ranc.Simulator(net)
+    sim = make_sim(ranc, net, kernel)
     sim.load_inputs(inp).run(T)
     cnt = sim.outputs()
     pot = sim.potentials()
@@ -113,13 +137,13 @@ def test_config3_full_size_sampled(ranc, oracle_mod):
 
 
 @pytest.mark.parametrize("variant", ["vmm32", "vmm60", "vmm256"])
-def test_vmm_closed_form_on_gpu(ranc, variant):
+def test_vmm_closed_form_on_gpu(ranc, variant, kernel):
     """P6: the GPU's class counts equal M+ x and M- x (numpy), independent of
     the oracle."""
     from workloads.gen import VMM_VARIANTS
     net, inp = vmm(S=200, seed=1004, **VMM_VARIANTS[variant])
     M, X = net.meta["M"], net.meta["X"]
-    sim = ranc.Simulator(net)
+    sim = make_sim(ranc, net, kernel)
     sim.load_inputs(inp).run(net.meta["T"])
     cnt = sim.outputs()
     assert np.array_equal(cnt[:, 0::2], X @ np.maximum(M, 0).T)
@@ -127,14 +151,14 @@ def test_vmm_closed_form_on_gpu(ranc, variant):
     sim.close()
 
 
-def test_vmm_small_vs_oracle(ranc, oracle_mod):
+def test_vmm_small_vs_oracle(ranc, oracle_mod, kernel):
     net, inp = vmm(16, 10, 7, 5, S=20, seed=5, block_in=8)
-    final_state(ranc, oracle_mod, net, inp, net.meta["T"])
+    final_state(ranc, oracle_mod, net, inp, net.meta["T"], kernel=kernel)
 
 
-def test_resumable_and_reload(ranc, oracle_mod):
+def test_resumable_and_reload(ranc, oracle_mod, kernel):
     net, inp = config1(T=40)
-    sim = ranc.Simulator(net)
+    sim = make_sim(ranc, net, kernel)
     sim.load_inputs(inp).run(7).run(0).run(33)
     p1, c1 = sim.potentials(), sim.outputs()
     sim.load_inputs(inp).run(40)
@@ -147,10 +171,10 @@ def test_resumable_and_reload(ranc, oracle_mod):
     sim.close()
 
 
-def test_ticks_beyond_inputs_and_zero_ticks(ranc, oracle_mod):
+def test_ticks_beyond_inputs_and_zero_ticks(ranc, oracle_mod, kernel):
     net, inp = config2(S=5)
-    final_state(ranc, oracle_mod, net, inp, 30)
-    sim = ranc.Simulator(net)
+    final_state(ranc, oracle_mod, net, inp, 30, kernel=kernel)
+    sim = make_sim(ranc, net, kernel)
     sim.load_inputs(inp).run(0)
     assert np.array_equal(sim.potentials(), np.broadcast_to(net.initial_potential, (5, 5, 256)))
     sim.close()
@@ -177,4 +201,35 @@ def test_call_order_errors(ranc):
     with pytest.raises(ranc.RancError) as ei:
         sim._ck(sim.lib.ranc_read_outputs(sim.h, None, 3))
     assert ei.value.code == "RANC_E_SIZE"
+    sim.close()
+
+
+def test_kernel_switch_at_reset(ranc, oracle_mod):
+    """The kernel variant is latched at reset; switching between runs gives
+    the same results (the potential layout is re-initialised)."""
+    net, inp = config2(S=70)
+    sim = ranc.Simulator(net)
+    assert sim.info()["kernel"] in (1, 2)
+    res = []
+    for k in (1, 2, 1):
+        sim.set_option(ranc.OPT_KERNEL, k)
+        sim.load_inputs(inp).run(9)
+        assert sim.info()["kernel"] == k
+        res.append((sim.potentials(), sim.outputs(), sim.pending()))
+    for r in res[1:]:
+        for a, b in zip(res[0], r):
+            assert np.array_equal(a, b)
+    o = oracle_mod.Oracle(net, inp).run(9)
+    assert np.array_equal(res[0][0], o.potentials())
+    sim.close()
+
+
+def test_tc_envelope_rejects_wide_weights(ranc):
+    from workloads.gen import random_network
+    net = random_network(3, 2, 1, 64, 64, 4, 3, wb=12)
+    net.weight[0, 0, 0] = 1000
+    sim = ranc.Simulator(net)
+    with pytest.raises(ranc.RancError) as ei:
+        sim.set_option(ranc.OPT_KERNEL, 2)
+    assert ei.value.code == "RANC_E_CONFIG"
     sim.close()
