@@ -59,12 +59,6 @@ def dist_env():
     return rank, world, local
 
 
-def shard(S, world, rank):
-    base, rem = divmod(S, world)
-    lo = rank * base + min(rank, rem)
-    return lo, lo + base + (1 if rank < rem else 0)
-
-
 # ----------------------------------------------------------------------------
 # clocks sampled during the timed region
 # ----------------------------------------------------------------------------
@@ -212,7 +206,8 @@ def run_ours(args, rank, world, local):
     dev = torch.device("cuda", local)
     net, inp_all = build_workload(args.samples)
     T = net.meta["T"]
-    lo, hi = shard(args.samples, world, rank)
+    from paper_2404_16208_b200.dist import init_comm, shard_range
+    lo, hi = shard_range(args.samples, world, rank)
     inp = inp_all.slice(lo, hi)
     stream = torch.cuda.Stream(device=dev)
     sim = Simulator(net, device=local, stream=stream)
@@ -220,9 +215,7 @@ def run_ours(args, rank, world, local):
         sim.set_option(OPT_SAMPLE_TILE, args.tile)
     sim.set_option(OPT_KERNEL, {"auto": 0, "popc": 1, "tc": 2}[args.kernel])
     if world > 1:
-        uid = [Simulator.unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        sim.comm_init(uid[0], world, rank)
+        init_comm(sim, world, rank)
     sim.load_inputs(inp)
 
     def barrier():
