@@ -92,7 +92,8 @@ ranc_status sync(ranc_ctx* ctx, const char* where) {
 
 void free_all(ranc_ctx* ctx) {
   DevBuf* bufs[] = {&ctx->d_xp, &ctx->d_wp, &ctx->d_pword, &ctx->d_prm, &ctx->d_route, &ctx->d_inl,
-                    &ctx->d_has_in, &ctx->d_init, &ctx->d_wfold, &ctx->d_pot, &ctx->d_ring, &ctx->d_counts, &ctx->d_lines,
+                    &ctx->d_has_in, &ctx->d_init, &ctx->d_wfold, &ctx->d_route_tc, &ctx->d_runs,
+                    &ctx->d_nruns, &ctx->d_pot, &ctx->d_ring, &ctx->d_counts, &ctx->d_lines,
                     &ctx->d_stage, &ctx->d_raster};
   for (DevBuf* b : bufs) dev_free(ctx, b);
 }
@@ -148,6 +149,14 @@ ranc_status ranc_load_network(const ranc_network_desc* net, int cuda_device, ran
   if (!s) s = upload(ctx, &ctx->d_has_in, c.has_in);
   if (!s) s = upload(ctx, &ctx->d_init, c.init);
   if (!s && c.tc_ok) s = upload(ctx, &ctx->d_wfold, c.wfold);
+  if (!s && c.tc_ok) s = upload(ctx, &ctx->d_route_tc, c.route_tc);
+  if (!s && c.tc_ok) s = upload(ctx, &ctx->d_runs, c.runs);
+  if (!s && c.tc_ok) s = upload(ctx, &ctx->d_nruns, c.nruns);
+  if (!s) {
+    int sms = 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cuda_device) == cudaSuccess && sms > 0)
+      ctx->num_sms = sms;
+  }
   if (!s) s = sync(ctx, "ranc_load_network");
   if (s) {
     g_load_err = ctx->err;
@@ -179,18 +188,18 @@ ranc_status ranc_load_inputs(ranc_ctx* ctx, const ranc_inputs_desc* in) {
   }
   CK(cudaSetDevice(ctx->device), "cudaSetDevice");
   const int64_t S = in->num_samples;
+  const int64_t Sr = (S + 63) / 64 * 64;   // ring / line sample stride (TMA-aligned tiles)
   if (S != ctx->S || !ctx->d_pot.p) {
     // room for either potential layout: [G][S][Npad] or [G][nT][Npad][NT]
-    const int64_t nT = (S + tc_tile() - 1) / tc_tile();
-    TRY(dev_alloc(ctx, &ctx->d_pot, (size_t)c.G * std::max<int64_t>(S, nT * tc_tile()) * c.Npad * sizeof(int16_t)));
-    TRY(dev_alloc(ctx, &ctx->d_ring, (size_t)c.Rp * c.G * S * c.W * sizeof(uint32_t)));
+    TRY(dev_alloc(ctx, &ctx->d_pot, (size_t)c.G * Sr * c.Npad * sizeof(int16_t)));
+    TRY(dev_alloc(ctx, &ctx->d_ring, (size_t)c.Rp * c.G * Sr * c.W * sizeof(uint32_t)));
     TRY(dev_alloc(ctx, &ctx->d_counts, (size_t)S * c.C * sizeof(int32_t)));
   }
-  if (ctx->d_lines.bytes != line_words * sizeof(uint32_t)) {
-    TRY(dev_alloc(ctx, &ctx->d_lines, line_words * 4));
-    TRY(dev_alloc(ctx, &ctx->d_stage, line_words * 4));
-  }
+  const size_t dev_line_words = (size_t)in->num_input_ticks * Sr * c.WIp;
+  if (ctx->d_lines.bytes != dev_line_words * sizeof(uint32_t)) TRY(dev_alloc(ctx, &ctx->d_lines, dev_line_words * 4));
+  if (ctx->d_stage.bytes != line_words * sizeof(uint32_t)) TRY(dev_alloc(ctx, &ctx->d_stage, line_words * 4));
   ctx->S = S;
+  ctx->Sr = Sr;
   ctx->first_sample = in->first_sample;
   ctx->T_in = in->num_input_ticks;
   if (line_words) {
@@ -215,7 +224,9 @@ ranc_status ranc_reset_state(ranc_ctx* ctx) {
   CK(cudaSetDevice(ctx->device), "cudaSetDevice");
   CK(launch_reset(ctx), "reset kernel");
   // latch the kernel variant (the potential layout is re-initialised here)
-  ctx->kernel_active = (ctx->kernel == RANC_KERNEL_POPC || !ctx->net.tc_ok) ? RANC_KERNEL_POPC : RANC_KERNEL_TC;
+  ctx->kernel_active = (ctx->kernel == RANC_KERNEL_POPC || !ctx->net.tc_ok || tc_smem_bytes(ctx->net) > 227 * 1024)
+                           ? RANC_KERNEL_POPC
+                           : RANC_KERNEL_TC;
   ctx->now = 0;
   ctx->raster_ticks = 0;
   return RANC_OK;
@@ -300,8 +311,9 @@ ranc_status ranc_read_potentials(ranc_ctx* ctx, int32_t* pot, size_t n) {
     for (int g = 0; g < c.G; ++g)
       for (int j = 0; j < c.N; ++j)
         pot[((size_t)s * c.G + g) * c.N + j] =
-            ctx->kernel_active == RANC_KERNEL_TC ? h[(((size_t)g * nT + s / NT) * c.Npad + j) * NT + s % NT]
-                                                 : h[((size_t)g * ctx->S + s) * c.Npad + j];
+            ctx->kernel_active == RANC_KERNEL_TC
+                ? h[(((size_t)g * nT + s / NT) * c.Npad + j) * NT + ((((s % NT) >> 3) ^ (j & 7)) << 3) + (s & 7)]
+                : h[((size_t)g * ctx->S + s) * c.Npad + j];
   return RANC_OK;
 }
 
@@ -319,7 +331,7 @@ ranc_status ranc_read_pending(ranc_ctx* ctx, uint32_t* bits, size_t n) {
     return RANC_E_SIZE;
   }
   CK(cudaSetDevice(ctx->device), "cudaSetDevice");
-  std::vector<uint32_t> h((size_t)c.Rp * c.G * ctx->S * c.W);
+  std::vector<uint32_t> h((size_t)c.Rp * c.G * ctx->Sr * c.W);
   CK(cudaMemcpyAsync(h.data(), ctx->d_ring.p, h.size() * 4, cudaMemcpyDeviceToHost, ctx->stream), "D2H ring");
   TRY(sync(ctx, "ranc_read_pending"));
   std::memset(bits, 0, want * 4);
@@ -327,9 +339,10 @@ ranc_status ranc_read_pending(ranc_ctx* ctx, uint32_t* bits, size_t n) {
     const int slot = (int)((ctx->now + j) & (c.Rp - 1));
     for (int64_t s = 0; s < ctx->S; ++s)
       for (int g = 0; g < c.G; ++g) {
-        const uint32_t* src = &h[(((size_t)slot * c.G + g) * ctx->S + s) * c.W];
+        const uint32_t* src = &h[(((size_t)slot * c.G + g) * ctx->Sr + s) * c.W];
         uint32_t* dst = bits + (((size_t)s * c.G + g) * c.D + j) * c.W;
-        const int32_t* perm = &c.perm[(size_t)g * c.A];
+        const int32_t* perm = ctx->kernel_active == RANC_KERNEL_TC ? &c.perm_tc[(size_t)g * c.A]
+                                                                   : &c.perm[(size_t)g * c.A];
         for (int ap = 0; ap < c.A; ++ap)
           if ((src[ap >> 5] >> (ap & 31)) & 1u) {
             const int a = perm[ap];

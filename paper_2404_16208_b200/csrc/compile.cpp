@@ -177,6 +177,7 @@ ranc_status validate_and_compile(const ranc_network_desc* d, Compiled* out, std:
   o.Kp = W * 32;
   o.Wn = (N + 31) / 32;
   o.WI = (I + 31) / 32;
+  o.WIp = (o.WI + 3) / 4 * 4;
   o.Rp = 1;
   while (o.Rp < D + 1) o.Rp <<= 1;
   o.perm.assign((size_t)G * A, 0);
@@ -269,21 +270,66 @@ ranc_status validate_and_compile(const ranc_network_desc* d, Compiled* out, std:
     for (size_t i = 0; ok && i < (size_t)G * N * K; ++i)
       if (d->weight[i] < -127 || d->weight[i] > 127) ok = false;
     o.tc_ok = ok;
-    if (ok) {
-      const size_t per = (size_t)o.Npad * o.Kp;
-      o.wfold.assign((size_t)G * per, 0);
-      for (int c = 0; c < G; ++c) {
-        const int32_t* inv = &o.inv[(size_t)c * A];
-        const uint8_t* ty = d->axon_type + (size_t)c * A;
-        int8_t* dst = &o.wfold[(size_t)c * per];
-        for (int n = 0; n < N; ++n) {
-          const size_t cn = (size_t)c * N + n;
-          const uint32_t* src = d->crossbar + cn * W;
-          for (int a = 0; a < A; ++a)
-            if ((src[a >> 5] >> (a & 31)) & 1u)
-              dst[tc_operand_offset((uint32_t)n, (uint32_t)inv[a], (uint32_t)o.Kp)] =
-                  (int8_t)d->weight[cn * K + ty[a]];
-        }
+  }
+  if (o.tc_ok) {
+    // Axon order of the tensor-core path: the types are folded into the
+    // weights, so instead of a type-sort the axons are sorted by input line
+    // (axons without a line keep their order, after the others).  External
+    // inputs then arrive as a few contiguous bit runs per core (a 16x16 image
+    // patch is 16 runs of 16) instead of one bit per axon.
+    o.perm_tc.assign((size_t)G * A, 0);
+    o.inv_tc.assign((size_t)G * A, 0);
+    std::vector<std::vector<int2>> runs(G);
+    int rmax = 1;
+    for (int c = 0; c < G; ++c) {
+      const int32_t* il = d->input_line + (size_t)c * A;
+      int32_t* perm = &o.perm_tc[(size_t)c * A];
+      for (int a = 0; a < A; ++a) perm[a] = a;
+      std::stable_sort(perm, perm + A, [&](int x, int y) {
+        const bool hx = il[x] >= 0, hy = il[y] >= 0;
+        if (hx != hy) return hx;
+        return hx && il[x] < il[y];
+      });
+      for (int ap = 0; ap < A; ++ap) o.inv_tc[(size_t)c * A + perm[ap]] = ap;
+      for (int ap = 0; ap < A && il[perm[ap]] >= 0;) {
+        int len = 1;
+        while (ap + len < A && len < 32 && il[perm[ap + len]] == il[perm[ap]] + len) ++len;
+        runs[c].push_back(int2{ap | (len << 16), il[perm[ap]]});
+        ap += len;
+      }
+      rmax = std::max<int>(rmax, (int)runs[c].size());
+    }
+    o.rmax = rmax;
+    o.runs.assign((size_t)G * rmax, int2{0, 0});
+    o.nruns.assign(G, 0);
+    for (int c = 0; c < G; ++c) {
+      o.nruns[c] = (int32_t)runs[c].size();
+      for (size_t r = 0; r < runs[c].size(); ++r) o.runs[(size_t)c * rmax + r] = runs[c][r];
+    }
+    // route words with destination axons in the tensor-core order
+    o.route_tc = o.route;
+    for (int c = 0; c < G; ++c)
+      for (int n = 0; n < N; ++n) {
+        const size_t cn = (size_t)c * N + n;
+        if (d->dest_kind[cn] != RK_ROUTE) continue;
+        uint2& r = o.route_tc[(size_t)c * Np + n];
+        const int dc = (int)r.y;
+        const int dap = o.inv_tc[(size_t)dc * A + d->dest_axon[cn]];
+        r.x = (r.x & 0xFFu) | ((uint32_t)dap << 8);
+      }
+    // folded weights in the canonical operand layout (tc.h)
+    const size_t per = (size_t)o.Npad * o.Kp;
+    o.wfold.assign((size_t)G * per, 0);
+    for (int c = 0; c < G; ++c) {
+      const int32_t* inv = &o.inv_tc[(size_t)c * A];
+      const uint8_t* ty = d->axon_type + (size_t)c * A;
+      int8_t* dst = &o.wfold[(size_t)c * per];
+      for (int n = 0; n < N; ++n) {
+        const size_t cn = (size_t)c * N + n;
+        const uint32_t* src = d->crossbar + cn * W;
+        for (int a = 0; a < A; ++a)
+          if ((src[a >> 5] >> (a & 31)) & 1u)
+            dst[tc_operand_offset((uint32_t)n, (uint32_t)inv[a], (uint32_t)o.Kp)] = (int8_t)d->weight[cn * K + ty[a]];
       }
     }
   }

@@ -13,12 +13,15 @@
 //     inl   i32 [G][A]         input line of permuted axon a' (-1 none)
 //   state (streamed every tick):
 //     pot   i16 [G][S][Npad]   membrane potentials (pb <= 16), popcount kernel;
-//           i16 [G][nT][Npad][NT] tile-blocked, tensor-core kernel (NT = 64)
-//     ring  u32 [Rp][G][S][W]  scheduler rings, W = ceil(A/32) words per row,
+//           i16 [G][nT][Npad][NT] tile-blocked, tensor-core kernel (NT = 64);
+//           within a tile row the 16-byte chunks are XOR-swizzled by (n & 7)
+//     ring  u32 [Rp][G][Sr][W] scheduler rings, W = ceil(A/32) words per row,
+//                              Sr = S rounded up to 64 (TMA-aligned tiles),
 //                              slot of tick t = t & (Rp-1), Rp = next_pow2(D+1)
 //     counts i32 [S][C]        output-bus class counts
-//     lines u32 [T_in][S][WI]  external input line bits (transposed at load so a
-//                              tile's rows of one tick are contiguous)
+//     lines u32 [T_in][Sr][WIp] external input line bits (transposed at load so a
+//                              tile's rows of one tick are contiguous; WIp = WI
+//                              rounded up to 4 words)
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -39,6 +42,8 @@ __host__ __device__ inline uint32_t route_axon(uint32_t x) { return (x >> 8) & 0
 
 struct TickParams {
   int32_t G, S, N, Npad, A, W, E, Wn, C, T_in, WI, ST;
+  int32_t Sr;               // sample stride of ring rows and input lines (S rounded up to 64)
+  int32_t WIp;              // u32 words per input-line row (WI rounded up to 4: 16-byte rows)
   int32_t rp_mask;          // Rp - 1
   int32_t pot_lo, pot_hi;   // saturation range of pb bits
   int32_t fresh;            // first tick after a reset: potentials start at init
@@ -46,6 +51,9 @@ struct TickParams {
   int64_t t;                // tick being executed
   int64_t raster_t0;        // first tick of the raster buffer
   const uint8_t* wfold;     // tensor-core path: [G][Npad*Kp] canonical-layout int8
+  const int2* runs;         // tensor-core path: input runs [G][rmax]
+  const int32_t* nruns;     // [G]
+  int32_t rmax;
   const uint32_t* xp;
   const int16_t* wp;
   const uint8_t* pword;
@@ -66,8 +74,14 @@ struct Compiled {
   int32_t G = 0, A = 0, N = 0, Npad = 0, K = 0, D = 0, C = 0, I = 0, W = 0, E = 0, Wn = 0, WI = 0;
   int32_t grid_w = 0, grid_h = 0, pb = 16, Rp = 2;
   int32_t Kp = 0;               // 32 * W
+  int32_t WIp = 0;              // WI rounded up to 4
   bool tc_ok = false;           // eligible for the tcgen05 kind::i8 path
-  std::vector<int8_t> wfold;    // [G][Npad*Kp] (empty unless tc_ok)
+  std::vector<int8_t> wfold;    // [G][Npad*Kp] canonical operand layout, tensor-core axon order
+  std::vector<int32_t> perm_tc, inv_tc;   // tensor-core axon order (sorted by input line)
+  std::vector<uint2> route_tc;  // route words with tensor-core destination axons
+  std::vector<int2> runs;       // [G][rmax] input runs: x = a'start | len<<16, y = first line
+  std::vector<int32_t> nruns;   // [G]
+  int32_t rmax = 0;
   std::vector<uint32_t> xp;     // [G][E][Npad]
   std::vector<int16_t> wp;      // [G][E][Npad]
   std::vector<uint8_t> pword;   // [G][E]
@@ -98,11 +112,13 @@ struct ranc_ctx {
   std::string err;
   ranc::Compiled net;
   // device: compiled network
-  ranc::DevBuf d_xp, d_wp, d_pword, d_prm, d_route, d_inl, d_has_in, d_init, d_wfold;
+  ranc::DevBuf d_xp, d_wp, d_pword, d_prm, d_route, d_inl, d_has_in, d_init, d_wfold, d_route_tc, d_runs, d_nruns;
+  int num_sms = 148;
   // device: state
   ranc::DevBuf d_pot, d_ring, d_counts, d_lines, d_stage, d_raster;
   bool fresh = false;            // no tick since the last reset: d_pot is stale, potentials = init
   int64_t S = 0, first_sample = 0;
+  int64_t Sr = 0;                // S rounded up to 64
   int32_t T_in = 0;
   bool have_inputs = false;
   int64_t now = 0;
@@ -132,6 +148,7 @@ int choose_sample_tile(const Compiled& n, int64_t S);
 int pieces_template(int E);
 // tick_tc.cu
 int tc_tile();
+size_t tc_smem_bytes(const Compiled& n);
 cudaError_t launch_ticks_tc(ranc_ctx* ctx, TickParams p, int64_t num_ticks);
 // api.cpp
 ranc_status dev_alloc(ranc_ctx* ctx, DevBuf* b, size_t bytes);

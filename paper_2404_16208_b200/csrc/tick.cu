@@ -63,7 +63,7 @@ __global__ void __launch_bounds__(kThreads, (E <= 12 ? 4 : (E <= 16 ? 3 : 2))) t
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int W = p.W;
-  const SmemLayout L = smem_layout(p.ST, p.Npad, W, E, p.WI);
+  const SmemLayout L = smem_layout(p.ST, p.Npad, W, E, p.WIp);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
   int16_t* pot_s = reinterpret_cast<int16_t*>(smem + L.pot);
   uint32_t* pk = reinterpret_cast<uint32_t*>(smem + L.pk);
@@ -85,15 +85,15 @@ __global__ void __launch_bounds__(kThreads, (E <= 12 ? 4 : (E <= 16 ? 3 : 2))) t
   }
   // a1: stage the current scheduler rows of (core c, samples s0..) and clear
   // them (the row is free again for spikes due at t + Rp).
-  uint32_t* row = p.ring + (((size_t)cur * p.G + c) * p.S + s0) * W;
+  uint32_t* row = p.ring + (((size_t)cur * p.G + c) * p.Sr + s0) * W;
   for (int i = tid; i < ns * W; i += blockDim.x) {
     raw[i] = row[i];
     row[i] = 0u;
   }
   const bool inject = p.t < p.T_in && p.has_in[c];
   if (inject) {
-    const uint32_t* lg = p.lines + ((size_t)p.t * p.S + s0) * p.WI;   // [T_in][S][WI]
-    for (int i = tid; i < ns * p.WI; i += blockDim.x) lines_s[i] = lg[i];
+    const uint32_t* lg = p.lines + ((size_t)p.t * p.Sr + s0) * p.WIp;   // [T_in][Sr][WIp]
+    for (int i = tid; i < ns * p.WIp; i += blockDim.x) lines_s[i] = lg[i];
   }
   __syncthreads();
   // a2: external input lines arriving at tick t (G8).  Thread <-> permuted
@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(kThreads, (E <= 12 ? 4 : (E <= 16 ? 3 : 2))) t
       const int32_t ln = ap < p.A ? p.inl[(size_t)c * p.A + ap] : -1;
       const int lw = ln >> 5, lb = ln & 31;
       for (int s = 0; s < ns; ++s) {
-        const bool bit = ln >= 0 && ((lines_s[s * p.WI + lw] >> lb) & 1u);
+        const bool bit = ln >= 0 && ((lines_s[s * p.WIp + lw] >> lb) & 1u);
         const uint32_t m = __ballot_sync(0xFFFFFFFFu, bit);
         if (lane == 0) raw[s * W + (ap0 >> 5)] |= m;
       }
@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(kThreads, (E <= 12 ? 4 : (E <= 16 ? 3 : 2))) t
         if (kind == RK_ROUTE) {
           const uint32_t ax = route_axon(rt.x);
           const int slot = (int)((p.t + route_delay(rt.x)) & p.rp_mask);
-          atomicOr(p.ring + (((size_t)slot * p.G + rt.y) * p.S + s0 + s) * W + (ax >> 5), 1u << (ax & 31));
+          atomicOr(p.ring + (((size_t)slot * p.G + rt.y) * p.Sr + s0 + s) * W + (ax >> 5), 1u << (ax & 31));
         } else {
           atomicAdd(p.counts + (size_t)(s0 + s) * p.C + rt.y, 1);
         }
@@ -185,14 +185,14 @@ __global__ void __launch_bounds__(kThreads, (E <= 12 ? 4 : (E <= 16 ? 3 : 2))) t
   }
 }
 
-// [S][T_in][WI] -> [T_in][S][WI]
+// [S][T_in][WI] -> [T_in][Sr][WIp] (padding words stay zero)
 __global__ void transpose_lines_kernel(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, int S, int T,
-                                       int WI) {
+                                       int WI, int Sr, int WIp) {
   const size_t total = (size_t)S * T * WI;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
     const size_t w = i % WI, st = i / WI;
     const size_t t = st % T, s = st / T;
-    out[(t * S + s) * WI + w] = in[i];
+    out[(t * Sr + s) * WIp + w] = in[i];
   }
 }
 
@@ -230,8 +230,10 @@ cudaError_t transpose_lines(ranc_ctx* ctx, const uint32_t* staging) {
   const size_t total = (size_t)ctx->S * ctx->T_in * n.WI;
   if (!total) return cudaSuccess;
   int blocks = (int)std::min<size_t>((total + 255) / 256, 148 * 8);
+  cudaError_t e = cudaMemsetAsync(ctx->d_lines.p, 0, ctx->d_lines.bytes, ctx->stream);
+  if (e != cudaSuccess) return e;
   transpose_lines_kernel<<<blocks, 256, 0, ctx->stream>>>(staging, (uint32_t*)ctx->d_lines.p, (int)ctx->S,
-                                                          ctx->T_in, n.WI);
+                                                          ctx->T_in, n.WI, (int)ctx->Sr, n.WIp);
   ctx->launches++;
   return cudaGetLastError();
 }
@@ -250,7 +252,7 @@ cudaError_t launch_reset(ranc_ctx* ctx) {
 cudaError_t launch_ticks(ranc_ctx* ctx, int64_t num_ticks) {
   const Compiled& n = ctx->net;
   TickParams p{};
-  p.G = n.G; p.S = (int)ctx->S; p.N = n.N; p.Npad = n.Npad; p.A = n.A; p.W = n.W; p.E = n.E;
+  p.G = n.G; p.S = (int)ctx->S; p.Sr = (int)ctx->Sr; p.WIp = n.WIp; p.N = n.N; p.Npad = n.Npad; p.A = n.A; p.W = n.W; p.E = n.E;
   p.Wn = n.Wn; p.C = n.C; p.T_in = ctx->T_in; p.WI = n.WI; p.ST = ctx->sample_tile;
   p.rp_mask = n.Rp - 1;
   p.pot_lo = -(1 << (n.pb - 1));
@@ -273,7 +275,7 @@ cudaError_t launch_ticks(ranc_ctx* ctx, int64_t num_ticks) {
   p.wfold = (const uint8_t*)ctx->d_wfold.p;
   if (ctx->kernel_active == RANC_KERNEL_TC) return launch_ticks_tc(ctx, p, num_ticks);
   const dim3 grid(n.G, (unsigned)((ctx->S + p.ST - 1) / p.ST));
-  const size_t smem = smem_layout(p.ST, n.Npad, n.W, n.E, n.WI).total;
+  const size_t smem = smem_layout(p.ST, n.Npad, n.W, n.E, n.WIp).total;
   for (int64_t i = 0; i < num_ticks; ++i) {
     p.t = ctx->now + i;
     p.fresh = ctx->fresh ? 1 : 0;

@@ -1,22 +1,32 @@
 // tick_tc.cu -- the tick kernel with synaptic integration on the 5th-gen tensor
 // cores (tcgen05.mma kind::i8, accumulators in TMEM).  SURVEY.md 8(f) row f1.
 //
-// Integration (Alg. 1 l.10-13) of one core over a tile of NT
+// Integration (Alg. 1 l.10-13) of one core over a tile of NT = 64
 // samples is the integer matrix product
 //     acc[n][s] = sum_a' Wfold[n][a'] * spike[s][a'],
 //     Wfold[n][a'] = conn[n][a'] * w[n][type(a')]
-// exact in int32 (|w| <= 127 checked at load, K <= 256 terms).  M = 128
-// neurons per MMA (two halves for 256 neurons), N = NT samples, K = 32 axons
+// exact in int32 (|w| <= 127 checked at load, K <= 1024 terms).  M = 128
+// neurons per MMA (two halves for 256 neurons), N = 64 samples, K = 32 axons
 // per instruction.  Wfold is pre-arranged on the host in the canonical
-// K-major core-matrix layout (tc.h) and lands in shared memory with one TMA
-// bulk copy; the spike bits of the tile are expanded to 0/1 bytes in the same
-// layout.  The epilogue (thread = neuron = TMEM lane) adds the accumulator to
-// the potential, applies leak / thresholds / reset (Alg. 1 l.14) and routes
-// the spikes exactly like the popcount kernel (tick.cu), which stays the path
-// for networks outside the int8 envelope.
+// K-major core-matrix layout (tc.h).
 //
-// Potential layout of this kernel: tile-blocked [G][nT][Np][NT] int16, so a
-// thread's 32 samples of one neuron are 64 contiguous bytes.
+// Persistent, warp-specialised: one CTA per SM walks a contiguous range of
+// (core, sample-tile) work items; the four roles overlap through mbarriers,
+// with two stages so that tile i+1 is loaded, expanded and multiplied while
+// the epilogue of tile i runs:
+//   warp 0      producer: TMA bulk loads of Wfold (on a core change) and of the
+//               tile's potentials (HBM -> shared)
+//   warp 1      MMA issuer (one elected thread) + TMEM allocation
+//   warps 2-3   spike stage: scheduler rows due now (a1, read + clear), input
+//               runs (a2), bits -> 0/1 bytes in the operand layout
+//   warps 4-11  epilogue, thread = neuron = TMEM lane: leak / thresholds /
+//               reset (a4), potentials back to shared and out with one TMA
+//               bulk store per tile, routing and output bus (a5, a6)
+// A tick is one launch; the kernel boundary is the tick barrier (a7).
+//
+// Potential layout: tile-blocked [G][nT][Np][64] int16, the eight 16-byte
+// chunks of a row XOR-swizzled with (n & 7) so that the epilogue's 16-byte
+// shared loads are bank-conflict free.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -30,217 +40,341 @@ namespace ranc {
 
 namespace {
 
-constexpr int kThreadsTC = 256;
+constexpr int NT = 64;                 // samples per tile (MMA N)
+constexpr int kExpWarps = 2;
+constexpr int kEpiWarps = 8;
+constexpr int kThreadsTC = 32 * (2 + kExpWarps + kEpiWarps);  // 384
+constexpr int kExpThreads = 32 * kExpWarps;
+constexpr int kEpiThreads = 32 * kEpiWarps;
+
+enum Bar { FULL0 = 0, BFULL0 = 2, BEMPTY0 = 4, ACCFULL0 = 6, ACCEMPTY0 = 8, SEMPTY0 = 10, WFULL = 12, WFREE = 13,
+           NBARS = 14 };
 
 struct TcLayout {
-  uint32_t w, b, raw, lines, total;
+  uint32_t w, stage, pot, b, raw, lines, stage_bytes, total;
 };
 
-__host__ __device__ inline TcLayout tc_layout(int Np, int Kp, int NT, int W, int WI) {
+// WIp: input-line row words (multiple of 4)
+__host__ __device__ inline TcLayout tc_layout(int Np, int Kp, int W, int WIp) {
   TcLayout L;
-  uint32_t o = 64;                          // mbarriers + TMEM address holder
-  L.w = 1024;  o = L.w + (uint32_t)Np * Kp; // Wfold, canonical layout
-  o = (o + 127) & ~127u;
-  L.b = o;     o += (uint32_t)NT * Kp;      // spikes as bytes, canonical layout
-  o = (o + 15) & ~15u;
-  L.raw = o;   o += (uint32_t)NT * W * 4;   // staged ring rows
-  o = (o + 15) & ~15u;
-  L.lines = o; o += (uint32_t)NT * WI * 4;  // staged input lines
-  L.total = (o + 127) & ~127u;
+  L.w = 1024;
+  uint32_t o = L.w + (uint32_t)Np * Kp;
+  L.stage = (o + 1023) & ~1023u;
+  uint32_t q = 0;
+  L.pot = q;   q += (uint32_t)Np * NT * 2;
+  q = (q + 127) & ~127u;
+  L.b = q;     q += (uint32_t)NT * Kp;
+  q = (q + 15) & ~15u;
+  L.raw = q;   q += (uint32_t)NT * W * 4;
+  q = (q + 15) & ~15u;
+  L.lines = q; q += (uint32_t)NT * WIp * 4;
+  L.stage_bytes = (q + 1023) & ~1023u;
+  L.total = L.stage + 2 * L.stage_bytes;
   return L;
 }
 
-template <int NT>
-__global__ void __launch_bounds__(kThreadsTC, 2) tick_tc_kernel(const TickParams p) {
+__device__ __forceinline__ void named_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+__device__ __forceinline__ int16_t* pot_tile(const TickParams& p, int c, int tile, int nT) {
+  return p.pot + ((size_t)c * nT + tile) * (size_t)p.Npad * NT;
+}
+
+__global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  uint64_t* bar_w = reinterpret_cast<uint64_t*>(smem);
-  uint64_t* bar_mma = reinterpret_cast<uint64_t*>(smem + 8);
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + 16);
-  const int Np = p.Npad, Kp = p.Kp, W = p.W;
-  const TcLayout L = tc_layout(Np, Kp, NT, W, p.WI);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + 8 * NBARS);
+  const int Np = p.Npad, Kp = p.Kp, W = p.W, WIp = p.WIp;
+  const TcLayout L = tc_layout(Np, Kp, W, WIp);
   uint8_t* w_s = smem + L.w;
-  uint8_t* b_s = smem + L.b;
-  uint32_t* raw = reinterpret_cast<uint32_t*>(smem + L.raw);
-  uint32_t* lines_s = reinterpret_cast<uint32_t*>(smem + L.lines);
-
-  const int c = blockIdx.x;
-  const int tile = blockIdx.y;
-  const int s0 = tile * NT;
-  const int ns = min(NT, p.S - s0);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int cur = (int)(p.t & p.rp_mask);
-  const int Mh = Np / 128;
+  const int Mh = Np >> 7;
   const int nT = (p.S + NT - 1) / NT;
+  const int total = p.G * nT;
+  const int lo = (int)((int64_t)blockIdx.x * total / gridDim.x);
+  const int hi = (int)((int64_t)(blockIdx.x + 1) * total / gridDim.x);
+  const int nwork = hi - lo;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t tcols = 2u * Mh * NT;  // two accumulator stages
+  const uint32_t acc_stride = (uint32_t)Mh * NT;
+  const uint32_t pot_bytes = (uint32_t)Np * NT * 2;
 
-  if (warp == 0) tc::alloc(tmem_holder, 2 * NT >= 32 ? 2 * NT : 32);
-  if (tid == 32) {
-    ptx::mbar_init(bar_w, 1);
-    ptx::mbar_init(bar_mma, 1);
+  if (warp == 1) tc::alloc(tmem_holder, tcols < 32 ? 32 : tcols);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&bars[FULL0 + i], 1);
+      ptx::mbar_init(&bars[BFULL0 + i], kExpThreads);
+      ptx::mbar_init(&bars[BEMPTY0 + i], 1);
+      ptx::mbar_init(&bars[ACCFULL0 + i], 1);
+      ptx::mbar_init(&bars[ACCEMPTY0 + i], kEpiWarps);
+      ptx::mbar_init(&bars[SEMPTY0 + i], 1);
+    }
+    ptx::mbar_init(&bars[WFULL], 1);
+    ptx::mbar_init(&bars[WFREE], 1);
     ptx::fence_mbar_init();
   }
-  __syncthreads();
-  if (tid == 32) {
-    const uint32_t bytes = (uint32_t)Np * Kp;
-    ptx::mbar_arrive_expect_tx(bar_w, bytes);
-    ptx::bulk_g2s(w_s, p.wfold + (size_t)c * bytes, bytes, bar_w);
-  }
-
-  // epilogue identity: neuron n = TMEM lane, half h
-  const int h = warp >> 2, q = warp & 3;
-  const int n = h * 128 + q * 32 + lane;
-  const bool in_tile = h < Mh;
-  // prefetch this thread's potentials for the whole tile (2*NT bytes)
-  uint32_t potw[NT / 2];   // 2 x int16 per word, samples in order
-  int16_t* pot_row = p.pot + (((size_t)c * nT + tile) * Np + (in_tile ? n : 0)) * NT;
-  if (in_tile && !p.fresh) {
-#pragma unroll
-    for (int i = 0; i < NT / 8; ++i) {
-      const uint4 v = reinterpret_cast<const uint4*>(pot_row)[i];
-      potw[4 * i + 0] = v.x;
-      potw[4 * i + 1] = v.y;
-      potw[4 * i + 2] = v.z;
-      potw[4 * i + 3] = v.w;
-    }
-  }
-
-  // a1: stage + clear the scheduler rows due now
-  uint32_t* row = p.ring + (((size_t)cur * p.G + c) * p.S + s0) * W;
-  for (int i = tid; i < ns * W; i += blockDim.x) {
-    raw[i] = row[i];
-    row[i] = 0u;
-  }
-  for (int i = ns * W + tid; i < NT * W; i += blockDim.x) raw[i] = 0u;  // tail samples: no spikes
-  const bool inject = p.t < p.T_in && p.has_in[c];
-  if (inject) {
-    const uint32_t* lg = p.lines + ((size_t)p.t * p.S + s0) * p.WI;
-    for (int i = tid; i < ns * p.WI; i += blockDim.x) lines_s[i] = lg[i];
-  }
-  __syncthreads();
-  // a2: input lines (ballot per 32-axon word, as in tick.cu)
-  if (inject) {
-    for (int ap0 = tid - lane; ap0 < W * 32; ap0 += blockDim.x) {
-      const int ap = ap0 + lane;
-      const int32_t ln = ap < p.A ? p.inl[(size_t)c * p.A + ap] : -1;
-      const int lw = ln >> 5, lb = ln & 31;
-      for (int s = 0; s < ns; ++s) {
-        const bool bit = ln >= 0 && ((lines_s[s * p.WI + lw] >> lb) & 1u);
-        const uint32_t m = __ballot_sync(0xFFFFFFFFu, bit);
-        if (lane == 0) raw[s * W + (ap0 >> 5)] |= m;
-      }
-    }
-    __syncthreads();
-  }
-  // spikes -> 0/1 bytes in the canonical K-major layout (B operand, N = samples)
-  const int K16 = Kp >> 4;
-  for (int i = tid; i < NT * K16; i += blockDim.x) {
-    const int s = i / K16, k16 = i - s * K16;
-    const uint32_t wv = raw[s * W + (k16 >> 1)];
-    const uint32_t bits = (k16 & 1) ? (wv >> 16) : (wv & 0xFFFFu);
-    uint4 v;
-    v.x = tc::nib2bytes(bits & 15u);
-    v.y = tc::nib2bytes((bits >> 4) & 15u);
-    v.z = tc::nib2bytes((bits >> 8) & 15u);
-    v.w = tc::nib2bytes((bits >> 12) & 15u);
-    *reinterpret_cast<uint4*>(b_s + tc::operand_offset(s, k16 * 16, Kp)) = v;
-  }
-  ptx::fence_proxy_async_smem();
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = *tmem_holder;
 
-  // a3: integration on the tensor cores
-  if (tid == 0) {
-    ptx::mbar_wait(bar_w, 0);
-    const uint32_t id = tc::idesc_i8(128, NT);
-    const uint32_t sbo = (uint32_t)Kp * 8;
-    for (int hh = 0; hh < Mh; ++hh)
-      for (int kk = 0; kk < Kp / 32; ++kk) {
-        const uint64_t ad = tc::smem_desc(ptx::smem_u32(w_s + hh * 128 * Kp + kk * 256), 128, sbo);
-        const uint64_t bd = tc::smem_desc(ptx::smem_u32(b_s + kk * 256), 128, sbo);
-        tc::mma_i8(tmem + hh * NT, ad, bd, id, kk > 0 ? 1u : 0u);
-      }
-    tc::commit(bar_mma);
-  }
-  ptx::mbar_wait(bar_mma, 0);
-  tc::fence_after();
-
-  // a4-a6: epilogue, thread = neuron, 32 samples per TMEM load
-  if (in_tile) {
-    const short4 prm = p.prm[(size_t)c * Np + n];
-    const uint2 rt = p.route[(size_t)c * Np + n];
-    const int init = p.init[(size_t)c * Np + n];
-    const uint32_t kind = route_kind(rt.x);
-    const bool lin = route_lin(rt.x);
-    const bool valid = n < p.N;
-    const int leak = prm.x, pth = prm.y, nth = prm.z, rst = prm.w;
-    const uint32_t ax = route_axon(rt.x);
-    const int slot = (int)((p.t + route_delay(rt.x)) & p.rp_mask);
-    uint32_t* ring_dst = p.ring + (((size_t)slot * p.G + rt.y) * p.S) * W + (ax >> 5);
-    const uint32_t axbit = 1u << (ax & 31);
-#pragma unroll
-    for (int j = 0; j < NT / 32; ++j) {
-      uint32_t acc[32];
-      tc::ld32(tmem + ((uint32_t)(q * 32) << 16) + h * NT + j * 32, acc);
-      tc::wait_ld();
-      uint32_t outw[16];
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const uint32_t word = potw[(j * 32 + i) >> 1];
-        const int pot = p.fresh ? init : (int)(int16_t)((i & 1) ? (word >> 16) : (word & 0xFFFFu));
-        const int v = pot + (int)acc[i] + leak;
-        const bool fire = v >= pth;
-        const bool neg = v < nth;
-        const int rv = lin ? v - (fire ? pth : nth) : (fire ? rst : -rst);
-        int nv = (fire || neg) ? rv : v;
-        nv = min(max(nv, p.pot_lo), p.pot_hi);
-        if (i & 1) outw[i >> 1] |= ((uint32_t)nv & 0xFFFFu) << 16;
-        else outw[i >> 1] = (uint32_t)nv & 0xFFFFu;
-        const int s = j * 32 + i;
-        const bool real = s < ns;
-        if (fire && valid && real && kind != RK_NONE) {
-          if (kind == RK_ROUTE) atomicOr(ring_dst + (size_t)(s0 + s) * W, axbit);
-          else atomicAdd(p.counts + (size_t)(s0 + s) * p.C + rt.y, 1);
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      const int cur = (int)(p.t & p.rp_mask);
+      int prev_core = -1, jw = -1;
+      for (int k = 0; k < nwork; ++k) {
+        const int idx = lo + k, c = idx / nT, tile = idx - c * nT;
+        const int s = k & 1, u = k >> 1;
+        ptx::mbar_wait(&bars[SEMPTY0 + s], (u & 1) ^ 1);
+        if (c != prev_core) {
+          ++jw;
+          if (jw > 0) ptx::mbar_wait(&bars[WFREE], (jw - 1) & 1);
+          const uint32_t wb = (uint32_t)Np * Kp;
+          ptx::mbar_arrive_expect_tx(&bars[WFULL], wb);
+          ptx::bulk_g2s(w_s, p.wfold + (size_t)c * wb, wb, &bars[WFULL]);
+          prev_core = c;
         }
-        if (p.raster) {
-          const uint32_t m = __ballot_sync(0xFFFFFFFFu, fire && valid);
-          if (lane == 0 && real && (n >> 5) < p.Wn)
-            p.raster[(((size_t)(p.t - p.raster_t0) * p.S + s0 + s) * p.G + c) * p.Wn + (n >> 5)] = m;
-        }
+        uint8_t* st = smem + L.stage + s * L.stage_bytes;
+        const int s0 = tile * NT;
+        const bool inject = p.t < p.T_in && p.nruns[c] > 0;
+        const uint32_t ring_bytes = (uint32_t)NT * W * 4, line_bytes = inject ? (uint32_t)NT * WIp * 4 : 0u;
+        ptx::mbar_arrive_expect_tx(&bars[FULL0 + s], (p.fresh ? 0u : pot_bytes) + ring_bytes + line_bytes);
+        if (!p.fresh) ptx::bulk_g2s(st + L.pot, pot_tile(p, c, tile, nT), pot_bytes, &bars[FULL0 + s]);
+        ptx::bulk_g2s(st + L.raw, p.ring + (((size_t)cur * p.G + c) * p.Sr + s0) * W, ring_bytes, &bars[FULL0 + s]);
+        if (inject)
+          ptx::bulk_g2s(st + L.lines, p.lines + ((size_t)p.t * p.Sr + s0) * WIp, line_bytes, &bars[FULL0 + s]);
       }
-      uint4* dst = reinterpret_cast<uint4*>(pot_row) + j * 4;
-      dst[0] = make_uint4(outw[0], outw[1], outw[2], outw[3]);
-      dst[1] = make_uint4(outw[4], outw[5], outw[6], outw[7]);
-      dst[2] = make_uint4(outw[8], outw[9], outw[10], outw[11]);
-      dst[3] = make_uint4(outw[12], outw[13], outw[14], outw[15]);
     }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      const uint32_t id = tc::idesc_i8(128, NT);
+      const uint32_t sbo = (uint32_t)Kp * 8;
+      int prev_core = -1, jw = -1;
+      for (int k = 0; k < nwork; ++k) {
+        const int idx = lo + k, c = idx / nT;
+        const int s = k & 1, u = k >> 1;
+        if (c != prev_core) {
+          ++jw;
+          ptx::mbar_wait(&bars[WFULL], jw & 1);
+          prev_core = c;
+        }
+        ptx::mbar_wait(&bars[BFULL0 + s], u & 1);
+        ptx::mbar_wait(&bars[ACCEMPTY0 + s], (u & 1) ^ 1);
+        tc::fence_after();
+        const uint8_t* b_s = smem + L.stage + s * L.stage_bytes + L.b;
+        const uint32_t acc = tmem + s * acc_stride;
+        for (int hh = 0; hh < Mh; ++hh)
+          for (int kk = 0; kk < Kp / 32; ++kk) {
+            const uint64_t ad = tc::smem_desc(ptx::smem_u32(w_s + hh * 128 * Kp + kk * 256), 128, sbo);
+            const uint64_t bd = tc::smem_desc(ptx::smem_u32(b_s + kk * 256), 128, sbo);
+            tc::mma_i8(acc + hh * NT, ad, bd, id, kk > 0 ? 1u : 0u);
+          }
+        tc::commit(&bars[BEMPTY0 + s]);
+        tc::commit(&bars[ACCFULL0 + s]);
+        const int next_core = (k + 1 < nwork) ? (lo + k + 1) / nT : -1;
+        if (next_core != c) tc::commit(&bars[WFREE]);
+      }
+    }
+    __syncwarp();
+  } else if (warp < 2 + kExpWarps) {
+    // ------------------------------------------------------------ spike stage
+    const int et = threadIdx.x - 64;
+    const int cur = (int)(p.t & p.rp_mask);
+    const int K16 = Kp >> 4;
+    for (int k = 0; k < nwork; ++k) {
+      const int idx = lo + k, c = idx / nT, tile = idx - c * nT;
+      const int s = k & 1, u = k >> 1;
+      const int s0 = tile * NT, ns = min(NT, p.S - s0);
+      uint8_t* st = smem + L.stage + s * L.stage_bytes;
+      uint32_t* raw = reinterpret_cast<uint32_t*>(st + L.raw);
+      uint32_t* lines = reinterpret_cast<uint32_t*>(st + L.lines);
+      // a1: the scheduler rows due now were staged by the producer (TMA);
+      // clear them in global memory (free again for spikes due at t + Rp)
+      ptx::mbar_wait(&bars[FULL0 + s], u & 1);
+      uint32_t* row = p.ring + (((size_t)cur * p.G + c) * p.Sr + s0) * W;
+      for (int i = et; i < ns * W; i += kExpThreads) row[i] = 0u;
+      const bool inject = p.t < p.T_in && p.nruns[c] > 0;
+      named_sync(2, kExpThreads);
+      // a2: external inputs, one contiguous run of lines -> axons per item
+      if (inject) {
+        const int nr = p.nruns[c];
+        const int2* runs = p.runs + (size_t)c * p.rmax;
+        for (int i = et; i < ns * nr; i += kExpThreads) {
+          const int sm = i / nr, r = i - sm * nr;
+          const int2 rn = runs[r];
+          const int ap = rn.x & 0xFFFF, len = rn.x >> 16, ln = rn.y;
+          const uint32_t* lr = lines + sm * WIp;
+          const int lw = ln >> 5, lb = ln & 31;
+          uint32_t x = lr[lw] >> lb;
+          if (lb + len > 32) x |= lr[lw + 1] << (32 - lb);
+          if (len < 32) x &= (1u << len) - 1u;
+          if (x) {
+            const int aw = ap >> 5, ab = ap & 31;
+            atomicOr(&raw[sm * W + aw], x << ab);
+            if (ab + len > 32) atomicOr(&raw[sm * W + aw + 1], x >> (32 - ab));
+          }
+        }
+        named_sync(2, kExpThreads);
+      }
+      // bits -> 0/1 bytes, canonical K-major operand (rows = samples)
+      ptx::mbar_wait(&bars[BEMPTY0 + s], (u & 1) ^ 1);
+      uint8_t* b_s = st + L.b;
+      for (int i = et; i < NT * K16; i += kExpThreads) {
+        const int sm = i / K16, k16 = i - sm * K16;
+        const uint32_t wv = raw[sm * W + (k16 >> 1)];
+        const uint32_t bits = (k16 & 1) ? (wv >> 16) : (wv & 0xFFFFu);
+        uint4 v;
+        v.x = tc::nib2bytes(bits & 15u);
+        v.y = tc::nib2bytes((bits >> 4) & 15u);
+        v.z = tc::nib2bytes((bits >> 8) & 15u);
+        v.w = tc::nib2bytes((bits >> 12) & 15u);
+        *reinterpret_cast<uint4*>(b_s + tc::operand_offset(sm, k16 * 16, Kp)) = v;
+      }
+      ptx::fence_proxy_async_smem();
+      ptx::mbar_arrive(&bars[BFULL0 + s]);
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const int ew = warp - (2 + kExpWarps);
+    const int h = ew >> 2, q = warp & 3;   // TMEM lane quarter = warp % 4
+    const int n = h * 128 + q * 32 + lane;
+    const bool active = h < Mh;
+    const bool valid = active && n < p.N;
+    int prev_core = -1;
+    int leak = 0, pth = 0, nth = 0, rst = 0, init = 0, bf = 0, bn = 0, linmask = 0;
+    uint32_t kind = RK_NONE, cls = 0, axbit = 0;
+    size_t ring_off = 0;
+    for (int k = 0; k < nwork; ++k) {
+      const int idx = lo + k, c = idx / nT, tile = idx - c * nT;
+      const int s = k & 1, u = k >> 1;
+      const int s0 = tile * NT, ns = min(NT, p.S - s0);
+      uint8_t* st = smem + L.stage + s * L.stage_bytes;
+      ptx::mbar_wait(&bars[ACCFULL0 + s], u & 1);
+      ptx::mbar_wait(&bars[FULL0 + s], u & 1);
+      tc::fence_after();
+      if (active) {
+        if (c != prev_core) {
+          const short4 prm = p.prm[(size_t)c * Np + n];
+          const uint2 rt = p.route[(size_t)c * Np + n];
+          leak = prm.x; pth = prm.y; nth = prm.z; rst = prm.w;
+          init = p.init[(size_t)c * Np + n];
+          kind = valid ? route_kind(rt.x) : RK_NONE;
+          const bool lin = route_lin(rt.x);
+          // nv = fire ? (v & linmask) + bf : neg ? (v & linmask) + bn : v
+          linmask = lin ? -1 : 0;
+          bf = lin ? -pth : rst;
+          bn = lin ? -nth : -rst;
+          cls = rt.y;
+          const uint32_t ax = route_axon(rt.x);
+          axbit = 1u << (ax & 31);
+          const int slot = (int)((p.t + route_delay(rt.x)) & p.rp_mask);
+          ring_off = (((size_t)slot * p.G + rt.y) * p.Sr) * W + (ax >> 5);
+          prev_core = c;
+        }
+        uint8_t* prow = st + L.pot + (size_t)n * NT * 2;
+        const uint32_t acc_addr = tmem + s * acc_stride + ((uint32_t)(q * 32) << 16) + h * NT;
+#pragma unroll
+        for (int j = 0; j < NT / 32; ++j) {
+          uint32_t acc[32];
+          tc::ld32(acc_addr + j * 32, acc);
+          uint4 pv[4];
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc)
+            pv[cc] = *reinterpret_cast<const uint4*>(prow + (((j * 4 + cc) ^ (n & 7)) << 4));
+          tc::wait_ld();
+          uint32_t fired = 0u;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const uint4& v4 = pv[i >> 3];
+            const uint32_t word = ((i >> 1) & 3) == 0 ? v4.x : ((i >> 1) & 3) == 1 ? v4.y : ((i >> 1) & 3) == 2 ? v4.z : v4.w;
+            const int pot = p.fresh ? init : (int)(int16_t)((i & 1) ? (word >> 16) : (word & 0xFFFFu));
+            const int v = pot + (int)acc[i] + leak;
+            const bool fire = v >= pth;
+            const bool neg = v < nth;
+            const int r = (v & linmask) + (fire ? bf : bn);
+            int nv = (fire || neg) ? r : v;
+            nv = min(max(nv, p.pot_lo), p.pot_hi);
+            acc[i] = (uint32_t)nv & 0xFFFFu;
+            fired |= (fire ? 1u : 0u) << i;
+          }
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc) {
+            const uint4 o = make_uint4(acc[8 * cc + 0] | (acc[8 * cc + 1] << 16), acc[8 * cc + 2] | (acc[8 * cc + 3] << 16),
+                                       acc[8 * cc + 4] | (acc[8 * cc + 5] << 16), acc[8 * cc + 6] | (acc[8 * cc + 7] << 16));
+            *reinterpret_cast<uint4*>(prow + (((j * 4 + cc) ^ (n & 7)) << 4)) = o;
+          }
+          // a5 / a6: route or count the spikes of real samples
+          const int lim = ns - j * 32;
+          uint32_t f = lim >= 32 ? fired : (lim > 0 ? fired & ((1u << lim) - 1u) : 0u);
+          if (kind == RK_ROUTE) {
+            while (f) {
+              const int i = __ffs(f) - 1;
+              f &= f - 1;
+              atomicOr(p.ring + ring_off + (size_t)(s0 + j * 32 + i) * W, axbit);
+            }
+          } else if (kind == RK_OUTPUT) {
+            while (f) {
+              const int i = __ffs(f) - 1;
+              f &= f - 1;
+              atomicAdd(p.counts + (size_t)(s0 + j * 32 + i) * p.C + cls, 1);
+            }
+          }
+          if (p.raster) {
+            const uint32_t fv = valid ? fired : 0u;
+            for (int i = 0; i < 32 && i < lim; ++i) {
+              const uint32_t m = __ballot_sync(0xFFFFFFFFu, (fv >> i) & 1u);
+              if (lane == 0 && (n >> 5) < p.Wn)
+                p.raster[(((size_t)(p.t - p.raster_t0) * p.S + s0 + j * 32 + i) * p.G + c) * p.Wn + (n >> 5)] = m;
+            }
+          }
+        }
+      }
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&bars[ACCEMPTY0 + s]);
+      ptx::fence_proxy_async_smem();
+      named_sync(1, kEpiThreads);
+      if (ew == 0 && lane == 0) {
+        ptx::bulk_s2g(pot_tile(p, c, tile, nT), st + L.pot, pot_bytes);
+        ptx::bulk_commit();
+        ptx::bulk_wait_read0();
+        ptx::mbar_arrive(&bars[SEMPTY0 + s]);
+      }
+    }
+    if (ew == 0 && lane == 0) ptx::bulk_wait0();
   }
   tc::fence_before();
   __syncthreads();
-  if (warp == 0) tc::dealloc(tmem, 2 * NT >= 32 ? 2 * NT : 32);
+  if (warp == 1) tc::dealloc(tmem, tcols < 32 ? 32 : tcols);
 }
 
 }  // namespace
 
-int tc_tile() { return 64; }
+int tc_tile() { return NT; }
 
-size_t tc_smem_bytes(const Compiled& n, int NT) { return tc_layout(n.Npad, n.Kp, NT, n.W, n.WI).total; }
+size_t tc_smem_bytes(const Compiled& n) { return tc_layout(n.Npad, n.Kp, n.W, n.WIp).total; }
 
 cudaError_t launch_ticks_tc(ranc_ctx* ctx, TickParams p, int64_t num_ticks) {
   const Compiled& n = ctx->net;
-  constexpr int NT = 64;
   p.ST = NT;
-  const dim3 grid(n.G, (unsigned)((ctx->S + NT - 1) / NT));
-  const size_t smem = tc_smem_bytes(n, NT);
+  p.route = (const uint2*)ctx->d_route_tc.p;
+  p.runs = (const int2*)ctx->d_runs.p;
+  p.nruns = (const int32_t*)ctx->d_nruns.p;
+  p.rmax = n.rmax;
+  const int64_t total = (int64_t)n.G * ((ctx->S + NT - 1) / NT);
+  const int grid = (int)std::min<int64_t>(total, ctx->num_sms);
+  const size_t smem = tc_layout(n.Npad, n.Kp, n.W, n.WIp).total;
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(tick_tc_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(tick_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     configured = true;
   }
   for (int64_t i = 0; i < num_ticks; ++i) {
     p.t = ctx->now + i;
     p.fresh = ctx->fresh ? 1 : 0;
-    tick_tc_kernel<NT><<<grid, kThreadsTC, smem, ctx->stream>>>(p);
+    tick_tc_kernel<<<grid, kThreadsTC, smem, ctx->stream>>>(p);
     ctx->launches++;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
