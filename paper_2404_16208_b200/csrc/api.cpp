@@ -312,7 +312,7 @@ ranc_status ranc_read_potentials(ranc_ctx* ctx, int32_t* pot, size_t n) {
       for (int j = 0; j < c.N; ++j)
         pot[((size_t)s * c.G + g) * c.N + j] =
             ctx->kernel_active == RANC_KERNEL_TC
-                ? h[(((size_t)g * nT + s / NT) * c.Npad + j) * NT + ((((s % NT) >> 3) ^ (j & 7)) << 3) + (s & 7)]
+                ? h[(((size_t)g * nT + s / NT) * c.Npad + j) * NT + s % NT]
                 : h[((size_t)g * ctx->S + s) * c.Npad + j];
   return RANC_OK;
 }

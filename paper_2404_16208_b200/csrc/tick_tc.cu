@@ -15,18 +15,19 @@
 // with two stages so that tile i+1 is loaded, expanded and multiplied while
 // the epilogue of tile i runs:
 //   warp 0      producer: TMA bulk loads of Wfold (on a core change) and of the
-//               tile's potentials (HBM -> shared)
-//   warp 1      MMA issuer (one elected thread) + TMEM allocation
-//   warps 2-3   spike stage: scheduler rows due now (a1, read + clear), input
-//               runs (a2), bits -> 0/1 bytes in the operand layout
-//   warps 4-11  epilogue, thread = neuron = TMEM lane: leak / thresholds /
-//               reset (a4), potentials back to shared and out with one TMA
-//               bulk store per tile, routing and output bus (a5, a6)
+//               tile's scheduler rows and input-line rows (4-stage ring)
+//   warp 1      MMA issuer (one elected thread) + TMEM allocation (up to 4
+//               accumulator stages)
+//   warps 2-5   spike stage: clear the rows read (a1), input runs (a2), bits
+//               -> 0/1 bytes in the operand layout
+//   warps 6-13  epilogue, thread = neuron = TMEM lane: potentials streamed
+//               HBM <-> registers (next tile prefetched while this one
+//               runs), leak / thresholds / reset (a4), routing and output bus
+//               (a5, a6)
 // A tick is one launch; the kernel boundary is the tick barrier (a7).
 //
-// Potential layout: tile-blocked [G][nT][Np][64] int16, the eight 16-byte
-// chunks of a row XOR-swizzled with (n & 7) so that the epilogue's 16-byte
-// shared loads are bank-conflict free.
+// Potential layout: tile-blocked [G][nT][Np][64] int16: a thread's 64 samples
+// of one neuron are 128 contiguous bytes.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -41,17 +42,18 @@ namespace ranc {
 namespace {
 
 constexpr int NT = 64;                 // samples per tile (MMA N)
-constexpr int kExpWarps = 2;
+constexpr int NS = 4;                  // spike-stage pipeline depth
+constexpr int kExpWarps = 4;
 constexpr int kEpiWarps = 8;
-constexpr int kThreadsTC = 32 * (2 + kExpWarps + kEpiWarps);  // 384
+constexpr int kFirstExp = 2, kFirstEpi = 2 + kExpWarps;
+constexpr int kThreadsTC = 32 * (2 + kExpWarps + kEpiWarps);  // 448
 constexpr int kExpThreads = 32 * kExpWarps;
-constexpr int kEpiThreads = 32 * kEpiWarps;
 
-enum Bar { FULL0 = 0, BFULL0 = 2, BEMPTY0 = 4, ACCFULL0 = 6, ACCEMPTY0 = 8, SEMPTY0 = 10, WFULL = 12, WFREE = 13,
-           NBARS = 14 };
+enum Bar { FULL0 = 0, SEMPTY0 = 4, BFULL0 = 8, BEMPTY0 = 12, ACCFULL0 = 16, ACCEMPTY0 = 20, WFULL = 24, WFREE = 25,
+           NBARS = 26 };
 
 struct TcLayout {
-  uint32_t w, stage, pot, b, raw, lines, stage_bytes, total;
+  uint32_t w, stage, b, raw, lines, stage_bytes, total;
 };
 
 // WIp: input-line row words (multiple of 4)
@@ -61,15 +63,13 @@ __host__ __device__ inline TcLayout tc_layout(int Np, int Kp, int W, int WIp) {
   uint32_t o = L.w + (uint32_t)Np * Kp;
   L.stage = (o + 1023) & ~1023u;
   uint32_t q = 0;
-  L.pot = q;   q += (uint32_t)Np * NT * 2;
-  q = (q + 127) & ~127u;
-  L.b = q;     q += (uint32_t)NT * Kp;
+  L.b = q;     q += (uint32_t)NT * Kp;       // spikes as 0/1 bytes, canonical layout
   q = (q + 15) & ~15u;
-  L.raw = q;   q += (uint32_t)NT * W * 4;
+  L.raw = q;   q += (uint32_t)NT * W * 4;    // scheduler rows due now (TMA)
   q = (q + 15) & ~15u;
-  L.lines = q; q += (uint32_t)NT * WIp * 4;
+  L.lines = q; q += (uint32_t)NT * WIp * 4;  // input line rows of this tick (TMA)
   L.stage_bytes = (q + 1023) & ~1023u;
-  L.total = L.stage + 2 * L.stage_bytes;
+  L.total = L.stage + NS * L.stage_bytes;
   return L;
 }
 
@@ -77,8 +77,8 @@ __device__ __forceinline__ void named_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
-__device__ __forceinline__ int16_t* pot_tile(const TickParams& p, int c, int tile, int nT) {
-  return p.pot + ((size_t)c * nT + tile) * (size_t)p.Npad * NT;
+__device__ __forceinline__ const uint4* pot_row(const TickParams& p, int c, int tile, int nT, int n) {
+  return reinterpret_cast<const uint4*>(p.pot + (((size_t)c * nT + tile) * (size_t)p.Npad + n) * NT);
 }
 
 __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams p) {
@@ -95,19 +95,22 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
   const int hi = (int)((int64_t)(blockIdx.x + 1) * total / gridDim.x);
   const int nwork = hi - lo;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t tcols = 2u * Mh * NT;  // two accumulator stages
-  const uint32_t acc_stride = (uint32_t)Mh * NT;
-  const uint32_t pot_bytes = (uint32_t)Np * NT * 2;
+  const uint32_t acc_stride = (uint32_t)Mh * NT;          // TMEM columns per accumulator stage
+  const int NA = (int)(512u / acc_stride) >= 4 ? 4 : (int)(512u / acc_stride);  // accumulator stages
+  const uint32_t tcols = acc_stride * NA;
+  const int cur = (int)(p.t & p.rp_mask);
 
   if (warp == 1) tc::alloc(tmem_holder, tcols < 32 ? 32 : tcols);
   if (threadIdx.x == 0) {
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < NS; ++i) {
       ptx::mbar_init(&bars[FULL0 + i], 1);
-      ptx::mbar_init(&bars[BFULL0 + i], kExpThreads);
+      ptx::mbar_init(&bars[SEMPTY0 + i], 1);
+      ptx::mbar_init(&bars[BFULL0 + i], 1);
       ptx::mbar_init(&bars[BEMPTY0 + i], 1);
+    }
+    for (int i = 0; i < 4; ++i) {
       ptx::mbar_init(&bars[ACCFULL0 + i], 1);
       ptx::mbar_init(&bars[ACCEMPTY0 + i], kEpiWarps);
-      ptx::mbar_init(&bars[SEMPTY0 + i], 1);
     }
     ptx::mbar_init(&bars[WFULL], 1);
     ptx::mbar_init(&bars[WFREE], 1);
@@ -119,14 +122,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
   const uint32_t tmem = *tmem_holder;
 
   if (warp == 0) {
-    // ------------------------------------------------------------ producer
+    // ------------------------------------------------------------ producer (TMA)
     if (lane == 0) {
-      const int cur = (int)(p.t & p.rp_mask);
       int prev_core = -1, jw = -1;
       for (int k = 0; k < nwork; ++k) {
         const int idx = lo + k, c = idx / nT, tile = idx - c * nT;
-        const int s = k & 1, u = k >> 1;
-        ptx::mbar_wait(&bars[SEMPTY0 + s], (u & 1) ^ 1);
+        const int s = k % NS, u = k / NS;
         if (c != prev_core) {
           ++jw;
           if (jw > 0) ptx::mbar_wait(&bars[WFREE], (jw - 1) & 1);
@@ -135,12 +136,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
           ptx::bulk_g2s(w_s, p.wfold + (size_t)c * wb, wb, &bars[WFULL]);
           prev_core = c;
         }
+        ptx::mbar_wait(&bars[SEMPTY0 + s], (u & 1) ^ 1);
         uint8_t* st = smem + L.stage + s * L.stage_bytes;
         const int s0 = tile * NT;
         const bool inject = p.t < p.T_in && p.nruns[c] > 0;
         const uint32_t ring_bytes = (uint32_t)NT * W * 4, line_bytes = inject ? (uint32_t)NT * WIp * 4 : 0u;
-        ptx::mbar_arrive_expect_tx(&bars[FULL0 + s], (p.fresh ? 0u : pot_bytes) + ring_bytes + line_bytes);
-        if (!p.fresh) ptx::bulk_g2s(st + L.pot, pot_tile(p, c, tile, nT), pot_bytes, &bars[FULL0 + s]);
+        ptx::mbar_arrive_expect_tx(&bars[FULL0 + s], ring_bytes + line_bytes);
         ptx::bulk_g2s(st + L.raw, p.ring + (((size_t)cur * p.G + c) * p.Sr + s0) * W, ring_bytes, &bars[FULL0 + s]);
         if (inject)
           ptx::bulk_g2s(st + L.lines, p.lines + ((size_t)p.t * p.Sr + s0) * WIp, line_bytes, &bars[FULL0 + s]);
@@ -154,17 +155,18 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       int prev_core = -1, jw = -1;
       for (int k = 0; k < nwork; ++k) {
         const int idx = lo + k, c = idx / nT;
-        const int s = k & 1, u = k >> 1;
+        const int s = k % NS, u = k / NS;
+        const int a = k % NA, ua = k / NA;
         if (c != prev_core) {
           ++jw;
           ptx::mbar_wait(&bars[WFULL], jw & 1);
           prev_core = c;
         }
         ptx::mbar_wait(&bars[BFULL0 + s], u & 1);
-        ptx::mbar_wait(&bars[ACCEMPTY0 + s], (u & 1) ^ 1);
+        ptx::mbar_wait(&bars[ACCEMPTY0 + a], (ua & 1) ^ 1);
         tc::fence_after();
         const uint8_t* b_s = smem + L.stage + s * L.stage_bytes + L.b;
-        const uint32_t acc = tmem + s * acc_stride;
+        const uint32_t acc = tmem + a * acc_stride;
         for (int hh = 0; hh < Mh; ++hh)
           for (int kk = 0; kk < Kp / 32; ++kk) {
             const uint64_t ad = tc::smem_desc(ptx::smem_u32(w_s + hh * 128 * Kp + kk * 256), 128, sbo);
@@ -172,33 +174,31 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
             tc::mma_i8(acc + hh * NT, ad, bd, id, kk > 0 ? 1u : 0u);
           }
         tc::commit(&bars[BEMPTY0 + s]);
-        tc::commit(&bars[ACCFULL0 + s]);
+        tc::commit(&bars[ACCFULL0 + a]);
         const int next_core = (k + 1 < nwork) ? (lo + k + 1) / nT : -1;
         if (next_core != c) tc::commit(&bars[WFREE]);
       }
     }
     __syncwarp();
-  } else if (warp < 2 + kExpWarps) {
+  } else if (warp < kFirstEpi) {
     // ------------------------------------------------------------ spike stage
-    const int et = threadIdx.x - 64;
-    const int cur = (int)(p.t & p.rp_mask);
+    const int et = threadIdx.x - 32 * kFirstExp;
     const int K16 = Kp >> 4;
+    const bool fast = (kExpThreads % K16) == 0;
     for (int k = 0; k < nwork; ++k) {
       const int idx = lo + k, c = idx / nT, tile = idx - c * nT;
-      const int s = k & 1, u = k >> 1;
+      const int s = k % NS, u = k / NS;
       const int s0 = tile * NT, ns = min(NT, p.S - s0);
       uint8_t* st = smem + L.stage + s * L.stage_bytes;
       uint32_t* raw = reinterpret_cast<uint32_t*>(st + L.raw);
-      uint32_t* lines = reinterpret_cast<uint32_t*>(st + L.lines);
+      const uint32_t* lines = reinterpret_cast<const uint32_t*>(st + L.lines);
       // a1: the scheduler rows due now were staged by the producer (TMA);
       // clear them in global memory (free again for spikes due at t + Rp)
       ptx::mbar_wait(&bars[FULL0 + s], u & 1);
       uint32_t* row = p.ring + (((size_t)cur * p.G + c) * p.Sr + s0) * W;
       for (int i = et; i < ns * W; i += kExpThreads) row[i] = 0u;
-      const bool inject = p.t < p.T_in && p.nruns[c] > 0;
-      named_sync(2, kExpThreads);
       // a2: external inputs, one contiguous run of lines -> axons per item
-      if (inject) {
+      if (p.t < p.T_in && p.nruns[c] > 0) {
         const int nr = p.nruns[c];
         const int2* runs = p.runs + (size_t)c * p.rmax;
         for (int i = et; i < ns * nr; i += kExpThreads) {
@@ -216,28 +216,41 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
             if (ab + len > 32) atomicOr(&raw[sm * W + aw + 1], x >> (32 - ab));
           }
         }
-        named_sync(2, kExpThreads);
       }
-      // bits -> 0/1 bytes, canonical K-major operand (rows = samples)
+      named_sync(2, kExpThreads);
+      // bits -> 0/1 bytes, canonical K-major operand (rows = samples);
+      // samples >= ns of a tail tile get no spikes
       ptx::mbar_wait(&bars[BEMPTY0 + s], (u & 1) ^ 1);
       uint8_t* b_s = st + L.b;
-      for (int i = et; i < NT * K16; i += kExpThreads) {
-        const int sm = i / K16, k16 = i - sm * K16;
-        const uint32_t wv = raw[sm * W + (k16 >> 1)];
-        const uint32_t bits = (k16 & 1) ? (wv >> 16) : (wv & 0xFFFFu);
+      auto expand = [&](int sm, int k16) {
+        uint32_t bits = 0u;
+        if (sm < ns) {
+          const uint32_t wv = raw[sm * W + (k16 >> 1)];
+          bits = (k16 & 1) ? (wv >> 16) : (wv & 0xFFFFu);
+        }
         uint4 v;
         v.x = tc::nib2bytes(bits & 15u);
         v.y = tc::nib2bytes((bits >> 4) & 15u);
         v.z = tc::nib2bytes((bits >> 8) & 15u);
         v.w = tc::nib2bytes((bits >> 12) & 15u);
         *reinterpret_cast<uint4*>(b_s + tc::operand_offset(sm, k16 * 16, Kp)) = v;
+      };
+      if (fast) {
+        const int k16 = et % K16, step = kExpThreads / K16;
+        for (int sm = et / K16; sm < NT; sm += step) expand(sm, k16);
+      } else {
+        for (int i = et; i < NT * K16; i += kExpThreads) expand(i / K16, i % K16);
       }
       ptx::fence_proxy_async_smem();
-      ptx::mbar_arrive(&bars[BFULL0 + s]);
+      named_sync(2, kExpThreads);
+      if (et == 0) {
+        ptx::mbar_arrive(&bars[BFULL0 + s]);
+        ptx::mbar_arrive(&bars[SEMPTY0 + s]);   // raw/lines of this stage are consumed
+      }
     }
   } else {
     // ------------------------------------------------------------ epilogue
-    const int ew = warp - (2 + kExpWarps);
+    const int ew = warp - kFirstEpi;
     const int h = ew >> 2, q = warp & 3;   // TMEM lane quarter = warp % 4
     const int n = h * 128 + q * 32 + lane;
     const bool active = h < Mh;
@@ -246,13 +259,23 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
     int leak = 0, pth = 0, nth = 0, rst = 0, init = 0, bf = 0, bn = 0, linmask = 0;
     uint32_t kind = RK_NONE, cls = 0, axbit = 0;
     size_t ring_off = 0;
+    uint4 pnext[NT / 8];
+    const bool load = active && !p.fresh;
+    if (load && nwork > 0) {
+      const int c0 = lo / nT;
+      const uint4* src = pot_row(p, c0, lo - c0 * nT, nT, n);
+#pragma unroll
+      for (int i = 0; i < NT / 8; ++i) pnext[i] = src[i];
+    }
     for (int k = 0; k < nwork; ++k) {
       const int idx = lo + k, c = idx / nT, tile = idx - c * nT;
-      const int s = k & 1, u = k >> 1;
+      const int a = k % NA, ua = k / NA;
       const int s0 = tile * NT, ns = min(NT, p.S - s0);
-      uint8_t* st = smem + L.stage + s * L.stage_bytes;
-      ptx::mbar_wait(&bars[ACCFULL0 + s], u & 1);
-      ptx::mbar_wait(&bars[FULL0 + s], u & 1);
+      // pnext holds this tile's potentials (prefetched during the previous
+      // tile); each chunk is refilled with the next tile's as soon as it is used
+      const bool pf = load && k + 1 < nwork;
+      const uint4* nsrc = pot_row(p, (idx + 1) / nT, (idx + 1) % nT, nT, n);
+      ptx::mbar_wait(&bars[ACCFULL0 + a], ua & 1);
       tc::fence_after();
       if (active) {
         if (c != prev_core) {
@@ -273,23 +296,19 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
           ring_off = (((size_t)slot * p.G + rt.y) * p.Sr) * W + (ax >> 5);
           prev_core = c;
         }
-        uint8_t* prow = st + L.pot + (size_t)n * NT * 2;
-        const uint32_t acc_addr = tmem + s * acc_stride + ((uint32_t)(q * 32) << 16) + h * NT;
+        uint4* dst = const_cast<uint4*>(pot_row(p, c, tile, nT, n));
+        const uint32_t acc_addr = tmem + a * acc_stride + ((uint32_t)(q * 32) << 16) + h * NT;
 #pragma unroll
         for (int j = 0; j < NT / 32; ++j) {
           uint32_t acc[32];
           tc::ld32(acc_addr + j * 32, acc);
-          uint4 pv[4];
-#pragma unroll
-          for (int cc = 0; cc < 4; ++cc)
-            pv[cc] = *reinterpret_cast<const uint4*>(prow + (((j * 4 + cc) ^ (n & 7)) << 4));
           tc::wait_ld();
           uint32_t fired = 0u;
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
-            const uint4& v4 = pv[i >> 3];
-            const uint32_t word = ((i >> 1) & 3) == 0 ? v4.x : ((i >> 1) & 3) == 1 ? v4.y : ((i >> 1) & 3) == 2 ? v4.z : v4.w;
-            const int pot = p.fresh ? init : (int)(int16_t)((i & 1) ? (word >> 16) : (word & 0xFFFFu));
+            const uint4 v4 = pnext[j * 4 + (i >> 3)];
+            const uint32_t w32 = ((i >> 1) & 3) == 0 ? v4.x : ((i >> 1) & 3) == 1 ? v4.y : ((i >> 1) & 3) == 2 ? v4.z : v4.w;
+            const int pot = p.fresh ? init : (int)(int16_t)((i & 1) ? (w32 >> 16) : (w32 & 0xFFFFu));
             const int v = pot + (int)acc[i] + leak;
             const bool fire = v >= pth;
             const bool neg = v < nth;
@@ -299,12 +318,14 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
             acc[i] = (uint32_t)nv & 0xFFFFu;
             fired |= (fire ? 1u : 0u) << i;
           }
+          if (pf) {
 #pragma unroll
-          for (int cc = 0; cc < 4; ++cc) {
-            const uint4 o = make_uint4(acc[8 * cc + 0] | (acc[8 * cc + 1] << 16), acc[8 * cc + 2] | (acc[8 * cc + 3] << 16),
-                                       acc[8 * cc + 4] | (acc[8 * cc + 5] << 16), acc[8 * cc + 6] | (acc[8 * cc + 7] << 16));
-            *reinterpret_cast<uint4*>(prow + (((j * 4 + cc) ^ (n & 7)) << 4)) = o;
+            for (int cc = 0; cc < 4; ++cc) pnext[j * 4 + cc] = nsrc[j * 4 + cc];
           }
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc)
+            dst[j * 4 + cc] = make_uint4(acc[8 * cc + 0] | (acc[8 * cc + 1] << 16), acc[8 * cc + 2] | (acc[8 * cc + 3] << 16),
+                                         acc[8 * cc + 4] | (acc[8 * cc + 5] << 16), acc[8 * cc + 6] | (acc[8 * cc + 7] << 16));
           // a5 / a6: route or count the spikes of real samples
           const int lim = ns - j * 32;
           uint32_t f = lim >= 32 ? fired : (lim > 0 ? fired & ((1u << lim) - 1u) : 0u);
@@ -333,17 +354,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       }
       tc::fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&bars[ACCEMPTY0 + s]);
-      ptx::fence_proxy_async_smem();
-      named_sync(1, kEpiThreads);
-      if (ew == 0 && lane == 0) {
-        ptx::bulk_s2g(pot_tile(p, c, tile, nT), st + L.pot, pot_bytes);
-        ptx::bulk_commit();
-        ptx::bulk_wait_read0();
-        ptx::mbar_arrive(&bars[SEMPTY0 + s]);
-      }
+      if (lane == 0) ptx::mbar_arrive(&bars[ACCEMPTY0 + a]);
     }
-    if (ew == 0 && lane == 0) ptx::bulk_wait0();
   }
   tc::fence_before();
   __syncthreads();
