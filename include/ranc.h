@@ -184,23 +184,49 @@ typedef struct {
   int64_t num_samples;        /* S_local                                                */
   int64_t device_bytes;       /* device memory held by the context                      */
   int64_t kernel_launches;    /* kernels launched by the library since load             */
-  int32_t kernel;             /* kernel variant in use                                  */
-  int32_t reserved[7];
+  int32_t kernel;             /* kernel variant in use: 1 popcount, 2 tensor core       */
+  int32_t core_lo;            /* first global core simulated by this context            */
+  int32_t cores_local;        /* number of cores simulated by this context              */
+  int32_t shard_mode;         /* RANC_SHARD_* (0 without a communicator)                */
+  int64_t exchange_bytes;     /* core-sharded: bytes sent per tick                      */
+  int32_t reserved[2];
 } ranc_info;
 ranc_status ranc_get_info(const ranc_ctx* ctx, ranc_info* info);
 
-/* Multi-GPU (one process per GPU).  ranc_comm_init joins an NCCL
- * communicator from a 128-byte ncclUniqueId (distributed by the caller, e.g.
- * over torch.distributed), `world` ranks, this `rank`.  mode: 0 = sample
- * sharded (each rank simulates its own samples of a replicated network).
- * ranc_gather_outputs: every rank calls it; `root` receives the class counts
- * of all ranks concatenated in rank order ([sum S_local][C] int32, n must be
- * that size on root, ignored elsewhere).  Synchronises. */
+/* Multi-GPU (one process per GPU).
+ *
+ * ranc_comm_init joins an NCCL communicator from a 128-byte ncclUniqueId
+ * (distributed by the caller, e.g. over torch.distributed), `world` ranks,
+ * this `rank`.  Modes:
+ *   RANC_SHARD_SAMPLES: every rank simulates its own samples of the
+ *     replicated network (independent simulations, G14); no collective on
+ *     the tick path.
+ *   RANC_SHARD_CORES: every rank simulates the cores of a band of grid rows
+ *     (rows [r*H/world, (r+1)*H/world)) for ALL samples.  After every tick the
+ *     fired bits of cores whose routes cross a band boundary are exchanged
+ *     with grouped ncclSend/ncclRecv and applied to the receivers' scheduler
+ *     rows (Alg. 1 l.15-20).  Must be called before
+ *     ranc_load_inputs.  The readers (potentials, pending, outputs, trace)
+ *     then cover the local cores only ([S][G_local]..., local output counts);
+ *     ranc_get_info reports core_lo / cores_local.
+ * ranc_gather_outputs: every rank calls it.  Sample mode: `root` receives the
+ * class counts of all ranks concatenated in rank order ([sum S_local][C]).
+ * Core mode: `root` receives the element-wise sum ([S][C]).  n is checked on
+ * root only.  Synchronises.  Errors: RANC_E_NCCL, RANC_E_STATE, RANC_E_SIZE. */
 #define RANC_SHARD_SAMPLES 0
+#define RANC_SHARD_CORES 1
 ranc_status ranc_comm_init(ranc_ctx* ctx, const void* nccl_unique_id, int world, int rank, int mode);
 ranc_status ranc_gather_outputs(ranc_ctx* ctx, int32_t* counts_global, size_t n, int root);
 /* Fill a 128-byte buffer with a fresh ncclUniqueId (call on one rank). */
 ranc_status ranc_comm_unique_id(void* out128);
+
+/* Loopback group: n contexts of this process (same device, same network)
+ * act as the n ranks of a core-sharded run, exchanging spikes with device
+ * copies instead of NCCL (mode must be RANC_SHARD_CORES).  Such contexts are
+ * advanced together with ranc_run_ticks_loopback (ranc_run_ticks on a member
+ * returns RANC_E_STATE); everything else is per context as above. */
+ranc_status ranc_comm_init_loopback(ranc_ctx* const* ctxs, int n, int mode);
+ranc_status ranc_run_ticks_loopback(ranc_ctx* const* ctxs, int n, int64_t num_ticks);
 
 /* Last error message of ctx, or (ctx == NULL) of the calling thread's last
  * failed ranc_load_network.  Never NULL. */

@@ -20,6 +20,7 @@ OPT_SAMPLE_TILE = 1
 OPT_USE_GRAPH = 2
 OPT_KERNEL = 3
 SHARD_SAMPLES = 0
+SHARD_CORES = 1
 
 
 class RancError(RuntimeError):
@@ -49,7 +50,8 @@ class Info(C.Structure):
         "grid_w", "grid_h", "axons", "neurons", "num_types", "max_delay", "num_classes", "num_lines",
         "ring_rows", "ring_words", "pieces", "sample_tile")] + [
         ("num_samples", C.c_int64), ("device_bytes", C.c_int64), ("kernel_launches", C.c_int64),
-        ("kernel", C.c_int32), ("reserved", C.c_int32 * 7)]
+        ("kernel", C.c_int32), ("core_lo", C.c_int32), ("cores_local", C.c_int32), ("shard_mode", C.c_int32),
+        ("exchange_bytes", C.c_int64), ("reserved", C.c_int32 * 2)]
 
 
 ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p)
@@ -59,7 +61,8 @@ EXPORTS = [
     "ranc_load_network", "ranc_load_inputs", "ranc_reset_state", "ranc_run_ticks", "ranc_now",
     "ranc_read_outputs", "ranc_read_potentials", "ranc_read_pending", "ranc_set_trace", "ranc_read_trace",
     "ranc_set_stream", "ranc_set_allocator", "ranc_set_option", "ranc_get_info", "ranc_comm_init",
-    "ranc_gather_outputs", "ranc_comm_unique_id", "ranc_last_error", "ranc_destroy",
+    "ranc_gather_outputs", "ranc_comm_unique_id", "ranc_comm_init_loopback", "ranc_run_ticks_loopback",
+    "ranc_last_error", "ranc_destroy",
 ]
 
 _lib = None
@@ -93,6 +96,8 @@ def load(path: str = LIB_PATH):
     L.ranc_comm_init.argtypes = [vp, vp, C.c_int, C.c_int, C.c_int]
     L.ranc_gather_outputs.argtypes = [vp, vp, C.c_size_t, C.c_int]
     L.ranc_comm_unique_id.argtypes = [vp]
+    L.ranc_comm_init_loopback.argtypes = [C.POINTER(vp), C.c_int, C.c_int]
+    L.ranc_run_ticks_loopback.argtypes = [C.POINTER(vp), C.c_int, C.c_int64]
     L.ranc_last_error.argtypes = [vp]
     L.ranc_last_error.restype = C.c_char_p
     L.ranc_destroy.argtypes = [vp]

@@ -94,7 +94,8 @@ void free_all(ranc_ctx* ctx) {
   DevBuf* bufs[] = {&ctx->d_xp, &ctx->d_wp, &ctx->d_pword, &ctx->d_prm, &ctx->d_route, &ctx->d_inl,
                     &ctx->d_has_in, &ctx->d_init, &ctx->d_wfold, &ctx->d_route_tc, &ctx->d_runs,
                     &ctx->d_nruns, &ctx->d_pot, &ctx->d_ring, &ctx->d_counts, &ctx->d_lines,
-                    &ctx->d_stage, &ctx->d_raster};
+                    &ctx->d_stage, &ctx->d_raster, &ctx->d_fired, &ctx->d_exports, &ctx->d_send, &ctx->d_recv,
+                    &ctx->d_send_list, &ctx->d_recv_list, &ctx->d_dbg};
   for (DevBuf* b : bufs) dev_free(ctx, b);
 }
 
@@ -139,6 +140,8 @@ ranc_status ranc_load_network(const ranc_network_desc* net, int cuda_device, ran
     return RANC_E_CUDA;
   }
   ctx->stream = ctx->own_stream;
+  ctx->c_lo = 0;
+  ctx->G_loc = ctx->net.G;
   const Compiled& c = ctx->net;
   s = upload(ctx, &ctx->d_xp, c.xp);
   if (!s) s = upload(ctx, &ctx->d_wp, c.wp);
@@ -191,8 +194,8 @@ ranc_status ranc_load_inputs(ranc_ctx* ctx, const ranc_inputs_desc* in) {
   const int64_t Sr = (S + 63) / 64 * 64;   // ring / line sample stride (TMA-aligned tiles)
   if (S != ctx->S || !ctx->d_pot.p) {
     // room for either potential layout: [G][S][Npad] or [G][nT][Npad][NT]
-    TRY(dev_alloc(ctx, &ctx->d_pot, (size_t)c.G * Sr * c.Npad * sizeof(int16_t)));
-    TRY(dev_alloc(ctx, &ctx->d_ring, (size_t)c.Rp * c.G * Sr * c.W * sizeof(uint32_t)));
+    TRY(dev_alloc(ctx, &ctx->d_pot, (size_t)ctx->G_loc * Sr * c.Npad * sizeof(int16_t)));
+    TRY(dev_alloc(ctx, &ctx->d_ring, (size_t)c.Rp * ctx->G_loc * Sr * c.W * sizeof(uint32_t)));
     TRY(dev_alloc(ctx, &ctx->d_counts, (size_t)S * c.C * sizeof(int32_t)));
   }
   const size_t dev_line_words = (size_t)in->num_input_ticks * Sr * c.WIp;
@@ -202,6 +205,7 @@ ranc_status ranc_load_inputs(ranc_ctx* ctx, const ranc_inputs_desc* in) {
   ctx->Sr = Sr;
   ctx->first_sample = in->first_sample;
   ctx->T_in = in->num_input_ticks;
+  TRY(alloc_exchange(ctx));
   if (line_words) {
     // H2D into a staging buffer, then a device transpose to [T_in][S][WI].
     // The host buffer must stay valid until the call returns: from pageable
@@ -232,8 +236,9 @@ ranc_status ranc_reset_state(ranc_ctx* ctx) {
   return RANC_OK;
 }
 
-ranc_status ranc_run_ticks(ranc_ctx* ctx, int64_t num_ticks) {
-  TRY(check_ctx(ctx));
+namespace {
+
+ranc_status prepare_run(ranc_ctx* ctx, int64_t num_ticks) {
   if (num_ticks < 0) {
     ctx->err = "num_ticks < 0";
     return RANC_E_ARG;
@@ -242,11 +247,15 @@ ranc_status ranc_run_ticks(ranc_ctx* ctx, int64_t num_ticks) {
     ctx->err = "ranc_run_ticks before ranc_load_inputs";
     return RANC_E_STATE;
   }
+  if (ctx->group_broken) {
+    ctx->err = "a member of this loopback group was destroyed";
+    return RANC_E_STATE;
+  }
   CK(cudaSetDevice(ctx->device), "cudaSetDevice");
   ctx->sample_tile = ctx->sample_tile_opt > 0 ? ctx->sample_tile_opt : choose_sample_tile(ctx->net, ctx->S);
   if (ctx->sample_tile > ctx->S) ctx->sample_tile = (int)ctx->S;
   if (ctx->trace_flags) {
-    const size_t bytes = (size_t)num_ticks * ctx->S * ctx->net.G * ctx->net.Wn * 4;
+    const size_t bytes = (size_t)num_ticks * ctx->S * ctx->G_loc * ctx->net.Wn * 4;
     if (ctx->d_raster.bytes < bytes) TRY(dev_alloc(ctx, &ctx->d_raster, bytes));
     if (bytes) CK(cudaMemsetAsync(ctx->d_raster.p, 0, bytes, ctx->stream), "raster clear");
     ctx->raster_t0 = ctx->now;
@@ -255,9 +264,67 @@ ranc_status ranc_run_ticks(ranc_ctx* ctx, int64_t num_ticks) {
     dev_free(ctx, &ctx->d_raster);
     ctx->raster_ticks = 0;
   }
-  CK(launch_ticks(ctx, num_ticks), "tick kernel launch");
-  ctx->now += num_ticks;
   return RANC_OK;
+}
+
+}  // namespace
+
+ranc_status ranc_run_ticks(ranc_ctx* ctx, int64_t num_ticks) {
+  TRY(check_ctx(ctx));
+  if (ctx->group) {
+    ctx->err = "this context belongs to a loopback group: use ranc_run_ticks_loopback";
+    return RANC_E_STATE;
+  }
+  TRY(prepare_run(ctx, num_ticks));
+  const bool exchange = ctx->shard_mode == RANC_SHARD_CORES && ctx->nccl_comm && ctx->world > 1;
+  for (int64_t i = 0; i < num_ticks; ++i) {
+    const int64_t t = ctx->now;
+    CK(launch_one_tick(ctx), "tick kernel launch");
+    if (exchange) TRY(exchange_nccl(ctx, t));
+  }
+  return RANC_OK;
+}
+
+ranc_status ranc_run_ticks_loopback(ranc_ctx* const* ctxs, int n, int64_t num_ticks) {
+  if (!ctxs || n < 1 || !ctxs[0]) return RANC_E_ARG;
+  ranc_group* g = ctxs[0]->group;
+  if (!g || (int)g->ctxs.size() != n) {
+    ctxs[0]->err = "contexts are not one loopback group";
+    return RANC_E_STATE;
+  }
+  for (int i = 0; i < n; ++i)
+    if (g->ctxs[i] != ctxs[i]) {
+      ctxs[0]->err = "contexts must be passed in group (rank) order";
+      return RANC_E_ARG;
+    }
+  for (int i = 0; i < n; ++i) {
+    TRY(prepare_run(ctxs[i], num_ticks));
+    if (ctxs[i]->now != ctxs[0]->now || ctxs[i]->S != ctxs[0]->S) {
+      ctxs[0]->err = "loopback members must be at the same tick with the same samples";
+      return RANC_E_STATE;
+    }
+  }
+  // one stream for the whole group (the exchange orders the members)
+  std::vector<cudaStream_t> saved(n);
+  for (int i = 0; i < n; ++i) {
+    saved[i] = ctxs[i]->stream;
+    ctxs[i]->stream = ctxs[0]->stream;
+  }
+  ranc_status st = RANC_OK;
+  for (int64_t k = 0; k < num_ticks && st == RANC_OK; ++k) {
+    const int64_t t = ctxs[0]->now;
+    for (int i = 0; i < n && st == RANC_OK; ++i) {
+      cudaError_t e = launch_one_tick(ctxs[i]);
+      if (e != cudaSuccess) st = set_cuda_error(ctxs[i], e, "tick kernel launch");
+    }
+    if (st == RANC_OK && n > 1) st = exchange_loopback(g, t);
+  }
+  for (int i = 0; i < n; ++i) ctxs[i]->stream = saved[i];
+  if (st == RANC_OK) {
+    cudaError_t e = cudaStreamSynchronize(ctxs[0]->stream);
+    if (e != cudaSuccess) st = set_cuda_error(ctxs[0], e, "ranc_run_ticks_loopback");
+  }
+  return st;
 }
 
 ranc_status ranc_now(const ranc_ctx* ctx, int64_t* tick) {
@@ -290,17 +357,19 @@ ranc_status ranc_read_potentials(ranc_ctx* ctx, int32_t* pot, size_t n) {
     return RANC_E_STATE;
   }
   const Compiled& c = ctx->net;
-  const size_t want = (size_t)ctx->S * c.G * c.N;
+  const int GL = ctx->G_loc;
+  const size_t want = (size_t)ctx->S * GL * c.N;
   if (n != want || !pot) {
-    ctx->err = "potentials buffer has " + std::to_string(n) + " elements, need S*G*N = " + std::to_string(want);
+    ctx->err = "potentials buffer has " + std::to_string(n) + " elements, need S*G_local*N = " + std::to_string(want);
     return RANC_E_SIZE;
   }
   CK(cudaSetDevice(ctx->device), "cudaSetDevice");
   if (ctx->fresh) {  // no tick since the reset: potentials are the initial ones
     TRY(sync(ctx, "ranc_read_potentials"));
     for (int64_t s = 0; s < ctx->S; ++s)
-      for (int g = 0; g < c.G; ++g)
-        for (int j = 0; j < c.N; ++j) pot[((size_t)s * c.G + g) * c.N + j] = c.init[(size_t)g * c.Npad + j];
+      for (int g = 0; g < GL; ++g)
+        for (int j = 0; j < c.N; ++j)
+          pot[((size_t)s * GL + g) * c.N + j] = c.init[(size_t)(ctx->c_lo + g) * c.Npad + j];
     return RANC_OK;
   }
   std::vector<int16_t> h(ctx->d_pot.bytes / 2);
@@ -308,9 +377,9 @@ ranc_status ranc_read_potentials(ranc_ctx* ctx, int32_t* pot, size_t n) {
   TRY(sync(ctx, "ranc_read_potentials"));
   const int64_t NT = tc_tile(), nT = (ctx->S + NT - 1) / NT;
   for (int64_t s = 0; s < ctx->S; ++s)
-    for (int g = 0; g < c.G; ++g)
+    for (int g = 0; g < GL; ++g)
       for (int j = 0; j < c.N; ++j)
-        pot[((size_t)s * c.G + g) * c.N + j] =
+        pot[((size_t)s * GL + g) * c.N + j] =
             ctx->kernel_active == RANC_KERNEL_TC
                 ? h[(((size_t)g * nT + s / NT) * c.Npad + j) * NT + s % NT]
                 : h[((size_t)g * ctx->S + s) * c.Npad + j];
@@ -324,25 +393,27 @@ ranc_status ranc_read_pending(ranc_ctx* ctx, uint32_t* bits, size_t n) {
     return RANC_E_STATE;
   }
   const Compiled& c = ctx->net;
-  const size_t want = (size_t)ctx->S * c.G * c.D * c.W;
+  const int GL = ctx->G_loc;
+  const size_t want = (size_t)ctx->S * GL * c.D * c.W;
   if (n != want || !bits) {
     ctx->err = "pending buffer has " + std::to_string(n) + " elements, need S*G*D*ceil(A/32) = " +
                std::to_string(want);
     return RANC_E_SIZE;
   }
   CK(cudaSetDevice(ctx->device), "cudaSetDevice");
-  std::vector<uint32_t> h((size_t)c.Rp * c.G * ctx->Sr * c.W);
+  std::vector<uint32_t> h((size_t)c.Rp * GL * ctx->Sr * c.W);
   CK(cudaMemcpyAsync(h.data(), ctx->d_ring.p, h.size() * 4, cudaMemcpyDeviceToHost, ctx->stream), "D2H ring");
   TRY(sync(ctx, "ranc_read_pending"));
   std::memset(bits, 0, want * 4);
   for (int j = 0; j < c.D; ++j) {
     const int slot = (int)((ctx->now + j) & (c.Rp - 1));
     for (int64_t s = 0; s < ctx->S; ++s)
-      for (int g = 0; g < c.G; ++g) {
-        const uint32_t* src = &h[(((size_t)slot * c.G + g) * ctx->Sr + s) * c.W];
-        uint32_t* dst = bits + (((size_t)s * c.G + g) * c.D + j) * c.W;
-        const int32_t* perm = ctx->kernel_active == RANC_KERNEL_TC ? &c.perm_tc[(size_t)g * c.A]
-                                                                   : &c.perm[(size_t)g * c.A];
+      for (int g = 0; g < GL; ++g) {
+        const uint32_t* src = &h[(((size_t)slot * GL + g) * ctx->Sr + s) * c.W];
+        uint32_t* dst = bits + (((size_t)s * GL + g) * c.D + j) * c.W;
+        const int gg = ctx->c_lo + g;
+        const int32_t* perm = ctx->kernel_active == RANC_KERNEL_TC ? &c.perm_tc[(size_t)gg * c.A]
+                                                                   : &c.perm[(size_t)gg * c.A];
         for (int ap = 0; ap < c.A; ++ap)
           if ((src[ap >> 5] >> (ap & 31)) & 1u) {
             const int a = perm[ap];
@@ -372,7 +443,8 @@ ranc_status ranc_read_trace(ranc_ctx* ctx, uint32_t kind, void* buf, size_t byte
     return RANC_E_STATE;
   }
   const Compiled& c = ctx->net;
-  const size_t rbytes = (size_t)ctx->raster_ticks * ctx->S * c.G * c.Wn * 4;
+  const int GL = ctx->G_loc;
+  const size_t rbytes = (size_t)ctx->raster_ticks * ctx->S * GL * c.Wn * 4;
   CK(cudaSetDevice(ctx->device), "cudaSetDevice");
   if (kind == RANC_TRACE_SPIKE_RASTER) {
     *written = rbytes;
@@ -390,8 +462,9 @@ ranc_status ranc_read_trace(ranc_ctx* ctx, uint32_t kind, void* buf, size_t byte
   std::vector<int64_t> ev;
   for (int64_t s = 0; s < ctx->S; ++s)
     for (int64_t t = 0; t < ctx->raster_ticks; ++t)
-      for (int g = 0; g < c.G; ++g) {
-        const uint32_t* w = &r[(((size_t)t * ctx->S + s) * c.G + g) * c.Wn];
+      for (int gl = 0; gl < GL; ++gl) {
+        const int g = ctx->c_lo + gl;
+        const uint32_t* w = &r[(((size_t)t * ctx->S + s) * GL + gl) * c.Wn];
         for (int j = 0; j < c.N; ++j)
           if (((w[j >> 5] >> (j & 31)) & 1u) && c.kind[(size_t)g * c.N + j] == RK_OUTPUT) {
             ev.push_back(ctx->first_sample + s);
@@ -473,6 +546,10 @@ ranc_status ranc_get_info(const ranc_ctx* ctx, ranc_info* info) {
   info->sample_tile = ctx->sample_tile; info->num_samples = ctx->S;
   info->device_bytes = ctx->device_bytes; info->kernel_launches = ctx->launches;
   info->kernel = ctx->kernel_active;
+  info->core_lo = ctx->c_lo;
+  info->cores_local = ctx->G_loc;
+  info->shard_mode = (ctx->nccl_comm || ctx->group) ? ctx->shard_mode : 0;
+  info->exchange_bytes = ctx->exchange_bytes;
   return RANC_OK;
 }
 

@@ -42,6 +42,7 @@ __host__ __device__ inline uint32_t route_axon(uint32_t x) { return (x >> 8) & 0
 struct TickParams {
   int32_t G, S, N, Npad, A, W, E, Wn, C, T_in, WI, ST;
   int32_t Sr;               // sample stride of ring rows and input lines (S rounded up to 64)
+  int32_t c_lo, G_loc;      // cores [c_lo, c_lo+G_loc) are simulated here (core-sharded mode)
   int32_t WIp;              // u32 words per input-line row (WI rounded up to 4: 16-byte rows)
   int32_t rp_mask;          // Rp - 1
   int32_t pot_lo, pot_hi;   // saturation range of pb bits
@@ -65,7 +66,10 @@ struct TickParams {
   int16_t* pot;
   uint32_t* ring;
   int32_t* counts;
-  uint32_t* raster;         // [T][S][G][Wn] or nullptr
+  uint32_t* raster;         // [T][S][G_loc][Wn] or nullptr
+  uint32_t* fired;          // core-sharded: [G_loc][Sr][Wn] fired bits of this tick (export cores)
+  const uint8_t* exports;   // [G] core has a neuron routing to another rank
+  unsigned long long* dbg;  // optional pipeline timeline (RANC_DEBUG_TIMELINE)
 };
 
 // Host copy of the compiled network.
@@ -101,6 +105,8 @@ struct DevBuf {
 
 }  // namespace ranc
 
+struct ranc_group;
+
 struct ranc_ctx {
   int device = 0;
   cudaStream_t own_stream = nullptr;
@@ -133,22 +139,45 @@ struct ranc_ctx {
   // multi-GPU
   void* nccl_comm = nullptr;
   int world = 1, rank = 0;
+  int shard_mode = 0;            // RANC_SHARD_SAMPLES or RANC_SHARD_CORES
+  int32_t c_lo = 0, G_loc = 0;   // local core range (G_loc = G unless core-sharded)
+  ranc_group* group = nullptr;   // loopback group (several contexts, one process)
+  bool group_broken = false;     // a member of the loopback group was destroyed
+  // core-sharded exchange
+  std::vector<std::vector<int32_t>> send_cores, recv_cores;  // per peer: local / global core ids
+  std::vector<int64_t> send_off, recv_off;                   // per peer, in u32 words
+  ranc::DevBuf d_fired, d_exports, d_send, d_recv, d_send_list, d_recv_list, d_recv_peer;
+  int64_t n_send_words = 0, n_recv_words = 0, n_recv_rows = 0;
+  int64_t exchange_bytes = 0;    // bytes sent per tick (introspection)
+  ranc::DevBuf d_dbg;            // RANC_DEBUG_TIMELINE
+};
+
+struct ranc_group {
+  std::vector<ranc_ctx*> ctxs;
 };
 
 namespace ranc {
 enum { RANC_KERNEL_AUTO = 0, RANC_KERNEL_POPC = 1, RANC_KERNEL_TC = 2 };
+// comm.cpp
+ranc_status setup_core_shards(ranc_ctx* ctx, int world, int rank);
+ranc_status alloc_exchange(ranc_ctx* ctx);
+ranc_status exchange_nccl(ranc_ctx* ctx, int64_t t);
+ranc_status exchange_loopback(ranc_group* g, int64_t t);
 // compile.cpp
 ranc_status validate_and_compile(const ranc_network_desc* d, Compiled* out, std::string* err);
 // tick.cu
 cudaError_t launch_reset(ranc_ctx* ctx);
 cudaError_t transpose_lines(ranc_ctx* ctx, const uint32_t* staging);
-cudaError_t launch_ticks(ranc_ctx* ctx, int64_t num_ticks);
+
+cudaError_t launch_one_tick(ranc_ctx* ctx);          // the tick kernel for tick ctx->now (no exchange)
+cudaError_t launch_pack(ranc_ctx* ctx);              // core-sharded: fired rows -> send buffer
+cudaError_t launch_unpack(ranc_ctx* ctx, int64_t t); // core-sharded: received rows -> local rings
 int choose_sample_tile(const Compiled& n, int64_t S);
 int pieces_template(int E);
 // tick_tc.cu
 int tc_tile();
 size_t tc_smem_bytes(const Compiled& n);
-cudaError_t launch_ticks_tc(ranc_ctx* ctx, TickParams p, int64_t num_ticks);
+cudaError_t launch_tick_tc(ranc_ctx* ctx, TickParams p);
 // api.cpp
 ranc_status dev_alloc(ranc_ctx* ctx, DevBuf* b, size_t bytes);
 void dev_free(ranc_ctx* ctx, DevBuf* b);

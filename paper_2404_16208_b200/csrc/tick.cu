@@ -57,7 +57,8 @@ __host__ __device__ inline SmemLayout smem_layout(int ST, int Npad, int W, int E
 template <int E>
 __global__ void __launch_bounds__(kThreads, (E <= 12 ? 4 : (E <= 16 ? 3 : 2))) tick_popc_kernel(const TickParams p) {
   extern __shared__ __align__(16) uint8_t smem[];
-  const int c = blockIdx.x;
+  const int cl = blockIdx.x;             // local core (state index)
+  const int c = p.c_lo + cl;             // global core (network index)
   const int s0 = blockIdx.y * p.ST;
   const int ns = min(p.ST, p.S - s0);
   const int tid = threadIdx.x;
@@ -71,7 +72,7 @@ __global__ void __launch_bounds__(kThreads, (E <= 12 ? 4 : (E <= 16 ? 3 : 2))) t
   uint32_t* lines_s = reinterpret_cast<uint32_t*>(smem + L.lines);
   const int cur = (int)(p.t & p.rp_mask);
   const uint32_t tile_bytes = (uint32_t)ns * p.Npad * 2;
-  int16_t* pot_g = p.pot + ((size_t)c * p.S + s0) * p.Npad;
+  int16_t* pot_g = p.pot + ((size_t)cl * p.S + s0) * p.Npad;
 
   if (tid == 0) {
     ptx::mbar_init(bar, 1);
@@ -85,7 +86,7 @@ __global__ void __launch_bounds__(kThreads, (E <= 12 ? 4 : (E <= 16 ? 3 : 2))) t
   }
   // a1: stage the current scheduler rows of (core c, samples s0..) and clear
   // them (the row is free again for spikes due at t + Rp).
-  uint32_t* row = p.ring + (((size_t)cur * p.G + c) * p.Sr + s0) * W;
+  uint32_t* row = p.ring + (((size_t)cur * p.G_loc + cl) * p.Sr + s0) * W;
   for (int i = tid; i < ns * W; i += blockDim.x) {
     raw[i] = row[i];
     row[i] = 0u;
@@ -136,6 +137,10 @@ __global__ void __launch_bounds__(kThreads, (E <= 12 ? 4 : (E <= 16 ? 3 : 2))) t
     const bool lin = route_lin(rt.x);
     const bool valid = n < p.N;
     const int leak = prm.x, pth = prm.y, nth = prm.z, rst = prm.w;
+    // a route to a core of another rank is delivered by the exchange step
+    const uint32_t dloc = rt.y - (uint32_t)p.c_lo;
+    const bool route_here = kind == RK_ROUTE && dloc < (uint32_t)p.G_loc;
+    const bool exporting = p.fired && p.exports[c];
 #pragma unroll 2
     for (int s = 0; s < ns; ++s) {
       // a3: integration
@@ -159,19 +164,22 @@ __global__ void __launch_bounds__(kThreads, (E <= 12 ? 4 : (E <= 16 ? 3 : 2))) t
       nv = min(max(nv, p.pot_lo), p.pot_hi);
       pot_s[s * p.Npad + n] = (int16_t)nv;
       // a5 / a6: route into the destination ring row of tick t+delay, or count
-      if (fire && valid && kind != RK_NONE) {
-        if (kind == RK_ROUTE) {
+      if (fire && valid) {
+        if (route_here) {
           const uint32_t ax = route_axon(rt.x);
           const int slot = (int)((p.t + route_delay(rt.x)) & p.rp_mask);
-          atomicOr(p.ring + (((size_t)slot * p.G + rt.y) * p.Sr + s0 + s) * W + (ax >> 5), 1u << (ax & 31));
-        } else {
+          atomicOr(p.ring + (((size_t)slot * p.G_loc + dloc) * p.Sr + s0 + s) * W + (ax >> 5), 1u << (ax & 31));
+        } else if (kind == RK_OUTPUT) {
           atomicAdd(p.counts + (size_t)(s0 + s) * p.C + rt.y, 1);
         }
       }
-      if (p.raster) {
+      if (p.raster || exporting) {
         const uint32_t m = __ballot_sync(0xFFFFFFFFu, fire && valid);
-        if (lane == 0 && (n >> 5) < p.Wn)
-          p.raster[(((size_t)(p.t - p.raster_t0) * p.S + s0 + s) * p.G + c) * p.Wn + (n >> 5)] = m;
+        if (lane == 0 && (n >> 5) < p.Wn) {
+          if (p.raster)
+            p.raster[(((size_t)(p.t - p.raster_t0) * p.S + s0 + s) * p.G_loc + cl) * p.Wn + (n >> 5)] = m;
+          if (exporting) p.fired[((size_t)cl * p.Sr + s0 + s) * p.Wn + (n >> 5)] = m;
+        }
       }
     }
   }
@@ -249,11 +257,14 @@ cudaError_t launch_reset(ranc_ctx* ctx) {
   return cudaSuccess;
 }
 
-cudaError_t launch_ticks(ranc_ctx* ctx, int64_t num_ticks) {
+namespace {
+
+TickParams make_params(ranc_ctx* ctx) {
   const Compiled& n = ctx->net;
   TickParams p{};
-  p.G = n.G; p.S = (int)ctx->S; p.Sr = (int)ctx->Sr; p.WIp = n.WIp; p.N = n.N; p.Npad = n.Npad; p.A = n.A; p.W = n.W; p.E = n.E;
-  p.Wn = n.Wn; p.C = n.C; p.T_in = ctx->T_in; p.WI = n.WI; p.ST = ctx->sample_tile;
+  p.G = n.G; p.S = (int)ctx->S; p.Sr = (int)ctx->Sr; p.WIp = n.WIp; p.N = n.N; p.Npad = n.Npad; p.A = n.A;
+  p.W = n.W; p.E = n.E; p.Wn = n.Wn; p.C = n.C; p.T_in = ctx->T_in; p.WI = n.WI; p.ST = ctx->sample_tile;
+  p.c_lo = ctx->c_lo; p.G_loc = ctx->G_loc;
   p.rp_mask = n.Rp - 1;
   p.pot_lo = -(1 << (n.pb - 1));
   p.pot_hi = (1 << (n.pb - 1)) - 1;
@@ -271,15 +282,26 @@ cudaError_t launch_ticks(ranc_ctx* ctx, int64_t num_ticks) {
   p.counts = (int32_t*)ctx->d_counts.p;
   p.raster = (uint32_t*)ctx->d_raster.p;
   p.raster_t0 = ctx->raster_t0;
+  p.fired = ctx->shard_mode == RANC_SHARD_CORES ? (uint32_t*)ctx->d_fired.p : nullptr;
+  p.exports = (const uint8_t*)ctx->d_exports.p;
   p.Kp = n.Kp;
   p.wfold = (const uint8_t*)ctx->d_wfold.p;
-  if (ctx->kernel_active == RANC_KERNEL_TC) return launch_ticks_tc(ctx, p, num_ticks);
-  const dim3 grid(n.G, (unsigned)((ctx->S + p.ST - 1) / p.ST));
-  const size_t smem = smem_layout(p.ST, n.Npad, n.W, n.E, n.WIp).total;
-  for (int64_t i = 0; i < num_ticks; ++i) {
-    p.t = ctx->now + i;
-    p.fresh = ctx->fresh ? 1 : 0;
-    cudaError_t e;
+  p.t = ctx->now;
+  p.fresh = ctx->fresh ? 1 : 0;
+  return p;
+}
+
+}  // namespace
+
+cudaError_t launch_one_tick(ranc_ctx* ctx) {
+  const Compiled& n = ctx->net;
+  TickParams p = make_params(ctx);
+  cudaError_t e;
+  if (ctx->kernel_active == RANC_KERNEL_TC) {
+    e = launch_tick_tc(ctx, p);
+  } else {
+    const dim3 grid(ctx->G_loc, (unsigned)((ctx->S + p.ST - 1) / p.ST));
+    const size_t smem = smem_layout(p.ST, n.Npad, n.W, n.E, n.WIp).total;
     switch (n.E) {
       case 4: e = launch_one<4>(p, grid, smem, ctx->stream); break;
       case 8: e = launch_one<8>(p, grid, smem, ctx->stream); break;
@@ -288,10 +310,11 @@ cudaError_t launch_ticks(ranc_ctx* ctx, int64_t num_ticks) {
       case 24: e = launch_one<24>(p, grid, smem, ctx->stream); break;
       default: e = launch_one<36>(p, grid, smem, ctx->stream); break;
     }
-    ctx->launches++;
-    if (e != cudaSuccess) return e;
-    ctx->fresh = false;
   }
+  ctx->launches++;
+  if (e != cudaSuccess) return e;
+  ctx->fresh = false;
+  ctx->now += 1;
   return cudaSuccess;
 }
 

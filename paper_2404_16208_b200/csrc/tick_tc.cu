@@ -32,6 +32,8 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 #include "internal.h"
 #include "ptx.h"
@@ -73,6 +75,11 @@ __host__ __device__ inline TcLayout tc_layout(int Np, int Kp, int W, int WIp) {
   return L;
 }
 
+// optional per-tile timeline of CTA 0 (debug builds of a run: p.dbg != nullptr)
+__device__ __forceinline__ void stamp(const TickParams& p, int k, int slot) {
+  if (p.dbg && blockIdx.x == 0 && k < 64) p.dbg[k * 16 + slot] = (unsigned long long)clock64();
+}
+
 __device__ __forceinline__ void named_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
@@ -90,7 +97,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
   uint8_t* w_s = smem + L.w;
   const int Mh = Np >> 7;
   const int nT = (p.S + NT - 1) / NT;
-  const int total = p.G * nT;
+  const int total = p.G_loc * nT;
   const int lo = (int)((int64_t)blockIdx.x * total / gridDim.x);
   const int hi = (int)((int64_t)(blockIdx.x + 1) * total / gridDim.x);
   const int nwork = hi - lo;
@@ -126,7 +133,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
     if (lane == 0) {
       int prev_core = -1, jw = -1;
       for (int k = 0; k < nwork; ++k) {
-        const int idx = lo + k, c = idx / nT, tile = idx - c * nT;
+        const int idx = lo + k, cl = idx / nT, tile = idx - cl * nT, c = p.c_lo + cl;
         const int s = k % NS, u = k / NS;
         if (c != prev_core) {
           ++jw;
@@ -136,13 +143,15 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
           ptx::bulk_g2s(w_s, p.wfold + (size_t)c * wb, wb, &bars[WFULL]);
           prev_core = c;
         }
+        stamp(p, k, 0);
         ptx::mbar_wait(&bars[SEMPTY0 + s], (u & 1) ^ 1);
+        stamp(p, k, 1);
         uint8_t* st = smem + L.stage + s * L.stage_bytes;
         const int s0 = tile * NT;
         const bool inject = p.t < p.T_in && p.nruns[c] > 0;
         const uint32_t ring_bytes = (uint32_t)NT * W * 4, line_bytes = inject ? (uint32_t)NT * WIp * 4 : 0u;
         ptx::mbar_arrive_expect_tx(&bars[FULL0 + s], ring_bytes + line_bytes);
-        ptx::bulk_g2s(st + L.raw, p.ring + (((size_t)cur * p.G + c) * p.Sr + s0) * W, ring_bytes, &bars[FULL0 + s]);
+        ptx::bulk_g2s(st + L.raw, p.ring + (((size_t)cur * p.G_loc + cl) * p.Sr + s0) * W, ring_bytes, &bars[FULL0 + s]);
         if (inject)
           ptx::bulk_g2s(st + L.lines, p.lines + ((size_t)p.t * p.Sr + s0) * WIp, line_bytes, &bars[FULL0 + s]);
       }
@@ -163,7 +172,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
           prev_core = c;
         }
         ptx::mbar_wait(&bars[BFULL0 + s], u & 1);
+        stamp(p, k, 5);
         ptx::mbar_wait(&bars[ACCEMPTY0 + a], (ua & 1) ^ 1);
+        stamp(p, k, 6);
         tc::fence_after();
         const uint8_t* b_s = smem + L.stage + s * L.stage_bytes + L.b;
         const uint32_t acc = tmem + a * acc_stride;
@@ -175,6 +186,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
           }
         tc::commit(&bars[BEMPTY0 + s]);
         tc::commit(&bars[ACCFULL0 + a]);
+        stamp(p, k, 7);
         const int next_core = (k + 1 < nwork) ? (lo + k + 1) / nT : -1;
         if (next_core != c) tc::commit(&bars[WFREE]);
       }
@@ -186,7 +198,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
     const int K16 = Kp >> 4;
     const bool fast = (kExpThreads % K16) == 0;
     for (int k = 0; k < nwork; ++k) {
-      const int idx = lo + k, c = idx / nT, tile = idx - c * nT;
+      const int idx = lo + k, cl = idx / nT, tile = idx - cl * nT, c = p.c_lo + cl;
       const int s = k % NS, u = k / NS;
       const int s0 = tile * NT, ns = min(NT, p.S - s0);
       uint8_t* st = smem + L.stage + s * L.stage_bytes;
@@ -195,7 +207,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       // a1: the scheduler rows due now were staged by the producer (TMA);
       // clear them in global memory (free again for spikes due at t + Rp)
       ptx::mbar_wait(&bars[FULL0 + s], u & 1);
-      uint32_t* row = p.ring + (((size_t)cur * p.G + c) * p.Sr + s0) * W;
+      if (et == 0) stamp(p, k, 2);
+      uint32_t* row = p.ring + (((size_t)cur * p.G_loc + cl) * p.Sr + s0) * W;
       for (int i = et; i < ns * W; i += kExpThreads) row[i] = 0u;
       // a2: external inputs, one contiguous run of lines -> axons per item
       if (p.t < p.T_in && p.nruns[c] > 0) {
@@ -221,6 +234,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       // bits -> 0/1 bytes, canonical K-major operand (rows = samples);
       // samples >= ns of a tail tile get no spikes
       ptx::mbar_wait(&bars[BEMPTY0 + s], (u & 1) ^ 1);
+      if (et == 0) stamp(p, k, 3);
       uint8_t* b_s = st + L.b;
       auto expand = [&](int sm, int k16) {
         uint32_t bits = 0u;
@@ -244,6 +258,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       ptx::fence_proxy_async_smem();
       named_sync(2, kExpThreads);
       if (et == 0) {
+        stamp(p, k, 4);
         ptx::mbar_arrive(&bars[BFULL0 + s]);
         ptx::mbar_arrive(&bars[SEMPTY0 + s]);   // raw/lines of this stage are consumed
       }
@@ -258,6 +273,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
     int prev_core = -1;
     int leak = 0, pth = 0, nth = 0, rst = 0, init = 0, bf = 0, bn = 0, linmask = 0;
     uint32_t kind = RK_NONE, cls = 0, axbit = 0;
+    bool route_here = false, exporting = false;
     size_t ring_off = 0;
     uint4 pnext[NT / 8];
     const bool load = active && !p.fresh;
@@ -268,7 +284,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       for (int i = 0; i < NT / 8; ++i) pnext[i] = src[i];
     }
     for (int k = 0; k < nwork; ++k) {
-      const int idx = lo + k, c = idx / nT, tile = idx - c * nT;
+      const int idx = lo + k, cl = idx / nT, tile = idx - cl * nT, c = p.c_lo + cl;
       const int a = k % NA, ua = k / NA;
       const int s0 = tile * NT, ns = min(NT, p.S - s0);
       // pnext holds this tile's potentials (prefetched during the previous
@@ -276,6 +292,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       const bool pf = load && k + 1 < nwork;
       const uint4* nsrc = pot_row(p, (idx + 1) / nT, (idx + 1) % nT, nT, n);
       ptx::mbar_wait(&bars[ACCFULL0 + a], ua & 1);
+      if (lane == 0 && (ew == 0 || ew == 7)) stamp(p, k, ew == 0 ? 8 : 10);
       tc::fence_after();
       if (active) {
         if (c != prev_core) {
@@ -293,10 +310,14 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
           const uint32_t ax = route_axon(rt.x);
           axbit = 1u << (ax & 31);
           const int slot = (int)((p.t + route_delay(rt.x)) & p.rp_mask);
-          ring_off = (((size_t)slot * p.G + rt.y) * p.Sr) * W + (ax >> 5);
+          // a route to a core of another rank is delivered by the exchange step
+          const uint32_t dloc = rt.y - (uint32_t)p.c_lo;
+          route_here = kind == RK_ROUTE && dloc < (uint32_t)p.G_loc;
+          ring_off = (((size_t)slot * p.G_loc + dloc) * p.Sr) * W + (ax >> 5);
+          exporting = p.fired && p.exports[c];
           prev_core = c;
         }
-        uint4* dst = const_cast<uint4*>(pot_row(p, c, tile, nT, n));
+        uint4* dst = const_cast<uint4*>(pot_row(p, cl, tile, nT, n));
         const uint32_t acc_addr = tmem + a * acc_stride + ((uint32_t)(q * 32) << 16) + h * NT;
 #pragma unroll
         for (int j = 0; j < NT / 32; ++j) {
@@ -329,7 +350,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
           // a5 / a6: route or count the spikes of real samples
           const int lim = ns - j * 32;
           uint32_t f = lim >= 32 ? fired : (lim > 0 ? fired & ((1u << lim) - 1u) : 0u);
-          if (kind == RK_ROUTE) {
+          if (route_here) {
             while (f) {
               const int i = __ffs(f) - 1;
               f &= f - 1;
@@ -342,19 +363,24 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
               atomicAdd(p.counts + (size_t)(s0 + j * 32 + i) * p.C + cls, 1);
             }
           }
-          if (p.raster) {
+          if (p.raster || exporting) {
             const uint32_t fv = valid ? fired : 0u;
             for (int i = 0; i < 32 && i < lim; ++i) {
               const uint32_t m = __ballot_sync(0xFFFFFFFFu, (fv >> i) & 1u);
-              if (lane == 0 && (n >> 5) < p.Wn)
-                p.raster[(((size_t)(p.t - p.raster_t0) * p.S + s0 + j * 32 + i) * p.G + c) * p.Wn + (n >> 5)] = m;
+              if (lane == 0 && (n >> 5) < p.Wn) {
+                const int sg = s0 + j * 32 + i;
+                if (p.raster) p.raster[(((size_t)(p.t - p.raster_t0) * p.S + sg) * p.G_loc + cl) * p.Wn + (n >> 5)] = m;
+                if (exporting) p.fired[((size_t)cl * p.Sr + sg) * p.Wn + (n >> 5)] = m;
+              }
             }
           }
         }
       }
       tc::fence_before();
       __syncwarp();
+      if (lane == 0 && (ew == 0 || ew == 7)) stamp(p, k, ew == 0 ? 9 : 11);
       if (lane == 0) ptx::mbar_arrive(&bars[ACCEMPTY0 + a]);
+      if (lane == 0 && (ew == 0 || ew == 7)) stamp(p, k, ew == 0 ? 12 : 13);
     }
   }
   tc::fence_before();
@@ -368,14 +394,14 @@ int tc_tile() { return NT; }
 
 size_t tc_smem_bytes(const Compiled& n) { return tc_layout(n.Npad, n.Kp, n.W, n.WIp).total; }
 
-cudaError_t launch_ticks_tc(ranc_ctx* ctx, TickParams p, int64_t num_ticks) {
+cudaError_t launch_tick_tc(ranc_ctx* ctx, TickParams p) {
   const Compiled& n = ctx->net;
   p.ST = NT;
   p.route = (const uint2*)ctx->d_route_tc.p;
   p.runs = (const int2*)ctx->d_runs.p;
   p.nruns = (const int32_t*)ctx->d_nruns.p;
   p.rmax = n.rmax;
-  const int64_t total = (int64_t)n.G * ((ctx->S + NT - 1) / NT);
+  const int64_t total = (int64_t)ctx->G_loc * ((ctx->S + NT - 1) / NT);
   const int grid = (int)std::min<int64_t>(total, ctx->num_sms);
   const size_t smem = tc_layout(n.Npad, n.Kp, n.W, n.WIp).total;
   static bool configured = false;
@@ -383,16 +409,26 @@ cudaError_t launch_ticks_tc(ranc_ctx* ctx, TickParams p, int64_t num_ticks) {
     cudaFuncSetAttribute(tick_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     configured = true;
   }
-  for (int64_t i = 0; i < num_ticks; ++i) {
-    p.t = ctx->now + i;
-    p.fresh = ctx->fresh ? 1 : 0;
-    tick_tc_kernel<<<grid, kThreadsTC, smem, ctx->stream>>>(p);
-    ctx->launches++;
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-    ctx->fresh = false;
+  static const bool dbg = getenv("RANC_DEBUG_TIMELINE") != nullptr;
+  if (dbg && !ctx->d_dbg.p) dev_alloc(ctx, &ctx->d_dbg, 64 * 16 * 8);
+  p.dbg = dbg ? (unsigned long long*)ctx->d_dbg.p : nullptr;
+  if (dbg) cudaMemsetAsync(ctx->d_dbg.p, 0, 64 * 16 * 8, ctx->stream);
+  tick_tc_kernel<<<grid, kThreadsTC, smem, ctx->stream>>>(p);
+  if (dbg) {
+    unsigned long long h[64 * 16];
+    cudaMemcpyAsync(h, ctx->d_dbg.p, sizeof h, cudaMemcpyDeviceToHost, ctx->stream);
+    cudaStreamSynchronize(ctx->stream);
+    const unsigned long long t0 = h[0];
+    fprintf(stderr, "timeline t=%lld grid=%d (cycles rel. to producer start)\n", (long long)p.t, grid);
+    fprintf(stderr, "  k  prodW prodGo expFull expBempty expBfull mmaB mmaAccE mmaCommit epi0Acc epi0Done epi7Acc epi7Done epi0Arr epi7Arr\n");
+    for (int k = 0; k < 64; ++k) {
+      fprintf(stderr, "%3d", k);
+      const int order[14] = {0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13};
+      for (int j : order) fprintf(stderr, " %8lld", h[k * 16 + j] ? (long long)(h[k * 16 + j] - t0) : -1LL);
+      fprintf(stderr, "\n");
+    }
   }
-  return cudaSuccess;
+  return cudaGetLastError();
 }
 
 }  // namespace ranc

@@ -128,16 +128,21 @@ class Simulator:
         self._ck(self.lib.ranc_now(self.h, C.byref(t)))
         return t.value
 
+    @property
+    def cores_local(self) -> int:
+        return self.info()["cores_local"]
+
     def potentials(self) -> np.ndarray:
+        """int32 [S][G_local][N] (G_local = G unless core-sharded)."""
         n = self.net
-        out = np.zeros((self.S, n.grid_w * n.grid_h, n.neurons), np.int32)
+        out = np.zeros((self.S, self.cores_local, n.neurons), np.int32)
         self._ck(self.lib.ranc_read_potentials(self.h, out.ctypes.data, out.size))
         return out
 
     def pending_words(self) -> np.ndarray:
         n = self.net
         W = (n.axons + 31) // 32
-        out = np.zeros((self.S, n.grid_w * n.grid_h, n.max_delay, W), np.uint32)
+        out = np.zeros((self.S, self.cores_local, n.max_delay, W), np.uint32)
         self._ck(self.lib.ranc_read_pending(self.h, out.ctypes.data, out.size))
         return out
 
@@ -166,8 +171,7 @@ class Simulator:
         self._ck(self.lib.ranc_read_trace(self.h, L.TRACE_SPIKE_RASTER, buf.ctypes.data, buf.nbytes,
                                           C.byref(got)))
         Wn = (n.neurons + 31) // 32
-        G = n.grid_w * n.grid_h
-        w = buf[:nb // 4].reshape(-1, self.S, G, Wn)
+        w = buf[:nb // 4].reshape(-1, self.S, self.cores_local, Wn)
         bits = np.unpackbits(w.view(np.uint8), axis=-1, bitorder="little")
         return bits[..., :n.neurons]
 
@@ -191,7 +195,20 @@ class Simulator:
         b = (C.c_char * 128).from_buffer_copy(uid)
         self._ck(self.lib.ranc_comm_init(self.h, b, int(world), int(rank), int(mode)))
 
+    @staticmethod
+    def init_loopback(sims, mode: int = L.SHARD_CORES):
+        """Make `sims` (one process, one GPU) the ranks of a core-sharded run."""
+        arr = (C.c_void_p * len(sims))(*[s.h.value for s in sims])
+        _check(sims[0].lib, sims[0].lib.ranc_comm_init_loopback(arr, len(sims), int(mode)), sims[0].h)
+
+    @staticmethod
+    def run_loopback(sims, ticks: int):
+        arr = (C.c_void_p * len(sims))(*[s.h.value for s in sims])
+        _check(sims[0].lib, sims[0].lib.ranc_run_ticks_loopback(arr, len(sims), int(ticks)), sims[0].h)
+
     def gather_outputs(self, total_samples: int, root: int = 0, rank: int = 0):
+        """Sample mode: [sum S_local][C] concatenated in rank order; core mode:
+        pass total_samples = S, returns the [S][C] sum.  None off-root."""
         C_ = int(self.net.num_classes)
         out = np.zeros((total_samples, C_), np.int32) if rank == root else np.zeros((1,), np.int32)
         n = out.size if rank == root else 0

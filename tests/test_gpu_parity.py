@@ -233,3 +233,70 @@ def test_tc_envelope_rejects_wide_weights(ranc):
         sim.set_option(ranc.OPT_KERNEL, 2)
     assert ei.value.code == "RANC_E_CONFIG"
     sim.close()
+
+
+# ---------------------------------------------------------------------------
+# core-sharded mode, exercised through a loopback group on one GPU
+# ---------------------------------------------------------------------------
+
+def _core_sharded(ranc, net, inp, T, world, kernel):
+    sims = []
+    for r in range(world):
+        sims.append(make_sim(ranc, net, kernel))
+    ranc.Simulator.init_loopback(sims)
+    for s in sims:
+        s.set_trace(ranc.TRACE_OUTPUT_EVENTS)
+        s.load_inputs(inp)
+    ranc.Simulator.run_loopback(sims, T)
+    return sims
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("variant", ["local", "global"])
+def test_core_sharded_loopback_matches_oracle(ranc, oracle_mod, kernel, world, variant):
+    net, inp = config5(S=4, T=30, grid=6, variant=variant)
+    T = 30
+    sims = _core_sharded(ranc, net, inp, T, world, kernel)
+    o = oracle_mod.Oracle(net, inp).run(T)
+    pot, pend = o.potentials(), o.pending()
+    counts = np.zeros_like(o.counts())
+    events = []
+    for s in sims:
+        i = s.info()
+        lo, g = i["core_lo"], i["cores_local"]
+        assert i["shard_mode"] == 1
+        assert np.array_equal(s.potentials(), pot[:, lo:lo + g]), "potentials of the local band"
+        assert np.array_equal(s.pending(), pend[:, lo:lo + g]), "pending of the local band"
+        counts += s.outputs()
+        events.append(s.events())
+    assert np.array_equal(counts, o.counts())
+    ev = np.concatenate(events)
+    ev = ev[np.lexsort((ev[:, 4], ev[:, 2], ev[:, 3], ev[:, 1], ev[:, 0]))]
+    assert np.array_equal(ev, o.events())
+    assert sum(s.info()["exchange_bytes"] for s in sims) > 0
+    for s in sims:
+        s.close()
+
+
+def test_core_sharded_random_corpus(ranc, oracle_mod, kernel):
+    from workloads.gen import random_network, random_inputs
+    for seed in range(6):
+        net = random_network(seed, 3, 4, 40, 33, 3, 4, C=3, I=20)
+        inp = random_inputs(seed, net, 3, 10, p=0.3)
+        sims = _core_sharded(ranc, net, inp, 12, 2, kernel)
+        o = oracle_mod.Oracle(net, inp).run(12)
+        got = np.concatenate([s.potentials() for s in sims], axis=1)
+        assert np.array_equal(got, o.potentials()), seed
+        assert np.array_equal(sum(s.outputs() for s in sims), o.counts()), seed
+        for s in sims:
+            s.close()
+
+
+def test_sample_sharded_comm_world1(ranc, oracle_mod):
+    """NCCL communicator with one rank: gather == local outputs."""
+    net, inp = config2(S=20)
+    sim = ranc.Simulator(net)
+    sim.comm_init(ranc.Simulator.unique_id(), 1, 0)
+    sim.load_inputs(inp).run(17)
+    assert np.array_equal(sim.gather_outputs(20, 0, 0), sim.outputs())
+    sim.close()
