@@ -317,6 +317,30 @@ ranc_status validate_and_compile(const ranc_network_desc* d, Compiled* out, std:
         const int dap = o.inv_tc[(size_t)dc * A + d->dest_axon[cn]];
         r.x = (r.x & 0xFFu) | ((uint32_t)dap << 8);
       }
+    // warps whose routing neurons all deposit into one ring word ("block
+    // routes", e.g. the 32 neurons of an MNIST-layer core feeding 32 axons
+    // of the next layer): the epilogue OR-reduces them into one deposit
+    o.wflags_tc.assign((size_t)G * (Np / 32), 0);
+    for (int c = 0; c < G; ++c)
+      for (int w = 0; w < Np / 32; ++w) {
+        bool any = false, same = true;
+        uint32_t key0 = 0, dc0 = 0;
+        for (int l = 0; l < 32; ++l) {
+          const int n = w * 32 + l;
+          if (n >= N) break;
+          const uint2 r = o.route_tc[(size_t)c * Np + n];
+          if (route_kind(r.x) != RK_ROUTE) continue;
+          const uint32_t key = (route_axon(r.x) >> 5) | (route_delay(r.x) << 16);
+          if (!any) {
+            any = true;
+            key0 = key;
+            dc0 = r.y;
+          } else if (key != key0 || r.y != dc0) {
+            same = false;
+          }
+        }
+        if (any && same) o.wflags_tc[(size_t)c * (Np / 32) + w] = 1;
+      }
     // folded weights in the canonical operand layout (tc.h)
     const size_t per = (size_t)o.Npad * o.Kp;
     o.wfold.assign((size_t)G * per, 0);

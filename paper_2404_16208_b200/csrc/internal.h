@@ -70,6 +70,7 @@ struct TickParams {
   uint32_t* fired;          // core-sharded: [G_loc][Sr][Wn] fired bits of this tick (export cores)
   const uint8_t* exports;   // [G] core has a neuron routing to another rank
   unsigned long long* dbg;  // optional pipeline timeline (RANC_DEBUG_TIMELINE)
+  const uint8_t* wflags;    // [G][Npad/32] per-warp flags (bit 0: block route), or nullptr
 };
 
 // Host copy of the compiled network.
@@ -84,6 +85,8 @@ struct Compiled {
   std::vector<uint2> route_tc;  // route words with tensor-core destination axons
   std::vector<int2> runs;       // [G][rmax] input runs: x = a'start | len<<16, y = first line
   std::vector<int32_t> nruns;   // [G]
+  std::vector<uint8_t> wflags_tc;  // [G][Npad/32] bit 0: all routing neurons of the warp share one
+                                   // (dest core, ring word, delay) in the tensor-core axon order
   int32_t rmax = 0;
   std::vector<uint32_t> xp;     // [G][E][Npad]
   std::vector<int16_t> wp;      // [G][E][Npad]
@@ -117,7 +120,7 @@ struct ranc_ctx {
   std::string err;
   ranc::Compiled net;
   // device: compiled network
-  ranc::DevBuf d_xp, d_wp, d_pword, d_prm, d_route, d_inl, d_has_in, d_init, d_wfold, d_route_tc, d_runs, d_nruns;
+  ranc::DevBuf d_xp, d_wp, d_pword, d_prm, d_route, d_inl, d_has_in, d_init, d_wfold, d_route_tc, d_runs, d_nruns, d_wflags_tc;
   int num_sms = 148;
   // device: state
   ranc::DevBuf d_pot, d_ring, d_counts, d_lines, d_stage, d_raster;

@@ -273,8 +273,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
     int prev_core = -1;
     int leak = 0, pth = 0, nth = 0, rst = 0, init = 0, bf = 0, bn = 0, linmask = 0;
     uint32_t kind = RK_NONE, cls = 0, axbit = 0;
-    bool route_here = false, exporting = false;
-    size_t ring_off = 0;
+    bool route_here = false, exporting = false, block_route = false, has_output = false;
+    size_t ring_off = 0, warp_ring_off = 0;
     uint4 pnext[NT / 8];
     const bool load = active && !p.fresh;
     if (load && nwork > 0) {
@@ -292,7 +292,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       const bool pf = load && k + 1 < nwork;
       const uint4* nsrc = pot_row(p, (idx + 1) / nT, (idx + 1) % nT, nT, n);
       ptx::mbar_wait(&bars[ACCFULL0 + a], ua & 1);
-      if (lane == 0 && (ew == 0 || ew == 7)) stamp(p, k, ew == 0 ? 8 : 10);
+
       tc::fence_after();
       if (active) {
         if (c != prev_core) {
@@ -315,6 +315,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
           route_here = kind == RK_ROUTE && dloc < (uint32_t)p.G_loc;
           ring_off = (((size_t)slot * p.G_loc + dloc) * p.Sr) * W + (ax >> 5);
           exporting = p.fired && p.exports[c];
+          block_route = p.wflags && (p.wflags[(size_t)c * (Np >> 5) + (n >> 5)] & 1u);
+          const uint32_t rmask = __ballot_sync(0xFFFFFFFFu, route_here);
+          warp_ring_off = rmask ? __shfl_sync(0xFFFFFFFFu, ring_off, __ffs(rmask) - 1) : 0;
+          has_output = __any_sync(0xFFFFFFFFu, kind == RK_OUTPUT);
           prev_core = c;
         }
         uint4* dst = const_cast<uint4*>(pot_row(p, cl, tile, nT, n));
@@ -350,17 +354,36 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
           // a5 / a6: route or count the spikes of real samples
           const int lim = ns - j * 32;
           uint32_t f = lim >= 32 ? fired : (lim > 0 ? fired & ((1u << lim) - 1u) : 0u);
-          if (route_here) {
-            while (f) {
-              const int i = __ffs(f) - 1;
-              f &= f - 1;
+          if (block_route) {
+            // every routing lane of this warp targets the same ring word:
+            // one OR-reduced 32-bit deposit per sample instead of one atomic
+            // per spike (idempotent OR, G11)
+            uint32_t any = __reduce_or_sync(0xFFFFFFFFu, route_here ? f : 0u);
+            while (any) {
+              const int i = __ffs(any) - 1;
+              any &= any - 1;
+              const uint32_t m = __reduce_or_sync(0xFFFFFFFFu, (route_here && ((f >> i) & 1u)) ? axbit : 0u);
+              if (lane == 0) atomicOr(p.ring + warp_ring_off + (size_t)(s0 + j * 32 + i) * W, m);
+            }
+          } else if (route_here) {
+            uint32_t g = f;
+            while (g) {
+              const int i = __ffs(g) - 1;
+              g &= g - 1;
               atomicOr(p.ring + ring_off + (size_t)(s0 + j * 32 + i) * W, axbit);
             }
-          } else if (kind == RK_OUTPUT) {
-            while (f) {
-              const int i = __ffs(f) - 1;
-              f &= f - 1;
-              atomicAdd(p.counts + (size_t)(s0 + j * 32 + i) * p.C + cls, 1);
+          }
+          if (has_output) {
+            // output bus: one add per (sample, class) present among the lanes
+            const bool out = kind == RK_OUTPUT;
+            uint32_t any = __reduce_or_sync(0xFFFFFFFFu, out ? f : 0u);
+            while (any) {
+              const int i = __ffs(any) - 1;
+              any &= any - 1;
+              const bool fl = out && ((f >> i) & 1u);
+              const uint32_t peers = __match_any_sync(0xFFFFFFFFu, fl ? cls : 0xFFFFFFFFu);
+              if (fl && lane == __ffs(peers) - 1)
+                atomicAdd(p.counts + (size_t)(s0 + j * 32 + i) * p.C + cls, (int)__popc(peers));
             }
           }
           if (p.raster || exporting) {
@@ -378,9 +401,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       }
       tc::fence_before();
       __syncwarp();
-      if (lane == 0 && (ew == 0 || ew == 7)) stamp(p, k, ew == 0 ? 9 : 11);
+      if (lane == 0) stamp(p, k, 8 + ew);
       if (lane == 0) ptx::mbar_arrive(&bars[ACCEMPTY0 + a]);
-      if (lane == 0 && (ew == 0 || ew == 7)) stamp(p, k, ew == 0 ? 12 : 13);
     }
   }
   tc::fence_before();
@@ -398,6 +420,7 @@ cudaError_t launch_tick_tc(ranc_ctx* ctx, TickParams p) {
   const Compiled& n = ctx->net;
   p.ST = NT;
   p.route = (const uint2*)ctx->d_route_tc.p;
+  p.wflags = (const uint8_t*)ctx->d_wflags_tc.p;
   p.runs = (const int2*)ctx->d_runs.p;
   p.nruns = (const int32_t*)ctx->d_nruns.p;
   p.rmax = n.rmax;
@@ -420,11 +443,10 @@ cudaError_t launch_tick_tc(ranc_ctx* ctx, TickParams p) {
     cudaStreamSynchronize(ctx->stream);
     const unsigned long long t0 = h[0];
     fprintf(stderr, "timeline t=%lld grid=%d (cycles rel. to producer start)\n", (long long)p.t, grid);
-    fprintf(stderr, "  k  prodW prodGo expFull expBempty expBfull mmaB mmaAccE mmaCommit epi0Acc epi0Done epi7Acc epi7Done epi0Arr epi7Arr\n");
+    fprintf(stderr, "  k  prodW prodGo expFull expBempty expBfull mmaB mmaAccE mmaCommit epiDone[ew=0..7]\n");
     for (int k = 0; k < 64; ++k) {
       fprintf(stderr, "%3d", k);
-      const int order[14] = {0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13};
-      for (int j : order) fprintf(stderr, " %8lld", h[k * 16 + j] ? (long long)(h[k * 16 + j] - t0) : -1LL);
+      for (int j = 0; j < 16; ++j) fprintf(stderr, " %8lld", h[k * 16 + j] ? (long long)(h[k * 16 + j] - t0) : -1LL);
       fprintf(stderr, "\n");
     }
   }
