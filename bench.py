@@ -35,7 +35,38 @@ sys.path.insert(0, ROOT)
 
 METRIC = "simulated core-ticks/sec & samples/sec, 512-core MNIST net, 1/2/4/8 B200"
 UNIT = "samples/s"
-ALG_BYTES_PER_CORE_TICK = 1088  # pot read+write 2*256*2 B + ring row read + clear 2*32 B
+
+
+def alg_bytes_per_core_tick(net):
+    """potentials read + written (int16) and the scheduler row due
+    now read + cleared; 1088 B at A = N = 256."""
+    return 2 * 2 * net.neurons + 2 * 4 * ((net.axons + 31) // 32)
+
+
+# name -> (builder(S) -> (net, inputs), default S, sharding at N > 1)
+def _vmm(variant):
+    def b(S):
+        from workloads.gen import config4
+        return config4(variant, S=S)
+    return b
+
+
+def _cfg(i, **kw):
+    def b(S):
+        from workloads import gen
+        return getattr(gen, f"config{i}")(S=S, **kw)
+    return b
+
+
+WORKLOADS = {
+    "config3": (_cfg(3), 10000, "samples"),
+    "config1": (_cfg(1), 1, "samples"),
+    "config2": (_cfg(2), 1000, "samples"),
+    "vmm32": (_vmm("vmm32"), 1000, "samples"),
+    "vmm256": (_vmm("vmm256"), 1000, "samples"),
+    "vmm1024": (_vmm("vmm1024"), 1000, "samples"),
+    "config5": (_cfg(5), 64, "cores"),
+}
 
 
 def parse():
@@ -44,7 +75,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--samples", type=int, default=10000)
+    ap.add_argument("--workload", default="config3", choices=sorted(WORKLOADS))
+    ap.add_argument("--samples", type=int, default=0, help="samples (0 = the workload's default)")
     ap.add_argument("--tile", type=int, default=0)
     ap.add_argument("--kernel", default="auto", choices=["auto", "popc", "tc"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -154,16 +186,18 @@ def host_cores():
 
 
 # ----------------------------------------------------------------------------
-def build_workload(S):
-    from workloads.gen import config3
-    net, inp = config3(S=S)
-    return net, inp
+def build_workload(args):
+    builder, S0, mode = WORKLOADS[args.workload]
+    if not args.samples:
+        args.samples = S0
+    net, inp = builder(args.samples)
+    return net, inp, mode
 
 
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    net, inp = build_workload(args.samples)
+    net, inp, _ = build_workload(args)
     T = net.meta["T"]
     cores = max(1, min(host_cores(), 32))
     n = args.cpu_samples or 2 * cores
@@ -178,14 +212,16 @@ def run_reference(args, rank, world):
     per_core = statistics.median([x[2] for x in vals])
     G = net.G
     line = {
-        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+        "impl": "reference",
+        "metric": METRIC if args.workload == "config3" else f"simulated core-ticks/sec & samples/sec, {net.name}",
+        "value": v, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "i64", "data": "synthetic",
-        "config": {"workload": "config3-mnist-512c", "samples": args.samples, "ticks": T, "cores": G,
+        "config": {"workload": net.name, "samples": args.samples, "ticks": T, "cores": G,
                    "step": f"oracle on {n} of the {args.samples} samples"},
         "core_ticks_per_s": v * G * T,
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
-                         "sample": f"{n} samples of config 3 (19 ticks each) per step over {cores} processes",
+                         "sample": f"{n} samples of {net.name} ({T} ticks each) per step over {cores} processes",
                          "per_core_value": per_core},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -204,10 +240,12 @@ def run_ours(args, rank, world, local):
         dist.barrier()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    net, inp_all = build_workload(args.samples)
+    net, inp_all, mode = build_workload(args)
     T = net.meta["T"]
+    from paper_2404_16208_b200 import SHARD_CORES, SHARD_SAMPLES
     from paper_2404_16208_b200.dist import init_comm, shard_range
-    lo, hi = shard_range(args.samples, world, rank)
+    core_sharded = mode == "cores" and world > 1
+    lo, hi = (0, args.samples) if core_sharded else shard_range(args.samples, world, rank)
     inp = inp_all.slice(lo, hi)
     stream = torch.cuda.Stream(device=dev)
     sim = Simulator(net, device=local, stream=stream)
@@ -215,7 +253,7 @@ def run_ours(args, rank, world, local):
         sim.set_option(OPT_SAMPLE_TILE, args.tile)
     sim.set_option(OPT_KERNEL, {"auto": 0, "popc": 1, "tc": 2}[args.kernel])
     if world > 1:
-        init_comm(sim, world, rank)
+        init_comm(sim, world, rank, mode=SHARD_CORES if core_sharded else SHARD_SAMPLES)
     sim.load_inputs(inp)
 
     def barrier():
@@ -251,6 +289,7 @@ def run_ours(args, rank, world, local):
     ms_step = ms / args.steps
     samples_s = args.samples / (ms_step / 1e3)
     core_ticks_s = samples_s * net.G * T
+    G_loc = sim.info()["cores_local"]
 
     # ---- end-to-end through the public API, host buffers --------------------
     pinned = torch.empty(inp.line_bits.size, dtype=torch.int32, pin_memory=True)
@@ -259,16 +298,17 @@ def run_ours(args, rank, world, local):
     hinp = Inputs(inp.num_samples, inp.num_input_ticks,
                   pinned.numpy().view(np.uint32).reshape(inp.line_bits.shape), inp.first_sample)
     counts = np.zeros((hi - lo, net.num_classes), np.int32)
+    gather_n = args.samples
     for _ in range(max(1, args.warmup)):
         sim.load_inputs(hinp).run(T).outputs(counts)
         if world > 1:
-            sim.gather_outputs(args.samples, 0, rank)
+            sim.gather_outputs(gather_n, 0, rank)
     barrier()
     t0 = time.perf_counter()
     for _ in range(args.steps):
         sim.load_inputs(hinp).run(T).outputs(counts)
         if world > 1:
-            sim.gather_outputs(args.samples, 0, rank)
+            sim.gather_outputs(gather_n, 0, rank)
     torch.cuda.synchronize(dev)
     e2e_s = time.perf_counter() - t0
     t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
@@ -282,16 +322,22 @@ def run_ours(args, rank, world, local):
             os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
         hbm = peaks.get("hbm_gbs", 6650.0)
         S_local = hi - lo
-        alg_bytes = ALG_BYTES_PER_CORE_TICK * net.G * S_local
+        bpt = alg_bytes_per_core_tick(net)
+        alg_bytes = bpt * G_loc * S_local
         achieved = alg_bytes / (tick_ms / 1e3) / 1e9
         info = sim.info()
+        state_gb = (2 * net.neurons * net.G + 4 * info["ring_rows"] * info["ring_words"] * net.G) * args.samples / 1e9
         line = {
-            "metric": METRIC, "value": samples_s, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "metric": METRIC if args.workload == "config3" else f"simulated core-ticks/sec & samples/sec, {net.name}",
+            "value": samples_s, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "i32", "data": "synthetic",
-            "config": {"workload": "config3-mnist-512c", "samples": args.samples, "ticks": T, "cores": net.G,
-                       "axons": net.axons, "neurons": net.neurons, "parallelism": f"sample-sharded dp{world}",
-                       "l2": "state (potentials 2.6 GB + rings 0.33 GB) exceeds the 126 MB L2; no flush needed",
+            "config": {"workload": net.name, "samples": args.samples, "ticks": T, "cores": net.G,
+                       "axons": net.axons, "neurons": net.neurons,
+                       "parallelism": f"core-sharded x{world} (row bands, per-tick NCCL exchange)" if core_sharded
+                       else f"sample-sharded dp{world}",
+                       "l2": (f"state {state_gb:.2f} GB exceeds the 126 MB L2; no flush needed" if state_gb > 0.126
+                              else f"state {state_gb * 1e3:.1f} MB fits in L2 (latency-bound workload)"),
                        "sample_tile": info["sample_tile"], "pieces": info["pieces"],
                        "kernel": "tcgen05 kind::i8" if info["kernel"] == 2 else "popcount"},
             "core_ticks_per_s": core_ticks_s,
@@ -300,7 +346,7 @@ def run_ours(args, rank, world, local):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": None,
                          "kernel": "tick_tc_kernel" if info["kernel"] == 2 else "tick_popc_kernel",
-                         "note": f"{ALG_BYTES_PER_CORE_TICK} B/core-tick x {net.G} cores x {S_local} samples per "
+                         "note": f"{bpt} B/core-tick x {G_loc} cores x {S_local} samples per "
                                  "launch / mean launch time (CUDA events on the launch stream); peak = "
                                  "MEASURED_PEAKS.json hbm_gbs"},
             "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(inp.line_bits.nbytes),
@@ -309,10 +355,10 @@ def run_ours(args, rank, world, local):
         }
         if not args.no_cpu_baseline and world == 1:
             cores = max(1, min(host_cores(), 32))
-            n = args.cpu_samples or 2 * cores
+            n = args.cpu_samples or min(args.samples, 2 * cores)
             v, wall, per_core = time_oracle(net, inp_all, n, cores)
             line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
-                                    "sample": f"{n} of the {args.samples} samples, full 19 ticks, over {cores} "
+                                    "sample": f"{n} of the {args.samples} samples, full {T} ticks, over {cores} "
                                               f"processes ({wall:.1f} s)", "per_core_value": per_core}
         print(json.dumps(line), flush=True)
     sim.close()

@@ -302,9 +302,22 @@ ranc_status validate_and_compile(const ranc_network_desc* d, Compiled* out, std:
     o.rmax = rmax;
     o.runs.assign((size_t)G * rmax, int2{0, 0});
     o.nruns.assign(G, 0);
+    o.word_runs.assign((size_t)G * W, 0);
     for (int c = 0; c < G; ++c) {
       o.nruns[c] = (int32_t)runs[c].size();
       for (size_t r = 0; r < runs[c].size(); ++r) o.runs[(size_t)c * rmax + r] = runs[c][r];
+      // runs are sorted by start axon, so the runs overlapping word w are contiguous
+      for (int w = 0; w < W; ++w) {
+        int first = -1, cnt = 0;
+        for (size_t r = 0; r < runs[c].size(); ++r) {
+          const int ap = runs[c][r].x & 0xFFFF, len = runs[c][r].x >> 16;
+          if (ap < 32 * (w + 1) && ap + len > 32 * w) {
+            if (first < 0) first = (int)r;
+            ++cnt;
+          }
+        }
+        o.word_runs[(size_t)c * W + w] = first < 0 ? 0 : (first | (cnt << 16));
+      }
     }
     // route words with destination axons in the tensor-core order
     o.route_tc = o.route;
@@ -323,13 +336,14 @@ ranc_status validate_and_compile(const ranc_network_desc* d, Compiled* out, std:
     o.wflags_tc.assign((size_t)G * (Np / 32), 0);
     for (int c = 0; c < G; ++c)
       for (int w = 0; w < Np / 32; ++w) {
-        bool any = false, same = true;
+        bool any = false, same = true, ident = true;
         uint32_t key0 = 0, dc0 = 0;
         for (int l = 0; l < 32; ++l) {
           const int n = w * 32 + l;
           if (n >= N) break;
           const uint2 r = o.route_tc[(size_t)c * Np + n];
           if (route_kind(r.x) != RK_ROUTE) continue;
+          if ((route_axon(r.x) & 31u) != (uint32_t)l) ident = false;
           const uint32_t key = (route_axon(r.x) >> 5) | (route_delay(r.x) << 16);
           if (!any) {
             any = true;
@@ -339,7 +353,8 @@ ranc_status validate_and_compile(const ranc_network_desc* d, Compiled* out, std:
             same = false;
           }
         }
-        if (any && same) o.wflags_tc[(size_t)c * (Np / 32) + w] = 1;
+        // bit 0: block route; bit 1: lane l deposits bit l (bit transpose)
+        if (any && same) o.wflags_tc[(size_t)c * (Np / 32) + w] = ident ? 3 : 1;
       }
     // folded weights in the canonical operand layout (tc.h)
     const size_t per = (size_t)o.Npad * o.Kp;

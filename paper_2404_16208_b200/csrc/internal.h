@@ -52,6 +52,7 @@ struct TickParams {
   int64_t raster_t0;        // first tick of the raster buffer
   const uint8_t* wfold;     // tensor-core path: [G][Npad*Kp] canonical-layout int8
   const int2* runs;         // tensor-core path: input runs [G][rmax]
+  const int32_t* word_runs; // [G][W]: runs overlapping ring word w: first | count << 16
   const int32_t* nruns;     // [G]
   int32_t rmax;
   const uint32_t* xp;
@@ -71,6 +72,7 @@ struct TickParams {
   const uint8_t* exports;   // [G] core has a neuron routing to another rank
   unsigned long long* dbg;  // optional pipeline timeline (RANC_DEBUG_TIMELINE)
   const uint8_t* wflags;    // [G][Npad/32] per-warp flags (bit 0: block route), or nullptr
+  int32_t dbgflags;         // RANC_DEBUG_FLAGS (timing experiments only; results invalid when set)
 };
 
 // Host copy of the compiled network.
@@ -85,6 +87,7 @@ struct Compiled {
   std::vector<uint2> route_tc;  // route words with tensor-core destination axons
   std::vector<int2> runs;       // [G][rmax] input runs: x = a'start | len<<16, y = first line
   std::vector<int32_t> nruns;   // [G]
+  std::vector<int32_t> word_runs;  // [G][W] first run | count << 16 (runs overlapping word w)
   std::vector<uint8_t> wflags_tc;  // [G][Npad/32] bit 0: all routing neurons of the warp share one
                                    // (dest core, ring word, delay) in the tensor-core axon order
   int32_t rmax = 0;
@@ -120,7 +123,8 @@ struct ranc_ctx {
   std::string err;
   ranc::Compiled net;
   // device: compiled network
-  ranc::DevBuf d_xp, d_wp, d_pword, d_prm, d_route, d_inl, d_has_in, d_init, d_wfold, d_route_tc, d_runs, d_nruns, d_wflags_tc;
+  ranc::DevBuf d_xp, d_wp, d_pword, d_prm, d_route, d_inl, d_has_in, d_init, d_wfold, d_route_tc, d_runs, d_nruns, d_wflags_tc,
+      d_word_runs;
   int num_sms = 148;
   // device: state
   ranc::DevBuf d_pot, d_ring, d_counts, d_lines, d_stage, d_raster;

@@ -33,6 +33,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <type_traits>
 #include <cstdlib>
 
 #include "internal.h"
@@ -75,9 +76,25 @@ __host__ __device__ inline TcLayout tc_layout(int Np, int Kp, int W, int WIp) {
   return L;
 }
 
+__device__ __forceinline__ bool getenv_swap_h(const TickParams& p) { return (p.dbgflags & 16) != 0; }
+
 // optional per-tile timeline of CTA 0 (debug builds of a run: p.dbg != nullptr)
 __device__ __forceinline__ void stamp(const TickParams& p, int k, int slot) {
   if (p.dbg && blockIdx.x == 0 && k < 64) p.dbg[k * 16 + slot] = (unsigned long long)clock64();
+}
+
+// 32x32 bit transpose across a warp: lane l holds row l (bit i = entry (l, i));
+// returns row `lane` of the transpose (bit l = entry (l, lane)).
+__device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
+  const uint32_t masks[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+  for (int st = 0; st < 5; ++st) {
+    const int j = 16 >> st;
+    const uint32_t M = masks[st];
+    const uint32_t o = __shfl_xor_sync(0xFFFFFFFFu, x, j);
+    x = (lane & j) ? (((o >> j) & M) | (x & ~M)) : ((x & M) | ((o & M) << j));
+  }
+  return x;
 }
 
 __device__ __forceinline__ void named_sync(int id, int n) {
@@ -107,7 +124,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
   const uint32_t tcols = acc_stride * NA;
   const int cur = (int)(p.t & p.rp_mask);
 
-  if (warp == 1) tc::alloc(tmem_holder, tcols < 32 ? 32 : tcols);
+  // role warps (debug flag 32 swaps the producer and MMA warps)
+  const int prod_warp = (p.dbgflags & 32) ? 1 : 0, mma_warp = 1 - prod_warp;
+  if (warp == mma_warp) tc::alloc(tmem_holder, tcols < 32 ? 32 : tcols);
   if (threadIdx.x == 0) {
     for (int i = 0; i < NS; ++i) {
       ptx::mbar_init(&bars[FULL0 + i], 1);
@@ -128,54 +147,60 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
   tc::fence_after();
   const uint32_t tmem = *tmem_holder;
 
-  if (warp == 0) {
+  if (warp == prod_warp) {
     // ------------------------------------------------------------ producer (TMA)
-    if (lane == 0) {
-      int prev_core = -1, jw = -1;
-      for (int k = 0; k < nwork; ++k) {
-        const int idx = lo + k, cl = idx / nT, tile = idx - cl * nT, c = p.c_lo + cl;
-        const int s = k % NS, u = k / NS;
-        if (c != prev_core) {
-          ++jw;
-          if (jw > 0) ptx::mbar_wait(&bars[WFREE], (jw - 1) & 1);
+    // the whole warp walks the work list (convergent waits); lane 0 issues
+    int prev_core = -1, jw = -1;
+    for (int k = 0; k < nwork; ++k) {
+      const int idx = lo + k, cl = idx / nT, tile = idx - cl * nT, c = p.c_lo + cl;
+      const int s = k % NS, u = k / NS;
+      if (c != prev_core) {
+        ++jw;
+        if (jw > 0) ptx::mbar_wait_sleep(&bars[WFREE], (jw - 1) & 1, 2000);
+        if (lane == 0) {
           const uint32_t wb = (uint32_t)Np * Kp;
           ptx::mbar_arrive_expect_tx(&bars[WFULL], wb);
           ptx::bulk_g2s(w_s, p.wfold + (size_t)c * wb, wb, &bars[WFULL]);
-          prev_core = c;
         }
-        stamp(p, k, 0);
-        ptx::mbar_wait(&bars[SEMPTY0 + s], (u & 1) ^ 1);
+        prev_core = c;
+      }
+      if (lane == 0) stamp(p, k, 0);
+      ptx::mbar_wait_sleep(&bars[SEMPTY0 + s], (u & 1) ^ 1, 2000);
+      if (lane == 0) {
         stamp(p, k, 1);
         uint8_t* st = smem + L.stage + s * L.stage_bytes;
         const int s0 = tile * NT;
         const bool inject = p.t < p.T_in && p.nruns[c] > 0;
         const uint32_t ring_bytes = (uint32_t)NT * W * 4, line_bytes = inject ? (uint32_t)NT * WIp * 4 : 0u;
         ptx::mbar_arrive_expect_tx(&bars[FULL0 + s], ring_bytes + line_bytes);
-        ptx::bulk_g2s(st + L.raw, p.ring + (((size_t)cur * p.G_loc + cl) * p.Sr + s0) * W, ring_bytes, &bars[FULL0 + s]);
+        ptx::bulk_g2s(st + L.raw, p.ring + (((size_t)cur * p.G_loc + cl) * p.Sr + s0) * W, ring_bytes,
+                      &bars[FULL0 + s]);
         if (inject)
           ptx::bulk_g2s(st + L.lines, p.lines + ((size_t)p.t * p.Sr + s0) * WIp, line_bytes, &bars[FULL0 + s]);
       }
+      __syncwarp();
     }
-  } else if (warp == 1) {
+  } else if (warp == mma_warp) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      const uint32_t id = tc::idesc_i8(128, NT);
-      const uint32_t sbo = (uint32_t)Kp * 8;
-      int prev_core = -1, jw = -1;
-      for (int k = 0; k < nwork; ++k) {
-        const int idx = lo + k, c = idx / nT;
-        const int s = k % NS, u = k / NS;
-        const int a = k % NA, ua = k / NA;
-        if (c != prev_core) {
-          ++jw;
-          ptx::mbar_wait(&bars[WFULL], jw & 1);
-          prev_core = c;
-        }
-        ptx::mbar_wait(&bars[BFULL0 + s], u & 1);
-        stamp(p, k, 5);
-        ptx::mbar_wait(&bars[ACCEMPTY0 + a], (ua & 1) ^ 1);
+    // convergent warp loop; one elected thread issues the tcgen05 operations
+    const uint32_t id = tc::idesc_i8(128, NT);
+    const uint32_t sbo = (uint32_t)Kp * 8;
+    int prev_core = -1, jw = -1;
+    for (int k = 0; k < nwork; ++k) {
+      const int idx = lo + k, c = idx / nT;
+      const int s = k % NS, u = k / NS;
+      const int a = k % NA, ua = k / NA;
+      if (c != prev_core) {
+        ++jw;
+        ptx::mbar_wait_sleep(&bars[WFULL], jw & 1, 2000);
+        prev_core = c;
+      }
+      ptx::mbar_wait_sleep(&bars[BFULL0 + s], u & 1, 2000);
+      if (lane == 0) stamp(p, k, 5);
+      ptx::mbar_wait_sleep(&bars[ACCEMPTY0 + a], (ua & 1) ^ 1, 2000);
+      tc::fence_after();
+      if (lane == 0) {
         stamp(p, k, 6);
-        tc::fence_after();
         const uint8_t* b_s = smem + L.stage + s * L.stage_bytes + L.b;
         const uint32_t acc = tmem + a * acc_stride;
         for (int hh = 0; hh < Mh; ++hh)
@@ -190,13 +215,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
         const int next_core = (k + 1 < nwork) ? (lo + k + 1) / nT : -1;
         if (next_core != c) tc::commit(&bars[WFREE]);
       }
+      __syncwarp();
     }
-    __syncwarp();
   } else if (warp < kFirstEpi) {
     // ------------------------------------------------------------ spike stage
     const int et = threadIdx.x - 32 * kFirstExp;
     const int K16 = Kp >> 4;
-    const bool fast = (kExpThreads % K16) == 0;
     for (int k = 0; k < nwork; ++k) {
       const int idx = lo + k, cl = idx / nT, tile = idx - cl * nT, c = p.c_lo + cl;
       const int s = k % NS, u = k / NS;
@@ -206,37 +230,45 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       const uint32_t* lines = reinterpret_cast<const uint32_t*>(st + L.lines);
       // a1: the scheduler rows due now were staged by the producer (TMA);
       // clear them in global memory (free again for spikes due at t + Rp)
-      ptx::mbar_wait(&bars[FULL0 + s], u & 1);
+      ptx::mbar_wait_sleep(&bars[FULL0 + s], u & 1, 2000);
       if (et == 0) stamp(p, k, 2);
       uint32_t* row = p.ring + (((size_t)cur * p.G_loc + cl) * p.Sr + s0) * W;
       for (int i = et; i < ns * W; i += kExpThreads) row[i] = 0u;
-      // a2: external inputs, one contiguous run of lines -> axons per item
+      // a2: external inputs.  Thread <-> (sample, ring word): OR in the line
+      // runs overlapping that word (no atomics: every word has one owner)
       if (p.t < p.T_in && p.nruns[c] > 0) {
-        const int nr = p.nruns[c];
         const int2* runs = p.runs + (size_t)c * p.rmax;
-        for (int i = et; i < ns * nr; i += kExpThreads) {
-          const int sm = i / nr, r = i - sm * nr;
-          const int2 rn = runs[r];
-          const int ap = rn.x & 0xFFFF, len = rn.x >> 16, ln = rn.y;
+        const int32_t* wr = p.word_runs + (size_t)c * W;
+        for (int i = et; i < ns * W; i += kExpThreads) {
+          const int sm = i / W, w = i - sm * W;
+          const int32_t fr = __ldg(wr + w);
+          const int r0 = fr & 0xFFFF, nrw = fr >> 16;
+          if (!nrw) continue;
           const uint32_t* lr = lines + sm * WIp;
-          const int lw = ln >> 5, lb = ln & 31;
-          uint32_t x = lr[lw] >> lb;
-          if (lb + len > 32) x |= lr[lw + 1] << (32 - lb);
-          if (len < 32) x &= (1u << len) - 1u;
-          if (x) {
-            const int aw = ap >> 5, ab = ap & 31;
-            atomicOr(&raw[sm * W + aw], x << ab);
-            if (ab + len > 32) atomicOr(&raw[sm * W + aw + 1], x >> (32 - ab));
+          uint32_t acc = 0u;
+          for (int r = r0; r < r0 + nrw; ++r) {
+            const int2 rn = __ldg(runs + r);
+            const int ap = rn.x & 0xFFFF, len = rn.x >> 16, ln = rn.y;
+            const int lw = ln >> 5, lb = ln & 31;
+            uint32_t x = lr[lw] >> lb;
+            if (lb + len > 32) x |= lr[lw + 1] << (32 - lb);
+            if (len < 32) x &= (1u << len) - 1u;
+            const int off = ap - 32 * w;   // bit position of the run inside word w
+            acc |= off >= 0 ? (x << off) : (x >> (-off));
           }
+          raw[sm * W + w] |= acc;
         }
       }
       named_sync(2, kExpThreads);
       // bits -> 0/1 bytes, canonical K-major operand (rows = samples);
-      // samples >= ns of a tail tile get no spikes
-      ptx::mbar_wait(&bars[BEMPTY0 + s], (u & 1) ^ 1);
+      // samples >= ns of a tail tile get no spikes.  Lanes take consecutive
+      // samples so each 8-lane phase of the 16-byte stores fills one core
+      // matrix (bank-conflict free).
+      ptx::mbar_wait_sleep(&bars[BEMPTY0 + s], (u & 1) ^ 1, 2000);
       if (et == 0) stamp(p, k, 3);
       uint8_t* b_s = st + L.b;
-      auto expand = [&](int sm, int k16) {
+      for (int i = et; i < NT * K16; i += kExpThreads) {
+        const int sm = i % NT, k16 = i / NT;
         uint32_t bits = 0u;
         if (sm < ns) {
           const uint32_t wv = raw[sm * W + (k16 >> 1)];
@@ -248,12 +280,6 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
         v.z = tc::nib2bytes((bits >> 8) & 15u);
         v.w = tc::nib2bytes((bits >> 12) & 15u);
         *reinterpret_cast<uint4*>(b_s + tc::operand_offset(sm, k16 * 16, Kp)) = v;
-      };
-      if (fast) {
-        const int k16 = et % K16, step = kExpThreads / K16;
-        for (int sm = et / K16; sm < NT; sm += step) expand(sm, k16);
-      } else {
-        for (int i = et; i < NT * K16; i += kExpThreads) expand(i / K16, i % K16);
       }
       ptx::fence_proxy_async_smem();
       named_sync(2, kExpThreads);
@@ -266,17 +292,25 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
   } else {
     // ------------------------------------------------------------ epilogue
     const int ew = warp - kFirstEpi;
-    const int h = ew >> 2, q = warp & 3;   // TMEM lane quarter = warp % 4
+    const int q = warp & 3;                // TMEM lane quarter = warp % 4
+    const int h = (getenv_swap_h(p) && Mh > 1) ? ((ew >> 2) ^ 1) : (ew >> 2);
     const int n = h * 128 + q * 32 + lane;
     const bool active = h < Mh;
     const bool valid = active && n < p.N;
     int prev_core = -1;
-    int leak = 0, pth = 0, nth = 0, rst = 0, init = 0, bf = 0, bn = 0, linmask = 0;
+    int leak = 0, pth = 0, nth = 0, rst = 0, init = 0, bf = 0, bn = 0, linmul = 0;
     uint32_t kind = RK_NONE, cls = 0, axbit = 0;
-    bool route_here = false, exporting = false, block_route = false, has_output = false;
+    bool route_here = false, exporting = false, block_route = false, block_identity = false, has_output = false,
+         need_fired = true;
     size_t ring_off = 0, warp_ring_off = 0;
     uint4 pnext[NT / 8];
     const bool load = active && !p.fresh;
+    if (p.fresh) {
+      // first tick after a reset: every potential starts at its initial value
+      // (the per-neuron init is set when the core is entered, see below)
+#pragma unroll
+      for (int i = 0; i < NT / 8; ++i) pnext[i] = make_uint4(0u, 0u, 0u, 0u);
+    }
     if (load && nwork > 0) {
       const int c0 = lo / nT;
       const uint4* src = pot_row(p, c0, lo - c0 * nT, nT, n);
@@ -291,8 +325,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       // tile); each chunk is refilled with the next tile's as soon as it is used
       const bool pf = load && k + 1 < nwork;
       const uint4* nsrc = pot_row(p, (idx + 1) / nT, (idx + 1) % nT, nT, n);
-      ptx::mbar_wait(&bars[ACCFULL0 + a], ua & 1);
-
+      ptx::mbar_wait_sleep(&bars[ACCFULL0 + a], ua & 1, 500);
+      if (lane == 0 && (ew == 0 || ew == 2)) stamp(p, k, ew == 0 ? 8 : 12);
       tc::fence_after();
       if (active) {
         if (c != prev_core) {
@@ -300,10 +334,15 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
           const uint2 rt = p.route[(size_t)c * Np + n];
           leak = prm.x; pth = prm.y; nth = prm.z; rst = prm.w;
           init = p.init[(size_t)c * Np + n];
+          if (p.fresh) {
+            const uint32_t ii = ((uint32_t)init & 0xFFFFu) * 0x10001u;
+#pragma unroll
+            for (int i = 0; i < NT / 8; ++i) pnext[i] = make_uint4(ii, ii, ii, ii);
+          }
           kind = valid ? route_kind(rt.x) : RK_NONE;
           const bool lin = route_lin(rt.x);
-          // nv = fire ? (v & linmask) + bf : neg ? (v & linmask) + bn : v
-          linmask = lin ? -1 : 0;
+          // nv = fire ? v*linmul + bf : neg ? v*linmul + bn : v
+          linmul = lin ? 1 : 0;
           bf = lin ? -pth : rst;
           bn = lin ? -nth : -rst;
           cls = rt.y;
@@ -315,10 +354,13 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
           route_here = kind == RK_ROUTE && dloc < (uint32_t)p.G_loc;
           ring_off = (((size_t)slot * p.G_loc + dloc) * p.Sr) * W + (ax >> 5);
           exporting = p.fired && p.exports[c];
-          block_route = p.wflags && (p.wflags[(size_t)c * (Np >> 5) + (n >> 5)] & 1u);
+          const uint32_t wf = p.wflags ? p.wflags[(size_t)c * (Np >> 5) + (n >> 5)] : 0u;
+          block_route = wf & 1u;
+          block_identity = (wf & 3u) == 3u;
           const uint32_t rmask = __ballot_sync(0xFFFFFFFFu, route_here);
           warp_ring_off = rmask ? __shfl_sync(0xFFFFFFFFu, ring_off, __ffs(rmask) - 1) : 0;
           has_output = __any_sync(0xFFFFFFFFu, kind == RK_OUTPUT);
+          need_fired = __any_sync(0xFFFFFFFFu, kind != RK_NONE) || p.raster || exporting;
           prev_core = c;
         }
         uint4* dst = const_cast<uint4*>(pot_row(p, cl, tile, nT, n));
@@ -328,36 +370,54 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
           uint32_t acc[32];
           tc::ld32(acc_addr + j * 32, acc);
           tc::wait_ld();
+          if (lane == 0 && (ew == 0 || ew == 2)) stamp(p, k, (ew == 0 ? 9 : 13) + j);
+          // a4: leak / thresholds / reset per sample.  ALU-pipe bound, so kept
+          // to ~10 ALU ops + 1 IMAD: reset value r = v*lin + (fire ? bf : bn)
           uint32_t fired = 0u;
+          uint32_t outw[16];
+          auto lif = [&](auto need_t) {
+            constexpr bool NEED = decltype(need_t)::value;  // fired bits are consumed
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const uint4 v4 = pnext[j * 4 + (i >> 3)];
-            const uint32_t w32 = ((i >> 1) & 3) == 0 ? v4.x : ((i >> 1) & 3) == 1 ? v4.y : ((i >> 1) & 3) == 2 ? v4.z : v4.w;
-            const int pot = p.fresh ? init : (int)(int16_t)((i & 1) ? (w32 >> 16) : (w32 & 0xFFFFu));
-            const int v = pot + (int)acc[i] + leak;
-            const bool fire = v >= pth;
-            const bool neg = v < nth;
-            const int r = (v & linmask) + (fire ? bf : bn);
-            int nv = (fire || neg) ? r : v;
-            nv = min(max(nv, p.pot_lo), p.pot_hi);
-            acc[i] = (uint32_t)nv & 0xFFFFu;
-            fired |= (fire ? 1u : 0u) << i;
-          }
-          if (pf) {
+            for (int i = 0; i < 32; ++i) {
+              const uint4 v4 = pnext[j * 4 + (i >> 3)];
+              const uint32_t w32 =
+                  ((i >> 1) & 3) == 0 ? v4.x : ((i >> 1) & 3) == 1 ? v4.y : ((i >> 1) & 3) == 2 ? v4.z : v4.w;
+              const int pot = (i & 1) ? ((int)w32 >> 16) : ((int)(w32 << 16) >> 16);
+              const int v = pot + (int)acc[i] + leak;
+              const bool fire = v >= pth;
+              const bool chg = fire || v < nth;
+              const int r = v * linmul + (fire ? bf : bn);
+              int nv = chg ? r : v;
+              nv = min(max(nv, p.pot_lo), p.pot_hi);
+              if (i & 1) outw[i >> 1] = __byte_perm(outw[i >> 1], (uint32_t)nv, 0x5410u);
+              else outw[i >> 1] = (uint32_t)nv;
+              if (NEED && fire) fired |= 1u << i;
+            }
+          };
+          if (need_fired) lif(std::true_type{});
+          else lif(std::false_type{});
+          if (pf && !(p.dbgflags & 4)) {
 #pragma unroll
             for (int cc = 0; cc < 4; ++cc) pnext[j * 4 + cc] = nsrc[j * 4 + cc];
           }
+          if (!(p.dbgflags & 8)) {
 #pragma unroll
-          for (int cc = 0; cc < 4; ++cc)
-            dst[j * 4 + cc] = make_uint4(acc[8 * cc + 0] | (acc[8 * cc + 1] << 16), acc[8 * cc + 2] | (acc[8 * cc + 3] << 16),
-                                         acc[8 * cc + 4] | (acc[8 * cc + 5] << 16), acc[8 * cc + 6] | (acc[8 * cc + 7] << 16));
+            for (int cc = 0; cc < 4; ++cc)
+              dst[j * 4 + cc] = make_uint4(outw[4 * cc + 0], outw[4 * cc + 1], outw[4 * cc + 2], outw[4 * cc + 3]);
+          }
           // a5 / a6: route or count the spikes of real samples
           const int lim = ns - j * 32;
           uint32_t f = lim >= 32 ? fired : (lim > 0 ? fired & ((1u << lim) - 1u) : 0u);
-          if (block_route) {
-            // every routing lane of this warp targets the same ring word:
-            // one OR-reduced 32-bit deposit per sample instead of one atomic
-            // per spike (idempotent OR, G11)
+          if (block_identity) {
+            // every routing lane l of this warp deposits bit l of one ring
+            // word: a 32x32 bit transpose turns the per-lane sample masks into
+            // per-sample deposit words, one RED per (sample, word) issued by
+            // the lane of that sample (idempotent OR, G11)
+            const uint32_t m = transpose32(route_here ? f : 0u, lane);
+            if (m) atomicOr(p.ring + warp_ring_off + (size_t)(s0 + j * 32 + lane) * W, m);
+          } else if (block_route) {
+            // every routing lane targets the same ring word: one OR-reduced
+            // deposit per sample
             uint32_t any = __reduce_or_sync(0xFFFFFFFFu, route_here ? f : 0u);
             while (any) {
               const int i = __ffs(any) - 1;
@@ -387,27 +447,25 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
             }
           }
           if (p.raster || exporting) {
-            const uint32_t fv = valid ? fired : 0u;
-            for (int i = 0; i < 32 && i < lim; ++i) {
-              const uint32_t m = __ballot_sync(0xFFFFFFFFu, (fv >> i) & 1u);
-              if (lane == 0 && (n >> 5) < p.Wn) {
-                const int sg = s0 + j * 32 + i;
-                if (p.raster) p.raster[(((size_t)(p.t - p.raster_t0) * p.S + sg) * p.G_loc + cl) * p.Wn + (n >> 5)] = m;
-                if (exporting) p.fired[((size_t)cl * p.Sr + sg) * p.Wn + (n >> 5)] = m;
-              }
+            // lane i receives the fired word (32 neurons) of sample i
+            const uint32_t m = transpose32(valid ? fired : 0u, lane);
+            if (lane < lim && (n >> 5) < p.Wn) {
+              const int sg = s0 + j * 32 + lane;
+              if (p.raster) p.raster[(((size_t)(p.t - p.raster_t0) * p.S + sg) * p.G_loc + cl) * p.Wn + (n >> 5)] = m;
+              if (exporting) p.fired[((size_t)cl * p.Sr + sg) * p.Wn + (n >> 5)] = m;
             }
           }
         }
       }
       tc::fence_before();
       __syncwarp();
-      if (lane == 0) stamp(p, k, 8 + ew);
+      if (lane == 0 && (ew == 0 || ew == 2)) stamp(p, k, ew == 0 ? 11 : 15);
       if (lane == 0) ptx::mbar_arrive(&bars[ACCEMPTY0 + a]);
     }
   }
   tc::fence_before();
   __syncthreads();
-  if (warp == 1) tc::dealloc(tmem, tcols < 32 ? 32 : tcols);
+  if (warp == mma_warp) tc::dealloc(tmem, tcols < 32 ? 32 : tcols);
 }
 
 }  // namespace
@@ -422,6 +480,7 @@ cudaError_t launch_tick_tc(ranc_ctx* ctx, TickParams p) {
   p.route = (const uint2*)ctx->d_route_tc.p;
   p.wflags = (const uint8_t*)ctx->d_wflags_tc.p;
   p.runs = (const int2*)ctx->d_runs.p;
+  p.word_runs = (const int32_t*)ctx->d_word_runs.p;
   p.nruns = (const int32_t*)ctx->d_nruns.p;
   p.rmax = n.rmax;
   const int64_t total = (int64_t)ctx->G_loc * ((ctx->S + NT - 1) / NT);
@@ -443,7 +502,7 @@ cudaError_t launch_tick_tc(ranc_ctx* ctx, TickParams p) {
     cudaStreamSynchronize(ctx->stream);
     const unsigned long long t0 = h[0];
     fprintf(stderr, "timeline t=%lld grid=%d (cycles rel. to producer start)\n", (long long)p.t, grid);
-    fprintf(stderr, "  k  prodW prodGo expFull expBempty expBfull mmaB mmaAccE mmaCommit epiDone[ew=0..7]\n");
+    fprintf(stderr, "  k  prodW prodGo expFull expBempty expBfull mmaB mmaAccE mmaCommit | ew0: acc ld0 ld1 done | ew2: acc ld0 ld1 done\n");
     for (int k = 0; k < 64; ++k) {
       fprintf(stderr, "%3d", k);
       for (int j = 0; j < 16; ++j) fprintf(stderr, " %8lld", h[k * 16 + j] ? (long long)(h[k * 16 + j] - t0) : -1LL);

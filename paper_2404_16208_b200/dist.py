@@ -18,12 +18,12 @@ def shard_range(S: int, world: int, rank: int) -> tuple[int, int]:
     return lo, lo + base + (1 if rank < rem else 0)
 
 
-def init_comm(sim, world: int, rank: int, group=None):
+def init_comm(sim, world: int, rank: int, group=None, mode: int = 0):
     """Join the NCCL communicator of libranc: rank 0 makes the unique id and
-    torch.distributed broadcasts it."""
+    torch.distributed broadcasts it.  mode: SHARD_SAMPLES (0) or SHARD_CORES (1)."""
     import torch.distributed as dist
     from .sim import Simulator
     uid = [Simulator.unique_id() if rank == 0 else None]
     dist.broadcast_object_list(uid, src=0, group=group)
-    sim.comm_init(uid[0], world, rank)
+    sim.comm_init(uid[0], world, rank, mode)
     return uid[0]
