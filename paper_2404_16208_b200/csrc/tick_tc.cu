@@ -56,14 +56,16 @@ enum Bar { FULL0 = 0, SEMPTY0 = 4, BFULL0 = 8, BEMPTY0 = 12, ACCFULL0 = 16, ACCE
            NBARS = 26 };
 
 struct TcLayout {
-  uint32_t w, stage, b, raw, lines, stage_bytes, total;
+  uint32_t w, runs, stage, b, raw, lines, stage_bytes, total;
 };
 
 // WIp: input-line row words (multiple of 4)
-__host__ __device__ inline TcLayout tc_layout(int Np, int Kp, int W, int WIp) {
+__host__ __device__ inline TcLayout tc_layout(int Np, int Kp, int W, int WIp, int rmax) {
   TcLayout L;
   L.w = 1024;
   uint32_t o = L.w + (uint32_t)Np * Kp;
+  L.runs = o;                                 // int2 [rmax] + int32 [W] of the current core
+  o += (uint32_t)rmax * 8 + (uint32_t)W * 4;
   L.stage = (o + 1023) & ~1023u;
   uint32_t q = 0;
   L.b = q;     q += (uint32_t)NT * Kp;       // spikes as 0/1 bytes, canonical layout
@@ -110,7 +112,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + 8 * NBARS);
   const int Np = p.Npad, Kp = p.Kp, W = p.W, WIp = p.WIp;
-  const TcLayout L = tc_layout(Np, Kp, W, WIp);
+  const TcLayout L = tc_layout(Np, Kp, W, WIp, p.rmax);
   uint8_t* w_s = smem + L.w;
   const int Mh = Np >> 7;
   const int nT = (p.S + NT - 1) / NT;
@@ -220,6 +222,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
   } else if (warp < kFirstEpi) {
     // ------------------------------------------------------------ spike stage
     const int et = threadIdx.x - 32 * kFirstExp;
+    int runs_core = -1;
     const int K16 = Kp >> 4;
     for (int k = 0; k < nwork; ++k) {
       const int idx = lo + k, cl = idx / nT, tile = idx - cl * nT, c = p.c_lo + cl;
@@ -234,20 +237,29 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       if (et == 0) stamp(p, k, 2);
       uint32_t* row = p.ring + (((size_t)cur * p.G_loc + cl) * p.Sr + s0) * W;
       for (int i = et; i < ns * W; i += kExpThreads) row[i] = 0u;
+      if (et == 0) stamp(p, k, 12);
       // a2: external inputs.  Thread <-> (sample, ring word): OR in the line
       // runs overlapping that word (no atomics: every word has one owner)
       if (p.t < p.T_in && p.nruns[c] > 0) {
-        const int2* runs = p.runs + (size_t)c * p.rmax;
-        const int32_t* wr = p.word_runs + (size_t)c * W;
+        // the core's input runs live in shared memory while its tiles are processed
+        int2* runs = reinterpret_cast<int2*>(smem + L.runs);
+        int32_t* wr = reinterpret_cast<int32_t*>(smem + L.runs + (uint32_t)p.rmax * 8);
+        if (c != runs_core) {
+          named_sync(2, kExpThreads);
+          for (int i = et; i < p.nruns[c]; i += kExpThreads) runs[i] = p.runs[(size_t)c * p.rmax + i];
+          for (int i = et; i < W; i += kExpThreads) wr[i] = p.word_runs[(size_t)c * W + i];
+          named_sync(2, kExpThreads);
+          runs_core = c;
+        }
         for (int i = et; i < ns * W; i += kExpThreads) {
           const int sm = i / W, w = i - sm * W;
-          const int32_t fr = __ldg(wr + w);
+          const int32_t fr = wr[w];
           const int r0 = fr & 0xFFFF, nrw = fr >> 16;
           if (!nrw) continue;
           const uint32_t* lr = lines + sm * WIp;
           uint32_t acc = 0u;
           for (int r = r0; r < r0 + nrw; ++r) {
-            const int2 rn = __ldg(runs + r);
+            const int2 rn = runs[r];
             const int ap = rn.x & 0xFFFF, len = rn.x >> 16, ln = rn.y;
             const int lw = ln >> 5, lb = ln & 31;
             uint32_t x = lr[lw] >> lb;
@@ -259,7 +271,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
           raw[sm * W + w] |= acc;
         }
       }
+      if (et == 0) stamp(p, k, 13);
       named_sync(2, kExpThreads);
+      if (et == 0) stamp(p, k, 14);
       // bits -> 0/1 bytes, canonical K-major operand (rows = samples);
       // samples >= ns of a tail tile get no spikes.  Lanes take consecutive
       // samples so each 8-lane phase of the 16-byte stores fills one core
@@ -281,6 +295,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
         v.w = tc::nib2bytes((bits >> 12) & 15u);
         *reinterpret_cast<uint4*>(b_s + tc::operand_offset(sm, k16 * 16, Kp)) = v;
       }
+      if (et == 0) stamp(p, k, 15);
       ptx::fence_proxy_async_smem();
       named_sync(2, kExpThreads);
       if (et == 0) {
@@ -326,7 +341,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       const bool pf = load && k + 1 < nwork;
       const uint4* nsrc = pot_row(p, (idx + 1) / nT, (idx + 1) % nT, nT, n);
       ptx::mbar_wait_sleep(&bars[ACCFULL0 + a], ua & 1, 500);
-      if (lane == 0 && (ew == 0 || ew == 2)) stamp(p, k, ew == 0 ? 8 : 12);
+      if (lane == 0 && ew == 0) stamp(p, k, 8);
       tc::fence_after();
       if (active) {
         if (c != prev_core) {
@@ -370,7 +385,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
           uint32_t acc[32];
           tc::ld32(acc_addr + j * 32, acc);
           tc::wait_ld();
-          if (lane == 0 && (ew == 0 || ew == 2)) stamp(p, k, (ew == 0 ? 9 : 13) + j);
+          if (lane == 0 && ew == 0) stamp(p, k, 9 + j);
           // a4: leak / thresholds / reset per sample.  ALU-pipe bound, so kept
           // to ~10 ALU ops + 1 IMAD: reset value r = v*lin + (fire ? bf : bn)
           uint32_t fired = 0u;
@@ -459,7 +474,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       }
       tc::fence_before();
       __syncwarp();
-      if (lane == 0 && (ew == 0 || ew == 2)) stamp(p, k, ew == 0 ? 11 : 15);
+      if (lane == 0 && ew == 0) stamp(p, k, 11);
       if (lane == 0) ptx::mbar_arrive(&bars[ACCEMPTY0 + a]);
     }
   }
@@ -472,7 +487,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
 
 int tc_tile() { return NT; }
 
-size_t tc_smem_bytes(const Compiled& n) { return tc_layout(n.Npad, n.Kp, n.W, n.WIp).total; }
+size_t tc_smem_bytes(const Compiled& n) { return tc_layout(n.Npad, n.Kp, n.W, n.WIp, n.rmax).total; }
 
 cudaError_t launch_tick_tc(ranc_ctx* ctx, TickParams p) {
   const Compiled& n = ctx->net;
@@ -485,7 +500,7 @@ cudaError_t launch_tick_tc(ranc_ctx* ctx, TickParams p) {
   p.rmax = n.rmax;
   const int64_t total = (int64_t)ctx->G_loc * ((ctx->S + NT - 1) / NT);
   const int grid = (int)std::min<int64_t>(total, ctx->num_sms);
-  const size_t smem = tc_layout(n.Npad, n.Kp, n.W, n.WIp).total;
+  const size_t smem = tc_layout(n.Npad, n.Kp, n.W, n.WIp, n.rmax).total;
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(tick_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -502,7 +517,7 @@ cudaError_t launch_tick_tc(ranc_ctx* ctx, TickParams p) {
     cudaStreamSynchronize(ctx->stream);
     const unsigned long long t0 = h[0];
     fprintf(stderr, "timeline t=%lld grid=%d (cycles rel. to producer start)\n", (long long)p.t, grid);
-    fprintf(stderr, "  k  prodW prodGo expFull expBempty expBfull mmaB mmaAccE mmaCommit | ew0: acc ld0 ld1 done | ew2: acc ld0 ld1 done\n");
+    fprintf(stderr, "  k  prodW prodGo expFull expBempty expBfull mmaB mmaAccE mmaCommit | ew0: acc ld0 ld1 done | exp: cleared injected synced expanded\n");
     for (int k = 0; k < 64; ++k) {
       fprintf(stderr, "%3d", k);
       for (int j = 0; j < 16; ++j) fprintf(stderr, " %8lld", h[k * 16 + j] ? (long long)(h[k * 16 + j] - t0) : -1LL);

@@ -10,4 +10,4 @@ from workloads.gen import config3  # noqa: E402
 net, inp = config3(S=int(sys.argv[1]) if len(sys.argv) > 1 else 10000)
 sim = Simulator(net)
 sim.load_inputs(inp)
-sim.run(3)
+sim.run(int(sys.argv[2]) if len(sys.argv) > 2 else 3)
