@@ -36,9 +36,9 @@ bool fits(int64_t v, int bits) {
   return v >= lo && v <= hi;
 }
 
-// canonical K-major core-matrix layout of a tensor-core operand (tc.h)
-inline uint32_t tc_operand_offset(uint32_t r, uint32_t k, uint32_t Kp) {
-  return (r >> 3) * (Kp * 8) + (k >> 4) * 128 + (r & 7) * 16 + (k & 15);
+// canonical K-major core-matrix layout of a tensor-core operand with R rows (tc.h)
+inline uint32_t tc_operand_offset(uint32_t r, uint32_t k, uint32_t R) {
+  return (k >> 4) * (R * 16) + (r >> 3) * 128 + (r & 7) * 16 + (k & 15);
 }
 
 ranc_status fail(std::string* err, ranc_status s, const std::string& m) {
@@ -368,7 +368,7 @@ ranc_status validate_and_compile(const ranc_network_desc* d, Compiled* out, std:
         const uint32_t* src = d->crossbar + cn * W;
         for (int a = 0; a < A; ++a)
           if ((src[a >> 5] >> (a & 31)) & 1u)
-            dst[tc_operand_offset((uint32_t)n, (uint32_t)inv[a], (uint32_t)o.Kp)] = (int8_t)d->weight[cn * K + ty[a]];
+            dst[tc_operand_offset((uint32_t)n, (uint32_t)inv[a], (uint32_t)o.Npad)] = (int8_t)d->weight[cn * K + ty[a]];
       }
     }
   }

@@ -4,11 +4,15 @@
 //
 // Operand layout: K-major, no swizzle ("interleaved" canonical layout).  A
 // core matrix is 8 rows x 16 bytes stored contiguously (128 B).  For an
-// operand with R rows and Kp bytes per row the byte offset of (r, k) is
-//   (r / 8) * SBO + (k / 16) * 128 + (r % 8) * 16 + (k % 16),  SBO = Kp * 8,
-// i.e. LBO (offset between the two 16-byte K chunks of one MMA) = 128 B and
-// SBO (offset between 8-row groups) = Kp * 8 B.  One kind::i8 MMA consumes
-// K = 32 bytes, so K-step kk starts at byte kk * 256.
+// operand with R rows the core matrices of one 16-byte K chunk are stored
+// back to back (R*16 bytes), chunk after chunk:
+//   offset(r, k) = (k / 16) * (R * 16) + (r / 8) * 128 + (r % 8) * 16 + (k % 16)
+// so SBO (offset between 8-row groups) = 128 B and LBO (offset between the
+// two 16-byte K chunks one MMA reads) = R*16 B.  The 16 core matrices the
+// tensor core reads for one K chunk of a 128-row operand are then one
+// contiguous 2 KB block (bank-conflict free; with the rows of a chunk spread
+// SBO = Kp*8 apart instead, every core matrix hits the same banks).  One
+// kind::i8 MMA consumes K = 32 bytes, so K-step kk starts at byte kk * 2*R*16.
 #pragma once
 #include <stdint.h>
 
@@ -17,8 +21,8 @@
 namespace ranc {
 namespace tc {
 
-__host__ __device__ constexpr uint32_t operand_offset(uint32_t r, uint32_t k, uint32_t Kp) {
-  return (r >> 3) * (Kp * 8) + (k >> 4) * 128 + (r & 7) * 16 + (k & 15);
+__host__ __device__ constexpr uint32_t operand_offset(uint32_t r, uint32_t k, uint32_t R) {
+  return (k >> 4) * (R * 16) + (r >> 3) * 128 + (r & 7) * 16 + (k & 15);
 }
 
 // shared-memory matrix descriptor (tcgen05 "version 1" format)

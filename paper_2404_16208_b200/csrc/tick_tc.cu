@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
     // ------------------------------------------------------------ MMA issuer
     // convergent warp loop; one elected thread issues the tcgen05 operations
     const uint32_t id = tc::idesc_i8(128, NT);
-    const uint32_t sbo = (uint32_t)Kp * 8;
+    const uint32_t lbo_a = (uint32_t)Np * 16, lbo_b = (uint32_t)NT * 16;   // tc.h layout
     int prev_core = -1, jw = -1;
     for (int k = 0; k < nwork; ++k) {
       const int idx = lo + k, c = idx / nT;
@@ -207,8 +207,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
         const uint32_t acc = tmem + a * acc_stride;
         for (int hh = 0; hh < Mh; ++hh)
           for (int kk = 0; kk < Kp / 32; ++kk) {
-            const uint64_t ad = tc::smem_desc(ptx::smem_u32(w_s + hh * 128 * Kp + kk * 256), 128, sbo);
-            const uint64_t bd = tc::smem_desc(ptx::smem_u32(b_s + kk * 256), 128, sbo);
+            const uint64_t ad = tc::smem_desc(ptx::smem_u32(w_s + hh * 2048 + kk * 2 * lbo_a), lbo_a, 128);
+            const uint64_t bd = tc::smem_desc(ptx::smem_u32(b_s + kk * 2 * lbo_b), lbo_b, 128);
             tc::mma_i8(acc + hh * NT, ad, bd, id, kk > 0 ? 1u : 0u);
           }
         tc::commit(&bars[BEMPTY0 + s]);
@@ -293,7 +293,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
         v.y = tc::nib2bytes((bits >> 4) & 15u);
         v.z = tc::nib2bytes((bits >> 8) & 15u);
         v.w = tc::nib2bytes((bits >> 12) & 15u);
-        *reinterpret_cast<uint4*>(b_s + tc::operand_offset(sm, k16 * 16, Kp)) = v;
+        *reinterpret_cast<uint4*>(b_s + tc::operand_offset(sm, k16 * 16, NT)) = v;
       }
       if (et == 0) stamp(p, k, 15);
       ptx::fence_proxy_async_smem();

@@ -24,11 +24,11 @@ __global__ void probe(const int8_t* A, const uint8_t* B, int32_t* D) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   for (int i = tid; i < MH * 128 * K; i += blockDim.x) {
     int r = i / K, k = i % K;
-    As[tc::operand_offset(r, k, K)] = (uint8_t)A[i];
+    As[tc::operand_offset(r, k, MH * 128)] = (uint8_t)A[i];
   }
   for (int i = tid; i < N * K; i += blockDim.x) {
     int r = i / K, k = i % K;
-    Bs[tc::operand_offset(r, k, K)] = B[i];
+    Bs[tc::operand_offset(r, k, N)] = B[i];
   }
   if (warp == 0) tc::alloc(&tbase, 512);
   if (tid == 0) {
@@ -44,8 +44,8 @@ __global__ void probe(const int8_t* A, const uint8_t* B, int32_t* D) {
     const uint32_t id = tc::idesc_i8(128, N);
     for (int h = 0; h < MH; ++h)
       for (int kk = 0; kk < K / 32; ++kk) {
-        uint64_t ad = tc::smem_desc(ptx::smem_u32(As + h * 128 * K + kk * 256), 128, K * 8);
-        uint64_t bd = tc::smem_desc(ptx::smem_u32(Bs + kk * 256), 128, K * 8);
+        uint64_t ad = tc::smem_desc(ptx::smem_u32(As + h * 2048 + kk * 2 * (MH * 128 * 16)), MH * 128 * 16, 128);
+        uint64_t bd = tc::smem_desc(ptx::smem_u32(Bs + kk * 2 * (N * 16)), N * 16, 128);
         tc::mma_i8(t0 + h * N, ad, bd, id, kk > 0);
       }
     tc::commit(&bar);
@@ -107,10 +107,63 @@ int run() {
   return bad != 0;
 }
 
+int rate_main();
+
 int main() {
+  rate_main();
   int f = 0;
   f |= run<64>();
   f |= run<128>();
   f |= run<256>();
   return f;
+}
+
+// ---- throughput of back-to-back MMAs for two operand layouts ---------------
+__global__ void mma_rate(int iters, uint32_t lbo_a, uint32_t sbo_a, uint32_t stepA, uint32_t lbo_b, uint32_t sbo_b,
+                         uint32_t stepB, unsigned long long* out) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase;
+  const int warp = threadIdx.x >> 5;
+  if (warp == 0) tc::alloc(&tbase, 512);
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(&bar, 1);
+    ptx::fence_mbar_init();
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  if (threadIdx.x == 0) {
+    const uint32_t id = tc::idesc_i8(128, 64);
+    unsigned long long t0 = clock64();
+    for (int it = 0; it < iters; ++it)
+      for (int kk = 0; kk < 8; ++kk) {
+        uint64_t ad = tc::smem_desc(ptx::smem_u32(sm + kk * stepA), lbo_a, sbo_a);
+        uint64_t bd = tc::smem_desc(ptx::smem_u32(sm + 65536 + kk * stepB), lbo_b, sbo_b);
+        tc::mma_i8(tbase, ad, bd, id, kk > 0);
+      }
+    tc::commit(&bar);
+    ptx::mbar_wait(&bar, 0);
+    out[0] = clock64() - t0;
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) tc::dealloc(tbase, 512);
+}
+
+int rate_main() {
+  unsigned long long* d;
+  cudaMalloc(&d, 16);
+  cudaFuncSetAttribute(mma_rate, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  const int iters = 2000;
+  // old: rows of a K chunk spread (LBO=128, SBO=K*8); new: chunk-contiguous (LBO=R*16, SBO=128)
+  const uint32_t cfg[2][6] = {{128, 256 * 8, 256, 128, 256 * 8, 256}, {256 * 16, 128, 2 * 256 * 16, 64 * 16, 128, 2 * 64 * 16}};
+  for (int v = 0; v < 2; ++v) {
+    mma_rate<<<1, 128, 100 * 1024>>>(iters, cfg[v][0], cfg[v][1], cfg[v][2], cfg[v][3], cfg[v][4], cfg[v][5], d);
+    unsigned long long h = 0;
+    cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+    printf("layout %s: %.1f cycles per MMA (M=128,N=64,K=32 i8)\n", v ? "chunk-contiguous" : "row-spread",
+           (double)h / (iters * 8));
+  }
+  return 0;
 }
