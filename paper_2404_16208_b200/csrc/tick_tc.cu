@@ -51,12 +51,13 @@ constexpr int kEpiWarps = 8;
 constexpr int kFirstExp = 2, kFirstEpi = 2 + kExpWarps;
 constexpr int kThreadsTC = 32 * (2 + kExpWarps + kEpiWarps);  // 448
 constexpr int kExpThreads = 32 * kExpWarps;
+static_assert(kExpThreads == 2 * NT, "spike stage maps thread -> (sample, 16-bit half)");
 
 enum Bar { FULL0 = 0, SEMPTY0 = 4, BFULL0 = 8, BEMPTY0 = 12, ACCFULL0 = 16, ACCEMPTY0 = 20, WFULL = 24, WFREE = 25,
            NBARS = 26 };
 
 struct TcLayout {
-  uint32_t w, runs, stage, b, raw, lines, stage_bytes, total;
+  uint32_t w, runs, lut, stage, b, raw, lines, stage_bytes, total;
 };
 
 // WIp: input-line row words (multiple of 4)
@@ -66,6 +67,9 @@ __host__ __device__ inline TcLayout tc_layout(int Np, int Kp, int W, int WIp, in
   uint32_t o = L.w + (uint32_t)Np * Kp;
   L.runs = o;                                 // int2 [rmax] + int32 [W] of the current core
   o += (uint32_t)rmax * 8 + (uint32_t)W * 4;
+  o = (o + 15) & ~15u;
+  L.lut = o;                                  // uint2 [256]: byte -> eight 0/1 bytes
+  o += 256 * 8;
   L.stage = (o + 1023) & ~1023u;
   uint32_t q = 0;
   L.b = q;     q += (uint32_t)NT * Kp;       // spikes as 0/1 bytes, canonical layout
@@ -223,7 +227,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
     // ------------------------------------------------------------ spike stage
     const int et = threadIdx.x - 32 * kFirstExp;
     int runs_core = -1;
-    const int K16 = Kp >> 4;
+    uint2* lut = reinterpret_cast<uint2*>(smem + L.lut);
+    for (int b = et; b < 256; b += kExpThreads)
+      lut[b] = make_uint2(tc::nib2bytes(b & 15u), tc::nib2bytes(b >> 4));
+    named_sync(2, kExpThreads);
     for (int k = 0; k < nwork; ++k) {
       const int idx = lo + k, cl = idx / nT, tile = idx - cl * nT, c = p.c_lo + cl;
       const int s = k % NS, u = k / NS;
@@ -233,7 +240,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       const uint32_t* lines = reinterpret_cast<const uint32_t*>(st + L.lines);
       // a1: the scheduler rows due now were staged by the producer (TMA);
       // clear them in global memory (free again for spikes due at t + Rp)
-      ptx::mbar_wait_sleep(&bars[FULL0 + s], u & 1, 2000);
+      ptx::mbar_wait(&bars[FULL0 + s], u & 1);
       if (et == 0) stamp(p, k, 2);
       uint32_t* row = p.ring + (((size_t)cur * p.G_loc + cl) * p.Sr + s0) * W;
       for (int i = et; i < ns * W; i += kExpThreads) row[i] = 0u;
@@ -251,24 +258,34 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
           named_sync(2, kExpThreads);
           runs_core = c;
         }
-        for (int i = et; i < ns * W; i += kExpThreads) {
-          const int sm = i / W, w = i - sm * W;
-          const int32_t fr = wr[w];
-          const int r0 = fr & 0xFFFF, nrw = fr >> 16;
-          if (!nrw) continue;
-          const uint32_t* lr = lines + sm * WIp;
-          uint32_t acc = 0u;
-          for (int r = r0; r < r0 + nrw; ++r) {
-            const int2 rn = runs[r];
-            const int ap = rn.x & 0xFFFF, len = rn.x >> 16, ln = rn.y;
-            const int lw = ln >> 5, lb = ln & 31;
-            uint32_t x = lr[lw] >> lb;
-            if (lb + len > 32) x |= lr[lw + 1] << (32 - lb);
-            if (len < 32) x &= (1u << len) - 1u;
-            const int off = ap - 32 * w;   // bit position of the run inside word w
-            acc |= off >= 0 ? (x << off) : (x >> (-off));
+        constexpr int B = 4;   // independent items in flight per thread
+        for (int base = et; base < ns * W; base += B * kExpThreads) {
+          uint32_t accs[B];
+#pragma unroll
+          for (int b = 0; b < B; ++b) {
+            const int i = base + b * kExpThreads;
+            accs[b] = 0u;
+            if (i >= ns * W) continue;
+            const int sm = i / W, w = i - sm * W;
+            const int32_t fr = wr[w];
+            const int r0 = fr & 0xFFFF, nrw = fr >> 16;
+            const uint32_t* lr = lines + sm * WIp;
+            for (int r = r0; r < r0 + nrw; ++r) {
+              const int2 rn = runs[r];
+              const int ap = rn.x & 0xFFFF, len = rn.x >> 16, ln = rn.y;
+              const int lw = ln >> 5, lb = ln & 31;
+              uint32_t x = lr[lw] >> lb;
+              if (lb + len > 32) x |= lr[lw + 1] << (32 - lb);
+              if (len < 32) x &= (1u << len) - 1u;
+              const int off = ap - 32 * w;   // bit position of the run inside word w
+              accs[b] |= off >= 0 ? (x << off) : (x >> (-off));
+            }
           }
-          raw[sm * W + w] |= acc;
+#pragma unroll
+          for (int b = 0; b < B; ++b) {
+            const int i = base + b * kExpThreads;
+            if (i < ns * W && accs[b]) raw[i] |= accs[b];
+          }
         }
       }
       if (et == 0) stamp(p, k, 13);
@@ -278,22 +295,25 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       // samples >= ns of a tail tile get no spikes.  Lanes take consecutive
       // samples so each 8-lane phase of the 16-byte stores fills one core
       // matrix (bank-conflict free).
-      ptx::mbar_wait_sleep(&bars[BEMPTY0 + s], (u & 1) ^ 1, 2000);
+      ptx::mbar_wait(&bars[BEMPTY0 + s], (u & 1) ^ 1);
       if (et == 0) stamp(p, k, 3);
       uint8_t* b_s = st + L.b;
-      for (int i = et; i < NT * K16; i += kExpThreads) {
-        const int sm = i % NT, k16 = i / NT;
-        uint32_t bits = 0u;
-        if (sm < ns) {
-          const uint32_t wv = raw[sm * W + (k16 >> 1)];
-          bits = (k16 & 1) ? (wv >> 16) : (wv & 0xFFFFu);
+      {
+        // thread <-> (sample sm, half hf): the 16-bit halves hf of the
+        // sample's W ring words become K chunks 2w+hf; lanes take consecutive
+        // samples so every 8-lane phase of the 16-byte stores fills one core
+        // matrix (bank-conflict free); bytes via a 256-entry table
+        const int sm = et % NT, hf = et / NT;   // kExpThreads == 2 * NT
+        const uint32_t* rrow = raw + sm * W;
+        const bool real = sm < ns;
+#pragma unroll 4
+        for (int w = 0; w < W; ++w) {
+          const uint32_t wv = real ? rrow[w] : 0u;
+          const uint32_t bits = hf ? (wv >> 16) : (wv & 0xFFFFu);
+          const uint2 lo = lut[bits & 0xFFu], hi = lut[bits >> 8];
+          *reinterpret_cast<uint4*>(b_s + tc::operand_offset(sm, (2 * w + hf) * 16, NT)) =
+              make_uint4(lo.x, lo.y, hi.x, hi.y);
         }
-        uint4 v;
-        v.x = tc::nib2bytes(bits & 15u);
-        v.y = tc::nib2bytes((bits >> 4) & 15u);
-        v.z = tc::nib2bytes((bits >> 8) & 15u);
-        v.w = tc::nib2bytes((bits >> 12) & 15u);
-        *reinterpret_cast<uint4*>(b_s + tc::operand_offset(sm, k16 * 16, NT)) = v;
       }
       if (et == 0) stamp(p, k, 15);
       ptx::fence_proxy_async_smem();
@@ -340,7 +360,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       // tile); each chunk is refilled with the next tile's as soon as it is used
       const bool pf = load && k + 1 < nwork;
       const uint4* nsrc = pot_row(p, (idx + 1) / nT, (idx + 1) % nT, nT, n);
-      ptx::mbar_wait_sleep(&bars[ACCFULL0 + a], ua & 1, 500);
+      ptx::mbar_wait(&bars[ACCFULL0 + a], ua & 1);
       if (lane == 0 && ew == 0) stamp(p, k, 8);
       tc::fence_after();
       if (active) {
