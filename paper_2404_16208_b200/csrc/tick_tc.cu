@@ -48,7 +48,10 @@ constexpr int NT = 64;                 // samples per tile (MMA N)
 constexpr int NS = 4;                  // spike-stage pipeline depth
 constexpr int kExpWarps = 4;
 constexpr int kEpiWarps = 8;
-constexpr int kFirstExp = 2, kFirstEpi = 2 + kExpWarps;
+// Warp ids: the SMSP issue arbiter prefers higher warp ids, and the epilogue
+// saturates the ALU pipe, so the spike stage (on the pipeline's critical
+// path) takes the highest ids: 0 producer, 1 MMA, 2..9 epilogue, 10..13 spike.
+constexpr int kFirstEpi = 2, kFirstExp = 2 + kEpiWarps;
 constexpr int kThreadsTC = 32 * (2 + kExpWarps + kEpiWarps);  // 448
 constexpr int kExpThreads = 32 * kExpWarps;
 static_assert(kExpThreads == 2 * NT, "spike stage maps thread -> (sample, 16-bit half)");
@@ -223,7 +226,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       }
       __syncwarp();
     }
-  } else if (warp < kFirstEpi) {
+  } else if (warp >= kFirstExp) {
     // ------------------------------------------------------------ spike stage
     const int et = threadIdx.x - 32 * kFirstExp;
     int runs_core = -1;
