@@ -383,7 +383,7 @@ ranc_status ranc_read_potentials(ranc_ctx* ctx, int32_t* pot, size_t n) {
       for (int j = 0; j < c.N; ++j)
         pot[((size_t)s * GL + g) * c.N + j] =
             ctx->kernel_active == RANC_KERNEL_TC
-                ? h[(((size_t)g * nT + s / NT) * c.Npad + j) * NT + s % NT]
+                ? h[(((size_t)g * nT + s / NT) * (NT / 8) + (s % NT) / 8) * c.Npad * 8 + (size_t)j * 8 + s % 8]
                 : h[((size_t)g * ctx->S + s) * c.Npad + j];
   return RANC_OK;
 }

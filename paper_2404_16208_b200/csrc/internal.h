@@ -13,7 +13,7 @@
 //     inl   i32 [G][A]         input line of permuted axon a' (-1 none)
 //   state (streamed every tick):
 //     pot   i16 [G][S][Npad]   membrane potentials (pb <= 16), popcount kernel;
-//           i16 [G][nT][Npad][NT] tile-blocked, tensor-core kernel (NT = 64)
+//           i16 [G][nT][NT/8][Npad][8] tile-blocked, tensor-core kernel (NT = 64)
 //     ring  u32 [Rp][G][Sr][W] scheduler rings, W = ceil(A/32) words per row,
 //                              Sr = S rounded up to 64 (TMA-aligned tiles),
 //                              slot of tick t = t & (Rp-1), Rp = next_pow2(D+1)

@@ -26,8 +26,8 @@
 //               (a5, a6)
 // A tick is one launch; the kernel boundary is the tick barrier (a7).
 //
-// Potential layout: tile-blocked [G][nT][Np][64] int16: a thread's 64 samples
-// of one neuron are 128 contiguous bytes.
+// Potential layout: tile-blocked [G][nT][8][Np][8] int16 (tile, 8-sample chunk,
+// neuron, sample in chunk): every 16-byte access of a warp is coalesced.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -110,8 +110,11 @@ __device__ __forceinline__ void named_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
-__device__ __forceinline__ const uint4* pot_row(const TickParams& p, int c, int tile, int nT, int n) {
-  return reinterpret_cast<const uint4*>(p.pot + (((size_t)c * nT + tile) * (size_t)p.Npad + n) * NT);
+// Potential tile layout [chunk q = s/8][neuron n][s%8] (int16): chunk q of
+// neuron n is the 16-byte uint4 at index q*Npad + n, so the 32 lanes (= 32
+// consecutive neurons) of a warp access 512 contiguous bytes per chunk.
+__device__ __forceinline__ uint4* pot_tile(const TickParams& p, int c, int tile, int nT, int n) {
+  return reinterpret_cast<uint4*>(p.pot + ((size_t)c * nT + tile) * (size_t)p.Npad * NT) + n;
 }
 
 __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams p) {
@@ -230,9 +233,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
     // ------------------------------------------------------------ spike stage
     const int et = threadIdx.x - 32 * kFirstExp;
     int runs_core = -1;
-    uint2* lut = reinterpret_cast<uint2*>(smem + L.lut);
-    for (int b = et; b < 256; b += kExpThreads)
-      lut[b] = make_uint2(tc::nib2bytes(b & 15u), tc::nib2bytes(b >> 4));
+    // nibble -> four 0/1 bytes; a 16-entry u32 table spans 16 distinct banks,
+    // so the lookups never conflict
+    uint32_t* lut = reinterpret_cast<uint32_t*>(smem + L.lut);
+    for (int b = et; b < 16; b += kExpThreads) lut[b] = tc::nib2bytes((uint32_t)b);
     named_sync(2, kExpThreads);
     for (int k = 0; k < nwork; ++k) {
       const int idx = lo + k, cl = idx / nT, tile = idx - cl * nT, c = p.c_lo + cl;
@@ -305,17 +309,26 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
         // thread <-> (sample sm, half hf): the 16-bit halves hf of the
         // sample's W ring words become K chunks 2w+hf; lanes take consecutive
         // samples so every 8-lane phase of the 16-byte stores fills one core
-        // matrix (bank-conflict free); bytes via a 256-entry table
+        // matrix (bank-conflict free); bytes via the nibble table
         const int sm = et % NT, hf = et / NT;   // kExpThreads == 2 * NT
         const uint32_t* rrow = raw + sm * W;
         const bool real = sm < ns;
-#pragma unroll 4
-        for (int w = 0; w < W; ++w) {
-          const uint32_t wv = real ? rrow[w] : 0u;
+        auto emit = [&](int w, uint32_t wv) {
           const uint32_t bits = hf ? (wv >> 16) : (wv & 0xFFFFu);
-          const uint2 lo = lut[bits & 0xFFu], hi = lut[bits >> 8];
           *reinterpret_cast<uint4*>(b_s + tc::operand_offset(sm, (2 * w + hf) * 16, NT)) =
-              make_uint4(lo.x, lo.y, hi.x, hi.y);
+              make_uint4(lut[bits & 15u], lut[(bits >> 4) & 15u], lut[(bits >> 8) & 15u], lut[bits >> 12]);
+        };
+        if ((W & 3) == 0) {
+          // 16-byte row loads: lanes 32 B apart -> at most 2-way bank conflicts
+          for (int w4 = 0; w4 < W; w4 += 4) {
+            const uint4 v = real ? *reinterpret_cast<const uint4*>(rrow + w4) : make_uint4(0u, 0u, 0u, 0u);
+            emit(w4 + 0, v.x);
+            emit(w4 + 1, v.y);
+            emit(w4 + 2, v.z);
+            emit(w4 + 3, v.w);
+          }
+        } else {
+          for (int w = 0; w < W; ++w) emit(w, real ? rrow[w] : 0u);
         }
       }
       if (et == 0) stamp(p, k, 15);
@@ -351,9 +364,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
     }
     if (load && nwork > 0) {
       const int c0 = lo / nT;
-      const uint4* src = pot_row(p, c0, lo - c0 * nT, nT, n);
+      const uint4* src = pot_tile(p, c0, lo - c0 * nT, nT, n);
 #pragma unroll
-      for (int i = 0; i < NT / 8; ++i) pnext[i] = src[i];
+      for (int i = 0; i < NT / 8; ++i) pnext[i] = src[(size_t)i * Np];
     }
     for (int k = 0; k < nwork; ++k) {
       const int idx = lo + k, cl = idx / nT, tile = idx - cl * nT, c = p.c_lo + cl;
@@ -362,7 +375,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       // pnext holds this tile's potentials (prefetched during the previous
       // tile); each chunk is refilled with the next tile's as soon as it is used
       const bool pf = load && k + 1 < nwork;
-      const uint4* nsrc = pot_row(p, (idx + 1) / nT, (idx + 1) % nT, nT, n);
+      const uint4* nsrc = pot_tile(p, (idx + 1) / nT, (idx + 1) % nT, nT, n);
       ptx::mbar_wait(&bars[ACCFULL0 + a], ua & 1);
       if (lane == 0 && ew == 0) stamp(p, k, 8);
       tc::fence_after();
@@ -401,7 +414,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
           need_fired = __any_sync(0xFFFFFFFFu, kind != RK_NONE) || p.raster || exporting;
           prev_core = c;
         }
-        uint4* dst = const_cast<uint4*>(pot_row(p, cl, tile, nT, n));
+        uint4* dst = pot_tile(p, cl, tile, nT, n);
         const uint32_t acc_addr = tmem + a * acc_stride + ((uint32_t)(q * 32) << 16) + h * NT;
 #pragma unroll
         for (int j = 0; j < NT / 32; ++j) {
@@ -436,12 +449,13 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
           else lif(std::false_type{});
           if (pf && !(p.dbgflags & 4)) {
 #pragma unroll
-            for (int cc = 0; cc < 4; ++cc) pnext[j * 4 + cc] = nsrc[j * 4 + cc];
+            for (int cc = 0; cc < 4; ++cc) pnext[j * 4 + cc] = nsrc[(size_t)(j * 4 + cc) * Np];
           }
           if (!(p.dbgflags & 8)) {
 #pragma unroll
             for (int cc = 0; cc < 4; ++cc)
-              dst[j * 4 + cc] = make_uint4(outw[4 * cc + 0], outw[4 * cc + 1], outw[4 * cc + 2], outw[4 * cc + 3]);
+              dst[(size_t)(j * 4 + cc) * Np] =
+                  make_uint4(outw[4 * cc + 0], outw[4 * cc + 1], outw[4 * cc + 2], outw[4 * cc + 3]);
           }
           // a5 / a6: route or count the spikes of real samples
           const int lim = ns - j * 32;
