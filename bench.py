@@ -147,24 +147,40 @@ class Clocks:
 # oracle timing (cpu_baseline and --impl reference)
 # ----------------------------------------------------------------------------
 def _oracle_worker(args):
-    idx, = args
+    idx, ticks = args
     from oracle.pyoracle import Oracle
     net, inp = _WORK["net"], _WORK["inp"]
     t0 = time.perf_counter()
-    Oracle(net, inp.subset(idx)).run(net.meta["T"])
+    Oracle(net, inp.subset(idx)).run(ticks)
     return time.perf_counter() - t0
 
 
 _WORK = {}
 
 
-def time_oracle(net, inp, n_samples, cores):
+ORACLE_CORE_TICK_BUDGET = 60000   # core-ticks per worker process (~10-20 s of serial oracle)
+
+
+def oracle_plan(net, n_samples, cores):
+    """Bound the oracle's work: all T ticks of n_samples samples when that fits
+    the per-core budget, else the first T' ticks (rate scaled to whole samples)."""
+    T = net.meta["T"]
+    per_worker = max(1, -(-n_samples // cores))
+    ticks = min(T, max(1, ORACLE_CORE_TICK_BUDGET // (net.G * per_worker)))
+    return ticks
+
+
+def time_oracle(net, inp, n_samples, cores, ticks=None):
     """Run the oracle on n_samples samples spread over `cores` worker
-    processes; returns (samples/s, wall seconds, per-core samples/s)."""
+    processes for `ticks` ticks (default: the workload's T); returns
+    (samples/s, wall seconds, per-core samples/s), a sample counting as all T
+    ticks (rate scaled by ticks/T when fewer ticks were run)."""
     import multiprocessing as mp
     from oracle import pyoracle
     pyoracle.build()
     _WORK["net"], _WORK["inp"] = net, inp
+    T = net.meta["T"]
+    ticks = ticks or T
     S = inp.num_samples
     pick = np.linspace(0, S - 1, n_samples).astype(int)
     chunks = [pick[i::cores] for i in range(cores)]
@@ -172,10 +188,11 @@ def time_oracle(net, inp, n_samples, cores):
     ctx = mp.get_context("fork")
     t0 = time.perf_counter()
     with ctx.Pool(len(chunks)) as pool:
-        per = pool.map(_oracle_worker, [(c,) for c in chunks])
+        per = pool.map(_oracle_worker, [(c, ticks) for c in chunks])
     wall = time.perf_counter() - t0
-    per_core = statistics.median([len(c) / p for c, p in zip(chunks, per)])
-    return n_samples / wall, wall, per_core
+    frac = ticks / T
+    per_core = statistics.median([len(c) * frac / p for c, p in zip(chunks, per)])
+    return n_samples * frac / wall, wall, per_core
 
 
 def host_cores():
@@ -200,12 +217,13 @@ def run_reference(args, rank, world):
     net, inp, _ = build_workload(args)
     T = net.meta["T"]
     cores = max(1, min(host_cores(), 32))
-    n = args.cpu_samples or 2 * cores
+    n = args.cpu_samples or min(args.samples, 2 * cores)
+    ticks = oracle_plan(net, n, cores)
     for _ in range(args.warmup):
-        time_oracle(net, inp, max(1, cores // 2), cores)
+        time_oracle(net, inp, max(1, cores // 2), cores, ticks)
     vals = []
     for _ in range(args.steps):
-        v, wall, per_core = time_oracle(net, inp, n, cores)
+        v, wall, per_core = time_oracle(net, inp, n, cores, ticks)
         vals.append((v, wall, per_core))
     v = statistics.median([x[0] for x in vals])
     wall = statistics.median([x[1] for x in vals])
@@ -218,10 +236,11 @@ def run_reference(args, rank, world):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "i64", "data": "synthetic",
         "config": {"workload": net.name, "samples": args.samples, "ticks": T, "cores": G,
-                   "step": f"oracle on {n} of the {args.samples} samples"},
+                   "step": f"oracle on {n} of the {args.samples} samples, {ticks} of {T} ticks"},
         "core_ticks_per_s": v * G * T,
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
-                         "sample": f"{n} samples of {net.name} ({T} ticks each) per step over {cores} processes",
+                         "sample": f"{n} samples of {net.name}, {ticks} of {T} ticks (rate scaled to whole "
+                                   f"samples), per step over {cores} processes",
                          "per_core_value": per_core},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -356,10 +375,12 @@ def run_ours(args, rank, world, local):
         if not args.no_cpu_baseline and world == 1:
             cores = max(1, min(host_cores(), 32))
             n = args.cpu_samples or min(args.samples, 2 * cores)
-            v, wall, per_core = time_oracle(net, inp_all, n, cores)
+            ticks = oracle_plan(net, n, cores)
+            v, wall, per_core = time_oracle(net, inp_all, n, cores, ticks)
             line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
-                                    "sample": f"{n} of the {args.samples} samples, full {T} ticks, over {cores} "
-                                              f"processes ({wall:.1f} s)", "per_core_value": per_core}
+                                    "sample": f"{n} of the {args.samples} samples, {ticks} of {T} ticks (rate scaled "
+                                              f"to whole samples), over {cores} processes ({wall:.1f} s)",
+                                    "per_core_value": per_core}
         print(json.dumps(line), flush=True)
     sim.close()
     if world > 1:

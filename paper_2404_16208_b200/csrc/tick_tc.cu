@@ -265,7 +265,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
           named_sync(2, kExpThreads);
           runs_core = c;
         }
-        constexpr int B = 4;   // independent items in flight per thread
+        constexpr int B = 2;   // independent items in flight per thread
         for (int base = et; base < ns * W; base += B * kExpThreads) {
           uint32_t accs[B];
 #pragma unroll
@@ -320,6 +320,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
         };
         if ((W & 3) == 0) {
           // 16-byte row loads: lanes 32 B apart -> at most 2-way bank conflicts
+#pragma unroll 1
           for (int w4 = 0; w4 < W; w4 += 4) {
             const uint4 v = real ? *reinterpret_cast<const uint4*>(rrow + w4) : make_uint4(0u, 0u, 0u, 0u);
             emit(w4 + 0, v.x);
@@ -328,6 +329,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
             emit(w4 + 3, v.w);
           }
         } else {
+#pragma unroll 1
           for (int w = 0; w < W; ++w) emit(w, real ? rrow[w] : 0u);
         }
       }
@@ -351,22 +353,26 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
     int prev_core = -1;
     int leak = 0, pth = 0, nth = 0, rst = 0, init = 0, bf = 0, bn = 0, linmul = 0;
     uint32_t kind = RK_NONE, cls = 0, axbit = 0;
-    bool route_here = false, exporting = false, block_route = false, block_identity = false, has_output = false,
-         need_fired = true;
+    bool route_here = false, exporting = false, block_route = false, block_identity = false, has_output = false;
     size_t ring_off = 0, warp_ring_off = 0;
-    uint4 pnext[NT / 8];
+    // Potentials of the tile being processed, two 32-sample chunks: `cur` is
+    // the chunk in work, `hold` the other one.  After a chunk is used its
+    // registers are refilled with the same chunk of the NEXT tile and the two
+    // are swapped, so one copy of the chunk code serves both chunks and the
+    // next tile is always prefetched (NT == 64).
+    static_assert(NT == 64, "two 32-sample chunks per tile");
+    uint4 cur[4], hold[4];
     const bool load = active && !p.fresh;
-    if (p.fresh) {
-      // first tick after a reset: every potential starts at its initial value
-      // (the per-neuron init is set when the core is entered, see below)
 #pragma unroll
-      for (int i = 0; i < NT / 8; ++i) pnext[i] = make_uint4(0u, 0u, 0u, 0u);
-    }
+    for (int i = 0; i < 4; ++i) cur[i] = hold[i] = make_uint4(0u, 0u, 0u, 0u);
     if (load && nwork > 0) {
       const int c0 = lo / nT;
       const uint4* src = pot_tile(p, c0, lo - c0 * nT, nT, n);
 #pragma unroll
-      for (int i = 0; i < NT / 8; ++i) pnext[i] = src[(size_t)i * Np];
+      for (int i = 0; i < 4; ++i) {
+        cur[i] = src[(size_t)i * Np];
+        hold[i] = src[(size_t)(4 + i) * Np];
+      }
     }
     for (int k = 0; k < nwork; ++k) {
       const int idx = lo + k, cl = idx / nT, tile = idx - cl * nT, c = p.c_lo + cl;
@@ -388,7 +394,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
           if (p.fresh) {
             const uint32_t ii = ((uint32_t)init & 0xFFFFu) * 0x10001u;
 #pragma unroll
-            for (int i = 0; i < NT / 8; ++i) pnext[i] = make_uint4(ii, ii, ii, ii);
+            for (int i = 0; i < 4; ++i) cur[i] = hold[i] = make_uint4(ii, ii, ii, ii);
           }
           kind = valid ? route_kind(rt.x) : RK_NONE;
           const bool lin = route_lin(rt.x);
@@ -411,12 +417,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
           const uint32_t rmask = __ballot_sync(0xFFFFFFFFu, route_here);
           warp_ring_off = rmask ? __shfl_sync(0xFFFFFFFFu, ring_off, __ffs(rmask) - 1) : 0;
           has_output = __any_sync(0xFFFFFFFFu, kind == RK_OUTPUT);
-          need_fired = __any_sync(0xFFFFFFFFu, kind != RK_NONE) || p.raster || exporting;
           prev_core = c;
         }
         uint4* dst = pot_tile(p, cl, tile, nT, n);
         const uint32_t acc_addr = tmem + a * acc_stride + ((uint32_t)(q * 32) << 16) + h * NT;
-#pragma unroll
+#pragma unroll 1
         for (int j = 0; j < NT / 32; ++j) {
           uint32_t acc[32];
           tc::ld32(acc_addr + j * 32, acc);
@@ -426,36 +431,38 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
           // to ~10 ALU ops + 1 IMAD: reset value r = v*lin + (fire ? bf : bn)
           uint32_t fired = 0u;
           uint32_t outw[16];
-          auto lif = [&](auto need_t) {
-            constexpr bool NEED = decltype(need_t)::value;  // fired bits are consumed
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              const uint4 v4 = pnext[j * 4 + (i >> 3)];
-              const uint32_t w32 =
-                  ((i >> 1) & 3) == 0 ? v4.x : ((i >> 1) & 3) == 1 ? v4.y : ((i >> 1) & 3) == 2 ? v4.z : v4.w;
-              const int pot = (i & 1) ? ((int)w32 >> 16) : ((int)(w32 << 16) >> 16);
-              const int v = pot + (int)acc[i] + leak;
-              const bool fire = v >= pth;
-              const bool chg = fire || v < nth;
-              const int r = v * linmul + (fire ? bf : bn);
-              int nv = chg ? r : v;
-              nv = min(max(nv, p.pot_lo), p.pot_hi);
-              if (i & 1) outw[i >> 1] = __byte_perm(outw[i >> 1], (uint32_t)nv, 0x5410u);
-              else outw[i >> 1] = (uint32_t)nv;
-              if (NEED && fire) fired |= 1u << i;
-            }
-          };
-          if (need_fired) lif(std::true_type{});
-          else lif(std::false_type{});
-          if (pf && !(p.dbgflags & 4)) {
-#pragma unroll
-            for (int cc = 0; cc < 4; ++cc) pnext[j * 4 + cc] = nsrc[(size_t)(j * 4 + cc) * Np];
+          for (int i = 0; i < 32; ++i) {
+            const uint4 v4 = cur[i >> 3];
+            const uint32_t w32 =
+                ((i >> 1) & 3) == 0 ? v4.x : ((i >> 1) & 3) == 1 ? v4.y : ((i >> 1) & 3) == 2 ? v4.z : v4.w;
+            const int pot = (i & 1) ? ((int)w32 >> 16) : ((int)(w32 << 16) >> 16);
+            const int v = pot + (int)acc[i] + leak;
+            const bool fire = v >= pth;
+            const bool chg = fire || v < nth;
+            const int r = v * linmul + (fire ? bf : bn);
+            int nv = chg ? r : v;
+            nv = min(max(nv, p.pot_lo), p.pot_hi);
+            if (i & 1) outw[i >> 1] = __byte_perm(outw[i >> 1], (uint32_t)nv, 0x5410u);
+            else outw[i >> 1] = (uint32_t)nv;
+            if (fire) fired |= 1u << i;
           }
           if (!(p.dbgflags & 8)) {
 #pragma unroll
             for (int cc = 0; cc < 4; ++cc)
               dst[(size_t)(j * 4 + cc) * Np] =
                   make_uint4(outw[4 * cc + 0], outw[4 * cc + 1], outw[4 * cc + 2], outw[4 * cc + 3]);
+          }
+          // refill with the next tile's chunk j, then bring the other chunk in
+          if (pf && !(p.dbgflags & 4)) {
+#pragma unroll
+            for (int cc = 0; cc < 4; ++cc) cur[cc] = nsrc[(size_t)(j * 4 + cc) * Np];
+          }
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc) {
+            const uint4 t = cur[cc];
+            cur[cc] = hold[cc];
+            hold[cc] = t;
           }
           // a5 / a6: route or count the spikes of real samples
           const int lim = ns - j * 32;
