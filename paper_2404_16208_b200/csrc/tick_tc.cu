@@ -60,7 +60,7 @@ enum Bar { FULL0 = 0, SEMPTY0 = 4, BFULL0 = 8, BEMPTY0 = 12, ACCFULL0 = 16, ACCE
            NBARS = 26 };
 
 struct TcLayout {
-  uint32_t w, runs, lut, stage, b, raw, lines, stage_bytes, total;
+  uint32_t w, runs, lut, potbuf, stage, b, raw, lines, stage_bytes, total;
 };
 
 // WIp: input-line row words (multiple of 4)
@@ -71,8 +71,11 @@ __host__ __device__ inline TcLayout tc_layout(int Np, int Kp, int W, int WIp, in
   L.runs = o;                                 // int2 [rmax] + int32 [W] of the current core
   o += (uint32_t)rmax * 8 + (uint32_t)W * 4;
   o = (o + 15) & ~15u;
-  L.lut = o;                                  // uint2 [256]: byte -> eight 0/1 bytes
+  L.lut = o;                                  // u32 [16]: nibble -> four 0/1 bytes
   o += 256 * 8;
+  o = (o + 127) & ~127u;
+  L.potbuf = o;                               // uint4 [NT/8][epilogue threads]: next tile's potentials
+  o += (NT / 8) * (32 * 8) * 16;
   L.stage = (o + 1023) & ~1023u;
   uint32_t q = 0;
   L.b = q;     q += (uint32_t)NT * Kp;       // spikes as 0/1 bytes, canonical layout
@@ -355,23 +358,25 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
     uint32_t kind = RK_NONE, cls = 0, axbit = 0;
     bool route_here = false, exporting = false, block_route = false, block_identity = false, has_output = false;
     size_t ring_off = 0, warp_ring_off = 0;
-    // Potentials of the tile being processed, two 32-sample chunks: `cur` is
-    // the chunk in work, `hold` the other one.  After a chunk is used its
-    // registers are refilled with the same chunk of the NEXT tile and the two
-    // are swapped, so one copy of the chunk code serves both chunks and the
-    // next tile is always prefetched (NT == 64).
+    // Potentials stream HBM -> shared memory with cp.async one tile ahead:
+    // potbuf[q][et] holds 16-byte chunk q (8 samples) of this thread's neuron.
+    // Chunk half j (q = 4j..4j+3) of the next tile is requested right after
+    // the same half of the current tile has been read out, so every load has
+    // about a tile of time to land; the per-thread commit groups are waited
+    // with cp.async.wait_group 1 (NT == 64: two halves).
     static_assert(NT == 64, "two 32-sample chunks per tile");
-    uint4 cur[4], hold[4];
+    uint4* pbuf = reinterpret_cast<uint4*>(smem + L.potbuf) + (threadIdx.x - 32 * kFirstEpi);
+    constexpr int PB = 32 * kEpiWarps;   // uint4 stride between chunks in potbuf
     const bool load = active && !p.fresh;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) cur[i] = hold[i] = make_uint4(0u, 0u, 0u, 0u);
+    uint4 initv = make_uint4(0u, 0u, 0u, 0u);
     if (load && nwork > 0) {
       const int c0 = lo / nT;
       const uint4* src = pot_tile(p, c0, lo - c0 * nT, nT, n);
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        cur[i] = src[(size_t)i * Np];
-        hold[i] = src[(size_t)(4 + i) * Np];
+      for (int hh = 0; hh < 2; ++hh) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) ptx::cp_async16(pbuf + (4 * hh + i) * PB, src + (size_t)(4 * hh + i) * Np);
+        ptx::cp_async_commit();
       }
     }
     for (int k = 0; k < nwork; ++k) {
@@ -393,8 +398,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
           init = p.init[(size_t)c * Np + n];
           if (p.fresh) {
             const uint32_t ii = ((uint32_t)init & 0xFFFFu) * 0x10001u;
-#pragma unroll
-            for (int i = 0; i < 4; ++i) cur[i] = hold[i] = make_uint4(ii, ii, ii, ii);
+            initv = make_uint4(ii, ii, ii, ii);
           }
           kind = valid ? route_kind(rt.x) : RK_NONE;
           const bool lin = route_lin(rt.x);
@@ -425,6 +429,21 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
         for (int j = 0; j < NT / 32; ++j) {
           uint32_t acc[32];
           tc::ld32(acc_addr + j * 32, acc);
+          uint4 cur[4];
+          if (load) {
+            ptx::cp_async_wait<1>();   // this half's group (issued a tile ago) has landed
+#pragma unroll
+            for (int i = 0; i < 4; ++i) cur[i] = pbuf[(4 * j + i) * PB];
+            // request the same half of the next tile into the slots just read
+            if (pf && !(p.dbgflags & 4)) {
+#pragma unroll
+              for (int i = 0; i < 4; ++i) ptx::cp_async16(pbuf + (4 * j + i) * PB, nsrc + (size_t)(4 * j + i) * Np);
+            }
+            ptx::cp_async_commit();   // (possibly empty) group: keeps the wait_group 1 accounting
+          } else {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) cur[i] = initv;
+          }
           tc::wait_ld();
           if (lane == 0 && ew == 0) stamp(p, k, 9 + j);
           // a4: leak / thresholds / reset per sample.  ALU-pipe bound, so kept
@@ -452,17 +471,6 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
             for (int cc = 0; cc < 4; ++cc)
               dst[(size_t)(j * 4 + cc) * Np] =
                   make_uint4(outw[4 * cc + 0], outw[4 * cc + 1], outw[4 * cc + 2], outw[4 * cc + 3]);
-          }
-          // refill with the next tile's chunk j, then bring the other chunk in
-          if (pf && !(p.dbgflags & 4)) {
-#pragma unroll
-            for (int cc = 0; cc < 4; ++cc) cur[cc] = nsrc[(size_t)(j * 4 + cc) * Np];
-          }
-#pragma unroll
-          for (int cc = 0; cc < 4; ++cc) {
-            const uint4 t = cur[cc];
-            cur[cc] = hold[cc];
-            hold[cc] = t;
           }
           // a5 / a6: route or count the spikes of real samples
           const int lim = ns - j * 32;
