@@ -167,10 +167,15 @@ ranc_status ranc_set_allocator(ranc_ctx* ctx, void* (*alloc)(size_t, void*),
                                void (*dealloc)(void*, void*), void* user);
 
 /* Tuning knobs (no effect on results).  RANC_OPT_SAMPLE_TILE: samples per CTA
- * of the tick kernel (default chosen from S).  RANC_OPT_USE_GRAPH: capture the
- * tick loop in a CUDA graph (1) or launch directly (0, default 1). */
+ * of the popcount tick kernel (default chosen from S).  RANC_OPT_INPUT_DECODE:
+ * tensor-core kernel only -- 1 (default): decode the input lines into per-core
+ * scheduler words once per ranc_load_inputs (Alg. 1 l.1, "input decode";
+ * T_in x input cores x S x ceil(A/32) x 4 bytes of device memory, skipped when
+ * that exceeds a quarter of the free memory); 0: gather the line runs every
+ * tick.  Takes effect at the next ranc_load_inputs / ranc_reset_state.
+ * RANC_OPT_KERNEL: 0 automatic, 1 popcount, 2 tensor core (see ranc_info.kernel). */
 #define RANC_OPT_SAMPLE_TILE 1
-#define RANC_OPT_USE_GRAPH 2
+#define RANC_OPT_INPUT_DECODE 2
 #define RANC_OPT_KERNEL 3
 ranc_status ranc_set_option(ranc_ctx* ctx, int option, int64_t value);
 

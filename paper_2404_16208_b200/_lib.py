@@ -17,7 +17,7 @@ STATUS = {0: "RANC_OK", 1: "RANC_E_ARG", 2: "RANC_E_CONFIG", 3: "RANC_E_BITWIDTH
 TRACE_SPIKE_RASTER = 1
 TRACE_OUTPUT_EVENTS = 2
 OPT_SAMPLE_TILE = 1
-OPT_USE_GRAPH = 2
+OPT_INPUT_DECODE = 2
 OPT_KERNEL = 3
 SHARD_SAMPLES = 0
 SHARD_CORES = 1

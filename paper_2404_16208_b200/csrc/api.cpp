@@ -95,8 +95,40 @@ void free_all(ranc_ctx* ctx) {
                     &ctx->d_has_in, &ctx->d_init, &ctx->d_wfold, &ctx->d_route_tc, &ctx->d_runs,
                     &ctx->d_nruns, &ctx->d_wflags_tc, &ctx->d_word_runs, &ctx->d_pot, &ctx->d_ring, &ctx->d_counts, &ctx->d_lines,
                     &ctx->d_stage, &ctx->d_raster, &ctx->d_fired, &ctx->d_exports, &ctx->d_send, &ctx->d_recv,
-                    &ctx->d_send_list, &ctx->d_recv_list, &ctx->d_dbg};
+                    &ctx->d_send_list, &ctx->d_recv_list, &ctx->d_dbg, &ctx->d_inw, &ctx->d_inslot,
+                    &ctx->d_slot_core};
   for (DevBuf* b : bufs) dev_free(ctx, b);
+}
+
+}  // namespace
+
+namespace {
+
+// Tensor-core path input decode (Alg. 1 l.1): lines -> per-core ring words,
+// kept while the inputs stay loaded.  Skipped (the kernel gathers the line
+// runs every tick instead) when the decoded array would exceed its budget.
+ranc_status prepare_inputs_tc(ranc_ctx* ctx) {
+  const Compiled& c = ctx->net;
+  if (ctx->inw_valid || !ctx->input_decode || ctx->kernel_active != RANC_KERNEL_TC || ctx->T_in == 0) return RANC_OK;
+  std::vector<int32_t> inslot(ctx->G_loc, -1), slot_core;
+  for (int g = 0; g < ctx->G_loc; ++g)
+    if (c.nruns[ctx->c_lo + g] > 0) {
+      inslot[g] = (int32_t)slot_core.size();
+      slot_core.push_back(ctx->c_lo + g);
+    }
+  ctx->n_inslots = (int32_t)slot_core.size();
+  if (slot_core.empty()) return RANC_OK;
+  const size_t bytes = (size_t)ctx->T_in * slot_core.size() * ctx->Sr * c.W * 4;
+  size_t free_b = 0, total_b = 0;
+  cudaMemGetInfo(&free_b, &total_b);
+  if (bytes > free_b / 4) return RANC_OK;   // keep the per-tick gather path
+  TRY(dev_alloc(ctx, &ctx->d_inw, bytes));
+  TRY(upload(ctx, &ctx->d_inslot, inslot));
+  TRY(upload(ctx, &ctx->d_slot_core, slot_core));
+  CK(cudaMemsetAsync(ctx->d_inw.p, 0, bytes, ctx->stream), "inw clear");
+  CK(decode_inputs_tc(ctx), "decode_inputs");
+  ctx->inw_valid = true;
+  return RANC_OK;
 }
 
 }  // namespace
@@ -203,6 +235,7 @@ ranc_status ranc_load_inputs(ranc_ctx* ctx, const ranc_inputs_desc* in) {
   const size_t dev_line_words = (size_t)in->num_input_ticks * Sr * c.WIp;
   if (ctx->d_lines.bytes != dev_line_words * sizeof(uint32_t)) TRY(dev_alloc(ctx, &ctx->d_lines, dev_line_words * 4));
   if (ctx->d_stage.bytes != line_words * sizeof(uint32_t)) TRY(dev_alloc(ctx, &ctx->d_stage, line_words * 4));
+  ctx->inw_valid = false;
   ctx->S = S;
   ctx->Sr = Sr;
   ctx->first_sample = in->first_sample;
@@ -233,6 +266,7 @@ ranc_status ranc_reset_state(ranc_ctx* ctx) {
   ctx->kernel_active = (ctx->kernel == RANC_KERNEL_POPC || !ctx->net.tc_ok || tc_smem_bytes(ctx->net) > 227 * 1024)
                            ? RANC_KERNEL_POPC
                            : RANC_KERNEL_TC;
+  TRY(prepare_inputs_tc(ctx));
   ctx->now = 0;
   ctx->raster_ticks = 0;
   return RANC_OK;
@@ -518,8 +552,9 @@ ranc_status ranc_set_option(ranc_ctx* ctx, int option, int64_t value) {
       }
       ctx->sample_tile_opt = (int32_t)value;
       return RANC_OK;
-    case RANC_OPT_USE_GRAPH:
-      ctx->use_graph = value ? 1 : 0;
+    case RANC_OPT_INPUT_DECODE:
+      ctx->input_decode = value ? 1 : 0;
+      ctx->inw_valid = false;
       return RANC_OK;
     case RANC_OPT_KERNEL:
       if (value < 0 || value > 2) {

@@ -53,6 +53,9 @@ struct TickParams {
   const uint8_t* wfold;     // tensor-core path: [G][Npad*Kp] canonical-layout int8
   const int2* runs;         // tensor-core path: input runs [G][rmax]
   const int32_t* word_runs; // [G][W]: runs overlapping ring word w: first | count << 16
+  const uint32_t* inw;      // decoded inputs [T_in][n_inslots][Sr][W] or nullptr
+  const int32_t* inslot;    // [G_loc] input slot of a local core (-1: no input lines)
+  int32_t n_inslots;
   const int32_t* nruns;     // [G]
   int32_t rmax;
   const uint32_t* xp;
@@ -136,7 +139,7 @@ struct ranc_ctx {
   int64_t now = 0;
   int32_t sample_tile = 0;       // in use (set by ranc_run_ticks)
   int32_t sample_tile_opt = 0;   // RANC_OPT_SAMPLE_TILE, 0 = automatic
-  int32_t use_graph = 1;
+  int32_t input_decode = 1;      // RANC_OPT_INPUT_DECODE
   int32_t kernel = 0;            // RANC_OPT_KERNEL request: 0 auto, 1 popcount, 2 tensor core
   int32_t kernel_active = 1;     // latched at every reset (the potential layout depends on it)
   int64_t launches = 0;
@@ -157,6 +160,10 @@ struct ranc_ctx {
   int64_t n_send_words = 0, n_recv_words = 0, n_recv_rows = 0;
   int64_t exchange_bytes = 0;    // bytes sent per tick (introspection)
   ranc::DevBuf d_dbg;            // RANC_DEBUG_TIMELINE
+  // tensor-core path: input decode (once per ranc_load_inputs)
+  ranc::DevBuf d_inw, d_inslot, d_slot_core;
+  int32_t n_inslots = 0;
+  bool inw_valid = false;
 };
 
 struct ranc_group {
@@ -185,6 +192,7 @@ int pieces_template(int E);
 int tc_tile();
 size_t tc_smem_bytes(const Compiled& n);
 cudaError_t launch_tick_tc(ranc_ctx* ctx, TickParams p);
+cudaError_t decode_inputs_tc(ranc_ctx* ctx);
 // api.cpp
 ranc_status dev_alloc(ranc_ctx* ctx, DevBuf* b, size_t bytes);
 void dev_free(ranc_ctx* ctx, DevBuf* b);

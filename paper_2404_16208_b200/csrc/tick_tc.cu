@@ -49,9 +49,9 @@ constexpr int NS = 4;                  // spike-stage pipeline depth
 constexpr int kExpWarps = 4;
 constexpr int kEpiWarps = 8;
 // Warp ids: the SMSP issue arbiter prefers higher warp ids, and the epilogue
-// saturates the ALU pipe, so the spike stage (on the pipeline's critical
-// path) takes the highest ids: 0 producer, 1 MMA, 2..9 epilogue, 10..13 spike.
-constexpr int kFirstEpi = 2, kFirstExp = 2 + kEpiWarps;
+// saturates the ALU pipe, so the short critical-path roles take the highest
+// ids: 0 producer, 1..8 epilogue, 9..12 spike stage, 13 MMA issuer.
+constexpr int kFirstEpi = 1, kFirstExp = 1 + kEpiWarps, kMmaWarp = kFirstExp + kExpWarps;
 constexpr int kThreadsTC = 32 * (2 + kExpWarps + kEpiWarps);  // 448
 constexpr int kExpThreads = 32 * kExpWarps;
 static_assert(kExpThreads == 2 * NT, "spike stage maps thread -> (sample, 16-bit half)");
@@ -82,7 +82,7 @@ __host__ __device__ inline TcLayout tc_layout(int Np, int Kp, int W, int WIp, in
   q = (q + 15) & ~15u;
   L.raw = q;   q += (uint32_t)NT * W * 4;    // scheduler rows due now (TMA)
   q = (q + 15) & ~15u;
-  L.lines = q; q += (uint32_t)NT * WIp * 4;  // input line rows of this tick (TMA)
+  L.lines = q; q += (uint32_t)NT * (WIp > W ? WIp : W) * 4;  // input line rows or decoded words (TMA)
   L.stage_bytes = (q + 1023) & ~1023u;
   L.total = L.stage + NS * L.stage_bytes;
   return L;
@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
   const int cur = (int)(p.t & p.rp_mask);
 
   // role warps (debug flag 32 swaps the producer and MMA warps)
-  const int prod_warp = (p.dbgflags & 32) ? 1 : 0, mma_warp = 1 - prod_warp;
+  const int prod_warp = 0, mma_warp = kMmaWarp;
   if (warp == mma_warp) tc::alloc(tmem_holder, tcols < 32 ? 32 : tcols);
   if (threadIdx.x == 0) {
     for (int i = 0; i < NS; ++i) {
@@ -186,11 +186,17 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
         uint8_t* st = smem + L.stage + s * L.stage_bytes;
         const int s0 = tile * NT;
         const bool inject = p.t < p.T_in && p.nruns[c] > 0;
-        const uint32_t ring_bytes = (uint32_t)NT * W * 4, line_bytes = inject ? (uint32_t)NT * WIp * 4 : 0u;
+        // decoded inputs: the tile's input words in ring-row layout; else the raw line rows
+        const int slot = p.inw ? p.inslot[cl] : -1;
+        const uint32_t ring_bytes = (uint32_t)NT * W * 4;
+        const uint32_t line_bytes = !inject ? 0u : (p.inw ? (uint32_t)NT * W * 4 : (uint32_t)NT * WIp * 4);
         ptx::mbar_arrive_expect_tx(&bars[FULL0 + s], ring_bytes + line_bytes);
         ptx::bulk_g2s(st + L.raw, p.ring + (((size_t)cur * p.G_loc + cl) * p.Sr + s0) * W, ring_bytes,
                       &bars[FULL0 + s]);
-        if (inject)
+        if (inject && p.inw)
+          ptx::bulk_g2s(st + L.lines, p.inw + (((size_t)p.t * p.n_inslots + slot) * p.Sr + s0) * W, line_bytes,
+                        &bars[FULL0 + s]);
+        else if (inject)
           ptx::bulk_g2s(st + L.lines, p.lines + ((size_t)p.t * p.Sr + s0) * WIp, line_bytes, &bars[FULL0 + s]);
       }
       __syncwarp();
@@ -232,7 +238,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       }
       __syncwarp();
     }
-  } else if (warp >= kFirstExp) {
+  } else if (warp >= kFirstExp && warp < kMmaWarp) {
     // ------------------------------------------------------------ spike stage
     const int et = threadIdx.x - 32 * kFirstExp;
     int runs_core = -1;
@@ -257,7 +263,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       if (et == 0) stamp(p, k, 12);
       // a2: external inputs.  Thread <-> (sample, ring word): OR in the line
       // runs overlapping that word (no atomics: every word has one owner)
-      if (p.t < p.T_in && p.nruns[c] > 0) {
+      if (p.t < p.T_in && p.nruns[c] > 0 && p.inw) {
+        // decoded input words (input decode done once at load, Alg. 1 l.1)
+        for (int i = et; i < ns * W; i += kExpThreads) raw[i] |= lines[i];
+      } else if (p.t < p.T_in && p.nruns[c] > 0) {
         // the core's input runs live in shared memory while its tiles are processed
         int2* runs = reinterpret_cast<int2*>(smem + L.runs);
         int32_t* wr = reinterpret_cast<int32_t*>(smem + L.runs + (uint32_t)p.rmax * 8);
@@ -535,7 +544,55 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
   if (warp == mma_warp) tc::dealloc(tmem, tcols < 32 ? 32 : tcols);
 }
 
+// Input decode (Alg. 1 l.1, "Initial setup and input decode"): the line
+// bits of every (tick, input core, sample) are mapped once onto the core's
+// ring-word layout, inw [T_in][slots][Sr][W], so the per-tick spike stage only
+// ORs a TMA-loaded row into the scheduler row.
+__global__ void decode_inputs_kernel(const uint32_t* __restrict__ lines, uint32_t* __restrict__ inw,
+                                     const int32_t* __restrict__ slot_core, const int2* __restrict__ runs,
+                                     const int32_t* __restrict__ word_runs, int n_slots, int T_in, int S, int Sr,
+                                     int W, int WIp, int rmax) {
+  const int64_t total = (int64_t)T_in * n_slots * S * W;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int w = (int)(i % W);
+    int64_t r = i / W;
+    const int s = (int)(r % S);
+    r /= S;
+    const int slot = (int)(r % n_slots);
+    const int t = (int)(r / n_slots);
+    const int c = slot_core[slot];
+    const int32_t fr = word_runs[(size_t)c * W + w];
+    const int r0 = fr & 0xFFFF, nrw = fr >> 16;
+    const uint32_t* lr = lines + ((size_t)t * Sr + s) * WIp;
+    uint32_t acc = 0u;
+    for (int q = r0; q < r0 + nrw; ++q) {
+      const int2 rn = runs[(size_t)c * rmax + q];
+      const int ap = rn.x & 0xFFFF, len = rn.x >> 16, ln = rn.y;
+      const int lw = ln >> 5, lb = ln & 31;
+      uint32_t x = lr[lw] >> lb;
+      if (lb + len > 32) x |= lr[lw + 1] << (32 - lb);
+      if (len < 32) x &= (1u << len) - 1u;
+      const int off = ap - 32 * w;
+      acc |= off >= 0 ? (x << off) : (x >> (-off));
+    }
+    inw[(((size_t)t * n_slots + slot) * Sr + s) * W + w] = acc;
+  }
+}
+
 }  // namespace
+
+cudaError_t decode_inputs_tc(ranc_ctx* ctx) {
+  const Compiled& n = ctx->net;
+  const int64_t total = (int64_t)ctx->T_in * ctx->n_inslots * ctx->S * n.W;
+  if (total == 0) return cudaSuccess;
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 148 * 16));
+  decode_inputs_kernel<<<blocks, 256, 0, ctx->stream>>>(
+      (const uint32_t*)ctx->d_lines.p, (uint32_t*)ctx->d_inw.p, (const int32_t*)ctx->d_slot_core.p,
+      (const int2*)ctx->d_runs.p, (const int32_t*)ctx->d_word_runs.p, ctx->n_inslots, ctx->T_in, (int)ctx->S,
+      (int)ctx->Sr, n.W, n.WIp, n.rmax);
+  ctx->launches++;
+  return cudaGetLastError();
+}
 
 int tc_tile() { return NT; }
 
@@ -548,6 +605,9 @@ cudaError_t launch_tick_tc(ranc_ctx* ctx, TickParams p) {
   p.wflags = (const uint8_t*)ctx->d_wflags_tc.p;
   p.runs = (const int2*)ctx->d_runs.p;
   p.word_runs = (const int32_t*)ctx->d_word_runs.p;
+  p.inw = ctx->inw_valid ? (const uint32_t*)ctx->d_inw.p : nullptr;
+  p.inslot = (const int32_t*)ctx->d_inslot.p;
+  p.n_inslots = ctx->n_inslots;
   p.nruns = (const int32_t*)ctx->d_nruns.p;
   p.rmax = n.rmax;
   const int64_t total = (int64_t)ctx->G_loc * ((ctx->S + NT - 1) / NT);

@@ -17,14 +17,17 @@ def ranc():
     return m
 
 
-KERNELS = {"popc": 1, "tc": 2}
+# "tc_gather": tensor-core kernel with the per-tick input-run gather instead
+# of the load-time input decode (RANC_OPT_INPUT_DECODE = 0)
+KERNELS = {"popc": 1, "tc": 2, "tc_gather": 2}
 
 
 def make_sim(ranc, net, kernel, **kw):
     sim = ranc.Simulator(net, **kw)
-    if kernel == "tc":
+    if kernel in ("tc", "tc_gather"):
         try:
             sim.set_option(ranc.OPT_KERNEL, KERNELS[kernel])
+            sim.set_option(ranc.OPT_INPUT_DECODE, 0 if kernel == "tc_gather" else 1)
         except ranc.RancError as e:
             sim.close()
             assert e.code == "RANC_E_CONFIG"
@@ -34,7 +37,7 @@ def make_sim(ranc, net, kernel, **kw):
     return sim
 
 
-@pytest.fixture(params=["popc", "tc"])
+@pytest.fixture(params=["popc", "tc", "tc_gather"])
 def kernel(request):
     return request.param
 
