@@ -364,7 +364,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
     const bool valid = active && n < p.N;
     int prev_core = -1;
     int leak = 0, pth = 0, nth = 0, rst = 0, init = 0, bf = 0, bn = 0, linmul = 0;
-    uint32_t kind = RK_NONE, cls = 0, axbit = 0;
+    uint32_t kind = RK_NONE, cls = 0, axbit = 0, out_lanes = 0, out_peers = 0;
     bool route_here = false, exporting = false, block_route = false, block_identity = false, has_output = false;
     size_t ring_off = 0, warp_ring_off = 0;
     // Potentials stream HBM -> shared memory with cp.async one tile ahead:
@@ -429,7 +429,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
           block_identity = (wf & 3u) == 3u;
           const uint32_t rmask = __ballot_sync(0xFFFFFFFFu, route_here);
           warp_ring_off = rmask ? __shfl_sync(0xFFFFFFFFu, ring_off, __ffs(rmask) - 1) : 0;
-          has_output = __any_sync(0xFFFFFFFFu, kind == RK_OUTPUT);
+          out_lanes = __ballot_sync(0xFFFFFFFFu, kind == RK_OUTPUT);
+          has_output = out_lanes != 0u;
+          // lanes of the same output class (classes are < C, never ~0u)
+          out_peers = __match_any_sync(0xFFFFFFFFu, kind == RK_OUTPUT ? cls : 0xFFFFFFFFu);
           prev_core = c;
         }
         uint4* dst = pot_tile(p, cl, tile, nT, n);
@@ -510,16 +513,17 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
             }
           }
           if (has_output) {
-            // output bus: one add per (sample, class) present among the lanes
-            const bool out = kind == RK_OUTPUT;
-            uint32_t any = __reduce_or_sync(0xFFFFFFFFu, out ? f : 0u);
-            while (any) {
-              const int i = __ffs(any) - 1;
-              any &= any - 1;
-              const bool fl = out && ((f >> i) & 1u);
-              const uint32_t peers = __match_any_sync(0xFFFFFFFFu, fl ? cls : 0xFFFFFFFFu);
-              if (fl && lane == __ffs(peers) - 1)
-                atomicAdd(p.counts + (size_t)(s0 + j * 32 + i) * p.C + cls, (int)__popc(peers));
+            // a6 output bus: lane i receives the output neurons (lanes) fired
+            // in sample i; one add per (sample, class group of lanes)
+            const uint32_t m = transpose32(kind == RK_OUTPUT ? f : 0u, lane);
+            uint32_t rem = out_lanes;
+            while (rem) {
+              const int l = __ffs(rem) - 1;
+              const uint32_t grp = __shfl_sync(0xFFFFFFFFu, out_peers, l);
+              const uint32_t cg = __shfl_sync(0xFFFFFFFFu, cls, l);
+              rem &= ~grp;
+              const int cnt = __popc(m & grp);
+              if (cnt) atomicAdd(p.counts + (size_t)(s0 + j * 32 + lane) * p.C + cg, cnt);
             }
           }
           if (p.raster || exporting) {
@@ -548,25 +552,30 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
 // bits of every (tick, input core, sample) are mapped once onto the core's
 // ring-word layout, inw [T_in][slots][Sr][W], so the per-tick spike stage only
 // ORs a TMA-loaded row into the scheduler row.
+// grid (sample blocks, slots, T_in); the core's runs are staged in shared memory
 __global__ void decode_inputs_kernel(const uint32_t* __restrict__ lines, uint32_t* __restrict__ inw,
                                      const int32_t* __restrict__ slot_core, const int2* __restrict__ runs,
-                                     const int32_t* __restrict__ word_runs, int n_slots, int T_in, int S, int Sr,
-                                     int W, int WIp, int rmax) {
-  const int64_t total = (int64_t)T_in * n_slots * S * W;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int w = (int)(i % W);
-    int64_t r = i / W;
-    const int s = (int)(r % S);
-    r /= S;
-    const int slot = (int)(r % n_slots);
-    const int t = (int)(r / n_slots);
-    const int c = slot_core[slot];
-    const int32_t fr = word_runs[(size_t)c * W + w];
+                                     const int32_t* __restrict__ word_runs, int S, int Sr, int W, int WIp,
+                                     int rmax) {
+  extern __shared__ int2 dec_sm[];
+  const int slot = blockIdx.y, t = blockIdx.z, n_slots = gridDim.y;
+  const int c = slot_core[slot];
+  int2* rs = dec_sm;
+  int32_t* wr = reinterpret_cast<int32_t*>(dec_sm + rmax);
+  for (int i = threadIdx.x; i < rmax; i += blockDim.x) rs[i] = runs[(size_t)c * rmax + i];
+  for (int i = threadIdx.x; i < W; i += blockDim.x) wr[i] = word_runs[(size_t)c * W + i];
+  __syncthreads();
+  const int per_block = (int)blockDim.x * 4;   // ring words per block
+  const int total = S * W;
+  for (int i = blockIdx.x * per_block + threadIdx.x; i < min(total, (blockIdx.x + 1) * per_block);
+       i += blockDim.x) {
+    const int s = i / W, w = i - s * W;
+    const int32_t fr = wr[w];
     const int r0 = fr & 0xFFFF, nrw = fr >> 16;
     const uint32_t* lr = lines + ((size_t)t * Sr + s) * WIp;
     uint32_t acc = 0u;
     for (int q = r0; q < r0 + nrw; ++q) {
-      const int2 rn = runs[(size_t)c * rmax + q];
+      const int2 rn = rs[q];
       const int ap = rn.x & 0xFFFF, len = rn.x >> 16, ln = rn.y;
       const int lw = ln >> 5, lb = ln & 31;
       uint32_t x = lr[lw] >> lb;
@@ -583,13 +592,17 @@ __global__ void decode_inputs_kernel(const uint32_t* __restrict__ lines, uint32_
 
 cudaError_t decode_inputs_tc(ranc_ctx* ctx) {
   const Compiled& n = ctx->net;
-  const int64_t total = (int64_t)ctx->T_in * ctx->n_inslots * ctx->S * n.W;
-  if (total == 0) return cudaSuccess;
-  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 148 * 16));
-  decode_inputs_kernel<<<blocks, 256, 0, ctx->stream>>>(
+  const int64_t words = (int64_t)ctx->S * n.W;
+  if (words == 0 || ctx->n_inslots == 0 || ctx->T_in == 0) return cudaSuccess;
+  if (words > INT32_MAX || ctx->T_in > 65535 || ctx->n_inslots > 65535) return cudaErrorInvalidValue;
+  const int threads = 256;
+  const dim3 grid((unsigned)((words + threads * 4 - 1) / (threads * 4)), (unsigned)ctx->n_inslots,
+                  (unsigned)ctx->T_in);
+  const size_t smem = (size_t)n.rmax * sizeof(int2) + (size_t)n.W * sizeof(int32_t);
+  decode_inputs_kernel<<<grid, threads, smem, ctx->stream>>>(
       (const uint32_t*)ctx->d_lines.p, (uint32_t*)ctx->d_inw.p, (const int32_t*)ctx->d_slot_core.p,
-      (const int2*)ctx->d_runs.p, (const int32_t*)ctx->d_word_runs.p, ctx->n_inslots, ctx->T_in, (int)ctx->S,
-      (int)ctx->Sr, n.W, n.WIp, n.rmax);
+      (const int2*)ctx->d_runs.p, (const int32_t*)ctx->d_word_runs.p, (int)ctx->S, (int)ctx->Sr, n.W, n.WIp,
+      n.rmax);
   ctx->launches++;
   return cudaGetLastError();
 }
