@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <new>
 #include <string>
 #include <vector>
@@ -105,27 +106,45 @@ void free_all(ranc_ctx* ctx) {
 namespace {
 
 // Tensor-core path input decode (Alg. 1 l.1): lines -> per-core ring words,
-// kept while the inputs stay loaded.  Skipped (the kernel gathers the line
-// runs every tick instead) when the decoded array would exceed its budget.
+// kept while the inputs stay loaded.  Input cores with the same line -> axon
+// map (identical runs) share one decoded slot.  Skipped (the kernel gathers
+// the line runs every tick instead) when the decoded array would exceed its
+// budget.
 ranc_status prepare_inputs_tc(ranc_ctx* ctx) {
   const Compiled& c = ctx->net;
   if (ctx->inw_valid || !ctx->input_decode || ctx->kernel_active != RANC_KERNEL_TC || ctx->T_in == 0) return RANC_OK;
   std::vector<int32_t> inslot(ctx->G_loc, -1), slot_core;
-  for (int g = 0; g < ctx->G_loc; ++g)
-    if (c.nruns[ctx->c_lo + g] > 0) {
-      inslot[g] = (int32_t)slot_core.size();
-      slot_core.push_back(ctx->c_lo + g);
+  std::map<std::vector<int32_t>, int32_t> seen;
+  for (int g = 0; g < ctx->G_loc; ++g) {
+    const int core = ctx->c_lo + g;
+    const int nr = c.nruns[core];
+    if (nr == 0) continue;
+    std::vector<int32_t> key;
+    key.reserve(2 * nr + c.W);
+    for (int q = 0; q < nr; ++q) {
+      key.push_back(c.runs[(size_t)core * c.rmax + q].x);
+      key.push_back(c.runs[(size_t)core * c.rmax + q].y);
     }
+    for (int w = 0; w < c.W; ++w) key.push_back(c.word_runs[(size_t)core * c.W + w]);
+    auto it = seen.find(key);
+    if (it == seen.end()) {
+      it = seen.emplace(std::move(key), (int32_t)slot_core.size()).first;
+      slot_core.push_back(core);
+    }
+    inslot[g] = it->second;
+  }
   ctx->n_inslots = (int32_t)slot_core.size();
   if (slot_core.empty()) return RANC_OK;
   const size_t bytes = (size_t)ctx->T_in * slot_core.size() * ctx->Sr * c.W * 4;
-  size_t free_b = 0, total_b = 0;
-  cudaMemGetInfo(&free_b, &total_b);
-  if (bytes > free_b / 4) return RANC_OK;   // keep the per-tick gather path
-  TRY(dev_alloc(ctx, &ctx->d_inw, bytes));
+  if (ctx->d_inw.bytes != bytes) {
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    if (bytes > (free_b + ctx->d_inw.bytes) / 4) return RANC_OK;   // keep the per-tick gather path
+    TRY(dev_alloc(ctx, &ctx->d_inw, bytes));
+  }
   TRY(upload(ctx, &ctx->d_inslot, inslot));
   TRY(upload(ctx, &ctx->d_slot_core, slot_core));
-  CK(cudaMemsetAsync(ctx->d_inw.p, 0, bytes, ctx->stream), "inw clear");
+  // rows s >= S of the last tile are never consumed (the kernel ORs i < ns*W)
   CK(decode_inputs_tc(ctx), "decode_inputs");
   ctx->inw_valid = true;
   return RANC_OK;
