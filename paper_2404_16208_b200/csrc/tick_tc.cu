@@ -120,6 +120,46 @@ __device__ __forceinline__ uint4* pot_tile(const TickParams& p, int c, int tile,
   return reinterpret_cast<uint4*>(p.pot + ((size_t)c * nT + tile) * (size_t)p.Npad * NT) + n;
 }
 
+// a4 for 32 samples of one neuron (Alg. 1 l.14-24): v = V + acc +
+// leak; fire if v >= theta+, negative reset if v < theta-; reset to R / -R
+// (ABS) or v - theta (LIN); saturate to pb bits once (G8).  Returns the fired
+// mask and the 32 new potentials packed as s16 pairs.  The reset is one IMAD:
+// r = v * lin + (fire ? bf : bn).  kSat16 (pb = 16): the saturation and the
+// packing of two potentials are one cvt.pack.sat.s16.s32.
+template <bool kSat16>
+__device__ __forceinline__ uint32_t lif32(const uint4 (&cur)[4], const uint32_t (&acc)[32], int leak, int pth,
+                                          int nth, int linmul, int bf, int bn, int lo, int hi,
+                                          uint32_t (&outw)[16]) {
+  uint32_t fired = 0u;
+#pragma unroll
+  for (int i2 = 0; i2 < 16; ++i2) {
+    const uint4 v4 = cur[i2 >> 2];
+    const uint32_t w32 = (i2 & 3) == 0 ? v4.x : (i2 & 3) == 1 ? v4.y : (i2 & 3) == 2 ? v4.z : v4.w;
+    int nvp[2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int i = 2 * i2 + e;
+      const int pot = e ? ((int)w32 >> 16) : ((int)(w32 << 16) >> 16);
+      const int v = pot + ((int)acc[i] + leak);
+      const bool fire = v >= pth;
+      const bool chg = fire || v < nth;
+      const int r = v * linmul + (fire ? bf : bn);
+      int nv = chg ? r : v;
+      if (!kSat16) nv = min(max(nv, lo), hi);
+      nvp[e] = nv;
+      if (fire) fired |= 1u << i;
+    }
+    if (kSat16) {
+      uint32_t d;
+      asm("cvt.pack.sat.s16.s32 %0, %1, %2;" : "=r"(d) : "r"(nvp[1]), "r"(nvp[0]));
+      outw[i2] = d;
+    } else {
+      outw[i2] = __byte_perm((uint32_t)nvp[0], (uint32_t)nvp[1], 0x5410u);
+    }
+  }
+  return fired;
+}
+
 __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
@@ -256,7 +296,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       const uint32_t* lines = reinterpret_cast<const uint32_t*>(st + L.lines);
       // a1: the scheduler rows due now were staged by the producer (TMA);
       // clear them in global memory (free again for spikes due at t + Rp)
-      ptx::mbar_wait(&bars[FULL0 + s], u & 1);
+      ptx::mbar_wait_sleep(&bars[FULL0 + s], u & 1, 2000);
       if (et == 0) stamp(p, k, 2);
       uint32_t* row = p.ring + (((size_t)cur * p.G_loc + cl) * p.Sr + s0) * W;
       for (int i = et; i < ns * W; i += kExpThreads) row[i] = 0u;
@@ -314,7 +354,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       // samples >= ns of a tail tile get no spikes.  Lanes take consecutive
       // samples so each 8-lane phase of the 16-byte stores fills one core
       // matrix (bank-conflict free).
-      ptx::mbar_wait(&bars[BEMPTY0 + s], (u & 1) ^ 1);
+      ptx::mbar_wait_sleep(&bars[BEMPTY0 + s], (u & 1) ^ 1, 2000);
       if (et == 0) stamp(p, k, 3);
       uint8_t* b_s = st + L.b;
       {
@@ -377,6 +417,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
     uint4* pbuf = reinterpret_cast<uint4*>(smem + L.potbuf) + (threadIdx.x - 32 * kFirstEpi);
     constexpr int PB = 32 * kEpiWarps;   // uint4 stride between chunks in potbuf
     const bool load = active && !p.fresh;
+    const bool sat16 = p.pot_lo == -32768 && p.pot_hi == 32767;
     uint4 initv = make_uint4(0u, 0u, 0u, 0u);
     if (load && nwork > 0) {
       const int c0 = lo / nT;
@@ -396,7 +437,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       // tile); each chunk is refilled with the next tile's as soon as it is used
       const bool pf = load && k + 1 < nwork;
       const uint4* nsrc = pot_tile(p, (idx + 1) / nT, (idx + 1) % nT, nT, n);
-      ptx::mbar_wait(&bars[ACCFULL0 + a], ua & 1);
+      ptx::mbar_wait_sleep(&bars[ACCFULL0 + a], ua & 1, 2000);
       if (lane == 0 && ew == 0) stamp(p, k, 8);
       tc::fence_after();
       if (active) {
@@ -458,26 +499,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
           }
           tc::wait_ld();
           if (lane == 0 && ew == 0) stamp(p, k, 9 + j);
-          // a4: leak / thresholds / reset per sample.  ALU-pipe bound, so kept
-          // to ~10 ALU ops + 1 IMAD: reset value r = v*lin + (fire ? bf : bn)
-          uint32_t fired = 0u;
+          // a4: leak / thresholds / reset per sample (ALU-pipe bound)
           uint32_t outw[16];
-#pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const uint4 v4 = cur[i >> 3];
-            const uint32_t w32 =
-                ((i >> 1) & 3) == 0 ? v4.x : ((i >> 1) & 3) == 1 ? v4.y : ((i >> 1) & 3) == 2 ? v4.z : v4.w;
-            const int pot = (i & 1) ? ((int)w32 >> 16) : ((int)(w32 << 16) >> 16);
-            const int v = pot + (int)acc[i] + leak;
-            const bool fire = v >= pth;
-            const bool chg = fire || v < nth;
-            const int r = v * linmul + (fire ? bf : bn);
-            int nv = chg ? r : v;
-            nv = min(max(nv, p.pot_lo), p.pot_hi);
-            if (i & 1) outw[i >> 1] = __byte_perm(outw[i >> 1], (uint32_t)nv, 0x5410u);
-            else outw[i >> 1] = (uint32_t)nv;
-            if (fire) fired |= 1u << i;
-          }
+          const uint32_t fired = sat16 ? lif32<true>(cur, acc, leak, pth, nth, linmul, bf, bn, 0, 0, outw)
+                                       : lif32<false>(cur, acc, leak, pth, nth, linmul, bf, bn, p.pot_lo, p.pot_hi, outw);
           if (!(p.dbgflags & 8)) {
 #pragma unroll
             for (int cc = 0; cc < 4; ++cc)
