@@ -139,15 +139,25 @@ __device__ __forceinline__ uint32_t lif32(const uint4 (&cur)[4], const uint32_t 
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
       const int i = 2 * i2 + e;
-      const int pot = e ? ((int)w32 >> 16) : ((int)(w32 << 16) >> 16);
-      const int v = pot + ((int)acc[i] + leak);
-      const bool fire = v >= pth;
-      const bool chg = fire || v < nth;
-      const int r = v * linmul + (fire ? bf : bn);
-      int nv = chg ? r : v;
+      // the sign-extended half plus the input: one LEA.HI.SX32 (the low half
+      // is first moved up with an IMAD on the FMA pipe)
+      const int src = e ? (int)w32 : (int)(w32 * 65536u);
+      const int v = (src >> 16) + ((int)acc[i] + leak);
+      // fire / change predicates; the reset value is selected with
+      // predicated IMADs (FMA pipe) instead of ALU selects:
+      //   r = v*lin + bn; fire: r = v*lin + bf; no change: r = v
+      int nv;
+      asm("{\n\t.reg .pred pf, pc;\n\t"
+          "setp.ge.s32 pf, %2, %3;\n\t"
+          "setp.lt.or.s32 pc, %2, %4, pf;\n\t"
+          "mad.lo.s32 %0, %2, %5, %7;\n\t"
+          "@pf mad.lo.s32 %0, %2, %5, %6;\n\t"
+          "@!pc mov.b32 %0, %2;\n\t"
+          "@pf add.u32 %1, %1, %8;\n\t}"
+          : "=&r"(nv), "+r"(fired)
+          : "r"(v), "r"(pth), "r"(nth), "r"(linmul), "r"(bf), "r"(bn), "r"(1u << i));
       if (!kSat16) nv = min(max(nv, lo), hi);
       nvp[e] = nv;
-      if (fire) fired |= 1u << i;
     }
     if (kSat16) {
       uint32_t d;
@@ -429,14 +439,19 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
         ptx::cp_async_commit();
       }
     }
-    for (int k = 0; k < nwork; ++k) {
-      const int idx = lo + k, cl = idx / nT, tile = idx - cl * nT, c = p.c_lo + cl;
+    // work item idx = cl * nT + tile, advanced incrementally (no divisions);
+    // its potential tile is pot + idx * tile_stride (pot_tile)
+    int cl = lo / nT, tile = lo - (lo / nT) * nT;
+    const size_t tile_stride = (size_t)Np * NT / 8;   // uint4 per potential tile
+    uint4* dst = pot_tile(p, cl, tile, nT, n);
+    for (int k = 0; k < nwork; ++k, dst += tile_stride) {
+      const int c = p.c_lo + cl;
       const int a = k % NA, ua = k / NA;
       const int s0 = tile * NT, ns = min(NT, p.S - s0);
-      // pnext holds this tile's potentials (prefetched during the previous
+      // potbuf holds this tile's potentials (prefetched during the previous
       // tile); each chunk is refilled with the next tile's as soon as it is used
       const bool pf = load && k + 1 < nwork;
-      const uint4* nsrc = pot_tile(p, (idx + 1) / nT, (idx + 1) % nT, nT, n);
+      const uint4* nsrc = dst + tile_stride;
       ptx::mbar_wait_sleep(&bars[ACCFULL0 + a], ua & 1, 2000);
       if (lane == 0 && ew == 0) stamp(p, k, 8);
       tc::fence_after();
@@ -476,7 +491,6 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
           out_peers = __match_any_sync(0xFFFFFFFFu, kind == RK_OUTPUT ? cls : 0xFFFFFFFFu);
           prev_core = c;
         }
-        uint4* dst = pot_tile(p, cl, tile, nT, n);
         const uint32_t acc_addr = tmem + a * acc_stride + ((uint32_t)(q * 32) << 16) + h * NT;
 #pragma unroll 1
         for (int j = 0; j < NT / 32; ++j) {
@@ -566,6 +580,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       __syncwarp();
       if (lane == 0 && ew == 0) stamp(p, k, 11);
       if (lane == 0) ptx::mbar_arrive(&bars[ACCEMPTY0 + a]);
+      if (++tile == nT) {
+        tile = 0;
+        ++cl;
+      }
     }
   }
   tc::fence_before();
