@@ -11,19 +11,19 @@
 // K-major core-matrix layout (tc.h).
 //
 // Persistent, warp-specialised: one CTA per SM walks a contiguous range of
-// (core, sample-tile) work items; the four roles overlap through mbarriers,
-// with two stages so that tile i+1 is loaded, expanded and multiplied while
-// the epilogue of tile i runs:
-//   warp 0      producer: TMA bulk loads of Wfold (on a core change) and of the
-//               tile's scheduler rows and input-line rows (4-stage ring)
-//   warp 1      MMA issuer (one elected thread) + TMEM allocation (up to 4
-//               accumulator stages)
-//   warps 2-5   spike stage: clear the rows read (a1), input runs (a2), bits
-//               -> 0/1 bytes in the operand layout
-//   warps 6-13  epilogue, thread = neuron = TMEM lane: potentials streamed
-//               HBM <-> registers (next tile prefetched while this one
-//               runs), leak / thresholds / reset (a4), routing and output bus
-//               (a5, a6)
+// (core, sample-tile) work items; the roles overlap through mbarriers (NS = 4
+// spike stages, up to 4 TMEM accumulator stages), so that the next tiles are
+// loaded, expanded and multiplied while the epilogue of this one runs:
+//   warps 0-15  epilogue, thread = neuron = TMEM lane (warp % 4 = lane
+//               quarter; neuron half and 32-sample half from the warp id):
+//               potentials streamed HBM -> shared (cp.async, one tile ahead)
+//               -> registers -> HBM, leak / thresholds / reset (a4), routing
+//               and output bus (a5, a6)
+//   warps 16-19 spike stage: clear the rows read (a1), input injection (a2),
+//               bits -> 0/1 bytes in the operand layout
+//   warp 20     producer: TMA bulk loads of Wfold (on a core change) and of
+//               the tile's scheduler rows and decoded input words
+//   warp 21     MMA issuer (one elected thread) + TMEM allocation
 // A tick is one launch; the kernel boundary is the tick barrier (a7).
 //
 // Potential layout: tile-blocked [G][nT][8][Np][8] int16 (tile, 8-sample chunk,
@@ -47,13 +47,14 @@ namespace {
 constexpr int NT = 64;                 // samples per tile (MMA N)
 constexpr int NS = 4;                  // spike-stage pipeline depth
 constexpr int kExpWarps = 4;
-constexpr int kEpiWarps = 8;
-// Warp ids: the SMSP issue arbiter prefers higher warp ids, and the epilogue
-// saturates the ALU pipe, so the short critical-path roles take the highest
-// ids: 0 producer, 1..8 epilogue, 9..12 spike stage, 13 MMA issuer.
-constexpr int kFirstEpi = 1, kFirstExp = 1 + kEpiWarps, kMmaWarp = kFirstExp + kExpWarps;
-constexpr int kThreadsTC = 32 * (2 + kExpWarps + kEpiWarps);  // 448
+constexpr int kEpiWarps = 16;
+// Warp ids: 0..15 epilogue (TMEM lane quarter = warp % 4, so every SMSP holds
+// four epilogue warps to hide the LIF's dependency latencies), 16..19 spike
+// stage, 20 producer, 21 MMA issuer.
+constexpr int kFirstEpi = 0, kFirstExp = kEpiWarps, kProdWarp = kFirstExp + 4, kMmaWarp = kProdWarp + 1;
+constexpr int kThreadsTC = 32 * (2 + kExpWarps + kEpiWarps);  // 704
 constexpr int kExpThreads = 32 * kExpWarps;
+constexpr int kSub = 16;               // samples per TMEM load / LIF pass of an epilogue warp
 static_assert(kExpThreads == 2 * NT, "spike stage maps thread -> (sample, 16-bit half)");
 
 enum Bar { FULL0 = 0, SEMPTY0 = 4, BFULL0 = 8, BEMPTY0 = 12, ACCFULL0 = 16, ACCEMPTY0 = 20, WFULL = 24, WFREE = 25,
@@ -75,7 +76,7 @@ __host__ __device__ inline TcLayout tc_layout(int Np, int Kp, int W, int WIp, in
   o += 256 * 8;
   o = (o + 127) & ~127u;
   L.potbuf = o;                               // uint4 [NT/8][epilogue threads]: next tile's potentials
-  o += (NT / 8) * (32 * 8) * 16;
+  o += (NT / 8) * (32 * 8) * 16;           // = 4 chunks x 512 epilogue threads
   L.stage = (o + 1023) & ~1023u;
   uint32_t q = 0;
   L.b = q;     q += (uint32_t)NT * Kp;       // spikes as 0/1 bytes, canonical layout
@@ -87,8 +88,6 @@ __host__ __device__ inline TcLayout tc_layout(int Np, int Kp, int W, int WIp, in
   L.total = L.stage + NS * L.stage_bytes;
   return L;
 }
-
-__device__ __forceinline__ bool getenv_swap_h(const TickParams& p) { return (p.dbgflags & 16) != 0; }
 
 // optional per-tile timeline of CTA 0 (debug builds of a run: p.dbg != nullptr)
 __device__ __forceinline__ void stamp(const TickParams& p, int k, int slot) {
@@ -120,19 +119,19 @@ __device__ __forceinline__ uint4* pot_tile(const TickParams& p, int c, int tile,
   return reinterpret_cast<uint4*>(p.pot + ((size_t)c * nT + tile) * (size_t)p.Npad * NT) + n;
 }
 
-// a4 for 32 samples of one neuron (Alg. 1 l.14-24): v = V + acc +
+// a4 for NE samples of one neuron (Alg. 1 l.14-24): v = V + acc +
 // leak; fire if v >= theta+, negative reset if v < theta-; reset to R / -R
 // (ABS) or v - theta (LIN); saturate to pb bits once (G8).  Returns the fired
 // mask and the 32 new potentials packed as s16 pairs.  The reset is one IMAD:
 // r = v * lin + (fire ? bf : bn).  kSat16 (pb = 16): the saturation and the
 // packing of two potentials are one cvt.pack.sat.s16.s32.
-template <bool kSat16>
-__device__ __forceinline__ uint32_t lif32(const uint4 (&cur)[4], const uint32_t (&acc)[32], int leak, int pth,
-                                          int nth, int linmul, int bf, int bn, int lo, int hi,
-                                          uint32_t (&outw)[16]) {
+template <bool kSat16, int NE>
+__device__ __forceinline__ uint32_t lif(const uint4 (&cur)[NE / 8], const uint32_t (&acc)[NE], int leak, int pth,
+                                        int nth, int linmul, int bf, int bn, int lo, int hi,
+                                        uint32_t (&outw)[NE / 2]) {
   uint32_t fired = 0u;
 #pragma unroll
-  for (int i2 = 0; i2 < 16; ++i2) {
+  for (int i2 = 0; i2 < NE / 2; ++i2) {
     const uint4 v4 = cur[i2 >> 2];
     const uint32_t w32 = (i2 & 3) == 0 ? v4.x : (i2 & 3) == 1 ? v4.y : (i2 & 3) == 2 ? v4.z : v4.w;
     int nvp[2];
@@ -190,7 +189,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
   const int cur = (int)(p.t & p.rp_mask);
 
   // role warps (debug flag 32 swaps the producer and MMA warps)
-  const int prod_warp = 0, mma_warp = kMmaWarp;
+  const int prod_warp = kProdWarp, mma_warp = kMmaWarp;
   if (warp == mma_warp) tc::alloc(tmem_holder, tcols < 32 ? 32 : tcols);
   if (threadIdx.x == 0) {
     for (int i = 0; i < NS; ++i) {
@@ -288,7 +287,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       }
       __syncwarp();
     }
-  } else if (warp >= kFirstExp && warp < kMmaWarp) {
+  } else if (warp >= kFirstExp && warp < kProdWarp) {
     // ------------------------------------------------------------ spike stage
     const int et = threadIdx.x - 32 * kFirstExp;
     int runs_core = -1;
@@ -406,9 +405,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
     }
   } else {
     // ------------------------------------------------------------ epilogue
+    // warp ew: TMEM lane quarter q = ew % 4 (thread = neuron n), neuron half
+    // h, sample half jj of the tile (32 samples, two LIF passes of kSub)
     const int ew = warp - kFirstEpi;
-    const int q = warp & 3;                // TMEM lane quarter = warp % 4
-    const int h = (getenv_swap_h(p) && Mh > 1) ? ((ew >> 2) ^ 1) : (ew >> 2);
+    const int q = warp & 3;
+    const int h = (ew >> 2) & 1, jj = ew >> 3;
     const int n = h * 128 + q * 32 + lane;
     const bool active = h < Mh;
     const bool valid = active && n < p.N;
@@ -418,38 +419,37 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
     bool route_here = false, exporting = false, block_route = false, block_identity = false, has_output = false;
     size_t ring_off = 0, warp_ring_off = 0;
     // Potentials stream HBM -> shared memory with cp.async one tile ahead:
-    // potbuf[q][et] holds 16-byte chunk q (8 samples) of this thread's neuron.
-    // Chunk half j (q = 4j..4j+3) of the next tile is requested right after
-    // the same half of the current tile has been read out, so every load has
-    // about a tile of time to land; the per-thread commit groups are waited
-    // with cp.async.wait_group 1 (NT == 64: two halves).
-    static_assert(NT == 64, "two 32-sample chunks per tile");
+    // pbuf[c * PB] holds 16-byte chunk c (8 samples) of this thread's 32
+    // samples.  The chunks of pass sb of the next tile are requested right
+    // after the same pass of the current tile has read them out, so every
+    // load has about a tile of time to land; one commit group per pass,
+    // waited with cp.async.wait_group 1.
+    static_assert(NT == 64 && kSub == 16, "two 32-sample halves, two passes each");
+    constexpr int kPass = 32 / kSub, kCh = kSub / 8;   // passes per half, chunks per pass
     uint4* pbuf = reinterpret_cast<uint4*>(smem + L.potbuf) + (threadIdx.x - 32 * kFirstEpi);
     constexpr int PB = 32 * kEpiWarps;   // uint4 stride between chunks in potbuf
     const bool load = active && !p.fresh;
     const bool sat16 = p.pot_lo == -32768 && p.pot_hi == 32767;
     uint4 initv = make_uint4(0u, 0u, 0u, 0u);
+    // work item idx = cl * nT + tile, advanced incrementally (no divisions);
+    // its potential tile is pot + idx * tile_stride (pot_tile); this warp's
+    // chunks start at chunk 4*jj
+    int cl = lo / nT, tile = lo - (lo / nT) * nT;
+    const size_t tile_stride = (size_t)Np * NT / 8;   // uint4 per potential tile
+    uint4* dst = pot_tile(p, cl, tile, nT, n) + (size_t)(4 * jj) * Np;
     if (load && nwork > 0) {
-      const int c0 = lo / nT;
-      const uint4* src = pot_tile(p, c0, lo - c0 * nT, nT, n);
 #pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
+      for (int sb = 0; sb < kPass; ++sb) {
 #pragma unroll
-        for (int i = 0; i < 4; ++i) ptx::cp_async16(pbuf + (4 * hh + i) * PB, src + (size_t)(4 * hh + i) * Np);
+        for (int i = 0; i < kCh; ++i)
+          ptx::cp_async16(pbuf + (kCh * sb + i) * PB, dst + (size_t)(kCh * sb + i) * Np);
         ptx::cp_async_commit();
       }
     }
-    // work item idx = cl * nT + tile, advanced incrementally (no divisions);
-    // its potential tile is pot + idx * tile_stride (pot_tile)
-    int cl = lo / nT, tile = lo - (lo / nT) * nT;
-    const size_t tile_stride = (size_t)Np * NT / 8;   // uint4 per potential tile
-    uint4* dst = pot_tile(p, cl, tile, nT, n);
     for (int k = 0; k < nwork; ++k, dst += tile_stride) {
       const int c = p.c_lo + cl;
       const int a = k % NA, ua = k / NA;
       const int s0 = tile * NT, ns = min(NT, p.S - s0);
-      // potbuf holds this tile's potentials (prefetched during the previous
-      // tile); each chunk is refilled with the next tile's as soon as it is used
       const bool pf = load && k + 1 < nwork;
       const uint4* nsrc = dst + tile_stride;
       ptx::mbar_wait_sleep(&bars[ACCFULL0 + a], ua & 1, 2000);
@@ -491,88 +491,91 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
           out_peers = __match_any_sync(0xFFFFFFFFu, kind == RK_OUTPUT ? cls : 0xFFFFFFFFu);
           prev_core = c;
         }
-        const uint32_t acc_addr = tmem + a * acc_stride + ((uint32_t)(q * 32) << 16) + h * NT;
+        const uint32_t acc_addr = tmem + a * acc_stride + ((uint32_t)(q * 32) << 16) + h * NT + jj * 32;
+        uint32_t fired = 0u;
 #pragma unroll 1
-        for (int j = 0; j < NT / 32; ++j) {
-          uint32_t acc[32];
-          tc::ld32(acc_addr + j * 32, acc);
-          uint4 cur[4];
+        for (int sb = 0; sb < kPass; ++sb) {
+          uint32_t acc[kSub];
+          tc::ld16(acc_addr + sb * kSub, acc);
+          uint4 cur[kCh];
           if (load) {
-            ptx::cp_async_wait<1>();   // this half's group (issued a tile ago) has landed
+            ptx::cp_async_wait<1>();   // this pass's group (issued a tile ago) has landed
 #pragma unroll
-            for (int i = 0; i < 4; ++i) cur[i] = pbuf[(4 * j + i) * PB];
-            // request the same half of the next tile into the slots just read
-            if (pf && !(p.dbgflags & 4)) {
+            for (int i = 0; i < kCh; ++i) cur[i] = pbuf[(kCh * sb + i) * PB];
+            // request the same chunks of the next tile into the slots just read
+            if (pf) {
 #pragma unroll
-              for (int i = 0; i < 4; ++i) ptx::cp_async16(pbuf + (4 * j + i) * PB, nsrc + (size_t)(4 * j + i) * Np);
+              for (int i = 0; i < kCh; ++i)
+                ptx::cp_async16(pbuf + (kCh * sb + i) * PB, nsrc + (size_t)(kCh * sb + i) * Np);
             }
             ptx::cp_async_commit();   // (possibly empty) group: keeps the wait_group 1 accounting
           } else {
 #pragma unroll
-            for (int i = 0; i < 4; ++i) cur[i] = initv;
+            for (int i = 0; i < kCh; ++i) cur[i] = initv;
           }
           tc::wait_ld();
-          if (lane == 0 && ew == 0) stamp(p, k, 9 + j);
-          // a4: leak / thresholds / reset per sample (ALU-pipe bound)
-          uint32_t outw[16];
-          const uint32_t fired = sat16 ? lif32<true>(cur, acc, leak, pth, nth, linmul, bf, bn, 0, 0, outw)
-                                       : lif32<false>(cur, acc, leak, pth, nth, linmul, bf, bn, p.pot_lo, p.pot_hi, outw);
-          if (!(p.dbgflags & 8)) {
+          if (lane == 0 && ew == 0) stamp(p, k, 9 + sb);
+          // a4: leak / thresholds / reset per sample
+          uint32_t outw[kSub / 2];
+          const uint32_t fb = sat16 ? lif<true, kSub>(cur, acc, leak, pth, nth, linmul, bf, bn, 0, 0, outw)
+                                    : lif<false, kSub>(cur, acc, leak, pth, nth, linmul, bf, bn, p.pot_lo, p.pot_hi,
+                                                       outw);
+          fired |= fb << (sb * kSub);
 #pragma unroll
-            for (int cc = 0; cc < 4; ++cc)
-              dst[(size_t)(j * 4 + cc) * Np] =
-                  make_uint4(outw[4 * cc + 0], outw[4 * cc + 1], outw[4 * cc + 2], outw[4 * cc + 3]);
+          for (int cc = 0; cc < kCh; ++cc)
+            dst[(size_t)(kCh * sb + cc) * Np] =
+                make_uint4(outw[4 * cc + 0], outw[4 * cc + 1], outw[4 * cc + 2], outw[4 * cc + 3]);
+        }
+        // a5 / a6: route or count the spikes of real samples
+        const int sj = s0 + jj * 32;          // first sample of this warp's half
+        const int lim = ns - jj * 32;
+        const uint32_t f = lim >= 32 ? fired : (lim > 0 ? fired & ((1u << lim) - 1u) : 0u);
+        if (block_identity) {
+          // every routing lane l of this warp deposits bit l of one ring
+          // word: a 32x32 bit transpose turns the per-lane sample masks into
+          // per-sample deposit words, one RED per (sample, word) issued by
+          // the lane of that sample (idempotent OR, G11)
+          const uint32_t m = transpose32(route_here ? f : 0u, lane);
+          if (m) atomicOr(p.ring + warp_ring_off + (size_t)(sj + lane) * W, m);
+        } else if (block_route) {
+          // every routing lane targets the same ring word: one OR-reduced
+          // deposit per sample
+          uint32_t any = __reduce_or_sync(0xFFFFFFFFu, route_here ? f : 0u);
+          while (any) {
+            const int i = __ffs(any) - 1;
+            any &= any - 1;
+            const uint32_t m = __reduce_or_sync(0xFFFFFFFFu, (route_here && ((f >> i) & 1u)) ? axbit : 0u);
+            if (lane == 0) atomicOr(p.ring + warp_ring_off + (size_t)(sj + i) * W, m);
           }
-          // a5 / a6: route or count the spikes of real samples
-          const int lim = ns - j * 32;
-          uint32_t f = lim >= 32 ? fired : (lim > 0 ? fired & ((1u << lim) - 1u) : 0u);
-          if (block_identity) {
-            // every routing lane l of this warp deposits bit l of one ring
-            // word: a 32x32 bit transpose turns the per-lane sample masks into
-            // per-sample deposit words, one RED per (sample, word) issued by
-            // the lane of that sample (idempotent OR, G11)
-            const uint32_t m = transpose32(route_here ? f : 0u, lane);
-            if (m) atomicOr(p.ring + warp_ring_off + (size_t)(s0 + j * 32 + lane) * W, m);
-          } else if (block_route) {
-            // every routing lane targets the same ring word: one OR-reduced
-            // deposit per sample
-            uint32_t any = __reduce_or_sync(0xFFFFFFFFu, route_here ? f : 0u);
-            while (any) {
-              const int i = __ffs(any) - 1;
-              any &= any - 1;
-              const uint32_t m = __reduce_or_sync(0xFFFFFFFFu, (route_here && ((f >> i) & 1u)) ? axbit : 0u);
-              if (lane == 0) atomicOr(p.ring + warp_ring_off + (size_t)(s0 + j * 32 + i) * W, m);
-            }
-          } else if (route_here) {
-            uint32_t g = f;
-            while (g) {
-              const int i = __ffs(g) - 1;
-              g &= g - 1;
-              atomicOr(p.ring + ring_off + (size_t)(s0 + j * 32 + i) * W, axbit);
-            }
+        } else if (route_here) {
+          uint32_t g = f;
+          while (g) {
+            const int i = __ffs(g) - 1;
+            g &= g - 1;
+            atomicOr(p.ring + ring_off + (size_t)(sj + i) * W, axbit);
           }
-          if (has_output) {
-            // a6 output bus: lane i receives the output neurons (lanes) fired
-            // in sample i; one add per (sample, class group of lanes)
-            const uint32_t m = transpose32(kind == RK_OUTPUT ? f : 0u, lane);
-            uint32_t rem = out_lanes;
-            while (rem) {
-              const int l = __ffs(rem) - 1;
-              const uint32_t grp = __shfl_sync(0xFFFFFFFFu, out_peers, l);
-              const uint32_t cg = __shfl_sync(0xFFFFFFFFu, cls, l);
-              rem &= ~grp;
-              const int cnt = __popc(m & grp);
-              if (cnt) atomicAdd(p.counts + (size_t)(s0 + j * 32 + lane) * p.C + cg, cnt);
-            }
+        }
+        if (has_output) {
+          // a6 output bus: lane i receives the output neurons (lanes) fired
+          // in sample i; one add per (sample, class group of lanes)
+          const uint32_t m = transpose32(kind == RK_OUTPUT ? f : 0u, lane);
+          uint32_t rem = out_lanes;
+          while (rem) {
+            const int l = __ffs(rem) - 1;
+            const uint32_t grp = __shfl_sync(0xFFFFFFFFu, out_peers, l);
+            const uint32_t cg = __shfl_sync(0xFFFFFFFFu, cls, l);
+            rem &= ~grp;
+            const int cnt = __popc(m & grp);
+            if (cnt) atomicAdd(p.counts + (size_t)(sj + lane) * p.C + cg, cnt);
           }
-          if (p.raster || exporting) {
-            // lane i receives the fired word (32 neurons) of sample i
-            const uint32_t m = transpose32(valid ? fired : 0u, lane);
-            if (lane < lim && (n >> 5) < p.Wn) {
-              const int sg = s0 + j * 32 + lane;
-              if (p.raster) p.raster[(((size_t)(p.t - p.raster_t0) * p.S + sg) * p.G_loc + cl) * p.Wn + (n >> 5)] = m;
-              if (exporting) p.fired[((size_t)cl * p.Sr + sg) * p.Wn + (n >> 5)] = m;
-            }
+        }
+        if (p.raster || exporting) {
+          // lane i receives the fired word (32 neurons) of sample i
+          const uint32_t m = transpose32(valid ? fired : 0u, lane);
+          if (lane < lim && (n >> 5) < p.Wn) {
+            const int sg = sj + lane;
+            if (p.raster) p.raster[(((size_t)(p.t - p.raster_t0) * p.S + sg) * p.G_loc + cl) * p.Wn + (n >> 5)] = m;
+            if (exporting) p.fired[((size_t)cl * p.Sr + sg) * p.Wn + (n >> 5)] = m;
           }
         }
       }
