@@ -49,6 +49,24 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, 
       : "memory");
 }
 
+// polling wait with a fixed back-off: for warps that are usually ahead of the
+// barrier (their wake-up latency is hidden), so that they do not re-poll on
+// every mbarrier event of the CTA as the suspend-hint wait does
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity, uint32_t ns) {
+  uint32_t ok;
+  for (;;) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (ok) break;
+    __nanosleep(ns);
+  }
+}
+
 // global -> shared bulk copy completing on an mbarrier (bytes % 16 == 0, 16-B aligned)
 __device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(

@@ -184,7 +184,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
   const int nwork = hi - lo;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t acc_stride = (uint32_t)Mh * NT;          // TMEM columns per accumulator stage
-  const int NA = (int)(512u / acc_stride) >= 4 ? 4 : (int)(512u / acc_stride);  // accumulator stages
+  constexpr int NA = 4;                                    // accumulator stages (Np <= 256: 4 x 128 columns)
   const uint32_t tcols = acc_stride * NA;
   const int cur = (int)(p.t & p.rp_mask);
 
@@ -210,13 +210,16 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = *tmem_holder;
+  unsigned long long gt_start = 0;
+  if (p.dbg && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt_start));
 
   if (warp == prod_warp) {
     // ------------------------------------------------------------ producer (TMA)
     // the whole warp walks the work list (convergent waits); lane 0 issues
     int prev_core = -1, jw = -1;
-    for (int k = 0; k < nwork; ++k) {
-      const int idx = lo + k, cl = idx / nT, tile = idx - cl * nT, c = p.c_lo + cl;
+    int cl = lo / nT, tile = lo - (lo / nT) * nT;   // work item lo + k, advanced incrementally
+    for (int k = 0; k < nwork; ++k, tile = (tile + 1 == nT) ? (++cl, 0) : tile + 1) {
+      const int c = p.c_lo + cl;
       const int s = k % NS, u = k / NS;
       if (c != prev_core) {
         ++jw;
@@ -256,8 +259,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
     const uint32_t id = tc::idesc_i8(128, NT);
     const uint32_t lbo_a = (uint32_t)Np * 16, lbo_b = (uint32_t)NT * 16;   // tc.h layout
     int prev_core = -1, jw = -1;
-    for (int k = 0; k < nwork; ++k) {
-      const int idx = lo + k, c = idx / nT;
+    int cl = lo / nT, tile = lo - (lo / nT) * nT;
+    for (int k = 0; k < nwork; ++k, tile = (tile + 1 == nT) ? (++cl, 0) : tile + 1) {
+      const int c = cl;
       const int s = k % NS, u = k / NS;
       const int a = k % NA, ua = k / NA;
       if (c != prev_core) {
@@ -282,8 +286,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
         tc::commit(&bars[BEMPTY0 + s]);
         tc::commit(&bars[ACCFULL0 + a]);
         stamp(p, k, 7);
-        const int next_core = (k + 1 < nwork) ? (lo + k + 1) / nT : -1;
-        if (next_core != c) tc::commit(&bars[WFREE]);
+        if (k + 1 == nwork || tile + 1 == nT) tc::commit(&bars[WFREE]);   // last tile of this core
       }
       __syncwarp();
     }
@@ -296,8 +299,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
     uint32_t* lut = reinterpret_cast<uint32_t*>(smem + L.lut);
     for (int b = et; b < 16; b += kExpThreads) lut[b] = tc::nib2bytes((uint32_t)b);
     named_sync(2, kExpThreads);
-    for (int k = 0; k < nwork; ++k) {
-      const int idx = lo + k, cl = idx / nT, tile = idx - cl * nT, c = p.c_lo + cl;
+    int cl = lo / nT, tile = lo - (lo / nT) * nT;
+    for (int k = 0; k < nwork; ++k, tile = (tile + 1 == nT) ? (++cl, 0) : tile + 1) {
+      const int c = p.c_lo + cl;
       const int s = k % NS, u = k / NS;
       const int s0 = tile * NT, ns = min(NT, p.S - s0);
       uint8_t* st = smem + L.stage + s * L.stage_bytes;
@@ -446,13 +450,17 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
         ptx::cp_async_commit();
       }
     }
+    long long dbg_wait = 0;
+    const long long dbg_t0 = p.dbg ? clock64() : 0;
     for (int k = 0; k < nwork; ++k, dst += tile_stride) {
       const int c = p.c_lo + cl;
       const int a = k % NA, ua = k / NA;
       const int s0 = tile * NT, ns = min(NT, p.S - s0);
       const bool pf = load && k + 1 < nwork;
       const uint4* nsrc = dst + tile_stride;
-      ptx::mbar_wait_sleep(&bars[ACCFULL0 + a], ua & 1, 2000);
+      const long long tw0 = p.dbg ? clock64() : 0;
+      ptx::mbar_wait_backoff(&bars[ACCFULL0 + a], ua & 1, 128);
+      if (p.dbg && blockIdx.x == 0) dbg_wait += clock64() - tw0;
       if (lane == 0 && ew == 0) stamp(p, k, 8);
       tc::fence_after();
       if (active) {
@@ -493,7 +501,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
         }
         const uint32_t acc_addr = tmem + a * acc_stride + ((uint32_t)(q * 32) << 16) + h * NT + jj * 32;
         uint32_t fired = 0u;
-#pragma unroll 1
+#pragma unroll
         for (int sb = 0; sb < kPass; ++sb) {
           uint32_t acc[kSub];
           tc::ld16(acc_addr + sb * kSub, acc);
@@ -588,10 +596,20 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
         ++cl;
       }
     }
+    if (p.dbg && blockIdx.x == 0 && lane == 0) {
+      p.dbg[64 * 16 + 2 * ew] = (unsigned long long)dbg_wait;
+      p.dbg[64 * 16 + 2 * ew + 1] = (unsigned long long)(clock64() - dbg_t0);
+    }
   }
   tc::fence_before();
   __syncthreads();
   if (warp == mma_warp) tc::dealloc(tmem, tcols < 32 ? 32 : tcols);
+  if (p.dbg && threadIdx.x == 0 && blockIdx.x < 256) {
+    unsigned long long gt_end;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt_end));
+    p.dbg[64 * 16 + 64 + 2 * blockIdx.x] = gt_start;
+    p.dbg[64 * 16 + 64 + 2 * blockIdx.x + 1] = gt_end;
+  }
 }
 
 // Input decode (Alg. 1 l.1, "Initial setup and input decode"): the line
@@ -678,12 +696,13 @@ cudaError_t launch_tick_tc(ranc_ctx* ctx, TickParams p) {
     configured = true;
   }
   static const bool dbg = getenv("RANC_DEBUG_TIMELINE") != nullptr;
-  if (dbg && !ctx->d_dbg.p) dev_alloc(ctx, &ctx->d_dbg, 64 * 16 * 8);
+  constexpr int kDbg = 64 * 16 + 64 + 512;   // timeline, per-warp wait/total, per-CTA start/end
+  if (dbg && !ctx->d_dbg.p) dev_alloc(ctx, &ctx->d_dbg, kDbg * 8);
   p.dbg = dbg ? (unsigned long long*)ctx->d_dbg.p : nullptr;
-  if (dbg) cudaMemsetAsync(ctx->d_dbg.p, 0, 64 * 16 * 8, ctx->stream);
+  if (dbg) cudaMemsetAsync(ctx->d_dbg.p, 0, kDbg * 8, ctx->stream);
   tick_tc_kernel<<<grid, kThreadsTC, smem, ctx->stream>>>(p);
   if (dbg) {
-    unsigned long long h[64 * 16];
+    static unsigned long long h[kDbg];
     cudaMemcpyAsync(h, ctx->d_dbg.p, sizeof h, cudaMemcpyDeviceToHost, ctx->stream);
     cudaStreamSynchronize(ctx->stream);
     const unsigned long long t0 = h[0];
@@ -694,6 +713,20 @@ cudaError_t launch_tick_tc(ranc_ctx* ctx, TickParams p) {
       for (int j = 0; j < 16; ++j) fprintf(stderr, " %8lld", h[k * 16 + j] ? (long long)(h[k * 16 + j] - t0) : -1LL);
       fprintf(stderr, "\n");
     }
+    fprintf(stderr, "epilogue warps of CTA 0: ACCFULL wait / total cycles\n");
+    for (int w = 0; w < kEpiWarps; ++w)
+      fprintf(stderr, "  ew%-2d %10llu %10llu\n", w, h[64 * 16 + 2 * w], h[64 * 16 + 2 * w + 1]);
+    unsigned long long s_min = ~0ull, e_min = ~0ull, e_max = 0;
+    for (int b = 0; b < std::min(grid, 256); ++b) {
+      s_min = std::min(s_min, h[64 * 16 + 64 + 2 * b]);
+      e_min = std::min(e_min, h[64 * 16 + 64 + 2 * b + 1]);
+      e_max = std::max(e_max, h[64 * 16 + 64 + 2 * b + 1]);
+    }
+    fprintf(stderr, "CTA end times (ns after first start): min %llu max %llu; slowest CTAs:", e_min - s_min,
+            e_max - s_min);
+    for (int b = 0; b < std::min(grid, 256); ++b)
+      if (h[64 * 16 + 64 + 2 * b + 1] + 20000 > e_max) fprintf(stderr, " %d", b);
+    fprintf(stderr, "\n");
   }
   return cudaGetLastError();
 }
