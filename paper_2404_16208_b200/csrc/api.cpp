@@ -94,7 +94,7 @@ ranc_status sync(ranc_ctx* ctx, const char* where) {
 void free_all(ranc_ctx* ctx) {
   DevBuf* bufs[] = {&ctx->d_xp, &ctx->d_wp, &ctx->d_pword, &ctx->d_prm, &ctx->d_route, &ctx->d_inl,
                     &ctx->d_has_in, &ctx->d_init, &ctx->d_wfold, &ctx->d_route_tc, &ctx->d_runs,
-                    &ctx->d_nruns, &ctx->d_wflags_tc, &ctx->d_word_runs, &ctx->d_pot, &ctx->d_ring, &ctx->d_counts, &ctx->d_lines,
+                    &ctx->d_nruns, &ctx->d_wflags_tc, &ctx->d_incoming, &ctx->d_word_runs, &ctx->d_pot, &ctx->d_ring, &ctx->d_counts, &ctx->d_lines,
                     &ctx->d_stage, &ctx->d_raster, &ctx->d_fired, &ctx->d_exports, &ctx->d_send, &ctx->d_recv,
                     &ctx->d_send_list, &ctx->d_recv_list, &ctx->d_dbg, &ctx->d_inw, &ctx->d_inslot,
                     &ctx->d_slot_core};
@@ -207,6 +207,7 @@ ranc_status ranc_load_network(const ranc_network_desc* net, int cuda_device, ran
   if (!s && c.tc_ok) s = upload(ctx, &ctx->d_runs, c.runs);
   if (!s && c.tc_ok) s = upload(ctx, &ctx->d_nruns, c.nruns);
   if (!s && c.tc_ok) s = upload(ctx, &ctx->d_wflags_tc, c.wflags_tc);
+  if (!s && c.tc_ok) s = upload(ctx, &ctx->d_incoming, c.incoming);
   if (!s && c.tc_ok) s = upload(ctx, &ctx->d_word_runs, c.word_runs);
   if (!s) {
     int sms = 0;

@@ -330,6 +330,12 @@ ranc_status validate_and_compile(const ranc_network_desc* d, Compiled* out, std:
         const int dap = o.inv_tc[(size_t)dc * A + d->dest_axon[cn]];
         r.x = (r.x & 0xFFu) | ((uint32_t)dap << 8);
       }
+    // cores that no neuron routes to keep an all-zero scheduler ring: the
+    // tensor-core tick neither loads nor clears their rows
+    o.incoming.assign(G, 0);
+    for (int c = 0; c < G; ++c)
+      for (int n = 0; n < N; ++n)
+        if (route_kind(o.route_tc[(size_t)c * Np + n].x) == RK_ROUTE) o.incoming[o.route_tc[(size_t)c * Np + n].y] = 1;
     // warps whose routing neurons all deposit into one ring word ("block
     // routes", e.g. the 32 neurons of an MNIST-layer core feeding 32 axons
     // of the next layer): the epilogue OR-reduces them into one deposit

@@ -75,6 +75,7 @@ struct TickParams {
   const uint8_t* exports;   // [G] core has a neuron routing to another rank
   unsigned long long* dbg;  // optional pipeline timeline (RANC_DEBUG_TIMELINE)
   const uint8_t* wflags;    // [G][Npad/32] per-warp flags (bit 0: block route), or nullptr
+  const uint8_t* incoming;  // [G] 1 if any neuron of the network routes to the core (its ring can be non-zero)
   int32_t dbgflags;         // RANC_DEBUG_FLAGS (timing experiments only; results invalid when set)
 };
 
@@ -91,6 +92,7 @@ struct Compiled {
   std::vector<int2> runs;       // [G][rmax] input runs: x = a'start | len<<16, y = first line
   std::vector<int32_t> nruns;   // [G]
   std::vector<int32_t> word_runs;  // [G][W] first run | count << 16 (runs overlapping word w)
+  std::vector<uint8_t> incoming;   // [G] 1 if some neuron routes to the core
   std::vector<uint8_t> wflags_tc;  // [G][Npad/32] bit 0: all routing neurons of the warp share one
                                    // (dest core, ring word, delay) in the tensor-core axon order
   int32_t rmax = 0;
@@ -126,7 +128,7 @@ struct ranc_ctx {
   std::string err;
   ranc::Compiled net;
   // device: compiled network
-  ranc::DevBuf d_xp, d_wp, d_pword, d_prm, d_route, d_inl, d_has_in, d_init, d_wfold, d_route_tc, d_runs, d_nruns, d_wflags_tc,
+  ranc::DevBuf d_xp, d_wp, d_pword, d_prm, d_route, d_inl, d_has_in, d_init, d_wfold, d_route_tc, d_runs, d_nruns, d_wflags_tc, d_incoming,
       d_word_runs;
   int num_sms = 148;
   // device: state

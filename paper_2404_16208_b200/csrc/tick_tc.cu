@@ -48,10 +48,12 @@ constexpr int NT = 64;                 // samples per tile (MMA N)
 constexpr int NS = 4;                  // spike-stage pipeline depth
 constexpr int kExpWarps = 4;
 constexpr int kEpiWarps = 16;
-// Warp ids: 0..15 epilogue (TMEM lane quarter = warp % 4, so every SMSP holds
-// four epilogue warps to hide the LIF's dependency latencies), 16..19 spike
-// stage, 20 producer, 21 MMA issuer.
-constexpr int kFirstEpi = 0, kFirstExp = kEpiWarps, kProdWarp = kFirstExp + 4, kMmaWarp = kProdWarp + 1;
+// Warp ids (SMSP = warp % 4): 0..15 epilogue (TMEM lane quarter = warp % 4,
+// so every SMSP holds four epilogue warps to hide the LIF's dependency
+// latencies); 16..19 spike stage; 20 producer; 21 MMA issuer.
+constexpr int kFirstEpi = 0, kProdWarp = kEpiWarps + 4, kMmaWarp = kEpiWarps + 5;
+__device__ __forceinline__ bool is_spike_warp(int w) { return w >= kEpiWarps && w < kEpiWarps + 4; }
+__device__ __forceinline__ int spike_thread(int w, int lane) { return 32 * (w - kEpiWarps) + lane; }
 constexpr int kThreadsTC = 32 * (2 + kExpWarps + kEpiWarps);  // 704
 constexpr int kExpThreads = 32 * kExpWarps;
 constexpr int kSub = 16;               // samples per TMEM load / LIF pass of an epilogue warp
@@ -240,11 +242,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
         const bool inject = p.t < p.T_in && p.nruns[c] > 0;
         // decoded inputs: the tile's input words in ring-row layout; else the raw line rows
         const int slot = p.inw ? p.inslot[cl] : -1;
-        const uint32_t ring_bytes = (uint32_t)NT * W * 4;
+        const uint32_t ring_bytes = p.incoming[c] ? (uint32_t)NT * W * 4 : 0u;
         const uint32_t line_bytes = !inject ? 0u : (p.inw ? (uint32_t)NT * W * 4 : (uint32_t)NT * WIp * 4);
         ptx::mbar_arrive_expect_tx(&bars[FULL0 + s], ring_bytes + line_bytes);
-        ptx::bulk_g2s(st + L.raw, p.ring + (((size_t)cur * p.G_loc + cl) * p.Sr + s0) * W, ring_bytes,
-                      &bars[FULL0 + s]);
+        if (ring_bytes)
+          ptx::bulk_g2s(st + L.raw, p.ring + (((size_t)cur * p.G_loc + cl) * p.Sr + s0) * W, ring_bytes,
+                        &bars[FULL0 + s]);
         if (inject && p.inw)
           ptx::bulk_g2s(st + L.lines, p.inw + (((size_t)p.t * p.n_inslots + slot) * p.Sr + s0) * W, line_bytes,
                         &bars[FULL0 + s]);
@@ -290,9 +293,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       }
       __syncwarp();
     }
-  } else if (warp >= kFirstExp && warp < kProdWarp) {
+  } else if (is_spike_warp(warp)) {
     // ------------------------------------------------------------ spike stage
-    const int et = threadIdx.x - 32 * kFirstExp;
+    const int et = spike_thread(warp, lane);
     int runs_core = -1;
     // nibble -> four 0/1 bytes; a 16-entry u32 table spans 16 distinct banks,
     // so the lookups never conflict
@@ -312,7 +315,14 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       ptx::mbar_wait_sleep(&bars[FULL0 + s], u & 1, 2000);
       if (et == 0) stamp(p, k, 2);
       uint32_t* row = p.ring + (((size_t)cur * p.G_loc + cl) * p.Sr + s0) * W;
-      for (int i = et; i < ns * W; i += kExpThreads) row[i] = 0u;
+      if (p.incoming[c]) {
+        // only the words that hold spikes need clearing
+        for (int i = et; i < ns * W; i += kExpThreads)
+          if (raw[i]) row[i] = 0u;
+      } else {
+        // no neuron routes here: the ring stays zero and was not loaded
+        for (int i = et; i < NT * W; i += kExpThreads) raw[i] = 0u;
+      }
       if (et == 0) stamp(p, k, 12);
       // a2: external inputs.  Thread <-> (sample, ring word): OR in the line
       // runs overlapping that word (no atomics: every word has one owner)
@@ -459,6 +469,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       const bool pf = load && k + 1 < nwork;
       const uint4* nsrc = dst + tile_stride;
       const long long tw0 = p.dbg ? clock64() : 0;
+      // one warp per lane quarter polls the accumulator barrier; the other
+      // three wait on the quarter's named barrier (no issue slots spent)
+      // back-off polling (measured best against the suspend-hint wait, a plain
+      // spin and a per-quarter named barrier)
       ptx::mbar_wait_backoff(&bars[ACCFULL0 + a], ua & 1, 128);
       if (p.dbg && blockIdx.x == 0) dbg_wait += clock64() - tw0;
       if (lane == 0 && ew == 0) stamp(p, k, 8);
@@ -680,6 +694,7 @@ cudaError_t launch_tick_tc(ranc_ctx* ctx, TickParams p) {
   p.ST = NT;
   p.route = (const uint2*)ctx->d_route_tc.p;
   p.wflags = (const uint8_t*)ctx->d_wflags_tc.p;
+  p.incoming = (const uint8_t*)ctx->d_incoming.p;
   p.runs = (const int2*)ctx->d_runs.p;
   p.word_runs = (const int32_t*)ctx->d_word_runs.p;
   p.inw = ctx->inw_valid ? (const uint32_t*)ctx->d_inw.p : nullptr;
@@ -695,6 +710,8 @@ cudaError_t launch_tick_tc(ranc_ctx* ctx, TickParams p) {
     cudaFuncSetAttribute(tick_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     configured = true;
   }
+  static const int dflags = getenv("RANC_DEBUG_FLAGS") ? atoi(getenv("RANC_DEBUG_FLAGS")) : 0;
+  p.dbgflags = dflags;
   static const bool dbg = getenv("RANC_DEBUG_TIMELINE") != nullptr;
   constexpr int kDbg = 64 * 16 + 64 + 512;   // timeline, per-warp wait/total, per-CTA start/end
   if (dbg && !ctx->d_dbg.p) dev_alloc(ctx, &ctx->d_dbg, kDbg * 8);
