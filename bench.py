@@ -66,6 +66,9 @@ WORKLOADS = {
     "vmm256": (_vmm("vmm256"), 1000, "samples"),
     "vmm1024": (_vmm("vmm1024"), 1000, "samples"),
     "config5": (_cfg(5), 64, "cores"),
+    # streaming: the config-3 net fed one image per tick,
+    # 10000 images in 10003 ticks, one sample (10010 ticks)
+    "stream": (lambda S: __import__("workloads.gen", fromlist=["x"]).config3_stream(10000), 1, "samples"),
 }
 
 
@@ -345,6 +348,12 @@ def run_ours(args, rank, world, local):
         alg_bytes = bpt * G_loc * S_local
         achieved = alg_bytes / (tick_ms / 1e3) / 1e9
         info = sim.info()
+        kname = ("tick_tc_kernel" if info["kernel"] == 2 else
+                 "tick_stream_kernel" if launches == args.steps else "tick_popc_kernel")
+        traffic = None   # measured DRAM bytes per launch (ncu --set full), when profiled for this workload
+        tpath = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tpath) and S_local == args.samples:
+            traffic = json.load(open(tpath)).get(kname, {}).get(net.name)
         state_gb = (2 * net.neurons * net.G + 4 * info["ring_rows"] * info["ring_words"] * net.G) * args.samples / 1e9
         line = {
             "metric": METRIC if args.workload == "config3" else f"simulated core-ticks/sec & samples/sec, {net.name}",
@@ -358,23 +367,27 @@ def run_ours(args, rank, world, local):
                        "l2": (f"state {state_gb:.2f} GB exceeds the 126 MB L2; no flush needed" if state_gb > 0.126
                               else f"state {state_gb * 1e3:.1f} MB fits in L2 (latency-bound workload)"),
                        "sample_tile": info["sample_tile"], "pieces": info["pieces"],
-                       "kernel": "tcgen05 kind::i8" if info["kernel"] == 2 else "popcount"},
+                       "kernel": ("tcgen05 kind::i8" if info["kernel"] == 2 else
+                                  "popcount, streaming (one cooperative launch per run)" if launches == args.steps
+                                  else "popcount")},
             "core_ticks_per_s": core_ticks_s,
+            "ticks_per_s": samples_s * T / max(1, args.samples),
             "tick_kernel_ms": tick_ms,
             "gpu_launches": launches,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "traffic": None,
-                         "kernel": "tick_tc_kernel" if info["kernel"] == 2 else "tick_popc_kernel",
+                         "frac": achieved / hbm, "traffic": traffic,
+                         "kernel": kname,
                          "note": f"{bpt} B/core-tick x {G_loc} cores x {S_local} samples per "
                                  "launch / mean launch time (CUDA events on the launch stream); peak = "
-                                 "MEASURED_PEAKS.json hbm_gbs"},
+                                 "MEASURED_PEAKS.json hbm_gbs; traffic = ncu dram bytes per launch "
+                                 "(profiles/traffic.json)"},
             "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(inp.line_bits.nbytes),
                     "d2h_bytes_per_step": int(counts.nbytes)},
             "clocks": clk.summary(),
         }
         if not args.no_cpu_baseline and world == 1:
             cores = max(1, min(host_cores(), 32))
-            n = args.cpu_samples or min(args.samples, 2 * cores)
+            n = args.cpu_samples or min(args.samples, 8 * cores)   # ~10-20 s of oracle work
             ticks = oracle_plan(net, n, cores)
             v, wall, per_core = time_oracle(net, inp_all, n, cores, ticks)
             line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",

@@ -173,9 +173,18 @@ ranc_status ranc_set_allocator(ranc_ctx* ctx, void* (*alloc)(size_t, void*),
  * T_in x input cores x S x ceil(A/32) x 4 bytes of device memory, skipped when
  * that exceeds a quarter of the free memory); 0: gather the line runs every
  * tick.  Takes effect at the next ranc_load_inputs / ranc_reset_state.
- * RANC_OPT_KERNEL: 0 automatic, 1 popcount, 2 tensor core (see ranc_info.kernel). */
+ * RANC_OPT_KERNEL: 0 automatic (tensor core when the network is eligible and
+ * S > 64, else popcount), 1 popcount, 2 tensor core (see ranc_info.kernel). */
 #define RANC_OPT_SAMPLE_TILE 1
 #define RANC_OPT_INPUT_DECODE 2
+/* RANC_OPT_STREAM (streaming mode: one long stream of inputs,
+ * ~1 image per tick): 0 (default) automatic -- when the popcount
+ * kernel is active, the context is not core-sharded and a tick has few
+ * (core, sample-tile) items, a ranc_run_ticks call of >= 2 ticks runs as ONE
+ * cooperative launch whose grid barrier is the tick barrier;
+ * 1 always per-tick launches; 2 always the cooperative launch when possible.
+ * Results are identical either way. */
+#define RANC_OPT_STREAM 4
 #define RANC_OPT_KERNEL 3
 ranc_status ranc_set_option(ranc_ctx* ctx, int option, int64_t value);
 

@@ -19,6 +19,7 @@ TRACE_OUTPUT_EVENTS = 2
 OPT_SAMPLE_TILE = 1
 OPT_INPUT_DECODE = 2
 OPT_KERNEL = 3
+OPT_STREAM = 4
 SHARD_SAMPLES = 0
 SHARD_CORES = 1
 

@@ -283,7 +283,11 @@ ranc_status ranc_reset_state(ranc_ctx* ctx) {
   CK(cudaSetDevice(ctx->device), "cudaSetDevice");
   CK(launch_reset(ctx), "reset kernel");
   // latch the kernel variant (the potential layout is re-initialised here)
-  ctx->kernel_active = (ctx->kernel == RANC_KERNEL_POPC || !ctx->net.tc_ok || tc_smem_bytes(ctx->net) > 227 * 1024)
+  // automatic choice: the tensor-core path needs whole 64-sample tiles to pay
+  // off; one tile or less per core (e.g. streaming, S = 1) runs the popcount path
+  const bool tc_auto = ctx->kernel == 0 && ctx->S > 64;
+  ctx->kernel_active = (ctx->kernel == RANC_KERNEL_POPC || (ctx->kernel == 0 && !tc_auto) || !ctx->net.tc_ok ||
+                        tc_smem_bytes(ctx->net) > 227 * 1024)
                            ? RANC_KERNEL_POPC
                            : RANC_KERNEL_TC;
   TRY(prepare_inputs_tc(ctx));
@@ -333,6 +337,16 @@ ranc_status ranc_run_ticks(ranc_ctx* ctx, int64_t num_ticks) {
   }
   TRY(prepare_run(ctx, num_ticks));
   const bool exchange = ctx->shard_mode == RANC_SHARD_CORES && ctx->nccl_comm && ctx->world > 1;
+  if (!exchange && stream_eligible(ctx, num_ticks)) {
+    // streaming mode: every tick of this call in one cooperative launch
+    int64_t left = num_ticks;
+    while (left > 0) {
+      const int64_t chunk = std::min<int64_t>(left, 1 << 30);
+      CK(launch_stream(ctx, chunk), "stream kernel launch");
+      left -= chunk;
+    }
+    return RANC_OK;
+  }
   for (int64_t i = 0; i < num_ticks; ++i) {
     const int64_t t = ctx->now;
     CK(launch_one_tick(ctx), "tick kernel launch");
@@ -575,6 +589,13 @@ ranc_status ranc_set_option(ranc_ctx* ctx, int option, int64_t value) {
     case RANC_OPT_INPUT_DECODE:
       ctx->input_decode = value ? 1 : 0;
       ctx->inw_valid = false;
+      return RANC_OK;
+    case RANC_OPT_STREAM:
+      if (value < 0 || value > 2) {
+        ctx->err = "stream option must be 0 (auto), 1 (per-tick launches) or 2 (one cooperative launch per run)";
+        return RANC_E_ARG;
+      }
+      ctx->stream_opt = (int32_t)value;
       return RANC_OK;
     case RANC_OPT_KERNEL:
       if (value < 0 || value > 2) {

@@ -142,6 +142,7 @@ struct ranc_ctx {
   int32_t sample_tile = 0;       // in use (set by ranc_run_ticks)
   int32_t sample_tile_opt = 0;   // RANC_OPT_SAMPLE_TILE, 0 = automatic
   int32_t input_decode = 1;      // RANC_OPT_INPUT_DECODE
+  int32_t stream_opt = 0;        // RANC_OPT_STREAM: 0 auto, 1 off, 2 on
   int32_t kernel = 0;            // RANC_OPT_KERNEL request: 0 auto, 1 popcount, 2 tensor core
   int32_t kernel_active = 1;     // latched at every reset (the potential layout depends on it)
   int64_t launches = 0;
@@ -195,6 +196,8 @@ int tc_tile();
 size_t tc_smem_bytes(const Compiled& n);
 cudaError_t launch_tick_tc(ranc_ctx* ctx, TickParams p);
 cudaError_t decode_inputs_tc(ranc_ctx* ctx);
+bool stream_eligible(const ranc_ctx* ctx, int64_t num_ticks);
+cudaError_t launch_stream(ranc_ctx* ctx, int64_t num_ticks);
 // api.cpp
 ranc_status dev_alloc(ranc_ctx* ctx, DevBuf* b, size_t bytes);
 void dev_free(ranc_ctx* ctx, DevBuf* b);

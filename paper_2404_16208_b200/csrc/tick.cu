@@ -25,10 +25,14 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cooperative_groups.h>
+
 #include <algorithm>
 
 #include "internal.h"
 #include "ptx.h"
+
+namespace cg = cooperative_groups;
 
 namespace ranc {
 
@@ -54,12 +58,13 @@ __host__ __device__ inline SmemLayout smem_layout(int ST, int Npad, int W, int E
   return L;
 }
 
-template <int E>
-__global__ void __launch_bounds__(kThreads, (E <= 12 ? 4 : (E <= 16 ? 3 : 2))) tick_popc_kernel(const TickParams p) {
-  extern __shared__ __align__(16) uint8_t smem[];
-  const int cl = blockIdx.x;             // local core (state index)
-  const int c = p.c_lo + cl;             // global core (network index)
-  const int s0 = blockIdx.y * p.ST;
+// One (core, sample tile) of one tick, executed by a whole CTA.  `phase` is
+// the parity of the CTA's potential-tile mbarrier (toggled per use, so that a
+// persistent CTA can process many tiles).
+template <int E, bool kPersistent>
+__device__ __forceinline__ void popc_tile(const TickParams& p, int cl, int tile, uint8_t* smem, uint32_t& phase) {
+  const int c = p.c_lo + cl;             // global core (network index); cl = local core (state index)
+  const int s0 = tile * p.ST;
   const int ns = min(p.ST, p.S - s0);
   const int tid = threadIdx.x;
   const int lane = tid & 31;
@@ -74,11 +79,6 @@ __global__ void __launch_bounds__(kThreads, (E <= 12 ? 4 : (E <= 16 ? 3 : 2))) t
   const uint32_t tile_bytes = (uint32_t)ns * p.Npad * 2;
   int16_t* pot_g = p.pot + ((size_t)cl * p.S + s0) * p.Npad;
 
-  if (tid == 0) {
-    ptx::mbar_init(bar, 1);
-    ptx::fence_mbar_init();
-  }
-  __syncthreads();
   // stream the tile's potentials in (TMA bulk copy) while the spikes are staged
   if (!p.fresh && tid == 0) {
     ptx::mbar_arrive_expect_tx(bar, tile_bytes);
@@ -120,7 +120,10 @@ __global__ void __launch_bounds__(kThreads, (E <= 12 ? 4 : (E <= 16 ? 3 : 2))) t
     pk[i] = raw[s * W + pword[e]];
   }
   __syncthreads();
-  if (!p.fresh) ptx::mbar_wait(bar, 0);
+  if (!p.fresh) {
+    ptx::mbar_wait(bar, phase);
+    phase ^= 1u;
+  }
 
   for (int n = tid; n < p.Npad; n += blockDim.x) {
     uint32_t xp[E];
@@ -189,7 +192,48 @@ __global__ void __launch_bounds__(kThreads, (E <= 12 ? 4 : (E <= 16 ? 3 : 2))) t
   if (tid == 0) {
     ptx::bulk_s2g(pot_g, pot_s, tile_bytes);
     ptx::bulk_commit();
-    ptx::bulk_wait_read0();
+    // persistent: all writes done (not only the shared-memory reads), as
+    // the tile is reloaded in the next tick; otherwise the kernel boundary
+    // completes them
+    if (kPersistent) ptx::bulk_wait0();
+    else ptx::bulk_wait_read0();
+  }
+  if (kPersistent) __syncthreads();   // the shared buffers are reused by the next tile
+}
+
+__device__ __forceinline__ void init_tile_barrier(uint8_t* smem) {
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(reinterpret_cast<uint64_t*>(smem), 1);
+    ptx::fence_mbar_init();
+  }
+  __syncthreads();
+}
+
+template <int E>
+__global__ void __launch_bounds__(kThreads, (E <= 12 ? 4 : (E <= 16 ? 3 : 2))) tick_popc_kernel(const TickParams p) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  init_tile_barrier(smem);
+  uint32_t phase = 0;
+  popc_tile<E, false>(p, blockIdx.x, blockIdx.y, smem, phase);
+}
+
+// Streaming mode (one long stream, few samples): all
+// ticks of a ranc_run_ticks call in one cooperative launch.  Each CTA walks
+// the (core, tile) items of a tick, then the grid barrier is the tick barrier
+// (a7): it orders the ring ORs and potential stores of tick t before
+// the reads of tick t+1.
+template <int E>
+__global__ void __launch_bounds__(kThreads, 1) tick_stream_kernel(TickParams p, int nticks, int n_tiles) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  init_tile_barrier(smem);
+  uint32_t phase = 0;
+  cg::grid_group grid = cg::this_grid();
+  const int items = p.G_loc * n_tiles;
+  for (int it = 0; it < nticks; ++it) {
+    for (int w = blockIdx.x; w < items; w += gridDim.x) popc_tile<E, true>(p, w % p.G_loc, w / p.G_loc, smem, phase);
+    p.fresh = 0;
+    ++p.t;
+    grid.sync();
   }
 }
 
@@ -213,6 +257,23 @@ cudaError_t launch_one(const TickParams& p, dim3 grid, size_t smem, cudaStream_t
   }
   tick_popc_kernel<E><<<grid, kThreads, smem, st>>>(p);
   return cudaGetLastError();
+}
+
+template <int E>
+cudaError_t launch_stream_e(TickParams p, int nticks, size_t smem, int n_tiles, int num_sms, cudaStream_t st) {
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(tick_stream_kernel<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    configured = true;
+  }
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tick_stream_kernel<E>, kThreads, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorCooperativeLaunchTooLarge;
+  const int items = p.G_loc * n_tiles;
+  const int grid = std::max(1, std::min(items, per_sm * num_sms));
+  void* args[] = {&p, &nticks, &n_tiles};
+  return cudaLaunchCooperativeKernel((const void*)tick_stream_kernel<E>, dim3(grid), dim3(kThreads), args, smem, st);
 }
 
 }  // namespace
@@ -292,6 +353,37 @@ TickParams make_params(ranc_ctx* ctx) {
 }
 
 }  // namespace
+
+bool stream_eligible(const ranc_ctx* ctx, int64_t num_ticks) {
+  if (ctx->kernel_active != RANC_KERNEL_POPC || ctx->shard_mode == RANC_SHARD_CORES || num_ticks < 2) return false;
+  if (ctx->stream_opt == 1) return false;
+  if (ctx->stream_opt == 2) return true;
+  // automatic: few (core, tile) items per tick, where per-tick launches dominate
+  const int64_t tiles = (ctx->S + ctx->sample_tile - 1) / ctx->sample_tile;
+  return (int64_t)ctx->G_loc * tiles <= 4 * 148 * 4;
+}
+
+cudaError_t launch_stream(ranc_ctx* ctx, int64_t num_ticks) {
+  const Compiled& n = ctx->net;
+  TickParams p = make_params(ctx);
+  const int n_tiles = (int)((ctx->S + p.ST - 1) / p.ST);
+  const size_t smem = smem_layout(p.ST, n.Npad, n.W, n.E, n.WIp).total;
+  const int nt = (int)std::min<int64_t>(num_ticks, 1 << 30);
+  cudaError_t e;
+  switch (n.E) {
+    case 4: e = launch_stream_e<4>(p, nt, smem, n_tiles, ctx->num_sms, ctx->stream); break;
+    case 8: e = launch_stream_e<8>(p, nt, smem, n_tiles, ctx->num_sms, ctx->stream); break;
+    case 12: e = launch_stream_e<12>(p, nt, smem, n_tiles, ctx->num_sms, ctx->stream); break;
+    case 16: e = launch_stream_e<16>(p, nt, smem, n_tiles, ctx->num_sms, ctx->stream); break;
+    case 24: e = launch_stream_e<24>(p, nt, smem, n_tiles, ctx->num_sms, ctx->stream); break;
+    default: e = launch_stream_e<36>(p, nt, smem, n_tiles, ctx->num_sms, ctx->stream); break;
+  }
+  ctx->launches++;
+  if (e != cudaSuccess) return e;
+  ctx->fresh = false;
+  ctx->now += nt;
+  return cudaSuccess;
+}
 
 cudaError_t launch_one_tick(ranc_ctx* ctx) {
   const Compiled& n = ctx->net;

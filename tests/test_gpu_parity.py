@@ -4,7 +4,7 @@ for every potential, pending spike, fired bit, output event and class count
 import numpy as np
 import pytest
 
-from workloads.gen import (config1, config2, config3, config5, corpus_case, tiny_case, vmm)
+from workloads.gen import (config1, config2, config3, config3_stream, config5, corpus_case, tiny_case, vmm)
 
 pytestmark = pytest.mark.gpu
 
@@ -302,4 +302,65 @@ def test_sample_sharded_comm_world1(ranc, oracle_mod):
     sim.comm_init(ranc.Simulator.unique_id(), 1, 0)
     sim.load_inputs(inp).run(17)
     assert np.array_equal(sim.gather_outputs(20, 0, 0), sim.outputs())
+    sim.close()
+
+
+# ---- streaming mode: one cooperative launch per run ----------
+
+
+def stream_run(ranc, oracle_mod, net, inp, pieces, stream, trace=True):
+    sim = ranc.Simulator(net)
+    sim.set_option(ranc.OPT_KERNEL, 1)
+    sim.set_option(ranc.OPT_STREAM, stream)
+    if trace:
+        sim.set_trace(ranc.TRACE_OUTPUT_EVENTS)
+    sim.load_inputs(inp)
+    assert sim.info()["kernel"] == 1
+    launches0 = sim.info()["kernel_launches"]
+    for k in pieces:
+        sim.run(k)
+    launches = sim.info()["kernel_launches"] - launches0
+    T = sum(pieces)
+    o = oracle_mod.Oracle(net, inp).run(T)
+    assert np.array_equal(sim.outputs(), o.counts())
+    assert np.array_equal(sim.potentials(), o.potentials())
+    assert np.array_equal(sim.pending(), o.pending())
+    if trace:
+        assert np.array_equal(sim.events(), o.events())
+    sim.close()
+    return launches
+
+
+@pytest.mark.parametrize("stream", [1, 2])
+def test_stream_config3_one_image_per_tick(ranc, oracle_mod, stream):
+    net, inp = config3_stream(40)
+    T = net.meta["T"]
+    launches = stream_run(ranc, oracle_mod, net, inp, [T], stream)
+    assert launches == (1 if stream == 2 else T)
+
+
+def test_stream_resumable_in_pieces(ranc, oracle_mod):
+    net, inp = config3_stream(30)
+    stream_run(ranc, oracle_mod, net, inp, [1, 7, 2, 13, 11], 2)
+
+
+@pytest.mark.parametrize("stream", [0, 2])
+def test_stream_config1_and_config2(ranc, oracle_mod, stream):
+    net, inp = config1(T=64)
+    stream_run(ranc, oracle_mod, net, inp, [64], stream)
+    net, inp = config2(S=48)
+    stream_run(ranc, oracle_mod, net, inp, [5, net.meta["T"] - 5], stream)
+
+
+@pytest.mark.parametrize("seed", range(0, 30))
+def test_stream_corpus(ranc, oracle_mod, seed):
+    net, inp = corpus_case(seed)
+    stream_run(ranc, oracle_mod, net, inp, [3, 17], 2, trace=False)
+
+
+def test_auto_kernel_small_batch_uses_popcount(ranc):
+    net, inp = config3_stream(5)
+    sim = ranc.Simulator(net)
+    sim.load_inputs(inp)
+    assert sim.info()["kernel"] == 1   # S = 1 <= 64: popcount path (+ streaming launch)
     sim.close()

@@ -110,6 +110,33 @@ def synthetic_digits(S, T_in, seed, protos=None):
     return inp, labels
 
 
+def stream_digits(n_images, seed, protos=None):
+    """Paper-faithful streaming input (10000 test
+    images in 10010 ticks): ONE sample whose input at tick t is image t
+    (prototype of class U{0..9}, shifted U[-2,2] px, 5% flips), each 'on'
+    pixel spiking once, at that tick.  Returns (Inputs, labels)."""
+    protos = digit_prototypes() if protos is None else protos
+    rng = substream(seed, "stream-digits")
+    labels = rng.ints(n_images, 0, 9)
+    shifts = rng.ints(2 * n_images, -2, 2).reshape(n_images, 2)
+    flips = rng.bernoulli(n_images * 784, 0.05).reshape(n_images, 28, 28)
+    spk = np.zeros((1, n_images, 784), bool)
+    for t in range(n_images):
+        img = np.roll(protos[labels[t]], (int(shifts[t, 0]), int(shifts[t, 1])), axis=(0, 1)) ^ flips[t]
+        spk[0, t] = img.reshape(784)
+    return Inputs.from_dense(spk, labels=labels), labels
+
+
+def config3_stream(n_images=10000, seed=1003, inputs_seed=2013):
+    """The config-3 network fed one image per tick (streaming, f2);
+    T = n_images + 3 drains the 4-layer pipeline."""
+    net, _ = config3(seed=seed, S=0)
+    net.name = "config3-stream"
+    inp, _ = stream_digits(n_images, inputs_seed)
+    net.meta.update(T=n_images + 3)
+    return net, inp
+
+
 # ----------------------------------------------------------------------------
 # config 1: single 256x256 core
 # ----------------------------------------------------------------------------
