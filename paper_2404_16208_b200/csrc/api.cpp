@@ -42,13 +42,16 @@ ranc_status dev_alloc(ranc_ctx* ctx, DevBuf* b, size_t bytes) {
   }
   b->p = p;
   b->bytes = bytes;
+  b->user = ctx->user_alloc != nullptr;
   ctx->device_bytes += (int64_t)bytes;
   return RANC_OK;
 }
 
 void dev_free(ranc_ctx* ctx, DevBuf* b) {
   if (!b->p) return;
-  if (ctx->user_free) ctx->user_free(b->p, ctx->user);
+  // a buffer is released by the allocator that made it (network buffers are
+  // allocated before ranc_set_allocator may be called)
+  if (b->user) ctx->user_free(b->p, ctx->user);
   else cudaFreeAsync(b->p, ctx->stream);
   ctx->device_bytes -= (int64_t)b->bytes;
   b->p = nullptr;

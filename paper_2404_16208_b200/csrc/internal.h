@@ -112,6 +112,7 @@ struct Compiled {
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
+  bool user = false;   // allocated by the ranc_set_allocator callback (freed by it too)
 };
 
 }  // namespace ranc
@@ -196,7 +197,7 @@ int tc_tile();
 size_t tc_smem_bytes(const Compiled& n);
 cudaError_t launch_tick_tc(ranc_ctx* ctx, TickParams p);
 cudaError_t decode_inputs_tc(ranc_ctx* ctx);
-bool stream_eligible(const ranc_ctx* ctx, int64_t num_ticks);
+bool stream_eligible(ranc_ctx* ctx, int64_t num_ticks);
 cudaError_t launch_stream(ranc_ctx* ctx, int64_t num_ticks);
 // api.cpp
 ranc_status dev_alloc(ranc_ctx* ctx, DevBuf* b, size_t bytes);

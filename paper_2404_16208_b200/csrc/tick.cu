@@ -28,6 +28,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "internal.h"
 #include "ptx.h"
@@ -61,8 +62,11 @@ __host__ __device__ inline SmemLayout smem_layout(int ST, int Npad, int W, int E
 // One (core, sample tile) of one tick, executed by a whole CTA.  `phase` is
 // the parity of the CTA's potential-tile mbarrier (toggled per use, so that a
 // persistent CTA can process many tiles).
-template <int E, bool kPersistent>
-__device__ __forceinline__ void popc_tile(const TickParams& p, int cl, int tile, uint8_t* smem, uint32_t& phase) {
+// kResident (streaming kernel): the tile's potentials live in shared memory
+// at pot_res for the whole run (no HBM round trip per tick).
+template <int E, bool kResident>
+__device__ __forceinline__ void popc_tile(const TickParams& p, int cl, int tile, uint8_t* smem, uint32_t& phase,
+                                          int16_t* pot_res) {
   const int c = p.c_lo + cl;             // global core (network index); cl = local core (state index)
   const int s0 = tile * p.ST;
   const int ns = min(p.ST, p.S - s0);
@@ -71,7 +75,7 @@ __device__ __forceinline__ void popc_tile(const TickParams& p, int cl, int tile,
   const int W = p.W;
   const SmemLayout L = smem_layout(p.ST, p.Npad, W, E, p.WIp);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
-  int16_t* pot_s = reinterpret_cast<int16_t*>(smem + L.pot);
+  int16_t* pot_s = kResident ? pot_res : reinterpret_cast<int16_t*>(smem + L.pot);
   uint32_t* pk = reinterpret_cast<uint32_t*>(smem + L.pk);
   uint32_t* raw = reinterpret_cast<uint32_t*>(smem + L.raw);
   uint32_t* lines_s = reinterpret_cast<uint32_t*>(smem + L.lines);
@@ -80,7 +84,7 @@ __device__ __forceinline__ void popc_tile(const TickParams& p, int cl, int tile,
   int16_t* pot_g = p.pot + ((size_t)cl * p.S + s0) * p.Npad;
 
   // stream the tile's potentials in (TMA bulk copy) while the spikes are staged
-  if (!p.fresh && tid == 0) {
+  if (!kResident && !p.fresh && tid == 0) {
     ptx::mbar_arrive_expect_tx(bar, tile_bytes);
     ptx::bulk_g2s(pot_s, pot_g, tile_bytes, bar);
   }
@@ -120,7 +124,7 @@ __device__ __forceinline__ void popc_tile(const TickParams& p, int cl, int tile,
     pk[i] = raw[s * W + pword[e]];
   }
   __syncthreads();
-  if (!p.fresh) {
+  if (!kResident && !p.fresh) {
     ptx::mbar_wait(bar, phase);
     phase ^= 1u;
   }
@@ -186,19 +190,18 @@ __device__ __forceinline__ void popc_tile(const TickParams& p, int cl, int tile,
       }
     }
   }
+  if (kResident) {
+    __syncthreads();   // the staging buffers are reused by the next tile
+    return;
+  }
   // stream the updated tile back (TMA bulk store)
   ptx::fence_proxy_async_smem();
   __syncthreads();
   if (tid == 0) {
     ptx::bulk_s2g(pot_g, pot_s, tile_bytes);
     ptx::bulk_commit();
-    // persistent: all writes done (not only the shared-memory reads), as
-    // the tile is reloaded in the next tick; otherwise the kernel boundary
-    // completes them
-    if (kPersistent) ptx::bulk_wait0();
-    else ptx::bulk_wait_read0();
+    ptx::bulk_wait_read0();
   }
-  if (kPersistent) __syncthreads();   // the shared buffers are reused by the next tile
 }
 
 __device__ __forceinline__ void init_tile_barrier(uint8_t* smem) {
@@ -214,27 +217,152 @@ __global__ void __launch_bounds__(kThreads, (E <= 12 ? 4 : (E <= 16 ? 3 : 2))) t
   extern __shared__ __align__(16) uint8_t smem[];
   init_tile_barrier(smem);
   uint32_t phase = 0;
-  popc_tile<E, false>(p, blockIdx.x, blockIdx.y, smem, phase);
+  popc_tile<E, false>(p, blockIdx.x, blockIdx.y, smem, phase, nullptr);
 }
 
 // Streaming mode (one long stream, few samples): all
-// ticks of a ranc_run_ticks call in one cooperative launch.  Each CTA walks
-// the (core, tile) items of a tick, then the grid barrier is the tick barrier
-// (a7): it orders the ring ORs and potential stores of tick t before
-// the reads of tick t+1.
+// ticks of a ranc_run_ticks call in one cooperative launch.  CTA b owns the
+// (core, tile) items b, b + grid, ...; their potentials stay in shared memory
+// for the whole run (loaded before the first tick, stored after the last),
+// so a tick only touches the scheduler rings (L2) and the input lines.  The
+// grid barrier is the tick barrier (a7): it orders the ring ORs of
+// tick t before the row reads of tick t+1.
 template <int E>
-__global__ void __launch_bounds__(kThreads, 1) tick_stream_kernel(TickParams p, int nticks, int n_tiles) {
+__global__ void __launch_bounds__(kThreads, 1) tick_stream_kernel(TickParams p, int nticks, int n_tiles,
+                                                                  uint32_t res_off) {
   extern __shared__ __align__(16) uint8_t smem[];
   init_tile_barrier(smem);
   uint32_t phase = 0;
   cg::grid_group grid = cg::this_grid();
   const int items = p.G_loc * n_tiles;
+  const size_t tile_elems = (size_t)p.ST * p.Npad;
+  int16_t* res = reinterpret_cast<int16_t*>(smem + res_off);
+  if (!p.fresh) {
+    int j = 0;
+    for (int w = blockIdx.x; w < items; w += gridDim.x, ++j) {
+      const int cl = w % p.G_loc, s0 = (w / p.G_loc) * p.ST, ns = min(p.ST, p.S - s0);
+      const int16_t* g = p.pot + ((size_t)cl * p.S + s0) * p.Npad;
+      for (int i = threadIdx.x; i < ns * p.Npad; i += blockDim.x) res[j * tile_elems + i] = g[i];
+    }
+    __syncthreads();
+  }
   for (int it = 0; it < nticks; ++it) {
-    for (int w = blockIdx.x; w < items; w += gridDim.x) popc_tile<E, true>(p, w % p.G_loc, w / p.G_loc, smem, phase);
+    int j = 0;
+    for (int w = blockIdx.x; w < items; w += gridDim.x, ++j)
+      popc_tile<E, true>(p, w % p.G_loc, w / p.G_loc, smem, phase, res + j * tile_elems);
     p.fresh = 0;
     ++p.t;
     grid.sync();
   }
+  int j = 0;
+  for (int w = blockIdx.x; w < items; w += gridDim.x, ++j) {
+    const int cl = w % p.G_loc, s0 = (w / p.G_loc) * p.ST, ns = min(p.ST, p.S - s0);
+    int16_t* g = p.pot + ((size_t)cl * p.S + s0) * p.Npad;
+    for (int i = threadIdx.x; i < ns * p.Npad; i += blockDim.x) g[i] = res[j * tile_elems + i];
+  }
+}
+
+// Streaming mode, one (core, sample tile) item per CTA (the common case:
+// S = 1 and at most ~4 x 148 cores): thread = neuron, the neuron's crossbar
+// pieces, weights and routing word stay in registers and the tile's
+// potentials in shared memory for the whole run, so a tick is: read + clear
+// the scheduler rows, OR in the input lines, integrate + LIF + route, grid
+// barrier (the tick barrier, a7).
+template <int E>
+__global__ void __launch_bounds__(kThreads, (E <= 12 ? 4 : (E <= 16 ? 3 : 2)))
+    tick_stream1_kernel(TickParams p, int nticks) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  cg::grid_group grid = cg::this_grid();
+  const int cl = blockIdx.x % p.G_loc, tile = blockIdx.x / p.G_loc;
+  const int c = p.c_lo + cl;
+  const int s0 = tile * p.ST, ns = min(p.ST, p.S - s0);
+  const int tid = threadIdx.x, lane = tid & 31, W = p.W, n = tid;
+  uint32_t* raw = reinterpret_cast<uint32_t*>(smem);                       // [ST][W]
+  int16_t* pot_s = reinterpret_cast<int16_t*>(smem + (size_t)p.ST * W * 4);  // [ST][Npad]
+  const bool has_n = n < p.Npad;
+  uint32_t xp[E];
+  int wp[E], pw[E];
+  short4 prm = make_short4(0, 0, 0, 0);
+  uint2 rt = make_uint2(0u, 0u);
+  int init = 0;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    xp[e] = has_n ? p.xp[((size_t)c * E + e) * p.Npad + n] : 0u;
+    wp[e] = has_n ? p.wp[((size_t)c * E + e) * p.Npad + n] : 0;
+    pw[e] = p.pword[(size_t)c * E + e];
+  }
+  if (has_n) {
+    prm = p.prm[(size_t)c * p.Npad + n];
+    rt = p.route[(size_t)c * p.Npad + n];
+    init = p.init[(size_t)c * p.Npad + n];
+  }
+  const uint32_t kind = route_kind(rt.x);
+  const bool lin = route_lin(rt.x);
+  const bool valid = n < p.N;
+  const int leak = prm.x, pth = prm.y, nth = prm.z, rst = prm.w;
+  const uint32_t dloc = rt.y - (uint32_t)p.c_lo;
+  const bool route_here = kind == RK_ROUTE && dloc < (uint32_t)p.G_loc;
+  const uint32_t ax = route_axon(rt.x);
+  if (has_n)
+    for (int s = 0; s < ns; ++s)
+      pot_s[s * p.Npad + n] = p.fresh ? (int16_t)init : p.pot[((size_t)cl * p.S + s0 + s) * p.Npad + n];
+  const bool has_in = p.has_in[c];
+  for (int it = 0; it < nticks; ++it) {
+    const int64_t t = p.t + it;
+    const int cur = (int)(t & p.rp_mask);
+    // a1: rows due now; clear the words that hold spikes
+    uint32_t* row = p.ring + (((size_t)cur * p.G_loc + cl) * p.Sr + s0) * W;
+    for (int i = tid; i < ns * W; i += blockDim.x) {
+      const uint32_t v = row[i];
+      raw[i] = v;
+      if (v) row[i] = 0u;
+    }
+    __syncthreads();
+    // a2: input lines arriving now, one ballot per 32-axon word
+    if (t < p.T_in && has_in) {
+      const uint32_t* lg = p.lines + ((size_t)t * p.Sr + s0) * p.WIp;
+      for (int ap0 = tid - lane; ap0 < W * 32; ap0 += blockDim.x) {
+        const int ap = ap0 + lane;
+        const int32_t ln = ap < p.A ? p.inl[(size_t)c * p.A + ap] : -1;
+        for (int s = 0; s < ns; ++s) {
+          const bool bit = ln >= 0 && ((lg[s * p.WIp + (ln >> 5)] >> (ln & 31)) & 1u);
+          const uint32_t m = __ballot_sync(0xFFFFFFFFu, bit);
+          if (lane == 0 && m) raw[s * W + (ap0 >> 5)] |= m;
+        }
+      }
+      __syncthreads();
+    }
+    if (has_n) {
+      for (int s = 0; s < ns; ++s) {
+        int acc = 0;
+#pragma unroll
+        for (int e = 0; e < E; ++e) acc += wp[e] * __popc(xp[e] & raw[s * W + pw[e]]);
+        const int v = (int)pot_s[s * p.Npad + n] + acc + leak;
+        const bool fire = v >= pth;
+        const bool neg = v < nth;
+        const int rv = lin ? v - (fire ? pth : nth) : (fire ? rst : -rst);
+        int nv = (fire || neg) ? rv : v;
+        nv = min(max(nv, p.pot_lo), p.pot_hi);
+        pot_s[s * p.Npad + n] = (int16_t)nv;
+        if (fire && valid) {
+          if (route_here) {
+            const int slot = (int)((t + route_delay(rt.x)) & p.rp_mask);
+            atomicOr(p.ring + (((size_t)slot * p.G_loc + dloc) * p.Sr + s0 + s) * W + (ax >> 5), 1u << (ax & 31));
+          } else if (kind == RK_OUTPUT) {
+            atomicAdd(p.counts + (size_t)(s0 + s) * p.C + rt.y, 1);
+          }
+        }
+        if (p.raster) {
+          const uint32_t m = __ballot_sync(0xFFFFFFFFu, fire && valid);
+          if (lane == 0 && (n >> 5) < p.Wn)
+            p.raster[(((size_t)(t - p.raster_t0) * p.S + s0 + s) * p.G_loc + cl) * p.Wn + (n >> 5)] = m;
+        }
+      }
+    }
+    grid.sync();   // a7: tick t's deliveries are visible to tick t+1's row reads
+  }
+  if (has_n)
+    for (int s = 0; s < ns; ++s) p.pot[((size_t)cl * p.S + s0 + s) * p.Npad + n] = pot_s[s * p.Npad + n];
 }
 
 // [S][T_in][WI] -> [T_in][Sr][WIp] (padding words stay zero)
@@ -259,21 +387,62 @@ cudaError_t launch_one(const TickParams& p, dim3 grid, size_t smem, cudaStream_t
   return cudaGetLastError();
 }
 
+// grid and shared memory of the streaming kernel: as many CTAs as can be
+// co-resident (cooperative launch), each holding its items' potentials
+struct StreamPlan {
+  int grid = 0;
+  uint32_t res_off = 0;
+  size_t smem = 0;
+};
+
 template <int E>
-cudaError_t launch_stream_e(TickParams p, int nticks, size_t smem, int n_tiles, int num_sms, cudaStream_t st) {
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(tick_stream_kernel<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    configured = true;
-  }
-  int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tick_stream_kernel<E>, kThreads, smem);
-  if (e != cudaSuccess) return e;
-  if (per_sm < 1) return cudaErrorCooperativeLaunchTooLarge;
+StreamPlan plan_stream_e(const TickParams& p, size_t scratch, int n_tiles, int num_sms) {
+  StreamPlan pl;
   const int items = p.G_loc * n_tiles;
-  const int grid = std::max(1, std::min(items, per_sm * num_sms));
-  void* args[] = {&p, &nticks, &n_tiles};
-  return cudaLaunchCooperativeKernel((const void*)tick_stream_kernel<E>, dim3(grid), dim3(kThreads), args, smem, st);
+  const size_t tile_bytes = (size_t)p.ST * p.Npad * 2;
+  pl.res_off = (uint32_t)((scratch + 15) & ~(size_t)15);
+  static const int force = getenv("RANC_STREAM_CTAS") ? atoi(getenv("RANC_STREAM_CTAS")) : 0;
+  for (int per_sm = 4; per_sm >= 1; --per_sm) {
+    const int grid = std::max(1, std::min(items, force > 0 ? force : per_sm * num_sms));
+    const size_t smem = pl.res_off + (size_t)((items + grid - 1) / grid) * tile_bytes;
+    if (smem > 200 * 1024) continue;
+    int fit = 0;
+    cudaFuncSetAttribute(tick_stream_kernel<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fit, tick_stream_kernel<E>, kThreads, smem) != cudaSuccess)
+      return pl;
+    if ((int64_t)fit * num_sms < grid) continue;
+    pl.grid = grid;
+    pl.smem = smem;
+    return pl;
+  }
+  return pl;   // grid 0: not possible (too many potentials to keep resident)
+}
+
+template <int E>
+cudaError_t launch_stream_e(TickParams p, int nticks, size_t scratch, int n_tiles, int num_sms, cudaStream_t st,
+                            bool dry, bool* ok) {
+  static const bool no1 = getenv("RANC_STREAM_MULTI") != nullptr;   // experiment: force the multi-item kernel
+  const int items = p.G_loc * n_tiles;
+  if (p.Npad <= kThreads && !no1) {
+    const size_t smem1 = (size_t)p.ST * p.W * 4 + (size_t)p.ST * p.Npad * 2;
+    int fit = 0;
+    if (smem1 <= 48 * 1024 &&
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fit, tick_stream1_kernel<E>, kThreads, smem1) == cudaSuccess &&
+        (int64_t)fit * num_sms >= items) {
+      *ok = true;
+      if (dry) return cudaSuccess;
+      void* args[] = {&p, &nticks};
+      return cudaLaunchCooperativeKernel((const void*)tick_stream1_kernel<E>, dim3(items), dim3(kThreads), args,
+                                         smem1, st);
+    }
+  }
+  const StreamPlan pl = plan_stream_e<E>(p, scratch, n_tiles, num_sms);
+  *ok = pl.grid > 0;
+  if (dry || !*ok) return cudaSuccess;
+  uint32_t res_off = pl.res_off;
+  void* args[] = {&p, &nticks, &n_tiles, &res_off};
+  return cudaLaunchCooperativeKernel((const void*)tick_stream_kernel<E>, dim3(pl.grid), dim3(kThreads), args,
+                                     pl.smem, st);
 }
 
 }  // namespace
@@ -354,32 +523,45 @@ TickParams make_params(ranc_ctx* ctx) {
 
 }  // namespace
 
-bool stream_eligible(const ranc_ctx* ctx, int64_t num_ticks) {
-  if (ctx->kernel_active != RANC_KERNEL_POPC || ctx->shard_mode == RANC_SHARD_CORES || num_ticks < 2) return false;
-  if (ctx->stream_opt == 1) return false;
-  if (ctx->stream_opt == 2) return true;
-  // automatic: few (core, tile) items per tick, where per-tick launches dominate
-  const int64_t tiles = (ctx->S + ctx->sample_tile - 1) / ctx->sample_tile;
-  return (int64_t)ctx->G_loc * tiles <= 4 * 148 * 4;
-}
+namespace {
 
-cudaError_t launch_stream(ranc_ctx* ctx, int64_t num_ticks) {
+cudaError_t stream_dispatch(ranc_ctx* ctx, int64_t num_ticks, bool dry, bool* ok) {
   const Compiled& n = ctx->net;
   TickParams p = make_params(ctx);
   const int n_tiles = (int)((ctx->S + p.ST - 1) / p.ST);
-  const size_t smem = smem_layout(p.ST, n.Npad, n.W, n.E, n.WIp).total;
+  const size_t scratch = smem_layout(p.ST, n.Npad, n.W, n.E, n.WIp).total;
   const int nt = (int)std::min<int64_t>(num_ticks, 1 << 30);
-  cudaError_t e;
   switch (n.E) {
-    case 4: e = launch_stream_e<4>(p, nt, smem, n_tiles, ctx->num_sms, ctx->stream); break;
-    case 8: e = launch_stream_e<8>(p, nt, smem, n_tiles, ctx->num_sms, ctx->stream); break;
-    case 12: e = launch_stream_e<12>(p, nt, smem, n_tiles, ctx->num_sms, ctx->stream); break;
-    case 16: e = launch_stream_e<16>(p, nt, smem, n_tiles, ctx->num_sms, ctx->stream); break;
-    case 24: e = launch_stream_e<24>(p, nt, smem, n_tiles, ctx->num_sms, ctx->stream); break;
-    default: e = launch_stream_e<36>(p, nt, smem, n_tiles, ctx->num_sms, ctx->stream); break;
+    case 4: return launch_stream_e<4>(p, nt, scratch, n_tiles, ctx->num_sms, ctx->stream, dry, ok);
+    case 8: return launch_stream_e<8>(p, nt, scratch, n_tiles, ctx->num_sms, ctx->stream, dry, ok);
+    case 12: return launch_stream_e<12>(p, nt, scratch, n_tiles, ctx->num_sms, ctx->stream, dry, ok);
+    case 16: return launch_stream_e<16>(p, nt, scratch, n_tiles, ctx->num_sms, ctx->stream, dry, ok);
+    case 24: return launch_stream_e<24>(p, nt, scratch, n_tiles, ctx->num_sms, ctx->stream, dry, ok);
+    default: return launch_stream_e<36>(p, nt, scratch, n_tiles, ctx->num_sms, ctx->stream, dry, ok);
   }
+}
+
+}  // namespace
+
+bool stream_eligible(ranc_ctx* ctx, int64_t num_ticks) {
+  if (ctx->kernel_active != RANC_KERNEL_POPC || ctx->shard_mode == RANC_SHARD_CORES || num_ticks < 2) return false;
+  if (ctx->stream_opt == 1) return false;
+  if (ctx->stream_opt == 0) {
+    // automatic: few (core, tile) items per tick, where per-tick launches dominate
+    const int64_t tiles = (ctx->S + ctx->sample_tile - 1) / ctx->sample_tile;
+    if ((int64_t)ctx->G_loc * tiles > 4 * 148 * 4) return false;
+  }
+  bool ok = false;
+  return stream_dispatch(ctx, num_ticks, true, &ok) == cudaSuccess && ok;
+}
+
+cudaError_t launch_stream(ranc_ctx* ctx, int64_t num_ticks) {
+  bool ok = false;
+  cudaError_t e = stream_dispatch(ctx, num_ticks, false, &ok);
   ctx->launches++;
   if (e != cudaSuccess) return e;
+  if (!ok) return cudaErrorCooperativeLaunchTooLarge;
+  const int nt = (int)std::min<int64_t>(num_ticks, 1 << 30);
   ctx->fresh = false;
   ctx->now += nt;
   return cudaSuccess;
