@@ -307,6 +307,15 @@ __global__ void __launch_bounds__(kThreads, (E <= 12 ? 4 : (E <= 16 ? 3 : 2)))
     for (int s = 0; s < ns; ++s)
       pot_s[s * p.Npad + n] = p.fresh ? (int16_t)init : p.pot[((size_t)cl * p.S + s0 + s) * p.Npad + n];
   const bool has_in = p.has_in[c];
+  // one sample and one axon per thread (the streaming case): the input bit
+  // of tick t+1 is fetched before tick t's barrier, off the critical path
+  const bool fast_in = has_in && ns == 1 && W * 32 <= (int)blockDim.x;
+  const int32_t my_ln = (fast_in && tid < p.A) ? p.inl[(size_t)c * p.A + tid] : -1;
+  auto line_bit = [&](int64_t tt) -> bool {
+    return my_ln >= 0 && tt < p.T_in &&
+           ((p.lines[((size_t)tt * p.Sr + s0) * p.WIp + (my_ln >> 5)] >> (my_ln & 31)) & 1u);
+  };
+  bool next_bit = fast_in ? line_bit(p.t) : false;
   for (int it = 0; it < nticks; ++it) {
     const int64_t t = p.t + it;
     const int cur = (int)(t & p.rp_mask);
@@ -319,7 +328,15 @@ __global__ void __launch_bounds__(kThreads, (E <= 12 ? 4 : (E <= 16 ? 3 : 2)))
     }
     __syncthreads();
     // a2: input lines arriving now, one ballot per 32-axon word
-    if (t < p.T_in && has_in) {
+    if (fast_in) {
+      const bool bit = next_bit;
+      next_bit = line_bit(t + 1);   // prefetch for the next tick
+      if (t < p.T_in && tid < W * 32) {
+        const uint32_t m = __ballot_sync(0xFFFFFFFFu, bit);
+        if (lane == 0 && m) raw[tid >> 5] |= m;
+      }
+      __syncthreads();
+    } else if (t < p.T_in && has_in) {
       const uint32_t* lg = p.lines + ((size_t)t * p.Sr + s0) * p.WIp;
       for (int ap0 = tid - lane; ap0 < W * 32; ap0 += blockDim.x) {
         const int ap = ap0 + lane;
