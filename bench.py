@@ -69,7 +69,18 @@ WORKLOADS = {
     # streaming: the config-3 net fed one image per tick,
     # 10000 images in 10003 ticks, one sample (10010 ticks)
     "stream": (lambda S: __import__("workloads.gen", fromlist=["x"]).config3_stream(10000), 1, "samples"),
+    # design-space sweep (f3): 8 variants of the config-3 net tiled into one
+    # 32x128 grid, 1250 samples each (the config-3 work per step); value counts
+    # variant-samples
+    "sweep8": (lambda S: _sweep(8, S), 1250, "samples"),
 }
+
+
+def _sweep(V, S):
+    from paper_2404_16208_b200.sweep import tile_variants
+    from workloads.gen import config3, sweep_variants
+    net, inp = config3(S=S)
+    return tile_variants(sweep_variants(net, V)), inp
 
 
 def parse():
@@ -309,8 +320,9 @@ def run_ours(args, rank, world, local):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms, tick_ms = float(t[0]), float(t[1])
     ms_step = ms / args.steps
-    samples_s = args.samples / (ms_step / 1e3)
-    core_ticks_s = samples_s * net.G * T
+    V = int(net.meta.get("variants", 1))   # sweep batching: a sample of every variant per sample
+    samples_s = args.samples * V / (ms_step / 1e3)
+    core_ticks_s = args.samples / (ms_step / 1e3) * net.G * T   # net.G counts every variant's cores
     G_loc = sim.info()["cores_local"]
 
     # ---- end-to-end through the public API, host buffers --------------------
@@ -337,7 +349,7 @@ def run_ours(args, rank, world, local):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     e2e_s = float(t[0])
-    e2e_val = args.samples * args.steps / e2e_s
+    e2e_val = args.samples * V * args.steps / e2e_s
 
     if rank == 0:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
@@ -371,7 +383,7 @@ def run_ours(args, rank, world, local):
                                   "popcount, streaming (one cooperative launch per run)" if launches == args.steps
                                   else "popcount")},
             "core_ticks_per_s": core_ticks_s,
-            "ticks_per_s": samples_s * T / max(1, args.samples),
+            "ticks_per_s": T / (ms_step / 1e3),
             "tick_kernel_ms": tick_ms,
             "gpu_launches": launches,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",

@@ -4,7 +4,8 @@ for every potential, pending spike, fired bit, output event and class count
 import numpy as np
 import pytest
 
-from workloads.gen import (config1, config2, config3, config3_stream, config5, corpus_case, tiny_case, vmm)
+from workloads.gen import (config1, config2, config3, config3_stream, config5, corpus_case, sweep_variants, tiny_case,
+                           vmm)
 
 pytestmark = pytest.mark.gpu
 
@@ -372,3 +373,23 @@ def test_stream_multi_item_kernel(ranc, oracle_mod):
     net, inp = config3(S=2)
     stream_run(ranc, oracle_mod, net, inp, [net.meta["T"]], 2)
     stream_run(ranc, oracle_mod, net, inp, [4, 15], 2, trace=False)
+
+
+# ---- design-space sweep batching ------------------------------
+
+
+def test_sweep_tiled_variants_on_gpu(ranc, oracle_mod, kernel):
+    from paper_2404_16208_b200.sweep import split_counts, split_potentials, tile_variants
+    net, inp = config2(S=130)
+    variants = sweep_variants(net, 5)
+    tiled = tile_variants(variants)
+    T = net.meta["T"]
+    sim = make_sim(ranc, tiled, kernel)
+    sim.load_inputs(inp).run(T)
+    cnt = split_counts(sim.outputs(), 5, net.num_classes)
+    pot = split_potentials(sim.potentials(), 5, net.G)
+    sim.close()
+    for v, vn in enumerate(variants):
+        o = oracle_mod.Oracle(vn, inp).run(T)
+        assert np.array_equal(cnt[:, v], o.counts()), f"variant {v}"
+        assert np.array_equal(pot[:, v], o.potentials()), f"variant {v}"

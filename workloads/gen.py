@@ -137,6 +137,28 @@ def config3_stream(n_images=10000, seed=1003, inputs_seed=2013):
     return net, inp
 
 
+def sweep_variants(net, V, seed=3000):
+    """V design-space variants of a network:
+    variant v scales the positive thresholds by (1 + v/4), shifts the leaks
+    by -(v mod 3) and flips the reset mode of a seeded 1/(v+2) fraction of
+    neurons; crossbars, weights and routes are shared.  Values stay inside the
+    network's bitwidths."""
+    import dataclasses
+    rng = substream(seed, f"sweep-{net.name}")
+    tmax = (1 << (net.threshold_bits - 1)) - 1
+    lmin = -(1 << (net.leak_bits - 1))
+    out = []
+    for v in range(V):
+        pt = np.clip(np.asarray(net.pos_threshold, np.int64) * (4 + v) // 4, 1, tmax).astype(np.int16)
+        lk = np.clip(np.asarray(net.leak, np.int64) - (v % 3), lmin, None).astype(np.int16)
+        flip = rng.bernoulli(net.G * net.neurons, 1.0 / (v + 2)).reshape(net.G, net.neurons)
+        rm = np.where(flip, 1 - np.asarray(net.reset_mode), net.reset_mode).astype(np.uint8)
+        vn = dataclasses.replace(net, pos_threshold=pt, leak=lk, reset_mode=rm, name=f"{net.name}-v{v}",
+                                 meta=dict(net.meta))
+        out.append(vn)
+    return out
+
+
 # ----------------------------------------------------------------------------
 # config 1: single 256x256 core
 # ----------------------------------------------------------------------------
