@@ -173,8 +173,9 @@ ranc_status ranc_set_allocator(ranc_ctx* ctx, void* (*alloc)(size_t, void*),
  * T_in x input cores x S x ceil(A/32) x 4 bytes of device memory, skipped when
  * that exceeds a quarter of the free memory); 0: gather the line runs every
  * tick.  Takes effect at the next ranc_load_inputs / ranc_reset_state.
- * RANC_OPT_KERNEL: 0 automatic (tensor core when the network is eligible and
- * S > 64, else popcount), 1 popcount, 2 tensor core (see ranc_info.kernel). */
+ * RANC_OPT_KERNEL: 0 automatic (tensor core when the network is eligible,
+ * unless S < 64 and cores x S <= 592, where the popcount path's streaming
+ * launch is faster), 1 popcount, 2 tensor core (see ranc_info.kernel). */
 #define RANC_OPT_SAMPLE_TILE 1
 #define RANC_OPT_INPUT_DECODE 2
 /* RANC_OPT_STREAM (streaming mode: one long stream of inputs,

@@ -286,9 +286,10 @@ ranc_status ranc_reset_state(ranc_ctx* ctx) {
   CK(cudaSetDevice(ctx->device), "cudaSetDevice");
   CK(launch_reset(ctx), "reset kernel");
   // latch the kernel variant (the potential layout is re-initialised here)
-  // automatic choice: the tensor-core path needs whole 64-sample tiles to pay
-  // off; one tile or less per core (e.g. streaming, S = 1) runs the popcount path
-  const bool tc_auto = ctx->kernel == 0 && ctx->S > 64;
+  // automatic choice: the tensor-core path unless the batch is a few samples
+  // of a small net (e.g. streaming, S = 1): then the popcount path runs all
+  // ticks of a call in one cooperative launch (one (core, sample) per CTA)
+  const bool tc_auto = ctx->kernel == 0 && !(ctx->S < 64 && (int64_t)ctx->G_loc * ctx->S <= 4 * 148);
   ctx->kernel_active = (ctx->kernel == RANC_KERNEL_POPC || (ctx->kernel == 0 && !tc_auto) || !ctx->net.tc_ok ||
                         tc_smem_bytes(ctx->net) > 227 * 1024)
                            ? RANC_KERNEL_POPC

@@ -28,6 +28,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "internal.h"
@@ -82,6 +83,16 @@ __device__ __forceinline__ void popc_tile(const TickParams& p, int cl, int tile,
   const int cur = (int)(p.t & p.rp_mask);
   const uint32_t tile_bytes = (uint32_t)ns * p.Npad * 2;
   int16_t* pot_g = p.pot + ((size_t)cl * p.S + s0) * p.Npad;
+  // RANC_DEBUG_PHASES: per-phase cycle sums over all CTAs (f4 profile)
+  const bool prof = !kResident && p.dbg && tid == 0;
+  long long ck = prof ? clock64() : 0;
+  auto phase_mark = [&](int k) {
+    if (prof) {
+      const long long now = clock64();
+      atomicAdd(reinterpret_cast<unsigned long long*>(p.dbg) + k, (unsigned long long)(now - ck));
+      ck = now;
+    }
+  };
 
   // stream the tile's potentials in (TMA bulk copy) while the spikes are staged
   if (!kResident && !p.fresh && tid == 0) {
@@ -101,6 +112,7 @@ __device__ __forceinline__ void popc_tile(const TickParams& p, int cl, int tile,
     for (int i = tid; i < ns * p.WIp; i += blockDim.x) lines_s[i] = lg[i];
   }
   __syncthreads();
+  phase_mark(0);   // a1 scheduler read + clear (and the line rows staged)
   // a2: external input lines arriving at tick t (G8).  Thread <-> permuted
   // axon a'; one warp ballot builds one 32-axon ring word, so the OR into the
   // staged row needs no atomics.
@@ -117,6 +129,7 @@ __device__ __forceinline__ void popc_tile(const TickParams& p, int cl, int tile,
     }
     __syncthreads();
   }
+  phase_mark(1);   // a2 input injection
   // expand to one spike word per piece
   const uint8_t* pword = p.pword + (size_t)c * E;
   for (int i = tid; i < ns * E; i += blockDim.x) {
@@ -124,10 +137,12 @@ __device__ __forceinline__ void popc_tile(const TickParams& p, int cl, int tile,
     pk[i] = raw[s * W + pword[e]];
   }
   __syncthreads();
+  phase_mark(2);   // spike words per crossbar piece
   if (!kResident && !p.fresh) {
     ptx::mbar_wait(bar, phase);
     phase ^= 1u;
   }
+  phase_mark(3);   // potential tile load (TMA) not hidden by a1-a2
 
   for (int n = tid; n < p.Npad; n += blockDim.x) {
     uint32_t xp[E];
@@ -197,11 +212,13 @@ __device__ __forceinline__ void popc_tile(const TickParams& p, int cl, int tile,
   // stream the updated tile back (TMA bulk store)
   ptx::fence_proxy_async_smem();
   __syncthreads();
+  phase_mark(4);   // a3-a6: integration, LIF, routing + output bus (fused per sample)
   if (tid == 0) {
     ptx::bulk_s2g(pot_g, pot_s, tile_bytes);
     ptx::bulk_commit();
     ptx::bulk_wait_read0();
   }
+  phase_mark(5);   // potential tile store
 }
 
 __device__ __forceinline__ void init_tile_barrier(uint8_t* smem) {
@@ -593,6 +610,12 @@ cudaError_t launch_one_tick(ranc_ctx* ctx) {
   } else {
     const dim3 grid(ctx->G_loc, (unsigned)((ctx->S + p.ST - 1) / p.ST));
     const size_t smem = smem_layout(p.ST, n.Npad, n.W, n.E, n.WIp).total;
+    static const bool phases = getenv("RANC_DEBUG_PHASES") != nullptr;
+    if (phases) {
+      if (!ctx->d_dbg.p) dev_alloc(ctx, &ctx->d_dbg, 4096 * 8);
+      cudaMemsetAsync(ctx->d_dbg.p, 0, 8 * 8, ctx->stream);
+      p.dbg = (unsigned long long*)ctx->d_dbg.p;
+    }
     switch (n.E) {
       case 4: e = launch_one<4>(p, grid, smem, ctx->stream); break;
       case 8: e = launch_one<8>(p, grid, smem, ctx->stream); break;
@@ -604,6 +627,13 @@ cudaError_t launch_one_tick(ranc_ctx* ctx) {
   }
   ctx->launches++;
   if (e != cudaSuccess) return e;
+  if (p.dbg && ctx->kernel_active != RANC_KERNEL_TC) {
+    unsigned long long h[6];
+    cudaMemcpyAsync(h, ctx->d_dbg.p, sizeof h, cudaMemcpyDeviceToHost, ctx->stream);
+    cudaStreamSynchronize(ctx->stream);
+    fprintf(stderr, "phases t=%lld cycles (sum over CTAs): a1 %llu a2 %llu expand %llu potwait %llu a3-a6 %llu store %llu\n",
+            (long long)p.t, h[0], h[1], h[2], h[3], h[4], h[5]);
+  }
   ctx->fresh = false;
   ctx->now += 1;
   return cudaSuccess;
