@@ -53,10 +53,11 @@ from workloads.gen import config5
 for drive in (True, False):
     net, inp = config5(S=64, T=60, grid=64, drive=drive)
     for k in (1, 2):
-        sim = Simulator(net, stream=torch.cuda.current_stream()); sim.set_option(OPT_KERNEL, k); sim.load_inputs(inp)
+        st = torch.cuda.Stream()
+        sim = Simulator(net, stream=st); sim.set_option(OPT_KERNEL, k); sim.load_inputs(inp)
         sim.run(10); torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        sim.reset(); a.record(); sim.run(60); b.record(); torch.cuda.synchronize()
+        sim.reset(); a.record(st); sim.run(60); b.record(st); torch.cuda.synchronize()
         fired = int(sim.outputs().sum())
         print(f"drive={drive} kernel={k} ms_per_tick={a.elapsed_time(b) / 60:.4f} outputs={fired}")
         sim.close()
