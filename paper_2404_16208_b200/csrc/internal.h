@@ -198,6 +198,8 @@ size_t tc_smem_bytes(const Compiled& n);
 cudaError_t launch_tick_tc(ranc_ctx* ctx, TickParams p);
 cudaError_t decode_inputs_tc(ranc_ctx* ctx);
 bool stream_eligible(ranc_ctx* ctx, int64_t num_ticks);
+bool tc_multi_eligible(const ranc_ctx* ctx, int64_t num_ticks);
+cudaError_t launch_tc_multi(ranc_ctx* ctx, TickParams p, int64_t num_ticks);
 cudaError_t launch_stream(ranc_ctx* ctx, int64_t num_ticks);
 // api.cpp
 ranc_status dev_alloc(ranc_ctx* ctx, DevBuf* b, size_t bytes);

@@ -578,6 +578,7 @@ cudaError_t stream_dispatch(ranc_ctx* ctx, int64_t num_ticks, bool dry, bool* ok
 }  // namespace
 
 bool stream_eligible(ranc_ctx* ctx, int64_t num_ticks) {
+  if (ctx->kernel_active == RANC_KERNEL_TC) return tc_multi_eligible(ctx, num_ticks);
   if (ctx->kernel_active != RANC_KERNEL_POPC || ctx->shard_mode == RANC_SHARD_CORES || num_ticks < 2) return false;
   if (ctx->stream_opt == 1) return false;
   if (ctx->stream_opt == 0) {
@@ -591,7 +592,13 @@ bool stream_eligible(ranc_ctx* ctx, int64_t num_ticks) {
 
 cudaError_t launch_stream(ranc_ctx* ctx, int64_t num_ticks) {
   bool ok = false;
-  cudaError_t e = stream_dispatch(ctx, num_ticks, false, &ok);
+  cudaError_t e;
+  if (ctx->kernel_active == RANC_KERNEL_TC) {
+    e = launch_tc_multi(ctx, make_params(ctx), num_ticks);
+    ok = true;
+  } else {
+    e = stream_dispatch(ctx, num_ticks, false, &ok);
+  }
   ctx->launches++;
   if (e != cudaSuccess) return e;
   if (!ok) return cudaErrorCooperativeLaunchTooLarge;

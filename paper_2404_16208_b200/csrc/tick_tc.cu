@@ -28,6 +28,7 @@
 //
 // Potential layout: tile-blocked [G][nT][8][Np][8] int16 (tile, 8-sample chunk,
 // neuron, sample in chunk): every 16-byte access of a warp is coalesced.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -41,6 +42,8 @@
 #include "tc.h"
 
 namespace ranc {
+
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -171,7 +174,13 @@ __device__ __forceinline__ uint32_t lif(const uint4 (&cur)[NE / 8], const uint32
   return fired;
 }
 
-__global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams p) {
+// nticks > 1 (cooperative launch, at most one work item per CTA): all ticks
+// of a ranc_run_ticks call in one launch; the grid barrier is the tick
+// barrier (a7) and each epilogue thread keeps its potentials in
+// registers between ticks (stored once, after the last tick).
+template <bool kMulti>
+__global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams p, const int nticks_arg) {
+  const int nticks = kMulti ? nticks_arg : 1;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + 8 * NBARS);
@@ -188,7 +197,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
   const uint32_t acc_stride = (uint32_t)Mh * NT;          // TMEM columns per accumulator stage
   constexpr int NA = 4;                                    // accumulator stages (Np <= 256: 4 x 128 columns)
   const uint32_t tcols = acc_stride * NA;
-  const int cur = (int)(p.t & p.rp_mask);
+  auto tick_barrier = [&]() {
+    if (kMulti) cg::this_grid().sync();
+  };
 
   // role warps (debug flag 32 swaps the producer and MMA warps)
   const int prod_warp = kProdWarp, mma_warp = kMmaWarp;
@@ -219,8 +230,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
     // ------------------------------------------------------------ producer (TMA)
     // the whole warp walks the work list (convergent waits); lane 0 issues
     int prev_core = -1, jw = -1;
+    for (int it = 0; it < nticks; ++it) {
+    const int64_t t = p.t + it;
+    const int cur = (int)(t & p.rp_mask);
     int cl = lo / nT, tile = lo - (lo / nT) * nT;   // work item lo + k, advanced incrementally
-    for (int k = 0; k < nwork; ++k, tile = (tile + 1 == nT) ? (++cl, 0) : tile + 1) {
+    for (int k0 = 0; k0 < nwork; ++k0, tile = (tile + 1 == nT) ? (++cl, 0) : tile + 1) {
+      const int k = it * nwork + k0;                 // pipeline index (barrier phases)
       const int c = p.c_lo + cl;
       const int s = k % NS, u = k / NS;
       if (c != prev_core) {
@@ -239,7 +254,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
         stamp(p, k, 1);
         uint8_t* st = smem + L.stage + s * L.stage_bytes;
         const int s0 = tile * NT;
-        const bool inject = p.t < p.T_in && p.nruns[c] > 0;
+        const bool inject = t < p.T_in && p.nruns[c] > 0;
         // decoded inputs: the tile's input words in ring-row layout; else the raw line rows
         const int slot = p.inw ? p.inslot[cl] : -1;
         const uint32_t ring_bytes = p.incoming[c] ? (uint32_t)NT * W * 4 : 0u;
@@ -249,12 +264,14 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
           ptx::bulk_g2s(st + L.raw, p.ring + (((size_t)cur * p.G_loc + cl) * p.Sr + s0) * W, ring_bytes,
                         &bars[FULL0 + s]);
         if (inject && p.inw)
-          ptx::bulk_g2s(st + L.lines, p.inw + (((size_t)p.t * p.n_inslots + slot) * p.Sr + s0) * W, line_bytes,
+          ptx::bulk_g2s(st + L.lines, p.inw + (((size_t)t * p.n_inslots + slot) * p.Sr + s0) * W, line_bytes,
                         &bars[FULL0 + s]);
         else if (inject)
-          ptx::bulk_g2s(st + L.lines, p.lines + ((size_t)p.t * p.Sr + s0) * WIp, line_bytes, &bars[FULL0 + s]);
+          ptx::bulk_g2s(st + L.lines, p.lines + ((size_t)t * p.Sr + s0) * WIp, line_bytes, &bars[FULL0 + s]);
       }
       __syncwarp();
+    }
+    tick_barrier();
     }
   } else if (warp == mma_warp) {
     // ------------------------------------------------------------ MMA issuer
@@ -262,8 +279,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
     const uint32_t id = tc::idesc_i8(128, NT);
     const uint32_t lbo_a = (uint32_t)Np * 16, lbo_b = (uint32_t)NT * 16;   // tc.h layout
     int prev_core = -1, jw = -1;
+    for (int it = 0; it < nticks; ++it) {
     int cl = lo / nT, tile = lo - (lo / nT) * nT;
-    for (int k = 0; k < nwork; ++k, tile = (tile + 1 == nT) ? (++cl, 0) : tile + 1) {
+    for (int k0 = 0; k0 < nwork; ++k0, tile = (tile + 1 == nT) ? (++cl, 0) : tile + 1) {
+      const int k = it * nwork + k0;
       const int c = cl;
       const int s = k % NS, u = k / NS;
       const int a = k % NA, ua = k / NA;
@@ -289,9 +308,13 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
         tc::commit(&bars[BEMPTY0 + s]);
         tc::commit(&bars[ACCFULL0 + a]);
         stamp(p, k, 7);
-        if (k + 1 == nwork || tile + 1 == nT) tc::commit(&bars[WFREE]);   // last tile of this core
+        // last tile of this core (in a multi-tick launch the next item is the
+        // same core again, except after the last tick)
+        if (k0 + 1 < nwork ? tile + 1 == nT : it + 1 == nticks) tc::commit(&bars[WFREE]);
       }
       __syncwarp();
+    }
+    tick_barrier();
     }
   } else if (is_spike_warp(warp)) {
     // ------------------------------------------------------------ spike stage
@@ -302,8 +325,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
     uint32_t* lut = reinterpret_cast<uint32_t*>(smem + L.lut);
     for (int b = et; b < 16; b += kExpThreads) lut[b] = tc::nib2bytes((uint32_t)b);
     named_sync(2, kExpThreads);
+    for (int it = 0; it < nticks; ++it) {
+    const int64_t t = p.t + it;
+    const int cur = (int)(t & p.rp_mask);
     int cl = lo / nT, tile = lo - (lo / nT) * nT;
-    for (int k = 0; k < nwork; ++k, tile = (tile + 1 == nT) ? (++cl, 0) : tile + 1) {
+    for (int k0 = 0; k0 < nwork; ++k0, tile = (tile + 1 == nT) ? (++cl, 0) : tile + 1) {
+      const int k = it * nwork + k0;
       const int c = p.c_lo + cl;
       const int s = k % NS, u = k / NS;
       const int s0 = tile * NT, ns = min(NT, p.S - s0);
@@ -326,10 +353,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       if (et == 0) stamp(p, k, 12);
       // a2: external inputs.  Thread <-> (sample, ring word): OR in the line
       // runs overlapping that word (no atomics: every word has one owner)
-      if (p.t < p.T_in && p.nruns[c] > 0 && p.inw) {
+      if (t < p.T_in && p.nruns[c] > 0 && p.inw) {
         // decoded input words (input decode done once at load, Alg. 1 l.1)
         for (int i = et; i < ns * W; i += kExpThreads) raw[i] |= lines[i];
-      } else if (p.t < p.T_in && p.nruns[c] > 0) {
+      } else if (t < p.T_in && p.nruns[c] > 0) {
         // the core's input runs live in shared memory while its tiles are processed
         int2* runs = reinterpret_cast<int2*>(smem + L.runs);
         int32_t* wr = reinterpret_cast<int32_t*>(smem + L.runs + (uint32_t)p.rmax * 8);
@@ -417,6 +444,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
         ptx::mbar_arrive(&bars[SEMPTY0 + s]);   // raw/lines of this stage are consumed
       }
     }
+    tick_barrier();
+    }
   } else {
     // ------------------------------------------------------------ epilogue
     // warp ew: TMEM lane quarter q = ew % 4 (thread = neuron n), neuron half
@@ -462,11 +491,23 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
     }
     long long dbg_wait = 0;
     const long long dbg_t0 = p.dbg ? clock64() : 0;
-    for (int k = 0; k < nwork; ++k, dst += tile_stride) {
+    const int cl0 = cl, tile0 = tile;
+    uint4* const dst0 = dst;
+    size_t ring_base = 0, warp_ring_base = 0;   // ring word offsets without the slot term
+    int rdelay = 0, warp_rdelay = 0;
+    const size_t slot_stride = (size_t)p.G_loc * p.Sr * W;
+    for (int it = 0; it < nticks; ++it) {
+    const int64_t t = p.t + it;
+    const bool first = it == 0, last = it + 1 == nticks;
+    cl = cl0;
+    tile = tile0;
+    dst = dst0;
+    for (int k0 = 0; k0 < nwork; ++k0, dst += tile_stride) {
+      const int k = it * nwork + k0;
       const int c = p.c_lo + cl;
       const int a = k % NA, ua = k / NA;
       const int s0 = tile * NT, ns = min(NT, p.S - s0);
-      const bool pf = load && k + 1 < nwork;
+      const bool pf = load && k0 + 1 < nwork;
       const uint4* nsrc = dst + tile_stride;
       const long long tw0 = p.dbg ? clock64() : 0;
       // one warp per lane quarter polls the accumulator barrier; the other
@@ -496,22 +537,32 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
           cls = rt.y;
           const uint32_t ax = route_axon(rt.x);
           axbit = 1u << (ax & 31);
-          const int slot = (int)((p.t + route_delay(rt.x)) & p.rp_mask);
+          rdelay = (int)route_delay(rt.x);
           // a route to a core of another rank is delivered by the exchange step
           const uint32_t dloc = rt.y - (uint32_t)p.c_lo;
           route_here = kind == RK_ROUTE && dloc < (uint32_t)p.G_loc;
-          ring_off = (((size_t)slot * p.G_loc + dloc) * p.Sr) * W + (ax >> 5);
+          ring_base = ((size_t)dloc * p.Sr) * W + (ax >> 5);
           exporting = p.fired && p.exports[c];
           const uint32_t wf = p.wflags ? p.wflags[(size_t)c * (Np >> 5) + (n >> 5)] : 0u;
           block_route = wf & 1u;
           block_identity = (wf & 3u) == 3u;
           const uint32_t rmask = __ballot_sync(0xFFFFFFFFu, route_here);
-          warp_ring_off = rmask ? __shfl_sync(0xFFFFFFFFu, ring_off, __ffs(rmask) - 1) : 0;
+          // block routes: all routing lanes share the destination word and delay
+          warp_ring_base = rmask ? __shfl_sync(0xFFFFFFFFu, ring_base, __ffs(rmask) - 1) : 0;
+          warp_rdelay = rmask ? __shfl_sync(0xFFFFFFFFu, rdelay, __ffs(rmask) - 1) : 0;
+          if (!kMulti) {   // one tick: the slots are fixed for the launch
+            ring_off = ring_base + (size_t)((p.t + rdelay) & p.rp_mask) * slot_stride;
+            warp_ring_off = warp_ring_base + (size_t)((p.t + warp_rdelay) & p.rp_mask) * slot_stride;
+          }
           out_lanes = __ballot_sync(0xFFFFFFFFu, kind == RK_OUTPUT);
           has_output = out_lanes != 0u;
           // lanes of the same output class (classes are < C, never ~0u)
           out_peers = __match_any_sync(0xFFFFFFFFu, kind == RK_OUTPUT ? cls : 0xFFFFFFFFu);
           prev_core = c;
+        }
+        if (kMulti) {   // ring slot of tick t + delay
+          ring_off = ring_base + (size_t)((t + rdelay) & p.rp_mask) * slot_stride;
+          warp_ring_off = warp_ring_base + (size_t)((t + warp_rdelay) & p.rp_mask) * slot_stride;
         }
         const uint32_t acc_addr = tmem + a * acc_stride + ((uint32_t)(q * 32) << 16) + h * NT + jj * 32;
         uint32_t fired = 0u;
@@ -520,7 +571,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
           uint32_t acc[kSub];
           tc::ld16(acc_addr + sb * kSub, acc);
           uint4 cur[kCh];
-          if (load) {
+          if (!first) {
+            // multi-tick launch: this tile's potentials of the previous tick
+#pragma unroll
+            for (int i = 0; i < kCh; ++i) cur[i] = pbuf[(kCh * sb + i) * PB];
+          } else if (load) {
             ptx::cp_async_wait<1>();   // this pass's group (issued a tile ago) has landed
 #pragma unroll
             for (int i = 0; i < kCh; ++i) cur[i] = pbuf[(kCh * sb + i) * PB];
@@ -544,9 +599,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
                                                        outw);
           fired |= fb << (sb * kSub);
 #pragma unroll
-          for (int cc = 0; cc < kCh; ++cc)
-            dst[(size_t)(kCh * sb + cc) * Np] =
-                make_uint4(outw[4 * cc + 0], outw[4 * cc + 1], outw[4 * cc + 2], outw[4 * cc + 3]);
+          for (int cc = 0; cc < kCh; ++cc) {
+            const uint4 o = make_uint4(outw[4 * cc + 0], outw[4 * cc + 1], outw[4 * cc + 2], outw[4 * cc + 3]);
+            if (!last) pbuf[(kCh * sb + cc) * PB] = o;   // kept on chip for the next tick
+            else dst[(size_t)(kCh * sb + cc) * Np] = o;
+          }
         }
         // a5 / a6: route or count the spikes of real samples
         const int sj = s0 + jj * 32;          // first sample of this warp's half
@@ -596,7 +653,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
           const uint32_t m = transpose32(valid ? fired : 0u, lane);
           if (lane < lim && (n >> 5) < p.Wn) {
             const int sg = sj + lane;
-            if (p.raster) p.raster[(((size_t)(p.t - p.raster_t0) * p.S + sg) * p.G_loc + cl) * p.Wn + (n >> 5)] = m;
+            if (p.raster) p.raster[(((size_t)(t - p.raster_t0) * p.S + sg) * p.G_loc + cl) * p.Wn + (n >> 5)] = m;
             if (exporting) p.fired[((size_t)cl * p.Sr + sg) * p.Wn + (n >> 5)] = m;
           }
         }
@@ -609,6 +666,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
         tile = 0;
         ++cl;
       }
+    }
+    tick_barrier();
     }
     if (p.dbg && blockIdx.x == 0 && lane == 0) {
       p.dbg[64 * 16 + 2 * ew] = (unsigned long long)dbg_wait;
@@ -689,7 +748,9 @@ int tc_tile() { return NT; }
 
 size_t tc_smem_bytes(const Compiled& n) { return tc_layout(n.Npad, n.Kp, n.W, n.WIp, n.rmax).total; }
 
-cudaError_t launch_tick_tc(ranc_ctx* ctx, TickParams p) {
+namespace {
+
+void tc_fill_params(ranc_ctx* ctx, TickParams& p) {
   const Compiled& n = ctx->net;
   p.ST = NT;
   p.route = (const uint2*)ctx->d_route_tc.p;
@@ -702,12 +763,40 @@ cudaError_t launch_tick_tc(ranc_ctx* ctx, TickParams p) {
   p.n_inslots = ctx->n_inslots;
   p.nruns = (const int32_t*)ctx->d_nruns.p;
   p.rmax = n.rmax;
+}
+
+}  // namespace
+
+bool tc_multi_eligible(const ranc_ctx* ctx, int64_t num_ticks) {
+  if (ctx->kernel_active != RANC_KERNEL_TC || ctx->shard_mode == RANC_SHARD_CORES || num_ticks < 2) return false;
+  if (ctx->stream_opt == 1 || getenv("RANC_DEBUG_TIMELINE")) return false;
+  const int64_t total = (int64_t)ctx->G_loc * ((ctx->S + NT - 1) / NT);
+  return total <= ctx->num_sms;   // one work item per CTA, one CTA per SM (cooperative launch)
+}
+
+// all ticks of a ranc_run_ticks call in one cooperative launch (small
+// batches: at most one (core, 64-sample tile) per SM)
+cudaError_t launch_tc_multi(ranc_ctx* ctx, TickParams p, int64_t num_ticks) {
+  const Compiled& n = ctx->net;
+  tc_fill_params(ctx, p);
+  const int grid = (int)((int64_t)ctx->G_loc * ((ctx->S + NT - 1) / NT));
+  const size_t smem = tc_layout(n.Npad, n.Kp, n.W, n.WIp, n.rmax).total;
+  cudaFuncSetAttribute(tick_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  int nt = (int)std::min<int64_t>(num_ticks, 1 << 30);
+  void* args[] = {&p, &nt};
+  return cudaLaunchCooperativeKernel((const void*)tick_tc_kernel<true>, dim3(grid), dim3(kThreadsTC), args, smem,
+                                     ctx->stream);
+}
+
+cudaError_t launch_tick_tc(ranc_ctx* ctx, TickParams p) {
+  const Compiled& n = ctx->net;
+  tc_fill_params(ctx, p);
   const int64_t total = (int64_t)ctx->G_loc * ((ctx->S + NT - 1) / NT);
   const int grid = (int)std::min<int64_t>(total, ctx->num_sms);
   const size_t smem = tc_layout(n.Npad, n.Kp, n.W, n.WIp, n.rmax).total;
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(tick_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(tick_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     configured = true;
   }
   static const int dflags = getenv("RANC_DEBUG_FLAGS") ? atoi(getenv("RANC_DEBUG_FLAGS")) : 0;
@@ -717,7 +806,7 @@ cudaError_t launch_tick_tc(ranc_ctx* ctx, TickParams p) {
   if (dbg && !ctx->d_dbg.p) dev_alloc(ctx, &ctx->d_dbg, kDbg * 8);
   p.dbg = dbg ? (unsigned long long*)ctx->d_dbg.p : nullptr;
   if (dbg) cudaMemsetAsync(ctx->d_dbg.p, 0, kDbg * 8, ctx->stream);
-  tick_tc_kernel<<<grid, kThreadsTC, smem, ctx->stream>>>(p);
+  tick_tc_kernel<false><<<grid, kThreadsTC, smem, ctx->stream>>>(p, 1);
   if (dbg) {
     static unsigned long long h[kDbg];
     cudaMemcpyAsync(h, ctx->d_dbg.p, sizeof h, cudaMemcpyDeviceToHost, ctx->stream);

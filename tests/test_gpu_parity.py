@@ -4,8 +4,8 @@ for every potential, pending spike, fired bit, output event and class count
 import numpy as np
 import pytest
 
-from workloads.gen import (config1, config2, config3, config3_stream, config5, corpus_case, sweep_variants, tiny_case,
-                           vmm)
+from workloads.gen import (config1, config2, config3, config3_stream, config4, config5, corpus_case, sweep_variants,
+                           tiny_case, vmm)
 
 pytestmark = pytest.mark.gpu
 
@@ -393,3 +393,41 @@ def test_sweep_tiled_variants_on_gpu(ranc, oracle_mod, kernel):
         o = oracle_mod.Oracle(vn, inp).run(T)
         assert np.array_equal(cnt[:, v], o.counts()), f"variant {v}"
         assert np.array_equal(pot[:, v], o.potentials()), f"variant {v}"
+
+
+# ---- tensor-core path: all ticks of a call in one cooperative launch -----------
+
+
+@pytest.mark.parametrize("stream", [1, 0])
+def test_tc_multi_tick_launch(ranc, oracle_mod, stream):
+    net, inp = config2(S=130)
+    T = net.meta["T"]
+    for pieces in ([T], [1, 6, T - 7]):
+        sim = ranc.Simulator(net)
+        sim.set_option(ranc.OPT_KERNEL, 2)
+        sim.set_option(ranc.OPT_STREAM, stream)
+        sim.set_trace(ranc.TRACE_OUTPUT_EVENTS)
+        sim.load_inputs(inp)
+        l0 = sim.info()["kernel_launches"]
+        for k in pieces:
+            sim.run(k)
+        launches = sim.info()["kernel_launches"] - l0
+        o = oracle_mod.Oracle(net, inp).run(T)
+        assert np.array_equal(sim.outputs(), o.counts())
+        assert np.array_equal(sim.potentials(), o.potentials())
+        assert np.array_equal(sim.pending(), o.pending())
+        if len(pieces) == 1:
+            assert np.array_equal(sim.events(), o.events())
+            assert launches == (1 if stream == 0 else T)
+        sim.close()
+
+
+def test_tc_multi_tick_corpus_and_vmm(ranc, oracle_mod):
+    for seed in range(12):
+        net, inp = corpus_case(seed)
+        try:
+            final_state(ranc, oracle_mod, net, inp, 20, kernel="tc")
+        except pytest.skip.Exception:
+            continue
+    net, inp = config4("vmm32", S=20)
+    final_state(ranc, oracle_mod, net, inp, net.meta["T"], kernel="tc", events=False)
