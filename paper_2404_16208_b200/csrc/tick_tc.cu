@@ -200,6 +200,13 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
   auto tick_barrier = [&]() {
     if (kMulti) cg::this_grid().sync();
   };
+  // pipeline waits: sleeping (issue slots left to the working warps) in the
+  // throughput kernel; spinning in the multi-tick kernel, whose ticks are a
+  // latency chain (producer -> spike stage -> MMA -> epilogue -> barrier)
+  auto wait = [&](uint64_t* bar, uint32_t parity) {
+    if (kMulti) ptx::mbar_wait(bar, parity);
+    else ptx::mbar_wait_sleep(bar, parity, 2000);
+  };
 
   // role warps (debug flag 32 swaps the producer and MMA warps)
   const int prod_warp = kProdWarp, mma_warp = kMmaWarp;
@@ -240,7 +247,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       const int s = k % NS, u = k / NS;
       if (c != prev_core) {
         ++jw;
-        if (jw > 0) ptx::mbar_wait_sleep(&bars[WFREE], (jw - 1) & 1, 2000);
+        if (jw > 0) wait(&bars[WFREE], (jw - 1) & 1);
         if (lane == 0) {
           const uint32_t wb = (uint32_t)Np * Kp;
           ptx::mbar_arrive_expect_tx(&bars[WFULL], wb);
@@ -249,7 +256,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
         prev_core = c;
       }
       if (lane == 0) stamp(p, k, 0);
-      ptx::mbar_wait_sleep(&bars[SEMPTY0 + s], (u & 1) ^ 1, 2000);
+      wait(&bars[SEMPTY0 + s], (u & 1) ^ 1);
       if (lane == 0) {
         stamp(p, k, 1);
         uint8_t* st = smem + L.stage + s * L.stage_bytes;
@@ -288,12 +295,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       const int a = k % NA, ua = k / NA;
       if (c != prev_core) {
         ++jw;
-        ptx::mbar_wait_sleep(&bars[WFULL], jw & 1, 2000);
+        wait(&bars[WFULL], jw & 1);
         prev_core = c;
       }
-      ptx::mbar_wait_sleep(&bars[BFULL0 + s], u & 1, 2000);
+      wait(&bars[BFULL0 + s], u & 1);
       if (lane == 0) stamp(p, k, 5);
-      ptx::mbar_wait_sleep(&bars[ACCEMPTY0 + a], (ua & 1) ^ 1, 2000);
+      wait(&bars[ACCEMPTY0 + a], (ua & 1) ^ 1);
       tc::fence_after();
       if (lane == 0) {
         stamp(p, k, 6);
@@ -339,7 +346,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       const uint32_t* lines = reinterpret_cast<const uint32_t*>(st + L.lines);
       // a1: the scheduler rows due now were staged by the producer (TMA);
       // clear them in global memory (free again for spikes due at t + Rp)
-      ptx::mbar_wait_sleep(&bars[FULL0 + s], u & 1, 2000);
+      wait(&bars[FULL0 + s], u & 1);
       if (et == 0) stamp(p, k, 2);
       uint32_t* row = p.ring + (((size_t)cur * p.G_loc + cl) * p.Sr + s0) * W;
       if (p.incoming[c]) {
@@ -404,7 +411,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       // samples >= ns of a tail tile get no spikes.  Lanes take consecutive
       // samples so each 8-lane phase of the 16-byte stores fills one core
       // matrix (bank-conflict free).
-      ptx::mbar_wait_sleep(&bars[BEMPTY0 + s], (u & 1) ^ 1, 2000);
+      wait(&bars[BEMPTY0 + s], (u & 1) ^ 1);
       if (et == 0) stamp(p, k, 3);
       uint8_t* b_s = st + L.b;
       {
@@ -514,7 +521,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       // three wait on the quarter's named barrier (no issue slots spent)
       // back-off polling (measured best against the suspend-hint wait, a plain
       // spin and a per-quarter named barrier)
-      ptx::mbar_wait_backoff(&bars[ACCFULL0 + a], ua & 1, 128);
+      if (kMulti) ptx::mbar_wait(&bars[ACCFULL0 + a], ua & 1);
+      else ptx::mbar_wait_backoff(&bars[ACCFULL0 + a], ua & 1, 128);
       if (p.dbg && blockIdx.x == 0) dbg_wait += clock64() - tw0;
       if (lane == 0 && ew == 0) stamp(p, k, 8);
       tc::fence_after();
