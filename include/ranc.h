@@ -151,9 +151,18 @@ ranc_status ranc_read_pending(ranc_ctx* ctx, uint32_t* bits, size_t n);
  * (sample, tick, x, y, neuron) of output-bus spikes, canonical order
  * (sample, tick, y, x, neuron).  Reading refers to the most recent
  * ranc_run_ticks call.  *written receives the bytes required/written;
- * a too-small buffer returns RANC_E_SIZE with *written = bytes required. */
+ * a too-small buffer returns RANC_E_SIZE with *written = bytes required.
+ * RANC_TRACE_STATE_DIGEST (per-tick parity at sizes where
+ * state dumps are too large): uint64 [ticks][S_local], per (tick, sample) the
+ * mod-2^64 sum over this context's cores of mix(((c*N+n)<<32) | (u32)pot)
+ * for every neuron after the tick, mix(K1 ^ (c*N+n)) for every neuron that
+ * fired in it and mix(K2 ^ (c*A+a)) for every axon spike it integrated
+ * (original indices; mix = SplitMix64 finaliser, K1 = 0x243F6A8885A308D3,
+ * K2 = 0x13198A2E03707344).  Sums over core shards add up to the whole
+ * network's digest.  Forces per-tick launches while enabled. */
 #define RANC_TRACE_SPIKE_RASTER 1u
 #define RANC_TRACE_OUTPUT_EVENTS 2u
+#define RANC_TRACE_STATE_DIGEST 4u
 ranc_status ranc_set_trace(ranc_ctx* ctx, uint32_t flags);
 ranc_status ranc_read_trace(ranc_ctx* ctx, uint32_t kind, void* buf, size_t bytes, size_t* written);
 

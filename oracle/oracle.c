@@ -252,3 +252,38 @@ int64_t oracle_get_events(const oracle_state* st, int64_t* out, int64_t cap) {
   }
   return total;
 }
+
+/* State digest of the last executed tick (per-(sample,
+ * tick) commutative digest for large-config parity; an instrument, not part
+ * of the method): for every sample, mod 2^64,
+ *   sum_{c,n} mix(((c*N+n) << 32) | (u32)pot)            potentials after the tick
+ * + sum_{c,n fired} mix(K1 ^ (c*N+n))                    spikes of the tick
+ * + sum_{c,a in spk_in} mix(K2 ^ (c*A+a))                 axon spikes integrated
+ * with mix = the SplitMix64 finaliser.  out: [S]. */
+static uint64_t digest_mix(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+void oracle_digest(const oracle_state* st, uint64_t* out) {
+  const uint64_t K1 = 0x243F6A8885A308D3ull, K2 = 0x13198A2E03707344ull;
+  const int G = st->G, A = st->net.axons, N = st->net.neurons, R = st->R;
+  const int prev = st->now > 0 ? (int)((st->now - 1) % R) : -1;
+  for (int32_t s = 0; s < st->S; ++s) {
+    uint64_t d = 0;
+    for (int c = 0; c < G; ++c)
+      for (int n = 0; n < N; ++n) {
+        const size_t cn = (size_t)c * N + n;
+        const uint64_t id = (uint64_t)cn;
+        d += digest_mix((id << 32) | (uint32_t)(int32_t)st->pot[(size_t)s * G * N + cn]);
+        if (st->fired[(size_t)s * G * N + cn]) d += digest_mix(K1 ^ id);
+      }
+    if (prev >= 0)
+      for (int c = 0; c < G; ++c)
+        for (int a = 0; a < A; ++a)
+          if (st->pend[(((size_t)s * G + c) * R + prev) * A + a]) d += digest_mix(K2 ^ (uint64_t)((size_t)c * A + a));
+    out[s] = d;
+  }
+}

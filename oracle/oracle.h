@@ -83,6 +83,8 @@ void    oracle_get_counts(const oracle_state* st, int64_t* out);       /* [S][C]
  * Returns the total number of events; copies min(total, cap) records of 5
  * int64 (s, t, x, y, n) into out. */
 int64_t oracle_get_events(const oracle_state* st, int64_t* out, int64_t cap);
+/* SURVEY G21 state digest of the last executed tick, per sample: [S] */
+void    oracle_digest(const oracle_state* st, uint64_t* out);
 
 #ifdef __cplusplus
 }

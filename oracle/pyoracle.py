@@ -58,7 +58,7 @@ def lib():
         _lib.oracle_now.restype = C.c_int64
         _lib.oracle_now.argtypes = [C.c_void_p]
         for f in ("oracle_get_potentials", "oracle_get_pending", "oracle_get_fired",
-                  "oracle_get_counts"):
+                  "oracle_get_counts", "oracle_digest"):
             getattr(_lib, f).argtypes = [C.c_void_p, C.c_void_p]
         _lib.oracle_get_events.restype = C.c_int64
         _lib.oracle_get_events.argtypes = [C.c_void_p, C.c_void_p, C.c_int64]
@@ -145,6 +145,12 @@ class Oracle:
         out = np.zeros((self.S, max(self.net.num_classes, 0)), np.int64)
         if out.size:
             lib().oracle_get_counts(self.h, out.ctypes.data)
+        return out
+
+    def digest(self):
+        """SURVEY G21 state digest of the last executed tick, uint64 [S]."""
+        out = np.zeros(self.S, np.uint64)
+        lib().oracle_digest(self.h, out.ctypes.data)
         return out
 
     def events(self):

@@ -16,6 +16,7 @@ STATUS = {0: "RANC_OK", 1: "RANC_E_ARG", 2: "RANC_E_CONFIG", 3: "RANC_E_BITWIDTH
           10: "RANC_E_OOM", 11: "RANC_E_NCCL"}
 TRACE_SPIKE_RASTER = 1
 TRACE_OUTPUT_EVENTS = 2
+TRACE_STATE_DIGEST = 4
 OPT_SAMPLE_TILE = 1
 OPT_INPUT_DECODE = 2
 OPT_KERNEL = 3

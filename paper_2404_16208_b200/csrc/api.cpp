@@ -100,7 +100,7 @@ void free_all(ranc_ctx* ctx) {
                     &ctx->d_nruns, &ctx->d_wflags_tc, &ctx->d_incoming, &ctx->d_word_runs, &ctx->d_pot, &ctx->d_ring, &ctx->d_counts, &ctx->d_lines,
                     &ctx->d_stage, &ctx->d_raster, &ctx->d_fired, &ctx->d_exports, &ctx->d_send, &ctx->d_recv,
                     &ctx->d_send_list, &ctx->d_recv_list, &ctx->d_dbg, &ctx->d_inw, &ctx->d_inslot,
-                    &ctx->d_slot_core};
+                    &ctx->d_slot_core, &ctx->d_spkin, &ctx->d_digest, &ctx->d_perm_dig};
   for (DevBuf* b : bufs) dev_free(ctx, b);
 }
 
@@ -324,6 +324,18 @@ ranc_status prepare_run(ranc_ctx* ctx, int64_t num_ticks) {
     if (bytes) CK(cudaMemsetAsync(ctx->d_raster.p, 0, bytes, ctx->stream), "raster clear");
     ctx->raster_t0 = ctx->now;
     ctx->raster_ticks = num_ticks;
+    if (ctx->trace_flags & RANC_TRACE_STATE_DIGEST) {
+      const Compiled& c = ctx->net;
+      const size_t sp = (size_t)ctx->S * ctx->G_loc * c.W * 4;
+      if (ctx->d_spkin.bytes < sp) TRY(dev_alloc(ctx, &ctx->d_spkin, sp));
+      const size_t db = std::max<size_t>(8, (size_t)num_ticks * ctx->S * 8);
+      if (ctx->d_digest.bytes < db) TRY(dev_alloc(ctx, &ctx->d_digest, db));
+      // a' -> a of the active kernel's axon order
+      if (!ctx->d_perm_dig.p || ctx->perm_dig_kernel != ctx->kernel_active) {
+        TRY(upload(ctx, &ctx->d_perm_dig, ctx->kernel_active == RANC_KERNEL_TC ? c.perm_tc : c.perm));
+        ctx->perm_dig_kernel = ctx->kernel_active;
+      }
+    }
   } else if (ctx->d_raster.p) {
     dev_free(ctx, &ctx->d_raster);
     ctx->raster_ticks = 0;
@@ -341,7 +353,8 @@ ranc_status ranc_run_ticks(ranc_ctx* ctx, int64_t num_ticks) {
   }
   TRY(prepare_run(ctx, num_ticks));
   const bool exchange = ctx->shard_mode == RANC_SHARD_CORES && ctx->nccl_comm && ctx->world > 1;
-  if (!exchange && stream_eligible(ctx, num_ticks)) {
+  const bool digest = (ctx->trace_flags & RANC_TRACE_STATE_DIGEST) != 0;
+  if (!exchange && !digest && stream_eligible(ctx, num_ticks)) {
     // streaming mode: every tick of this call in one cooperative launch
     int64_t left = num_ticks;
     while (left > 0) {
@@ -355,6 +368,7 @@ ranc_status ranc_run_ticks(ranc_ctx* ctx, int64_t num_ticks) {
     const int64_t t = ctx->now;
     CK(launch_one_tick(ctx), "tick kernel launch");
     if (exchange) TRY(exchange_nccl(ctx, t));
+    if (digest) CK(launch_digest(ctx, i), "digest kernel launch");
   }
   return RANC_OK;
 }
@@ -392,6 +406,11 @@ ranc_status ranc_run_ticks_loopback(ranc_ctx* const* ctxs, int n, int64_t num_ti
       if (e != cudaSuccess) st = set_cuda_error(ctxs[i], e, "tick kernel launch");
     }
     if (st == RANC_OK && n > 1) st = exchange_loopback(g, t);
+    for (int i = 0; i < n && st == RANC_OK; ++i)
+      if (ctxs[i]->trace_flags & RANC_TRACE_STATE_DIGEST) {
+        cudaError_t e = launch_digest(ctxs[i], k);
+        if (e != cudaSuccess) st = set_cuda_error(ctxs[i], e, "digest kernel launch");
+      }
   }
   for (int i = 0; i < n; ++i) ctxs[i]->stream = saved[i];
   if (st == RANC_OK) {
@@ -500,7 +519,7 @@ ranc_status ranc_read_pending(ranc_ctx* ctx, uint32_t* bits, size_t n) {
 
 ranc_status ranc_set_trace(ranc_ctx* ctx, uint32_t flags) {
   TRY(check_ctx(ctx));
-  if (flags & ~(RANC_TRACE_SPIKE_RASTER | RANC_TRACE_OUTPUT_EVENTS)) {
+  if (flags & ~(RANC_TRACE_SPIKE_RASTER | RANC_TRACE_OUTPUT_EVENTS | RANC_TRACE_STATE_DIGEST)) {
     ctx->err = "unknown trace flags";
     return RANC_E_ARG;
   }
@@ -512,12 +531,24 @@ ranc_status ranc_read_trace(ranc_ctx* ctx, uint32_t kind, void* buf, size_t byte
   TRY(check_ctx(ctx));
   if (!written) return RANC_E_ARG;
   *written = 0;
-  if (!(ctx->trace_flags & kind) || (kind != RANC_TRACE_SPIKE_RASTER && kind != RANC_TRACE_OUTPUT_EVENTS)) {
+  if (!(ctx->trace_flags & kind) ||
+      (kind != RANC_TRACE_SPIKE_RASTER && kind != RANC_TRACE_OUTPUT_EVENTS && kind != RANC_TRACE_STATE_DIGEST)) {
     ctx->err = "trace kind not enabled (ranc_set_trace) or unknown";
     return RANC_E_STATE;
   }
   const Compiled& c = ctx->net;
   const int GL = ctx->G_loc;
+  if (kind == RANC_TRACE_STATE_DIGEST) {
+    const size_t dbytes = (size_t)ctx->raster_ticks * ctx->S * 8;
+    *written = dbytes;
+    if (bytes < dbytes || (!buf && dbytes)) {
+      ctx->err = "digest buffer too small";
+      return RANC_E_SIZE;
+    }
+    CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+    if (dbytes) CK(cudaMemcpyAsync(buf, ctx->d_digest.p, dbytes, cudaMemcpyDeviceToHost, ctx->stream), "D2H digest");
+    return sync(ctx, "ranc_read_trace");
+  }
   const size_t rbytes = (size_t)ctx->raster_ticks * ctx->S * GL * c.Wn * 4;
   CK(cudaSetDevice(ctx->device), "cudaSetDevice");
   if (kind == RANC_TRACE_SPIKE_RASTER) {

@@ -76,6 +76,7 @@ struct TickParams {
   unsigned long long* dbg;  // optional pipeline timeline (RANC_DEBUG_TIMELINE)
   const uint8_t* wflags;    // [G][Npad/32] per-warp flags (bit 0: block route), or nullptr
   const uint8_t* incoming;  // [G] 1 if any neuron of the network routes to the core (its ring can be non-zero)
+  uint32_t* spkin;          // RANC_TRACE_STATE_DIGEST: [S][G_loc][W] axon spikes integrated this tick, or nullptr
   int32_t dbgflags;         // RANC_DEBUG_FLAGS (timing experiments only; results invalid when set)
 };
 
@@ -166,6 +167,9 @@ struct ranc_ctx {
   ranc::DevBuf d_dbg;            // RANC_DEBUG_TIMELINE
   // tensor-core path: input decode (once per ranc_load_inputs)
   ranc::DevBuf d_inw, d_inslot, d_slot_core;
+  // RANC_TRACE_STATE_DIGEST
+  ranc::DevBuf d_spkin, d_digest, d_perm_dig;
+  int32_t perm_dig_kernel = 0;   // kernel whose axon order d_perm_dig holds
   int32_t n_inslots = 0;
   bool inw_valid = false;
 };
@@ -200,6 +204,7 @@ cudaError_t decode_inputs_tc(ranc_ctx* ctx);
 bool stream_eligible(ranc_ctx* ctx, int64_t num_ticks);
 bool tc_multi_eligible(const ranc_ctx* ctx, int64_t num_ticks);
 cudaError_t launch_tc_multi(ranc_ctx* ctx, TickParams p, int64_t num_ticks);
+cudaError_t launch_digest(ranc_ctx* ctx, int64_t tick_index);
 cudaError_t launch_stream(ranc_ctx* ctx, int64_t num_ticks);
 // api.cpp
 ranc_status dev_alloc(ranc_ctx* ctx, DevBuf* b, size_t bytes);

@@ -129,6 +129,9 @@ __device__ __forceinline__ void popc_tile(const TickParams& p, int cl, int tile,
     }
     __syncthreads();
   }
+  if (p.spkin)   // RANC_TRACE_STATE_DIGEST: the axon spikes integrated this tick
+    for (int i = tid; i < ns * W; i += blockDim.x)
+      p.spkin[((size_t)(s0 + i / W) * p.G_loc + cl) * W + i % W] = raw[i];
   phase_mark(1);   // a2 input injection
   // expand to one spike word per piece
   const uint8_t* pword = p.pword + (size_t)c * E;
@@ -399,6 +402,54 @@ __global__ void __launch_bounds__(kThreads, (E <= 12 ? 4 : (E <= 16 ? 3 : 2)))
     for (int s = 0; s < ns; ++s) p.pot[((size_t)cl * p.S + s0 + s) * p.Npad + n] = pot_s[s * p.Npad + n];
 }
 
+// RANC_TRACE_STATE_DIGEST: one block per sample sums,
+// mod 2^64, mix() of every (neuron, potential), every fired neuron and every
+// integrated axon spike of this context's cores (original indices).
+__device__ __forceinline__ uint64_t digest_mix(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__global__ void digest_kernel(const int16_t* __restrict__ pot, int tc_layout, const uint32_t* __restrict__ raster,
+                              const uint32_t* __restrict__ spkin, const int32_t* __restrict__ perm, int c_lo,
+                              int G_loc, int S, int N, int Npad, int A, int W, int Wn, uint64_t* __restrict__ out) {
+  const uint64_t K1 = 0x243F6A8885A308D3ull, K2 = 0x13198A2E03707344ull;
+  constexpr int TNT = 64;   // tensor-core potential tile (tick_tc.cu NT)
+  const int nT = (S + TNT - 1) / TNT;
+  for (int s = blockIdx.x; s < S; s += gridDim.x) {
+    uint64_t d = 0;
+    for (int i = threadIdx.x; i < G_loc * N; i += blockDim.x) {
+      const int cl = i / N, n = i - cl * N;
+      const uint64_t id = (uint64_t)(c_lo + cl) * N + n;
+      const size_t pi = tc_layout
+                            ? ((((size_t)cl * nT + s / TNT) * (TNT / 8) + (s % TNT) / 8) * Npad + n) * 8 + s % 8
+                            : ((size_t)cl * S + s) * Npad + n;
+      d += digest_mix((id << 32) | (uint32_t)(int32_t)pot[pi]);
+      if ((raster[((size_t)s * G_loc + cl) * Wn + (n >> 5)] >> (n & 31)) & 1u) d += digest_mix(K1 ^ id);
+    }
+    for (int i = threadIdx.x; i < G_loc * W * 32; i += blockDim.x) {
+      const int cl = i / (W * 32), ap = i - cl * W * 32;
+      if (ap < A && ((spkin[((size_t)s * G_loc + cl) * W + (ap >> 5)] >> (ap & 31)) & 1u)) {
+        const int c = c_lo + cl;
+        d += digest_mix(K2 ^ (uint64_t)((size_t)c * A + perm[(size_t)c * A + ap]));
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xFFFFFFFFu, d, o);
+    __shared__ uint64_t part[32];
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = d;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint64_t tot = 0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += part[w];
+      out[s] = tot;
+    }
+    __syncthreads();
+  }
+}
+
 // [S][T_in][WI] -> [T_in][Sr][WIp] (padding words stay zero)
 __global__ void transpose_lines_kernel(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, int S, int T,
                                        int WI, int Sr, int WIp) {
@@ -547,6 +598,7 @@ TickParams make_params(ranc_ctx* ctx) {
   p.raster = (uint32_t*)ctx->d_raster.p;
   p.raster_t0 = ctx->raster_t0;
   p.fired = ctx->shard_mode == RANC_SHARD_CORES ? (uint32_t*)ctx->d_fired.p : nullptr;
+  p.spkin = (ctx->trace_flags & RANC_TRACE_STATE_DIGEST) ? (uint32_t*)ctx->d_spkin.p : nullptr;
   p.exports = (const uint8_t*)ctx->d_exports.p;
   p.Kp = n.Kp;
   p.wfold = (const uint8_t*)ctx->d_wfold.p;
@@ -606,6 +658,19 @@ cudaError_t launch_stream(ranc_ctx* ctx, int64_t num_ticks) {
   ctx->fresh = false;
   ctx->now += nt;
   return cudaSuccess;
+}
+
+cudaError_t launch_digest(ranc_ctx* ctx, int64_t tick_index) {
+  const Compiled& n = ctx->net;
+  const uint32_t* raster = (const uint32_t*)ctx->d_raster.p + (size_t)tick_index * ctx->S * ctx->G_loc * n.Wn;
+  uint64_t* out = (uint64_t*)ctx->d_digest.p + (size_t)tick_index * ctx->S;
+  const int grid = (int)std::min<int64_t>(ctx->S, 148 * 8);
+  digest_kernel<<<grid, 256, 0, ctx->stream>>>((const int16_t*)ctx->d_pot.p, ctx->kernel_active == RANC_KERNEL_TC ? 1 : 0,
+                                               raster, (const uint32_t*)ctx->d_spkin.p,
+                                               (const int32_t*)ctx->d_perm_dig.p, ctx->c_lo, ctx->G_loc, (int)ctx->S,
+                                               n.N, n.Npad, n.A, n.W, n.Wn, out);
+  ctx->launches++;
+  return cudaGetLastError();
 }
 
 cudaError_t launch_one_tick(ranc_ctx* ctx) {

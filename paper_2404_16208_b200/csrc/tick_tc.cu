@@ -404,6 +404,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
           }
         }
       }
+      if (p.spkin)   // RANC_TRACE_STATE_DIGEST: the axon spikes integrated this tick
+        for (int i = et; i < ns * W; i += kExpThreads)
+          p.spkin[((size_t)(s0 + i / W) * p.G_loc + cl) * W + i % W] = raw[i];
       if (et == 0) stamp(p, k, 13);
       named_sync(2, kExpThreads);
       if (et == 0) stamp(p, k, 14);

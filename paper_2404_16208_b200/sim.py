@@ -183,6 +183,16 @@ class Simulator:
                                           C.byref(got)))
         return buf[:nb // 8].reshape(-1, 5)
 
+    def digests(self) -> np.ndarray:
+        """uint64 [ticks][S] state digests (RANC_TRACE_STATE_DIGEST)
+        of the last run() call."""
+        nb = self._trace_bytes(L.TRACE_STATE_DIGEST)
+        buf = np.zeros(max(nb // 8, 1), np.uint64)
+        got = C.c_size_t(0)
+        self._ck(self.lib.ranc_read_trace(self.h, L.TRACE_STATE_DIGEST, buf.ctypes.data, buf.nbytes,
+                                          C.byref(got)))
+        return buf[:nb // 8].reshape(-1, self.S)
+
     # -- multi-GPU ----------------------------------------------------------
     @staticmethod
     def unique_id() -> bytes:

@@ -431,3 +431,57 @@ def test_tc_multi_tick_corpus_and_vmm(ranc, oracle_mod):
             continue
     net, inp = config4("vmm32", S=20)
     final_state(ranc, oracle_mod, net, inp, net.meta["T"], kernel="tc", events=False)
+
+
+# ---- state digest (RANC_TRACE_STATE_DIGEST) ---------------------
+
+
+def digest_check(ranc, oracle_mod, net, inp, T, kernel):
+    sim = make_sim(ranc, net, kernel)
+    sim.set_trace(ranc.TRACE_STATE_DIGEST)
+    sim.load_inputs(inp).run(T)
+    got = sim.digests()
+    sim.close()
+    o = oracle_mod.Oracle(net, inp)
+    for t in range(T):
+        o.run(1)
+        assert np.array_equal(got[t], o.digest()), f"{net.name} tick {t}"
+
+
+def test_digest_config2_every_tick(ranc, oracle_mod, kernel):
+    net, inp = config2(S=70)
+    digest_check(ranc, oracle_mod, net, inp, net.meta["T"], kernel)
+
+
+@pytest.mark.parametrize("seed", range(0, 10))
+def test_digest_corpus(ranc, oracle_mod, seed, kernel):
+    net, inp = corpus_case(seed)
+    digest_check(ranc, oracle_mod, net, inp, 12, kernel)
+
+
+def test_digest_config3_full_width(ranc, oracle_mod):
+    # all 512 cores, a 3-sample slice checked against the oracle tick by tick
+    net, inp = config3(S=3)
+    digest_check(ranc, oracle_mod, net, inp, net.meta["T"], "tc")
+
+
+def test_digest_core_sharded_shards_add_up(ranc, oracle_mod, kernel):
+    # the digest is a sum over cores: the shards' digests add up (mod 2^64)
+    # to the whole network's, tick by tick
+    net, inp = config5(S=3, T=14, grid=6, variant="global")
+    T = 14
+    sims = [make_sim(ranc, net, kernel) for _ in range(3)]
+    ranc.Simulator.init_loopback(sims)
+    for s in sims:
+        s.set_trace(ranc.TRACE_STATE_DIGEST)
+        s.load_inputs(inp)
+    ranc.Simulator.run_loopback(sims, T)
+    total = sims[0].digests().copy()
+    for s in sims[1:]:
+        total += s.digests()   # uint64 wrap-around = mod 2^64
+    for s in sims:
+        s.close()
+    o = oracle_mod.Oracle(net, inp)
+    for t in range(T):
+        o.run(1)
+        assert np.array_equal(total[t], o.digest()), f"tick {t}"
