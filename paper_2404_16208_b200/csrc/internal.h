@@ -77,7 +77,6 @@ struct TickParams {
   const uint8_t* wflags;    // [G][Npad/32] per-warp flags (bit 0: block route), or nullptr
   const uint8_t* incoming;  // [G] 1 if any neuron of the network routes to the core (its ring can be non-zero)
   uint32_t* spkin;          // RANC_TRACE_STATE_DIGEST: [S][G_loc][W] axon spikes integrated this tick, or nullptr
-  int32_t dbgflags;         // RANC_DEBUG_FLAGS (timing experiments only; results invalid when set)
 };
 
 // Host copy of the compiled network.

@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
     else ptx::mbar_wait_sleep(bar, parity, 2000);
   };
 
-  // role warps (debug flag 32 swaps the producer and MMA warps)
+  // role warps
   const int prod_warp = kProdWarp, mma_warp = kMmaWarp;
   if (warp == mma_warp) tc::alloc(tmem_holder, tcols < 32 ? 32 : tcols);
   if (threadIdx.x == 0) {
@@ -810,8 +810,6 @@ cudaError_t launch_tick_tc(ranc_ctx* ctx, TickParams p) {
     cudaFuncSetAttribute(tick_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     configured = true;
   }
-  static const int dflags = getenv("RANC_DEBUG_FLAGS") ? atoi(getenv("RANC_DEBUG_FLAGS")) : 0;
-  p.dbgflags = dflags;
   static const bool dbg = getenv("RANC_DEBUG_TIMELINE") != nullptr;
   constexpr int kDbg = 64 * 16 + 64 + 512;   // timeline, per-warp wait/total, per-CTA start/end
   if (dbg && !ctx->d_dbg.p) dev_alloc(ctx, &ctx->d_dbg, kDbg * 8);
