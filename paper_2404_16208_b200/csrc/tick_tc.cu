@@ -130,9 +130,11 @@ __device__ __forceinline__ uint4* pot_tile(const TickParams& p, int c, int tile,
 // mask and the 32 new potentials packed as s16 pairs.  The reset is one IMAD:
 // r = v * lin + (fire ? bf : bn).  kSat16 (pb = 16): the saturation and the
 // packing of two potentials are one cvt.pack.sat.s16.s32.
+// `one` is 1 at run time but opaque to the compiler, so that the "no change"
+// move stays a predicated IMAD (FMA pipe) instead of becoming an ALU select.
 template <bool kSat16, int NE>
 __device__ __forceinline__ uint32_t lif(const uint4 (&cur)[NE / 8], const uint32_t (&acc)[NE], int leak, int pth,
-                                        int nth, int linmul, int bf, int bn, int lo, int hi,
+                                        int nth, int linmul, int bf, int bn, int lo, int hi, int one,
                                         uint32_t (&outw)[NE / 2]) {
   uint32_t fired = 0u;
 #pragma unroll
@@ -145,8 +147,9 @@ __device__ __forceinline__ uint32_t lif(const uint4 (&cur)[NE / 8], const uint32
       const int i = 2 * i2 + e;
       // the sign-extended half plus the input: one LEA.HI.SX32 (the low half
       // is first moved up with an IMAD on the FMA pipe)
-      const int src = e ? (int)w32 : (int)(w32 * 65536u);
-      const int v = (src >> 16) + ((int)acc[i] + leak);
+      uint32_t src = w32;
+      if (!e) asm("mul.lo.u32 %0, %1, 65536;" : "=r"(src) : "r"(w32));   // IMAD.SHL (FMA pipe)
+      const int v = ((int)src >> 16) + ((int)acc[i] + leak);
       // fire / change predicates; the reset value is selected with
       // predicated IMADs (FMA pipe) instead of ALU selects:
       //   r = v*lin + bn; fire: r = v*lin + bf; no change: r = v
@@ -156,10 +159,10 @@ __device__ __forceinline__ uint32_t lif(const uint4 (&cur)[NE / 8], const uint32
           "setp.lt.or.s32 pc, %2, %4, pf;\n\t"
           "mad.lo.s32 %0, %2, %5, %7;\n\t"
           "@pf mad.lo.s32 %0, %2, %5, %6;\n\t"
-          "@!pc mov.b32 %0, %2;\n\t"
+          "@!pc mad.lo.s32 %0, %2, %9, 0;\n\t"
           "@pf add.u32 %1, %1, %8;\n\t}"
           : "=&r"(nv), "+r"(fired)
-          : "r"(v), "r"(pth), "r"(nth), "r"(linmul), "r"(bf), "r"(bn), "r"(1u << i));
+          : "r"(v), "r"(pth), "r"(nth), "r"(linmul), "r"(bf), "r"(bn), "r"(1u << i), "r"(one));
       if (!kSat16) nv = min(max(nv, lo), hi);
       nvp[e] = nv;
     }
@@ -483,6 +486,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
     constexpr int PB = 32 * kEpiWarps;   // uint4 stride between chunks in potbuf
     const bool load = active && !p.fresh;
     const bool sat16 = p.pot_lo == -32768 && p.pot_hi == 32767;
+    const int one = 1 + (p.N >> 30);   // N <= 1024: 1 (see lif)
     uint4 initv = make_uint4(0u, 0u, 0u, 0u);
     // work item idx = cl * nT + tile, advanced incrementally (no divisions);
     // its potential tile is pot + idx * tile_stride (pot_tile); this warp's
@@ -605,9 +609,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
           if (lane == 0 && ew == 0) stamp(p, k, 9 + sb);
           // a4: leak / thresholds / reset per sample
           uint32_t outw[kSub / 2];
-          const uint32_t fb = sat16 ? lif<true, kSub>(cur, acc, leak, pth, nth, linmul, bf, bn, 0, 0, outw)
+          const uint32_t fb = sat16 ? lif<true, kSub>(cur, acc, leak, pth, nth, linmul, bf, bn, 0, 0, one, outw)
                                     : lif<false, kSub>(cur, acc, leak, pth, nth, linmul, bf, bn, p.pot_lo, p.pot_hi,
-                                                       outw);
+                                                       one, outw);
           fired |= fb << (sb * kSub);
 #pragma unroll
           for (int cc = 0; cc < kCh; ++cc) {
