@@ -181,9 +181,15 @@ __device__ __forceinline__ uint32_t lif(const uint4 (&cur)[NE / 8], const uint32
 // of a ranc_run_ticks call in one launch; the grid barrier is the tick
 // barrier (a7) and each epilogue thread keeps its potentials in
 // registers between ticks (stored once, after the last tick).
-template <bool kMulti>
+template <bool kMulti, bool kDebug>
 __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams p, const int nticks_arg) {
   const int nticks = kMulti ? nticks_arg : 1;
+  // kDebug: the RANC_DEBUG_TIMELINE instrumentation (a separate instantiation,
+  // so that the product kernel issues none of it)
+  auto stamp_k = [&](int k, int slot) {
+    if (kDebug) stamp(p, k, slot);
+  };
+  const bool dbg_on = kDebug && p.dbg;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + 8 * NBARS);
@@ -234,7 +240,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
   tc::fence_after();
   const uint32_t tmem = *tmem_holder;
   unsigned long long gt_start = 0;
-  if (p.dbg && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt_start));
+  if (dbg_on && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt_start));
 
   if (warp == prod_warp) {
     // ------------------------------------------------------------ producer (TMA)
@@ -258,10 +264,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
         }
         prev_core = c;
       }
-      if (lane == 0) stamp(p, k, 0);
+      if (lane == 0) stamp_k(k, 0);
       wait(&bars[SEMPTY0 + s], (u & 1) ^ 1);
       if (lane == 0) {
-        stamp(p, k, 1);
+        stamp_k(k, 1);
         uint8_t* st = smem + L.stage + s * L.stage_bytes;
         const int s0 = tile * NT;
         const bool inject = t < p.T_in && p.nruns[c] > 0;
@@ -302,11 +308,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
         prev_core = c;
       }
       wait(&bars[BFULL0 + s], u & 1);
-      if (lane == 0) stamp(p, k, 5);
+      if (lane == 0) stamp_k(k, 5);
       wait(&bars[ACCEMPTY0 + a], (ua & 1) ^ 1);
       tc::fence_after();
       if (lane == 0) {
-        stamp(p, k, 6);
+        stamp_k(k, 6);
         const uint8_t* b_s = smem + L.stage + s * L.stage_bytes + L.b;
         const uint32_t acc = tmem + a * acc_stride;
         for (int hh = 0; hh < Mh; ++hh)
@@ -317,7 +323,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
           }
         tc::commit(&bars[BEMPTY0 + s]);
         tc::commit(&bars[ACCFULL0 + a]);
-        stamp(p, k, 7);
+        stamp_k(k, 7);
         // last tile of this core (in a multi-tick launch the next item is the
         // same core again, except after the last tick)
         if (k0 + 1 < nwork ? tile + 1 == nT : it + 1 == nticks) tc::commit(&bars[WFREE]);
@@ -350,7 +356,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       // a1: the scheduler rows due now were staged by the producer (TMA);
       // clear them in global memory (free again for spikes due at t + Rp)
       wait(&bars[FULL0 + s], u & 1);
-      if (et == 0) stamp(p, k, 2);
+      if (et == 0) stamp_k(k, 2);
       uint32_t* row = p.ring + (((size_t)cur * p.G_loc + cl) * p.Sr + s0) * W;
       if (p.incoming[c]) {
         // only the words that hold spikes need clearing
@@ -360,7 +366,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
         // no neuron routes here: the ring stays zero and was not loaded
         for (int i = et; i < NT * W; i += kExpThreads) raw[i] = 0u;
       }
-      if (et == 0) stamp(p, k, 12);
+      if (et == 0) stamp_k(k, 12);
       // a2: external inputs.  Thread <-> (sample, ring word): OR in the line
       // runs overlapping that word (no atomics: every word has one owner)
       if (t < p.T_in && p.nruns[c] > 0 && p.inw) {
@@ -410,15 +416,15 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       if (p.spkin)   // RANC_TRACE_STATE_DIGEST: the axon spikes integrated this tick
         for (int i = et; i < ns * W; i += kExpThreads)
           p.spkin[((size_t)(s0 + i / W) * p.G_loc + cl) * W + i % W] = raw[i];
-      if (et == 0) stamp(p, k, 13);
+      if (et == 0) stamp_k(k, 13);
       named_sync(2, kExpThreads);
-      if (et == 0) stamp(p, k, 14);
+      if (et == 0) stamp_k(k, 14);
       // bits -> 0/1 bytes, canonical K-major operand (rows = samples);
       // samples >= ns of a tail tile get no spikes.  Lanes take consecutive
       // samples so each 8-lane phase of the 16-byte stores fills one core
       // matrix (bank-conflict free).
       wait(&bars[BEMPTY0 + s], (u & 1) ^ 1);
-      if (et == 0) stamp(p, k, 3);
+      if (et == 0) stamp_k(k, 3);
       uint8_t* b_s = st + L.b;
       {
         // thread <-> (sample sm, half hf): the 16-bit halves hf of the
@@ -448,11 +454,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
           for (int w = 0; w < W; ++w) emit(w, real ? rrow[w] : 0u);
         }
       }
-      if (et == 0) stamp(p, k, 15);
+      if (et == 0) stamp_k(k, 15);
       ptx::fence_proxy_async_smem();
       named_sync(2, kExpThreads);
       if (et == 0) {
-        stamp(p, k, 4);
+        stamp_k(k, 4);
         ptx::mbar_arrive(&bars[BFULL0 + s]);
         ptx::mbar_arrive(&bars[SEMPTY0 + s]);   // raw/lines of this stage are consumed
       }
@@ -504,8 +510,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       }
     }
     long long dbg_wait = 0;
-    const long long dbg_t0 = p.dbg ? clock64() : 0;
+    const long long dbg_t0 = dbg_on ? clock64() : 0;
     const int cl0 = cl, tile0 = tile;
+    // this thread's TMEM lane and column offset (the stage adds a * acc_stride)
+    const uint32_t tmem_lane_base = tmem + ((uint32_t)(q * 32) << 16) + h * NT + jj * 32;
+    // chunk c of this thread's 32 samples sits c * Np uint4 after chunk 0
+    const size_t np4 = (size_t)Np;
     uint4* const dst0 = dst;
     size_t ring_base = 0, warp_ring_base = 0;   // ring word offsets without the slot term
     int rdelay = 0, warp_rdelay = 0;
@@ -523,15 +533,15 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       const int s0 = tile * NT, ns = min(NT, p.S - s0);
       const bool pf = load && k0 + 1 < nwork;
       const uint4* nsrc = dst + tile_stride;
-      const long long tw0 = p.dbg ? clock64() : 0;
+      const long long tw0 = dbg_on ? clock64() : 0;
       // one warp per lane quarter polls the accumulator barrier; the other
       // three wait on the quarter's named barrier (no issue slots spent)
       // back-off polling (measured best against the suspend-hint wait, a plain
       // spin and a per-quarter named barrier)
       if (kMulti) ptx::mbar_wait(&bars[ACCFULL0 + a], ua & 1);
       else ptx::mbar_wait_backoff(&bars[ACCFULL0 + a], ua & 1, 128);
-      if (p.dbg && blockIdx.x == 0) dbg_wait += clock64() - tw0;
-      if (lane == 0 && ew == 0) stamp(p, k, 8);
+      if (dbg_on && blockIdx.x == 0) dbg_wait += clock64() - tw0;
+      if (lane == 0 && ew == 0) stamp_k(k, 8);
       tc::fence_after();
       if (active) {
         if (c != prev_core) {
@@ -575,38 +585,37 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
           out_peers = __match_any_sync(0xFFFFFFFFu, kind == RK_OUTPUT ? cls : 0xFFFFFFFFu);
           prev_core = c;
         }
+        if (first && !load) {   // first tick after a reset: initial potentials
+#pragma unroll
+          for (int i = 0; i < kPass * kCh; ++i) pbuf[i * PB] = initv;
+        }
         if (kMulti) {   // ring slot of tick t + delay
           ring_off = ring_base + (size_t)((t + rdelay) & p.rp_mask) * slot_stride;
           warp_ring_off = warp_ring_base + (size_t)((t + warp_rdelay) & p.rp_mask) * slot_stride;
         }
-        const uint32_t acc_addr = tmem + a * acc_stride + ((uint32_t)(q * 32) << 16) + h * NT + jj * 32;
+        const uint32_t acc_addr = tmem_lane_base + a * acc_stride;
         uint32_t fired = 0u;
 #pragma unroll
         for (int sb = 0; sb < kPass; ++sb) {
           uint32_t acc[kSub];
           tc::ld16(acc_addr + sb * kSub, acc);
+          // this pass's potentials are in pbuf: prefetched a tile ago
+          // (cp.async), kept from the previous tick (multi-tick launch), or
+          // the initial potentials (first tick after a reset, filled below)
+          if (first && load) ptx::cp_async_wait<1>();   // this pass's group has landed
           uint4 cur[kCh];
-          if (!first) {
-            // multi-tick launch: this tile's potentials of the previous tick
 #pragma unroll
-            for (int i = 0; i < kCh; ++i) cur[i] = pbuf[(kCh * sb + i) * PB];
-          } else if (load) {
-            ptx::cp_async_wait<1>();   // this pass's group (issued a tile ago) has landed
-#pragma unroll
-            for (int i = 0; i < kCh; ++i) cur[i] = pbuf[(kCh * sb + i) * PB];
+          for (int i = 0; i < kCh; ++i) cur[i] = pbuf[(kCh * sb + i) * PB];
+          if (first && load) {
             // request the same chunks of the next tile into the slots just read
             if (pf) {
 #pragma unroll
-              for (int i = 0; i < kCh; ++i)
-                ptx::cp_async16(pbuf + (kCh * sb + i) * PB, nsrc + (size_t)(kCh * sb + i) * Np);
+              for (int i = 0; i < kCh; ++i) ptx::cp_async16(pbuf + (kCh * sb + i) * PB, nsrc + (kCh * sb + i) * np4);
             }
             ptx::cp_async_commit();   // (possibly empty) group: keeps the wait_group 1 accounting
-          } else {
-#pragma unroll
-            for (int i = 0; i < kCh; ++i) cur[i] = initv;
           }
           tc::wait_ld();
-          if (lane == 0 && ew == 0) stamp(p, k, 9 + sb);
+          if (lane == 0 && ew == 0) stamp_k(k, 9 + sb);
           // a4: leak / thresholds / reset per sample
           uint32_t outw[kSub / 2];
           const uint32_t fb = sat16 ? lif<true, kSub>(cur, acc, leak, pth, nth, linmul, bf, bn, 0, 0, one, outw)
@@ -617,7 +626,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
           for (int cc = 0; cc < kCh; ++cc) {
             const uint4 o = make_uint4(outw[4 * cc + 0], outw[4 * cc + 1], outw[4 * cc + 2], outw[4 * cc + 3]);
             if (!last) pbuf[(kCh * sb + cc) * PB] = o;   // kept on chip for the next tick
-            else dst[(size_t)(kCh * sb + cc) * Np] = o;
+            else dst[(kCh * sb + cc) * np4] = o;
           }
         }
         // a5 / a6: route or count the spikes of real samples
@@ -675,7 +684,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       }
       tc::fence_before();
       __syncwarp();
-      if (lane == 0 && ew == 0) stamp(p, k, 11);
+      if (lane == 0 && ew == 0) stamp_k(k, 11);
       if (lane == 0) ptx::mbar_arrive(&bars[ACCEMPTY0 + a]);
       if (++tile == nT) {
         tile = 0;
@@ -684,7 +693,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
     }
     tick_barrier();
     }
-    if (p.dbg && blockIdx.x == 0 && lane == 0) {
+    if (dbg_on && blockIdx.x == 0 && lane == 0) {
       p.dbg[64 * 16 + 2 * ew] = (unsigned long long)dbg_wait;
       p.dbg[64 * 16 + 2 * ew + 1] = (unsigned long long)(clock64() - dbg_t0);
     }
@@ -692,7 +701,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
   tc::fence_before();
   __syncthreads();
   if (warp == mma_warp) tc::dealloc(tmem, tcols < 32 ? 32 : tcols);
-  if (p.dbg && threadIdx.x == 0 && blockIdx.x < 256) {
+  if (dbg_on && threadIdx.x == 0 && blockIdx.x < 256) {
     unsigned long long gt_end;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt_end));
     p.dbg[64 * 16 + 64 + 2 * blockIdx.x] = gt_start;
@@ -796,11 +805,11 @@ cudaError_t launch_tc_multi(ranc_ctx* ctx, TickParams p, int64_t num_ticks) {
   tc_fill_params(ctx, p);
   const int grid = (int)((int64_t)ctx->G_loc * ((ctx->S + NT - 1) / NT));
   const size_t smem = tc_layout(n.Npad, n.Kp, n.W, n.WIp, n.rmax).total;
-  cudaFuncSetAttribute(tick_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  cudaFuncSetAttribute(tick_tc_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   int nt = (int)std::min<int64_t>(num_ticks, 1 << 30);
   void* args[] = {&p, &nt};
-  return cudaLaunchCooperativeKernel((const void*)tick_tc_kernel<true>, dim3(grid), dim3(kThreadsTC), args, smem,
-                                     ctx->stream);
+  return cudaLaunchCooperativeKernel((const void*)tick_tc_kernel<true, false>, dim3(grid), dim3(kThreadsTC), args,
+                                     smem, ctx->stream);
 }
 
 cudaError_t launch_tick_tc(ranc_ctx* ctx, TickParams p) {
@@ -811,7 +820,8 @@ cudaError_t launch_tick_tc(ranc_ctx* ctx, TickParams p) {
   const size_t smem = tc_layout(n.Npad, n.Kp, n.W, n.WIp, n.rmax).total;
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(tick_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(tick_tc_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(tick_tc_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     configured = true;
   }
   static const bool dbg = getenv("RANC_DEBUG_TIMELINE") != nullptr;
@@ -819,7 +829,10 @@ cudaError_t launch_tick_tc(ranc_ctx* ctx, TickParams p) {
   if (dbg && !ctx->d_dbg.p) dev_alloc(ctx, &ctx->d_dbg, kDbg * 8);
   p.dbg = dbg ? (unsigned long long*)ctx->d_dbg.p : nullptr;
   if (dbg) cudaMemsetAsync(ctx->d_dbg.p, 0, kDbg * 8, ctx->stream);
-  tick_tc_kernel<false><<<grid, kThreadsTC, smem, ctx->stream>>>(p, 1);
+  if (dbg)
+    tick_tc_kernel<false, true><<<grid, kThreadsTC, smem, ctx->stream>>>(p, 1);
+  else
+    tick_tc_kernel<false, false><<<grid, kThreadsTC, smem, ctx->stream>>>(p, 1);
   if (dbg) {
     static unsigned long long h[kDbg];
     cudaMemcpyAsync(h, ctx->d_dbg.p, sizeof h, cudaMemcpyDeviceToHost, ctx->stream);
