@@ -514,8 +514,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
     const int cl0 = cl, tile0 = tile;
     // this thread's TMEM lane and column offset (the stage adds a * acc_stride)
     const uint32_t tmem_lane_base = tmem + ((uint32_t)(q * 32) << 16) + h * NT + jj * 32;
-    // chunk c of this thread's 32 samples sits c * Np uint4 after chunk 0
-    const size_t np4 = (size_t)Np;
+    // chunk c of this thread's 32 samples sits c * Np * 16 bytes after chunk 0
+    const uint32_t chunk_bytes = (uint32_t)Np * 16u;
     uint4* const dst0 = dst;
     size_t ring_base = 0, warp_ring_base = 0;   // ring word offsets without the slot term
     int rdelay = 0, warp_rdelay = 0;
@@ -549,9 +549,15 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
           const uint2 rt = p.route[(size_t)c * Np + n];
           leak = prm.x; pth = prm.y; nth = prm.z; rst = prm.w;
           init = p.init[(size_t)c * Np + n];
-          if (p.fresh) {
+          if (p.fresh && first) {
+            // first tick after a reset: the pass inputs are the initial
+            // potentials; pbuf is not refilled while this core's tiles run
+            // (the new potentials go to HBM, or to pbuf only after the
+            // single tile of a multi-tick launch has read it)
             const uint32_t ii = ((uint32_t)init & 0xFFFFu) * 0x10001u;
             initv = make_uint4(ii, ii, ii, ii);
+#pragma unroll
+            for (int i = 0; i < kPass * kCh; ++i) pbuf[i * PB] = initv;
           }
           kind = valid ? route_kind(rt.x) : RK_NONE;
           const bool lin = route_lin(rt.x);
@@ -585,10 +591,6 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
           out_peers = __match_any_sync(0xFFFFFFFFu, kind == RK_OUTPUT ? cls : 0xFFFFFFFFu);
           prev_core = c;
         }
-        if (first && !load) {   // first tick after a reset: initial potentials
-#pragma unroll
-          for (int i = 0; i < kPass * kCh; ++i) pbuf[i * PB] = initv;
-        }
         if (kMulti) {   // ring slot of tick t + delay
           ring_off = ring_base + (size_t)((t + rdelay) & p.rp_mask) * slot_stride;
           warp_ring_off = warp_ring_base + (size_t)((t + warp_rdelay) & p.rp_mask) * slot_stride;
@@ -609,8 +611,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
           if (first && load) {
             // request the same chunks of the next tile into the slots just read
             if (pf) {
+              const char* nb = reinterpret_cast<const char*>(nsrc);
 #pragma unroll
-              for (int i = 0; i < kCh; ++i) ptx::cp_async16(pbuf + (kCh * sb + i) * PB, nsrc + (kCh * sb + i) * np4);
+              for (int i = 0; i < kCh; ++i)
+                ptx::cp_async16(pbuf + (kCh * sb + i) * PB, nb + (uint32_t)((kCh * sb + i) * chunk_bytes));
             }
             ptx::cp_async_commit();   // (possibly empty) group: keeps the wait_group 1 accounting
           }
@@ -626,7 +630,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
           for (int cc = 0; cc < kCh; ++cc) {
             const uint4 o = make_uint4(outw[4 * cc + 0], outw[4 * cc + 1], outw[4 * cc + 2], outw[4 * cc + 3]);
             if (!last) pbuf[(kCh * sb + cc) * PB] = o;   // kept on chip for the next tick
-            else dst[(kCh * sb + cc) * np4] = o;
+            else *reinterpret_cast<uint4*>(reinterpret_cast<char*>(dst) + (uint32_t)((kCh * sb + cc) * chunk_bytes)) = o;
           }
         }
         // a5 / a6: route or count the spikes of real samples
