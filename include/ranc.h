@@ -196,6 +196,15 @@ ranc_status ranc_set_allocator(ranc_ctx* ctx, void* (*alloc)(size_t, void*),
  * Results are identical either way. */
 #define RANC_OPT_STREAM 4
 #define RANC_OPT_KERNEL 3
+/* RANC_OPT_RING_LAYOUT (tensor-core kernel only; device memory layout of the
+ * scheduler rings, Alg. 1 l.3-5 and l.15-20, P:79-82 / P:102-110): 0 (default)
+ * automatic -- word-major when most routing neurons of the network have their
+ * own destination word (e.g. the random mesh of config 5), sample-major when
+ * they deposit whole words together (layered MNIST nets); 1 sample-major
+ * [Rp][G][S][W]; 2 word-major [Rp][G][W][S] (a warp's deposits for 32 samples
+ * of one route hit one 128-byte line).  Takes effect at the next
+ * ranc_load_inputs / ranc_reset_state.  Results are identical either way. */
+#define RANC_OPT_RING_LAYOUT 5
 ranc_status ranc_set_option(ranc_ctx* ctx, int option, int64_t value);
 
 /* Introspection of the compiled network and of the last run. */
@@ -213,7 +222,8 @@ typedef struct {
   int32_t cores_local;        /* number of cores simulated by this context              */
   int32_t shard_mode;         /* RANC_SHARD_* (0 without a communicator)                */
   int64_t exchange_bytes;     /* core-sharded: bytes sent per tick                      */
-  int32_t reserved[2];
+  int32_t ring_layout;        /* scheduler ring layout in use: 1 sample-major, 2 word-major (RANC_OPT_RING_LAYOUT) */
+  int32_t reserved;
 } ranc_info;
 ranc_status ranc_get_info(const ranc_ctx* ctx, ranc_info* info);
 

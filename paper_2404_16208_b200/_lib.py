@@ -8,7 +8,7 @@ import ctypes as C
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libranc.so")
+LIB_PATH = os.environ.get("RANC_LIB") or os.path.join(PKG, "libranc.so")   # RANC_LIB: A/B builds
 
 RANC_ABI_VERSION = 1
 STATUS = {0: "RANC_OK", 1: "RANC_E_ARG", 2: "RANC_E_CONFIG", 3: "RANC_E_BITWIDTH", 4: "RANC_E_RANGE",
@@ -21,6 +21,7 @@ OPT_SAMPLE_TILE = 1
 OPT_INPUT_DECODE = 2
 OPT_KERNEL = 3
 OPT_STREAM = 4
+OPT_RING_LAYOUT = 5
 SHARD_SAMPLES = 0
 SHARD_CORES = 1
 
@@ -53,7 +54,7 @@ class Info(C.Structure):
         "ring_rows", "ring_words", "pieces", "sample_tile")] + [
         ("num_samples", C.c_int64), ("device_bytes", C.c_int64), ("kernel_launches", C.c_int64),
         ("kernel", C.c_int32), ("core_lo", C.c_int32), ("cores_local", C.c_int32), ("shard_mode", C.c_int32),
-        ("exchange_bytes", C.c_int64), ("reserved", C.c_int32 * 2)]
+        ("exchange_bytes", C.c_int64), ("ring_layout", C.c_int32), ("reserved", C.c_int32)]
 
 
 ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p)

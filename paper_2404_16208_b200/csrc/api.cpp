@@ -294,6 +294,10 @@ ranc_status ranc_reset_state(ranc_ctx* ctx) {
                         tc_smem_bytes(ctx->net) > 227 * 1024)
                            ? RANC_KERNEL_POPC
                            : RANC_KERNEL_TC;
+  const bool wmajor = ctx->kernel_active == RANC_KERNEL_TC &&
+                      (ctx->ring_layout == 2 || (ctx->ring_layout == 0 && ctx->net.tc_wmajor));
+  if (wmajor != ctx->ring_wmajor) ctx->inw_valid = false;   // decoded inputs follow the ring layout
+  ctx->ring_wmajor = wmajor;
   TRY(prepare_inputs_tc(ctx));
   ctx->now = 0;
   ctx->raster_ticks = 0;
@@ -502,13 +506,17 @@ ranc_status ranc_read_pending(ranc_ctx* ctx, uint32_t* bits, size_t n) {
     const int slot = (int)((ctx->now + j) & (c.Rp - 1));
     for (int64_t s = 0; s < ctx->S; ++s)
       for (int g = 0; g < GL; ++g) {
-        const uint32_t* src = &h[(((size_t)slot * GL + g) * ctx->Sr + s) * c.W];
+        // ring [Rp][G][Sr][W], or word-major [Rp][G][W][Sr]
+        const bool wmajor = ctx->ring_wmajor;
+        const size_t base = wmajor ? ((size_t)slot * GL + g) * c.W * ctx->Sr + s
+                                   : (((size_t)slot * GL + g) * ctx->Sr + s) * c.W;
+        const size_t wst = wmajor ? (size_t)ctx->Sr : 1;
         uint32_t* dst = bits + (((size_t)s * GL + g) * c.D + j) * c.W;
         const int gg = ctx->c_lo + g;
         const int32_t* perm = ctx->kernel_active == RANC_KERNEL_TC ? &c.perm_tc[(size_t)gg * c.A]
                                                                    : &c.perm[(size_t)gg * c.A];
         for (int ap = 0; ap < c.A; ++ap)
-          if ((src[ap >> 5] >> (ap & 31)) & 1u) {
+          if ((h[base + (ap >> 5) * wst] >> (ap & 31)) & 1u) {
             const int a = perm[ap];
             dst[a >> 5] |= 1u << (a & 31);
           }
@@ -643,6 +651,13 @@ ranc_status ranc_set_option(ranc_ctx* ctx, int option, int64_t value) {
       }
       ctx->kernel = (int32_t)value;  // takes effect at the next ranc_load_inputs / ranc_reset_state
       return RANC_OK;
+    case RANC_OPT_RING_LAYOUT:
+      if (value < 0 || value > 2) {
+        ctx->err = "ring layout must be 0 (auto), 1 (sample-major) or 2 (word-major, tensor-core path)";
+        return RANC_E_ARG;
+      }
+      ctx->ring_layout = (int32_t)value;  // takes effect at the next ranc_load_inputs / ranc_reset_state
+      return RANC_OK;
     default:
       ctx->err = "unknown option";
       return RANC_E_ARG;
@@ -659,6 +674,7 @@ ranc_status ranc_get_info(const ranc_ctx* ctx, ranc_info* info) {
   info->sample_tile = ctx->sample_tile; info->num_samples = ctx->S;
   info->device_bytes = ctx->device_bytes; info->kernel_launches = ctx->launches;
   info->kernel = ctx->kernel_active;
+  info->ring_layout = ctx->ring_wmajor ? 2 : 1;
   info->core_lo = ctx->c_lo;
   info->cores_local = ctx->G_loc;
   info->shard_mode = (ctx->nccl_comm || ctx->group) ? ctx->shard_mode : 0;

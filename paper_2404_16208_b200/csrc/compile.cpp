@@ -362,6 +362,18 @@ ranc_status validate_and_compile(const ranc_network_desc* d, Compiled* out, std:
         // bit 0: block route; bit 1: lane l deposits bit l (bit transpose)
         if (any && same) o.wflags_tc[(size_t)c * (Np / 32) + w] = ident ? 3 : 1;
       }
+    // ring layout: per-neuron routes deposit one bit per (neuron, sample);
+    // word-major rows make a warp's 32 samples of one deposit one 128-byte
+    // line.  Block routes already deposit one whole word per sample and keep
+    // the sample-major rows (one bulk copy per tile).
+    {
+      int64_t scattered = 0, blocked = 0;
+      for (int c = 0; c < G; ++c)
+        for (int n = 0; n < N; ++n)
+          if (route_kind(o.route_tc[(size_t)c * Np + n].x) == RK_ROUTE)
+            ++(o.wflags_tc[(size_t)c * (Np / 32) + n / 32] ? blocked : scattered);
+      o.tc_wmajor = scattered > blocked;
+    }
     // folded weights in the canonical operand layout (tc.h)
     const size_t per = (size_t)o.Npad * o.Kp;
     o.wfold.assign((size_t)G * per, 0);

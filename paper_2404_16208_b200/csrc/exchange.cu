@@ -36,7 +36,7 @@ __global__ void pack_kernel(const uint32_t* __restrict__ fired, uint32_t* __rest
 
 __global__ void unpack_kernel(const uint32_t* __restrict__ recv, const int32_t* __restrict__ recv_list, int64_t rows,
                               int S, int Wn, const uint2* __restrict__ route, int Npad, int N, int c_lo, int G_loc,
-                              uint32_t* __restrict__ ring, int Sr, int W, int64_t t, int rp_mask) {
+                              uint32_t* __restrict__ ring, int Sr, int W, int64_t t, int rp_mask, int wmajor) {
   const int64_t total = rows * S * Wn;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     uint32_t word = recv[i];
@@ -56,7 +56,10 @@ __global__ void unpack_kernel(const uint32_t* __restrict__ recv, const int32_t* 
       if (dl >= (uint32_t)G_loc) continue;
       const uint32_t ax = route_axon(rt.x);
       const int slot = (int)((t + route_delay(rt.x)) & rp_mask);
-      atomicOr(ring + (((size_t)slot * G_loc + dl) * Sr + s) * W + (ax >> 5), 1u << (ax & 31));
+      // ring layout of the active kernel: [Rp][G][Sr][W] (popcount) or word-major [Rp][G][W][Sr] (tensor core)
+      const size_t row = (size_t)slot * G_loc + dl;
+      const size_t wi = wmajor ? (row * W + (ax >> 5)) * Sr + s : (row * Sr + s) * W + (ax >> 5);
+      atomicOr(ring + wi, 1u << (ax & 31));
     }
   }
 }
@@ -84,7 +87,8 @@ cudaError_t launch_unpack(ranc_ctx* ctx, int64_t t) {
   const uint2* route = (const uint2*)(ctx->kernel_active == RANC_KERNEL_TC ? ctx->d_route_tc.p : ctx->d_route.p);
   unpack_kernel<<<blocks_for(ctx->n_recv_words), 256, 0, ctx->stream>>>(
       (const uint32_t*)ctx->d_recv.p, (const int32_t*)ctx->d_recv_list.p, rows, (int)ctx->S, n.Wn, route, n.Npad, n.N,
-      ctx->c_lo, ctx->G_loc, (uint32_t*)ctx->d_ring.p, (int)ctx->Sr, n.W, t, n.Rp - 1);
+      ctx->c_lo, ctx->G_loc, (uint32_t*)ctx->d_ring.p, (int)ctx->Sr, n.W, t, n.Rp - 1,
+      ctx->ring_wmajor ? 1 : 0);
   ctx->launches++;
   return cudaGetLastError();
 }

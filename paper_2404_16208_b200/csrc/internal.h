@@ -14,7 +14,10 @@
 //   state (streamed every tick):
 //     pot   i16 [G][S][Npad]   membrane potentials (pb <= 16), popcount kernel;
 //           i16 [G][nT][NT/8][Npad][8] tile-blocked, tensor-core kernel (NT = 64)
-//     ring  u32 [Rp][G][Sr][W] scheduler rings, W = ceil(A/32) words per row,
+//     ring  u32 [Rp][G][Sr][W] scheduler rings, W = ceil(A/32) words per row;
+//           u32 [Rp][G][W][Sr] word-major (tensor-core kernel, networks with per-neuron
+//                              routes: the 32 sample words a warp deposits for one
+//                              route are one 128-byte line; RANC_OPT_RING_LAYOUT),
 //                              Sr = S rounded up to 64 (TMA-aligned tiles),
 //                              slot of tick t = t & (Rp-1), Rp = next_pow2(D+1)
 //     counts i32 [S][C]        output-bus class counts
@@ -47,13 +50,14 @@ struct TickParams {
   int32_t rp_mask;          // Rp - 1
   int32_t pot_lo, pot_hi;   // saturation range of pb bits
   int32_t fresh;            // first tick after a reset: potentials start at init
+  int32_t wmajor;           // tensor-core path: ring and decoded inputs word-major [..][W][Sr]
   int32_t Kp;               // tensor-core path: K bytes per operand row (= 32*W)
   int64_t t;                // tick being executed
   int64_t raster_t0;        // first tick of the raster buffer
   const uint8_t* wfold;     // tensor-core path: [G][Npad*Kp] canonical-layout int8
   const int2* runs;         // tensor-core path: input runs [G][rmax]
   const int32_t* word_runs; // [G][W]: runs overlapping ring word w: first | count << 16
-  const uint32_t* inw;      // decoded inputs [T_in][n_inslots][Sr][W] or nullptr
+  const uint32_t* inw;      // decoded inputs [T_in][n_inslots][Sr][W] or [..][W][Sr] (the ring's layout), or nullptr
   const int32_t* inslot;    // [G_loc] input slot of a local core (-1: no input lines)
   int32_t n_inslots;
   const int32_t* nruns;     // [G]
@@ -86,6 +90,8 @@ struct Compiled {
   int32_t Kp = 0;               // 32 * W
   int32_t WIp = 0;              // WI rounded up to 4
   bool tc_ok = false;           // eligible for the tcgen05 kind::i8 path
+  bool tc_wmajor = false;       // automatic ring layout: word-major when most routing neurons sit in
+                                // warps without a shared destination word (per-neuron routes)
   std::vector<int8_t> wfold;    // [G][Npad*Kp] canonical operand layout, tensor-core axon order
   std::vector<int32_t> perm_tc, inv_tc;   // tensor-core axon order (sorted by input line)
   std::vector<uint2> route_tc;  // route words with tensor-core destination axons
@@ -146,6 +152,8 @@ struct ranc_ctx {
   int32_t stream_opt = 0;        // RANC_OPT_STREAM: 0 auto, 1 off, 2 on
   int32_t kernel = 0;            // RANC_OPT_KERNEL request: 0 auto, 1 popcount, 2 tensor core
   int32_t kernel_active = 1;     // latched at every reset (the potential layout depends on it)
+  int32_t ring_layout = 0;       // RANC_OPT_RING_LAYOUT request: 0 auto, 1 sample-major, 2 word-major
+  bool ring_wmajor = false;      // latched at every reset: tensor-core ring word-major [Rp][G][W][Sr]
   int64_t launches = 0;
   int64_t device_bytes = 0;
   uint32_t trace_flags = 0;

@@ -41,6 +41,12 @@
 #include "ptx.h"
 #include "tc.h"
 
+#ifdef RANC_POT_STCS
+#define POT_STORE(ptr, v) ptx::st16_cs(ptr, v)
+#else
+#define POT_STORE(ptr, v) (*reinterpret_cast<uint4*>(ptr) = (v))
+#endif
+
 namespace ranc {
 
 namespace cg = cooperative_groups;
@@ -181,7 +187,9 @@ __device__ __forceinline__ uint32_t lif(const uint4 (&cur)[NE / 8], const uint32
 // of a ranc_run_ticks call in one launch; the grid barrier is the tick
 // barrier (a7) and each epilogue thread keeps its potentials in
 // registers between ticks (stored once, after the last tick).
-template <bool kMulti, bool kDebug>
+// kWm: word-major scheduler rings (compile-time, so each instantiation only
+// carries its own layout's code)
+template <bool kMulti, bool kDebug, bool kWm>
 __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams p, const int nticks_arg) {
   const int nticks = kMulti ? nticks_arg : 1;
   // kDebug: the RANC_DEBUG_TIMELINE instrumentation (a separate instantiation,
@@ -276,12 +284,22 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
         const uint32_t ring_bytes = p.incoming[c] ? (uint32_t)NT * W * 4 : 0u;
         const uint32_t line_bytes = !inject ? 0u : (p.inw ? (uint32_t)NT * W * 4 : (uint32_t)NT * WIp * 4);
         ptx::mbar_arrive_expect_tx(&bars[FULL0 + s], ring_bytes + line_bytes);
-        if (ring_bytes)
-          ptx::bulk_g2s(st + L.raw, p.ring + (((size_t)cur * p.G_loc + cl) * p.Sr + s0) * W, ring_bytes,
-                        &bars[FULL0 + s]);
-        if (inject && p.inw)
-          ptx::bulk_g2s(st + L.lines, p.inw + (((size_t)t * p.n_inslots + slot) * p.Sr + s0) * W, line_bytes,
-                        &bars[FULL0 + s]);
+        // ring rows and decoded inputs: sample-major [..][Sr][W] is one bulk
+        // copy per tile, staged [NT][W]; word-major [..][W][Sr] one copy of
+        // the tile's 64 samples per ring word, staged [W][NT]
+        const size_t rrow0 = (size_t)cur * p.G_loc + cl, irow0 = (size_t)t * p.n_inslots + slot;
+        if (ring_bytes) {
+          if (!kWm)
+            ptx::bulk_g2s(st + L.raw, p.ring + (rrow0 * p.Sr + s0) * W, ring_bytes, &bars[FULL0 + s]);
+          else
+            for (int w = 0; w < W; ++w)
+              ptx::bulk_g2s(st + L.raw + w * NT * 4, p.ring + (rrow0 * W + w) * p.Sr + s0, NT * 4, &bars[FULL0 + s]);
+        }
+        if (inject && p.inw && !kWm)
+          ptx::bulk_g2s(st + L.lines, p.inw + (irow0 * p.Sr + s0) * W, line_bytes, &bars[FULL0 + s]);
+        else if (inject && p.inw)
+          for (int w = 0; w < W; ++w)
+            ptx::bulk_g2s(st + L.lines + w * NT * 4, p.inw + (irow0 * W + w) * p.Sr + s0, NT * 4, &bars[FULL0 + s]);
         else if (inject)
           ptx::bulk_g2s(st + L.lines, p.lines + ((size_t)t * p.Sr + s0) * WIp, line_bytes, &bars[FULL0 + s]);
       }
@@ -357,11 +375,22 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       // clear them in global memory (free again for spikes due at t + Rp)
       wait(&bars[FULL0 + s], u & 1);
       if (et == 0) stamp_k(k, 2);
-      uint32_t* row = p.ring + (((size_t)cur * p.G_loc + cl) * p.Sr + s0) * W;
+      // staged rows: raw[sm * W + w] (sample-major) or raw[w * NT + sm]
+      // (word-major) = ring word w of sample s0 + sm
+      constexpr bool wm = kWm;
       if (p.incoming[c]) {
         // only the words that hold spikes need clearing
-        for (int i = et; i < ns * W; i += kExpThreads)
-          if (raw[i]) row[i] = 0u;
+        if (!wm) {
+          uint32_t* row = p.ring + (((size_t)cur * p.G_loc + cl) * p.Sr + s0) * W;
+          for (int i = et; i < ns * W; i += kExpThreads)
+            if (raw[i]) row[i] = 0u;
+        } else {
+          uint32_t* row = p.ring + ((size_t)cur * p.G_loc + cl) * W * p.Sr + s0;
+          for (int i = et; i < NT * W; i += kExpThreads) {
+            const int w = i / NT, sm = i % NT;
+            if (sm < ns && raw[i]) row[(size_t)w * p.Sr + sm] = 0u;
+          }
+        }
       } else {
         // no neuron routes here: the ring stays zero and was not loaded
         for (int i = et; i < NT * W; i += kExpThreads) raw[i] = 0u;
@@ -371,7 +400,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       // runs overlapping that word (no atomics: every word has one owner)
       if (t < p.T_in && p.nruns[c] > 0 && p.inw) {
         // decoded input words (input decode done once at load, Alg. 1 l.1)
-        for (int i = et; i < ns * W; i += kExpThreads) raw[i] |= lines[i];
+        // same layout as the staged ring rows; rows of samples >= ns are never read
+        for (int i = et; i < NT * W; i += kExpThreads) raw[i] |= lines[i];
       } else if (t < p.T_in && p.nruns[c] > 0) {
         // the core's input runs live in shared memory while its tiles are processed
         int2* runs = reinterpret_cast<int2*>(smem + L.runs);
@@ -384,14 +414,14 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
           runs_core = c;
         }
         constexpr int B = 2;   // independent items in flight per thread
-        for (int base = et; base < ns * W; base += B * kExpThreads) {
+        for (int base = et; base < NT * W; base += B * kExpThreads) {
           uint32_t accs[B];
 #pragma unroll
           for (int b = 0; b < B; ++b) {
             const int i = base + b * kExpThreads;
             accs[b] = 0u;
-            if (i >= ns * W) continue;
-            const int sm = i / W, w = i - sm * W;
+            const int w = wm ? i / NT : i % W, sm = wm ? i % NT : i / W;
+            if (i >= NT * W || sm >= ns) continue;
             const int32_t fr = wr[w];
             const int r0 = fr & 0xFFFF, nrw = fr >> 16;
             const uint32_t* lr = lines + sm * WIp;
@@ -409,13 +439,15 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
 #pragma unroll
           for (int b = 0; b < B; ++b) {
             const int i = base + b * kExpThreads;
-            if (i < ns * W && accs[b]) raw[i] |= accs[b];
+            if (i < NT * W && accs[b]) raw[i] |= accs[b];
           }
         }
       }
       if (p.spkin)   // RANC_TRACE_STATE_DIGEST: the axon spikes integrated this tick
-        for (int i = et; i < ns * W; i += kExpThreads)
-          p.spkin[((size_t)(s0 + i / W) * p.G_loc + cl) * W + i % W] = raw[i];
+        for (int i = et; i < NT * W; i += kExpThreads) {
+          const int w = wm ? i / NT : i % W, sm = wm ? i % NT : i / W;
+          if (sm < ns) p.spkin[((size_t)(s0 + sm) * p.G_loc + cl) * W + w] = raw[i];
+        }
       if (et == 0) stamp_k(k, 13);
       named_sync(2, kExpThreads);
       if (et == 0) stamp_k(k, 14);
@@ -432,26 +464,38 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
         // samples so every 8-lane phase of the 16-byte stores fills one core
         // matrix (bank-conflict free); bytes via the nibble table
         const int sm = et % NT, hf = et / NT;   // kExpThreads == 2 * NT
-        const uint32_t* rrow = raw + sm * W;
-        const bool real = sm < ns;
+        // word-major staging: lanes read consecutive words (conflict free);
+        // K chunk 2w+hf of sample sm sits w * 2*NT*16 bytes after chunk hf
+        const uint32_t* rcol = raw + sm;
+        uint8_t* bdst = b_s + tc::operand_offset(sm, hf * 16, NT);
+        const uint32_t sh = hf * 16;
         auto emit = [&](int w, uint32_t wv) {
-          const uint32_t bits = hf ? (wv >> 16) : (wv & 0xFFFFu);
-          *reinterpret_cast<uint4*>(b_s + tc::operand_offset(sm, (2 * w + hf) * 16, NT)) =
+          const uint32_t bits = (wv >> sh) & 0xFFFFu;
+          *reinterpret_cast<uint4*>(bdst + w * (2 * NT * 16)) =
               make_uint4(lut[bits & 15u], lut[(bits >> 4) & 15u], lut[(bits >> 8) & 15u], lut[bits >> 12]);
         };
-        if ((W & 3) == 0) {
-          // 16-byte row loads: lanes 32 B apart -> at most 2-way bank conflicts
+        if (sm >= ns) {   // tail samples of a ragged tile get no spikes
+          for (int w = 0; w < W; ++w) *reinterpret_cast<uint4*>(bdst + w * (2 * NT * 16)) = make_uint4(0u, 0u, 0u, 0u);
+        } else if (!wm && (W & 3) == 0) {
+          // sample-major: 16-byte row loads, lanes 32 B apart (<= 2-way conflicts)
+          const uint32_t* rrow = raw + sm * W;
 #pragma unroll 1
           for (int w4 = 0; w4 < W; w4 += 4) {
-            const uint4 v = real ? *reinterpret_cast<const uint4*>(rrow + w4) : make_uint4(0u, 0u, 0u, 0u);
+            const uint4 v = *reinterpret_cast<const uint4*>(rrow + w4);
             emit(w4 + 0, v.x);
             emit(w4 + 1, v.y);
             emit(w4 + 2, v.z);
             emit(w4 + 3, v.w);
           }
-        } else {
+        } else if (!wm) {
 #pragma unroll 1
-          for (int w = 0; w < W; ++w) emit(w, real ? rrow[w] : 0u);
+          for (int w = 0; w < W; ++w) emit(w, raw[sm * W + w]);
+        } else if (W == 8) {   // A = 256 (the paper's core): fully unrolled
+#pragma unroll
+          for (int w = 0; w < 8; ++w) emit(w, rcol[w * NT]);
+        } else {
+#pragma unroll 4
+          for (int w = 0; w < W; ++w) emit(w, rcol[w * NT]);
         }
       }
       if (et == 0) stamp_k(k, 15);
@@ -519,7 +563,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
     uint4* const dst0 = dst;
     size_t ring_base = 0, warp_ring_base = 0;   // ring word offsets without the slot term
     int rdelay = 0, warp_rdelay = 0;
+    // ring [Rp][G_loc][Sr][W] (sample stride W) or word-major [Rp][G_loc][W][Sr]
+    // (sample stride 1: a ring word's samples are contiguous)
     const size_t slot_stride = (size_t)p.G_loc * p.Sr * W;
+    constexpr bool wm = kWm;
+    const uint32_t ss = wm ? 1u : (uint32_t)W;
     for (int it = 0; it < nticks; ++it) {
     const int64_t t = p.t + it;
     const bool first = it == 0, last = it + 1 == nticks;
@@ -572,7 +620,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
           // a route to a core of another rank is delivered by the exchange step
           const uint32_t dloc = rt.y - (uint32_t)p.c_lo;
           route_here = kind == RK_ROUTE && dloc < (uint32_t)p.G_loc;
-          ring_base = ((size_t)dloc * p.Sr) * W + (ax >> 5);
+          ring_base = wm ? ((size_t)dloc * W + (ax >> 5)) * p.Sr : (size_t)dloc * p.Sr * W + (ax >> 5);
           exporting = p.fired && p.exports[c];
           const uint32_t wf = p.wflags ? p.wflags[(size_t)c * (Np >> 5) + (n >> 5)] : 0u;
           block_route = wf & 1u;
@@ -630,7 +678,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
           for (int cc = 0; cc < kCh; ++cc) {
             const uint4 o = make_uint4(outw[4 * cc + 0], outw[4 * cc + 1], outw[4 * cc + 2], outw[4 * cc + 3]);
             if (!last) pbuf[(kCh * sb + cc) * PB] = o;   // kept on chip for the next tick
-            else *reinterpret_cast<uint4*>(reinterpret_cast<char*>(dst) + (uint32_t)((kCh * sb + cc) * chunk_bytes)) = o;
+            else POT_STORE(reinterpret_cast<char*>(dst) + (uint32_t)((kCh * sb + cc) * chunk_bytes), o);
           }
         }
         // a5 / a6: route or count the spikes of real samples
@@ -643,23 +691,40 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
           // per-sample deposit words, one RED per (sample, word) issued by
           // the lane of that sample (idempotent OR, G11)
           const uint32_t m = transpose32(route_here ? f : 0u, lane);
-          if (m) atomicOr(p.ring + warp_ring_off + (size_t)(sj + lane) * W, m);
+          if (m) atomicOr(p.ring + warp_ring_off + (sj + lane) * ss, m);
         } else if (block_route) {
-          // every routing lane targets the same ring word: one OR-reduced
-          // deposit per sample
+          // every routing lane targets the same ring word: the OR-reduced
+          // deposit of sample i is kept by lane i, then one coalesced RED
           uint32_t any = __reduce_or_sync(0xFFFFFFFFu, route_here ? f : 0u);
+          uint32_t mine = 0u;
           while (any) {
             const int i = __ffs(any) - 1;
             any &= any - 1;
             const uint32_t m = __reduce_or_sync(0xFFFFFFFFu, (route_here && ((f >> i) & 1u)) ? axbit : 0u);
-            if (lane == 0) atomicOr(p.ring + warp_ring_off + (size_t)(sj + i) * W, m);
+            if (lane == i) mine = m;
           }
-        } else if (route_here) {
-          uint32_t g = f;
-          while (g) {
-            const int i = __ffs(g) - 1;
-            g &= g - 1;
-            atomicOr(p.ring + ring_off + (size_t)(sj + i) * W, axbit);
+          if (mine) atomicOr(p.ring + warp_ring_off + (sj + lane) * ss, mine);
+        } else if (!wm) {
+          if (route_here) {
+            uint32_t g = f;
+            while (g) {
+              const int i = __ffs(g) - 1;
+              g &= g - 1;
+              atomicOr(p.ring + ring_off + (size_t)(sj + i) * W, axbit);
+            }
+          }
+        } else {
+          // per-neuron destinations: lane i receives the routing neurons
+          // (lanes) fired in sample i; for each such neuron the warp issues
+          // one RED over its 32 contiguous sample words (one 128-byte line)
+          uint32_t src = __ballot_sync(0xFFFFFFFFu, route_here && f != 0u);
+          const uint32_t m = src ? transpose32(route_here ? f : 0u, lane) : 0u;
+          while (src) {
+            const int l = __ffs(src) - 1;
+            src &= src - 1;
+            const size_t off = __shfl_sync(0xFFFFFFFFu, ring_off, l);
+            const uint32_t bit = __shfl_sync(0xFFFFFFFFu, axbit, l);
+            if ((m >> l) & 1u) atomicOr(p.ring + off + sj + lane, bit);
           }
         }
         if (has_output) {
@@ -721,7 +786,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
 __global__ void decode_inputs_kernel(const uint32_t* __restrict__ lines, uint32_t* __restrict__ inw,
                                      const int32_t* __restrict__ slot_core, const int2* __restrict__ runs,
                                      const int32_t* __restrict__ word_runs, int S, int Sr, int W, int WIp,
-                                     int rmax) {
+                                     int rmax, int wmajor) {
   extern __shared__ int2 dec_sm[];
   const int slot = blockIdx.y, t = blockIdx.z, n_slots = gridDim.y;
   const int c = slot_core[slot];
@@ -734,7 +799,8 @@ __global__ void decode_inputs_kernel(const uint32_t* __restrict__ lines, uint32_
   const int total = S * W;
   for (int i = blockIdx.x * per_block + threadIdx.x; i < min(total, (blockIdx.x + 1) * per_block);
        i += blockDim.x) {
-    const int s = i / W, w = i - s * W;
+    // word-major: consecutive threads take consecutive samples of one word
+    const int w = wmajor ? i / S : i % W, s = wmajor ? i - w * S : i / W;
     const int32_t fr = wr[w];
     const int r0 = fr & 0xFFFF, nrw = fr >> 16;
     const uint32_t* lr = lines + ((size_t)t * Sr + s) * WIp;
@@ -749,7 +815,8 @@ __global__ void decode_inputs_kernel(const uint32_t* __restrict__ lines, uint32_
       const int off = ap - 32 * w;
       acc |= off >= 0 ? (x << off) : (x >> (-off));
     }
-    inw[(((size_t)t * n_slots + slot) * Sr + s) * W + w] = acc;
+    const size_t row = (size_t)t * n_slots + slot;   // same layout as the ring
+    inw[wmajor ? (row * W + w) * Sr + s : (row * Sr + s) * W + w] = acc;
   }
 }
 
@@ -767,7 +834,7 @@ cudaError_t decode_inputs_tc(ranc_ctx* ctx) {
   decode_inputs_kernel<<<grid, threads, smem, ctx->stream>>>(
       (const uint32_t*)ctx->d_lines.p, (uint32_t*)ctx->d_inw.p, (const int32_t*)ctx->d_slot_core.p,
       (const int2*)ctx->d_runs.p, (const int32_t*)ctx->d_word_runs.p, (int)ctx->S, (int)ctx->Sr, n.W, n.WIp,
-      n.rmax);
+      n.rmax, ctx->ring_wmajor ? 1 : 0);
   ctx->launches++;
   return cudaGetLastError();
 }
@@ -791,6 +858,7 @@ void tc_fill_params(ranc_ctx* ctx, TickParams& p) {
   p.n_inslots = ctx->n_inslots;
   p.nruns = (const int32_t*)ctx->d_nruns.p;
   p.rmax = n.rmax;
+  p.wmajor = ctx->ring_wmajor ? 1 : 0;
 }
 
 }  // namespace
@@ -809,10 +877,11 @@ cudaError_t launch_tc_multi(ranc_ctx* ctx, TickParams p, int64_t num_ticks) {
   tc_fill_params(ctx, p);
   const int grid = (int)((int64_t)ctx->G_loc * ((ctx->S + NT - 1) / NT));
   const size_t smem = tc_layout(n.Npad, n.Kp, n.W, n.WIp, n.rmax).total;
-  cudaFuncSetAttribute(tick_tc_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  const void* fn = p.wmajor ? (const void*)tick_tc_kernel<true, false, true> : (const void*)tick_tc_kernel<true, false, false>;
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   int nt = (int)std::min<int64_t>(num_ticks, 1 << 30);
   void* args[] = {&p, &nt};
-  return cudaLaunchCooperativeKernel((const void*)tick_tc_kernel<true, false>, dim3(grid), dim3(kThreadsTC), args,
+  return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kThreadsTC), args,
                                      smem, ctx->stream);
 }
 
@@ -824,8 +893,10 @@ cudaError_t launch_tick_tc(ranc_ctx* ctx, TickParams p) {
   const size_t smem = tc_layout(n.Npad, n.Kp, n.W, n.WIp, n.rmax).total;
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(tick_tc_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaFuncSetAttribute(tick_tc_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(tick_tc_kernel<false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(tick_tc_kernel<false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(tick_tc_kernel<false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(tick_tc_kernel<false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     configured = true;
   }
   static const bool dbg = getenv("RANC_DEBUG_TIMELINE") != nullptr;
@@ -833,10 +904,14 @@ cudaError_t launch_tick_tc(ranc_ctx* ctx, TickParams p) {
   if (dbg && !ctx->d_dbg.p) dev_alloc(ctx, &ctx->d_dbg, kDbg * 8);
   p.dbg = dbg ? (unsigned long long*)ctx->d_dbg.p : nullptr;
   if (dbg) cudaMemsetAsync(ctx->d_dbg.p, 0, kDbg * 8, ctx->stream);
-  if (dbg)
-    tick_tc_kernel<false, true><<<grid, kThreadsTC, smem, ctx->stream>>>(p, 1);
+  if (dbg && p.wmajor)
+    tick_tc_kernel<false, true, true><<<grid, kThreadsTC, smem, ctx->stream>>>(p, 1);
+  else if (dbg)
+    tick_tc_kernel<false, true, false><<<grid, kThreadsTC, smem, ctx->stream>>>(p, 1);
+  else if (p.wmajor)
+    tick_tc_kernel<false, false, true><<<grid, kThreadsTC, smem, ctx->stream>>>(p, 1);
   else
-    tick_tc_kernel<false, false><<<grid, kThreadsTC, smem, ctx->stream>>>(p, 1);
+    tick_tc_kernel<false, false, false><<<grid, kThreadsTC, smem, ctx->stream>>>(p, 1);
   if (dbg) {
     static unsigned long long h[kDbg];
     cudaMemcpyAsync(h, ctx->d_dbg.p, sizeof h, cudaMemcpyDeviceToHost, ctx->stream);

@@ -18,17 +18,21 @@ def ranc():
     return m
 
 
-# "tc_gather": tensor-core kernel with the per-tick input-run gather instead
-# of the load-time input decode (RANC_OPT_INPUT_DECODE = 0)
-KERNELS = {"popc": 1, "tc": 2, "tc_gather": 2}
+# "tc": tensor-core kernel, sample-major scheduler rings; "tc_wm": word-major
+# rings (RANC_OPT_RING_LAYOUT = 2); "tc_gather": word-major rings and the
+# per-tick input-run gather instead of the load-time input decode
+# (RANC_OPT_INPUT_DECODE = 0)
+KERNELS = {"popc": 1, "tc": 2, "tc_wm": 2, "tc_gather": 2}
+RING = {"tc": 1, "tc_wm": 2, "tc_gather": 2}
 
 
 def make_sim(ranc, net, kernel, **kw):
     sim = ranc.Simulator(net, **kw)
-    if kernel in ("tc", "tc_gather"):
+    if kernel in RING:
         try:
             sim.set_option(ranc.OPT_KERNEL, KERNELS[kernel])
             sim.set_option(ranc.OPT_INPUT_DECODE, 0 if kernel == "tc_gather" else 1)
+            sim.set_option(ranc.OPT_RING_LAYOUT, RING[kernel])
         except ranc.RancError as e:
             sim.close()
             assert e.code == "RANC_E_CONFIG"
@@ -38,7 +42,7 @@ def make_sim(ranc, net, kernel, **kw):
     return sim
 
 
-@pytest.fixture(params=["popc", "tc", "tc_gather"])
+@pytest.fixture(params=["popc", "tc", "tc_wm", "tc_gather"])
 def kernel(request):
     return request.param
 
@@ -51,6 +55,8 @@ def per_tick(ranc, oracle_mod, net, inp, T, tile=None, kernel=None):
     sim.load_inputs(inp)
     if kernel:
         assert sim.info()["kernel"] == KERNELS[kernel]
+    if kernel in RING:
+        assert sim.info()["ring_layout"] == RING[kernel]
     o = oracle_mod.Oracle(net, inp)
     for t in range(T):
         sim.run(1)
@@ -225,6 +231,38 @@ def test_kernel_switch_at_reset(ranc, oracle_mod):
             assert np.array_equal(a, b)
     o = oracle_mod.Oracle(net, inp).run(9)
     assert np.array_equal(res[0][0], o.potentials())
+    sim.close()
+
+
+def test_ring_layout_switch_at_reset(ranc, oracle_mod):
+    """The ring layout is latched at reset (decoded inputs follow it); every
+    layout gives the oracle's results, and the automatic choice is sample-major
+    for the block-routed MNIST net and word-major for the random mesh."""
+    net, inp = config2(S=70)
+    sim = ranc.Simulator(net)
+    sim.set_option(ranc.OPT_KERNEL, 2)
+    o = oracle_mod.Oracle(net, inp).run(9)
+    for lay, want in ((0, 1), (2, 2), (1, 1), (2, 2)):
+        sim.set_option(ranc.OPT_RING_LAYOUT, lay)
+        sim.load_inputs(inp).run(4)
+        assert sim.info()["ring_layout"] == want
+        sim.run(5)
+        assert np.array_equal(sim.potentials(), o.potentials())
+        assert np.array_equal(sim.outputs(), o.counts())
+        assert np.array_equal(sim.pending(), o.pending())
+    sim.close()
+    with pytest.raises(ranc.RancError) as ei:
+        s2 = ranc.Simulator(net)
+        try:
+            s2.set_option(ranc.OPT_RING_LAYOUT, 3)
+        finally:
+            s2.close()
+    assert ei.value.code == "RANC_E_ARG"
+    net5, inp5 = config5(S=64, T=4, grid=8)
+    sim = ranc.Simulator(net5)
+    sim.set_option(ranc.OPT_KERNEL, 2)
+    sim.load_inputs(inp5)
+    assert sim.info()["ring_layout"] == 2
     sim.close()
 
 
