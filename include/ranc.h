@@ -198,9 +198,9 @@ ranc_status ranc_set_allocator(ranc_ctx* ctx, void* (*alloc)(size_t, void*),
 #define RANC_OPT_KERNEL 3
 /* RANC_OPT_RING_LAYOUT (tensor-core kernel only; device memory layout of the
  * scheduler rings, Alg. 1 l.3-5 and l.15-20, P:79-82 / P:102-110): 0 (default)
- * automatic -- word-major when most routing neurons of the network have their
- * own destination word (e.g. the random mesh of config 5), sample-major when
- * they deposit whole words together (layered MNIST nets); 1 sample-major
+ * automatic -- word-major when more than 2/3 of all neurons route to their
+ * own destination word (e.g. the random mesh of config 5), else sample-major
+ * (layered MNIST nets deposit whole words together); 1 sample-major
  * [Rp][G][S][W]; 2 word-major [Rp][G][W][S] (a warp's deposits for 32 samples
  * of one route hit one 128-byte line).  Takes effect at the next
  * ranc_load_inputs / ranc_reset_state.  Results are identical either way. */
