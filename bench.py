@@ -73,6 +73,9 @@ WORKLOADS = {
     # 32x128 grid, 1250 samples each (the config-3 work per step); value counts
     # variant-samples
     "sweep8": (lambda S: _sweep(8, S), 1250, "samples"),
+    # config 3 with weights / leaks / thresholds x16 (13-bit weights, beyond
+    # int8): the tensor-core wide-weight variant (two int8 operands)
+    "config3w": (lambda S: __import__("workloads.gen", fromlist=["x"]).config3_wide(S=S), 10000, "samples"),
 }
 
 

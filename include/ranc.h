@@ -184,7 +184,10 @@ ranc_status ranc_set_allocator(ranc_ctx* ctx, void* (*alloc)(size_t, void*),
  * tick.  Takes effect at the next ranc_load_inputs / ranc_reset_state.
  * RANC_OPT_KERNEL: 0 automatic (tensor core when the network is eligible,
  * unless S < 64 and cores x S <= 592, where the popcount path's streaming
- * launch is faster), 1 popcount, 2 tensor core (see ranc_info.kernel). */
+ * launch is faster), 1 popcount, 2 tensor core (see ranc_info.kernel).
+ * Tensor-core eligibility: <= 256 neurons, 32*ceil(A/32)*Npad <= 64 KB and
+ * every weight within 15 bits (|w| <= 127: one int8 operand; larger: a
+ * lo/hi int8 split, two MMAs); otherwise RANC_E_CONFIG for value 2. */
 #define RANC_OPT_SAMPLE_TILE 1
 #define RANC_OPT_INPUT_DECODE 2
 /* RANC_OPT_STREAM (streaming mode: one long stream of inputs,

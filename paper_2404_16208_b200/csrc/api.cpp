@@ -646,7 +646,7 @@ ranc_status ranc_set_option(ranc_ctx* ctx, int option, int64_t value) {
         return RANC_E_ARG;
       }
       if (value == RANC_KERNEL_TC && !ctx->net.tc_ok) {
-        ctx->err = "network is outside the tensor-core envelope (|w| <= 127, Npad*32*ceil(A/32) <= 64 KB)";
+        ctx->err = "network is outside the tensor-core envelope (|w| <= 16383, Npad*32*ceil(A/32) <= 64 KB)";
         return RANC_E_CONFIG;
       }
       ctx->kernel = (int32_t)value;  // takes effect at the next ranc_load_inputs / ranc_reset_state

@@ -263,13 +263,19 @@ ranc_status validate_and_compile(const ranc_network_desc* d, Compiled* out, std:
       o.route[cp] = uint2{x, y};
     }
   }
-  // tensor-core eligibility: folded weights fit int8 and Wfold of one core fits
-  // the 64 KB shared-memory operand budget (<= 256 neurons)
+  // tensor-core eligibility: Wfold of one core fits the 64 KB shared-memory
+  // operand budget (<= 256 neurons) and the folded weights fit int8, or, split
+  // as w = 128*hi + lo (lo in [0,127], hi in [-128,127]), 15 bits; the kernel's
+  // shared-memory layout is checked against 227 KB when the path is chosen
   {
     bool ok = o.Npad <= 256 && (size_t)o.Npad * o.Kp <= 65536;
-    for (size_t i = 0; ok && i < (size_t)G * N * K; ++i)
-      if (d->weight[i] < -127 || d->weight[i] > 127) ok = false;
+    bool wide = false;
+    for (size_t i = 0; ok && i < (size_t)G * N * K; ++i) {
+      if (d->weight[i] < -127 || d->weight[i] > 127) wide = true;
+      if (d->weight[i] < -16384 || d->weight[i] > 16383) ok = false;
+    }
     o.tc_ok = ok;
+    o.tc_wide = ok && wide;
   }
   if (o.tc_ok) {
     // Axon order of the tensor-core path: the types are folded into the
@@ -378,18 +384,28 @@ ranc_status validate_and_compile(const ranc_network_desc* d, Compiled* out, std:
       o.tc_wmajor = 3 * scattered > 2 * (int64_t)G * N;
     }
     // folded weights in the canonical operand layout (tc.h)
-    const size_t per = (size_t)o.Npad * o.Kp;
-    o.wfold.assign((size_t)G * per, 0);
+    // (wide weights: [lo | hi] per core, w = 128*hi + lo)
+    const size_t per = (size_t)o.Npad * o.Kp, parts = o.tc_wide ? 2 : 1;
+    o.wfold.assign((size_t)G * parts * per, 0);
     for (int c = 0; c < G; ++c) {
       const int32_t* inv = &o.inv_tc[(size_t)c * A];
       const uint8_t* ty = d->axon_type + (size_t)c * A;
-      int8_t* dst = &o.wfold[(size_t)c * per];
+      int8_t* dst = &o.wfold[(size_t)c * parts * per];
       for (int n = 0; n < N; ++n) {
         const size_t cn = (size_t)c * N + n;
         const uint32_t* src = d->crossbar + cn * W;
         for (int a = 0; a < A; ++a)
-          if ((src[a >> 5] >> (a & 31)) & 1u)
-            dst[tc_operand_offset((uint32_t)n, (uint32_t)inv[a], (uint32_t)o.Npad)] = (int8_t)d->weight[cn * K + ty[a]];
+          if ((src[a >> 5] >> (a & 31)) & 1u) {
+            const int w = d->weight[cn * K + ty[a]];
+            const size_t off = tc_operand_offset((uint32_t)n, (uint32_t)inv[a], (uint32_t)o.Npad);
+            if (!o.tc_wide) {
+              dst[off] = (int8_t)w;
+            } else {
+              const int hi = w >> 7;   // floor(w / 128): arithmetic shift
+              dst[off] = (int8_t)(w - 128 * hi);
+              dst[per + off] = (int8_t)hi;
+            }
+          }
       }
     }
   }

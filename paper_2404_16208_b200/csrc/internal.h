@@ -90,6 +90,7 @@ struct Compiled {
   int32_t Kp = 0;               // 32 * W
   int32_t WIp = 0;              // WI rounded up to 4
   bool tc_ok = false;           // eligible for the tcgen05 kind::i8 path
+  bool tc_wide = false;         // some |weight| > 127: Wfold split into lo/hi int8 operands [G][2][Npad*Kp]
   bool tc_wmajor = false;       // automatic ring layout: word-major when most routing neurons sit in
                                 // warps without a shared destination word (per-neuron routes)
   std::vector<int8_t> wfold;    // [G][Npad*Kp] canonical operand layout, tensor-core axon order

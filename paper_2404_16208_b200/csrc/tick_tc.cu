@@ -76,10 +76,14 @@ struct TcLayout {
 };
 
 // WIp: input-line row words (multiple of 4)
-__host__ __device__ inline TcLayout tc_layout(int Np, int Kp, int W, int WIp, int rmax) {
+// wide: weights beyond int8 are split w = 128*hi + lo (lo in [0,127], hi in
+// [-128,127]); the two folded operands double the weight buffer and the
+// spike pipeline keeps 2 stages (NS_WIDE) to stay inside 227 KB
+constexpr int NS_WIDE = 2;
+__host__ __device__ inline TcLayout tc_layout(int Np, int Kp, int W, int WIp, int rmax, bool wide) {
   TcLayout L;
   L.w = 1024;
-  uint32_t o = L.w + (uint32_t)Np * Kp;
+  uint32_t o = L.w + (uint32_t)Np * Kp * (wide ? 2u : 1u);
   L.runs = o;                                 // int2 [rmax] + int32 [W] of the current core
   o += (uint32_t)rmax * 8 + (uint32_t)W * 4;
   o = (o + 15) & ~15u;
@@ -96,7 +100,7 @@ __host__ __device__ inline TcLayout tc_layout(int Np, int Kp, int W, int WIp, in
   q = (q + 15) & ~15u;
   L.lines = q; q += (uint32_t)NT * (WIp > W ? WIp : W) * 4;  // input line rows or decoded words (TMA)
   L.stage_bytes = (q + 1023) & ~1023u;
-  L.total = L.stage + NS * L.stage_bytes;
+  L.total = L.stage + (wide ? NS_WIDE : NS) * L.stage_bytes;
   return L;
 }
 
@@ -189,7 +193,9 @@ __device__ __forceinline__ uint32_t lif(const uint4 (&cur)[NE / 8], const uint32
 // registers between ticks (stored once, after the last tick).
 // kWm: word-major scheduler rings (compile-time, so each instantiation only
 // carries its own layout's code)
-template <bool kMulti, bool kDebug, bool kWm>
+// kWide: weights split into lo/hi int8 operands, two MMAs and two TMEM
+// accumulators per tile, acc = acc_lo + 128 * acc_hi in the epilogue
+template <bool kMulti, bool kDebug, bool kWm, bool kWide>
 __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams p, const int nticks_arg) {
   const int nticks = kMulti ? nticks_arg : 1;
   // kDebug: the RANC_DEBUG_TIMELINE instrumentation (a separate instantiation,
@@ -202,7 +208,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + 8 * NBARS);
   const int Np = p.Npad, Kp = p.Kp, W = p.W, WIp = p.WIp;
-  const TcLayout L = tc_layout(Np, Kp, W, WIp, p.rmax);
+  const TcLayout L = tc_layout(Np, Kp, W, WIp, p.rmax, kWide);
+  constexpr int NS = kWide ? NS_WIDE : ranc::NS;   // spike stages in use
   uint8_t* w_s = smem + L.w;
   const int Mh = Np >> 7;
   const int nT = (p.S + NT - 1) / NT;
@@ -211,8 +218,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
   const int hi = (int)((int64_t)(blockIdx.x + 1) * total / gridDim.x);
   const int nwork = hi - lo;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t acc_stride = (uint32_t)Mh * NT;          // TMEM columns per accumulator stage
-  constexpr int NA = 4;                                    // accumulator stages (Np <= 256: 4 x 128 columns)
+  // TMEM columns per accumulator stage (wide: the hi accumulator follows the lo one)
+  const uint32_t acc_stride = (uint32_t)Mh * NT * (kWide ? 2u : 1u);
+  constexpr int NA = kWide ? 2 : 4;                        // accumulator stages (Np <= 256: 512 columns)
   const uint32_t tcols = acc_stride * NA;
   auto tick_barrier = [&]() {
     if (kMulti) cg::this_grid().sync();
@@ -266,7 +274,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
         ++jw;
         if (jw > 0) wait(&bars[WFREE], (jw - 1) & 1);
         if (lane == 0) {
-          const uint32_t wb = (uint32_t)Np * Kp;
+          const uint32_t wb = (uint32_t)Np * Kp * (kWide ? 2u : 1u);   // wide: [lo | hi]
           ptx::mbar_arrive_expect_tx(&bars[WFULL], wb);
           ptx::bulk_g2s(w_s, p.wfold + (size_t)c * wb, wb, &bars[WFULL]);
         }
@@ -338,6 +346,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
             const uint64_t ad = tc::smem_desc(ptx::smem_u32(w_s + hh * 2048 + kk * 2 * lbo_a), lbo_a, 128);
             const uint64_t bd = tc::smem_desc(ptx::smem_u32(b_s + kk * 2 * lbo_b), lbo_b, 128);
             tc::mma_i8(acc + hh * NT, ad, bd, id, kk > 0 ? 1u : 0u);
+            if (kWide) {
+              const uint64_t ah = tc::smem_desc(ptx::smem_u32(w_s + Np * Kp + hh * 2048 + kk * 2 * lbo_a), lbo_a, 128);
+              tc::mma_i8(acc + (Mh + hh) * NT, ah, bd, id, kk > 0 ? 1u : 0u);
+            }
           }
         tc::commit(&bars[BEMPTY0 + s]);
         tc::commit(&bars[ACCFULL0 + a]);
@@ -649,6 +661,13 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
         for (int sb = 0; sb < kPass; ++sb) {
           uint32_t acc[kSub];
           tc::ld16(acc_addr + sb * kSub, acc);
+          if (kWide) {   // acc = lo + 128 * hi (exact in int32)
+            uint32_t hi[kSub];
+            tc::ld16(acc_addr + Mh * NT + sb * kSub, hi);
+            tc::wait_ld();
+#pragma unroll
+            for (int i = 0; i < kSub; ++i) acc[i] += hi[i] << 7;
+          }
           // this pass's potentials are in pbuf: prefetched a tile ago
           // (cp.async), kept from the previous tick (multi-tick launch), or
           // the initial potentials (first tick after a reset, filled below)
@@ -841,7 +860,7 @@ cudaError_t decode_inputs_tc(ranc_ctx* ctx) {
 
 int tc_tile() { return NT; }
 
-size_t tc_smem_bytes(const Compiled& n) { return tc_layout(n.Npad, n.Kp, n.W, n.WIp, n.rmax).total; }
+size_t tc_smem_bytes(const Compiled& n) { return tc_layout(n.Npad, n.Kp, n.W, n.WIp, n.rmax, n.tc_wide).total; }
 
 namespace {
 
@@ -865,7 +884,7 @@ void tc_fill_params(ranc_ctx* ctx, TickParams& p) {
 
 bool tc_multi_eligible(const ranc_ctx* ctx, int64_t num_ticks) {
   if (ctx->kernel_active != RANC_KERNEL_TC || ctx->shard_mode == RANC_SHARD_CORES || num_ticks < 2) return false;
-  if (ctx->stream_opt == 1 || getenv("RANC_DEBUG_TIMELINE")) return false;
+  if (ctx->stream_opt == 1 || getenv("RANC_DEBUG_TIMELINE") || ctx->net.tc_wide) return false;
   const int64_t total = (int64_t)ctx->G_loc * ((ctx->S + NT - 1) / NT);
   return total <= ctx->num_sms;   // one work item per CTA, one CTA per SM (cooperative launch)
 }
@@ -876,8 +895,9 @@ cudaError_t launch_tc_multi(ranc_ctx* ctx, TickParams p, int64_t num_ticks) {
   const Compiled& n = ctx->net;
   tc_fill_params(ctx, p);
   const int grid = (int)((int64_t)ctx->G_loc * ((ctx->S + NT - 1) / NT));
-  const size_t smem = tc_layout(n.Npad, n.Kp, n.W, n.WIp, n.rmax).total;
-  const void* fn = p.wmajor ? (const void*)tick_tc_kernel<true, false, true> : (const void*)tick_tc_kernel<true, false, false>;
+  const size_t smem = tc_smem_bytes(n);
+  const void* fn = p.wmajor ? (const void*)tick_tc_kernel<true, false, true, false>
+                            : (const void*)tick_tc_kernel<true, false, false, false>;
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   int nt = (int)std::min<int64_t>(num_ticks, 1 << 30);
   void* args[] = {&p, &nt};
@@ -890,28 +910,36 @@ cudaError_t launch_tick_tc(ranc_ctx* ctx, TickParams p) {
   tc_fill_params(ctx, p);
   const int64_t total = (int64_t)ctx->G_loc * ((ctx->S + NT - 1) / NT);
   const int grid = (int)std::min<int64_t>(total, ctx->num_sms);
-  const size_t smem = tc_layout(n.Npad, n.Kp, n.W, n.WIp, n.rmax).total;
+  const size_t smem = tc_smem_bytes(n);
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(tick_tc_kernel<false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaFuncSetAttribute(tick_tc_kernel<false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaFuncSetAttribute(tick_tc_kernel<false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaFuncSetAttribute(tick_tc_kernel<false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    const void* fns[] = {(const void*)tick_tc_kernel<false, false, false, false>,
+                         (const void*)tick_tc_kernel<false, true, false, false>,
+                         (const void*)tick_tc_kernel<false, false, true, false>,
+                         (const void*)tick_tc_kernel<false, true, true, false>,
+                         (const void*)tick_tc_kernel<false, false, false, true>,
+                         (const void*)tick_tc_kernel<false, false, true, true>};
+    for (const void* f : fns) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     configured = true;
   }
-  static const bool dbg = getenv("RANC_DEBUG_TIMELINE") != nullptr;
+  static const bool dbg_env = getenv("RANC_DEBUG_TIMELINE") != nullptr;
+  const bool dbg = dbg_env && !n.tc_wide;
   constexpr int kDbg = 64 * 16 + 64 + 512;   // timeline, per-warp wait/total, per-CTA start/end
   if (dbg && !ctx->d_dbg.p) dev_alloc(ctx, &ctx->d_dbg, kDbg * 8);
   p.dbg = dbg ? (unsigned long long*)ctx->d_dbg.p : nullptr;
   if (dbg) cudaMemsetAsync(ctx->d_dbg.p, 0, kDbg * 8, ctx->stream);
-  if (dbg && p.wmajor)
-    tick_tc_kernel<false, true, true><<<grid, kThreadsTC, smem, ctx->stream>>>(p, 1);
+  if (n.tc_wide && p.wmajor)   // wide weights: no timeline instrumentation
+    tick_tc_kernel<false, false, true, true><<<grid, kThreadsTC, smem, ctx->stream>>>(p, 1);
+  else if (n.tc_wide)
+    tick_tc_kernel<false, false, false, true><<<grid, kThreadsTC, smem, ctx->stream>>>(p, 1);
+  else if (dbg && p.wmajor)
+    tick_tc_kernel<false, true, true, false><<<grid, kThreadsTC, smem, ctx->stream>>>(p, 1);
   else if (dbg)
-    tick_tc_kernel<false, true, false><<<grid, kThreadsTC, smem, ctx->stream>>>(p, 1);
+    tick_tc_kernel<false, true, false, false><<<grid, kThreadsTC, smem, ctx->stream>>>(p, 1);
   else if (p.wmajor)
-    tick_tc_kernel<false, false, true><<<grid, kThreadsTC, smem, ctx->stream>>>(p, 1);
+    tick_tc_kernel<false, false, true, false><<<grid, kThreadsTC, smem, ctx->stream>>>(p, 1);
   else
-    tick_tc_kernel<false, false, false><<<grid, kThreadsTC, smem, ctx->stream>>>(p, 1);
+    tick_tc_kernel<false, false, false, false><<<grid, kThreadsTC, smem, ctx->stream>>>(p, 1);
   if (dbg) {
     static unsigned long long h[kDbg];
     cudaMemcpyAsync(h, ctx->d_dbg.p, sizeof h, cudaMemcpyDeviceToHost, ctx->stream);

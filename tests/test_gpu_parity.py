@@ -267,14 +267,39 @@ def test_ring_layout_switch_at_reset(ranc, oracle_mod):
 
 
 def test_tc_envelope_rejects_wide_weights(ranc):
+    """|w| <= 127: one int8 operand; |w| <= 16383: the lo/hi split (wide
+    variant); beyond 15 bits the tensor-core path is refused."""
     from workloads.gen import random_network
-    net = random_network(3, 2, 1, 64, 64, 4, 3, wb=12)
+    net = random_network(3, 2, 1, 64, 64, 4, 3, wb=16)
+    net.weight[:] = np.clip(net.weight, -16384, 16383)
     net.weight[0, 0, 0] = 1000
+    sim = ranc.Simulator(net)
+    sim.set_option(ranc.OPT_KERNEL, 2)   # 15-bit weights: accepted
+    sim.close()
+    net.weight[0, 0, 1] = 20000
     sim = ranc.Simulator(net)
     with pytest.raises(ranc.RancError) as ei:
         sim.set_option(ranc.OPT_KERNEL, 2)
     assert ei.value.code == "RANC_E_CONFIG"
     sim.close()
+
+
+@pytest.mark.parametrize("seed", range(4))
+@pytest.mark.parametrize("wk", ["tc", "tc_wm"])
+def test_wide_weights_every_tick(ranc, oracle_mod, seed, wk):
+    """Weights beyond int8 (wb 10..15, full range, incl. the extremes and
+    multiples of 128) on the tensor-core path: w = 128*hi + lo, two MMAs, two
+    TMEM accumulators; full state against the oracle every tick, 70 samples
+    (a ragged second tile)."""
+    from workloads.gen import bernoulli_inputs, random_network
+    from workloads.rng import substream
+    wb = 10 + seed + (seed == 3)                 # 10, 11, 12, 15 bits
+    net = random_network(100 + seed, 3, 2, 256, 256, 4, 3, wb=wb, I=64)
+    lo, hi = -(1 << (wb - 1)), (1 << (wb - 1)) - 1
+    net.weight[0, :4, :] = [[lo, hi, -128, 128], [127, -127, 0, -129], [255, -256, 384, -385], [lo, lo, hi, hi]]
+    inp = bernoulli_inputs(substream(200 + seed, "wide-inputs"), 70, 6, net.num_lines, 0.3)
+    o = per_tick(ranc, oracle_mod, net, inp, 10, kernel=wk)
+    assert o.counts().sum() > 0
 
 
 # ---------------------------------------------------------------------------

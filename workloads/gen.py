@@ -213,6 +213,23 @@ def config2(seed=1002, S=1000, T_in=16):
 # ----------------------------------------------------------------------------
 
 
+def config3_wide(seed=1003, S=10000, scale=16, **kw):
+    """The config-3 net with every weight, leak, threshold and reset scaled by
+    `scale` (16: weights up to +-128, beyond int8), so integration needs
+    13-bit weights while the dynamics stay those of config 3 (a perf workload
+    for the tensor-core wide-weight variant)."""
+    net, inp = config3(seed=seed, S=S, **kw)
+    for f in ("weight", "leak", "pos_threshold", "neg_threshold", "reset_potential", "initial_potential"):
+        setattr(net, f, (getattr(net, f).astype(np.int32) * scale).astype(np.int16))
+    extra = int(np.ceil(np.log2(scale)))
+    net.weight_bits += extra
+    net.leak_bits += extra
+    net.threshold_bits += extra
+    net.reset_bits += extra
+    net.name = f"config3-wide-x{scale}"
+    return net, inp
+
+
 def config3_layout():
     """Core coordinates of the 4 layers on the 32x16 grid."""
     W = 32
