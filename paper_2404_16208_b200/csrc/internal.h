@@ -51,6 +51,7 @@ struct TickParams {
   int32_t pot_lo, pot_hi;   // saturation range of pb bits
   int32_t fresh;            // first tick after a reset: potentials start at init
   int32_t wmajor;           // tensor-core path: ring and decoded inputs word-major [..][W][Sr]
+  int32_t any_route;        // some neuron routes (multi-tick tensor-core launch needs the grid barrier)
   int32_t Kp;               // tensor-core path: K bytes per operand row (= 32*W)
   int64_t t;                // tick being executed
   int64_t raster_t0;        // first tick of the raster buffer
@@ -90,6 +91,7 @@ struct Compiled {
   int32_t Kp = 0;               // 32 * W
   int32_t WIp = 0;              // WI rounded up to 4
   bool tc_ok = false;           // eligible for the tcgen05 kind::i8 path
+  bool any_route = false;       // some neuron has dest_kind ROUTE
   bool tc_wide = false;         // some |weight| > 127: Wfold split into lo/hi int8 operands [G][2][Npad*Kp]
   bool tc_wmajor = false;       // automatic ring layout: word-major when most routing neurons sit in
                                 // warps without a shared destination word (per-neuron routes)

@@ -222,14 +222,21 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
   const uint32_t acc_stride = (uint32_t)Mh * NT * (kWide ? 2u : 1u);
   constexpr int NA = kWide ? 2 : 4;                        // accumulator stages (Np <= 256: 512 columns)
   const uint32_t tcols = acc_stride * NA;
+  // a7: the grid barrier orders tick t's ring deposits before tick t+1's
+  // reads.  A network without routes has no cross-CTA state (each CTA owns
+  // one (core, tile) and its potentials), so its ticks need no barrier and
+  // the roles' mbarrier pipelines overlap consecutive ticks.
   auto tick_barrier = [&]() {
-    if (kMulti) cg::this_grid().sync();
+    if (kMulti && p.any_route) cg::this_grid().sync();
   };
   // pipeline waits: sleeping (issue slots left to the working warps) in the
   // throughput kernel; spinning in the multi-tick kernel, whose ticks are a
   // latency chain (producer -> spike stage -> MMA -> epilogue -> barrier)
+  // (measured: spinning stays best in the multi-tick launch even when its
+  // ticks overlap, i.e. without routes)
+  constexpr bool spin = kMulti;
   auto wait = [&](uint64_t* bar, uint32_t parity) {
-    if (kMulti) ptx::mbar_wait(bar, parity);
+    if (spin) ptx::mbar_wait(bar, parity);
     else ptx::mbar_wait_sleep(bar, parity, 2000);
   };
 
@@ -598,7 +605,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       // three wait on the quarter's named barrier (no issue slots spent)
       // back-off polling (measured best against the suspend-hint wait, a plain
       // spin and a per-quarter named barrier)
-      if (kMulti) ptx::mbar_wait(&bars[ACCFULL0 + a], ua & 1);
+      if (spin) ptx::mbar_wait(&bars[ACCFULL0 + a], ua & 1);
       else ptx::mbar_wait_backoff(&bars[ACCFULL0 + a], ua & 1, 128);
       if (dbg_on && blockIdx.x == 0) dbg_wait += clock64() - tw0;
       if (lane == 0 && ew == 0) stamp_k(k, 8);
@@ -878,6 +885,7 @@ void tc_fill_params(ranc_ctx* ctx, TickParams& p) {
   p.nruns = (const int32_t*)ctx->d_nruns.p;
   p.rmax = n.rmax;
   p.wmajor = ctx->ring_wmajor ? 1 : 0;
+  p.any_route = n.any_route ? 1 : 0;
 }
 
 }  // namespace
