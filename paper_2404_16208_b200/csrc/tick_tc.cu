@@ -542,6 +542,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
     int leak = 0, pth = 0, nth = 0, rst = 0, init = 0, bf = 0, bn = 0, linmul = 0;
     uint32_t kind = RK_NONE, cls = 0, axbit = 0, out_lanes = 0, out_peers = 0;
     bool route_here = false, exporting = false, block_route = false, block_identity = false, has_output = false;
+    bool out_scatter = false;
     size_t ring_off = 0, warp_ring_off = 0;
     // Potentials stream HBM -> shared memory with cp.async one tile ahead:
     // pbuf[c * PB] holds 16-byte chunk c (8 samples) of this thread's 32
@@ -656,6 +657,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
           has_output = out_lanes != 0u;
           // lanes of the same output class (classes are < C, never ~0u)
           out_peers = __match_any_sync(0xFFFFFFFFu, kind == RK_OUTPUT ? cls : 0xFFFFFFFFu);
+          // more than 8 class groups: per-lane adds (see the output bus below)
+          out_scatter = __popc(__ballot_sync(0xFFFFFFFFu, kind == RK_OUTPUT && __ffs(out_peers) - 1 == lane)) > 8;
           prev_core = c;
         }
         if (kMulti) {   // ring slot of tick t + delay
@@ -753,7 +756,18 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
             if ((m >> l) & 1u) atomicOr(p.ring + off + sj + lane, bit);
           }
         }
-        if (has_output) {
+        if (has_output && out_scatter) {
+          // a6 output bus, many classes in the warp (e.g. VMM: one class per
+          // neuron): each lane adds its own fired samples; the lanes' classes
+          // are neighbouring words of one counts row, so a warp's add touches
+          // one or two lines instead of 32
+          uint32_t g = kind == RK_OUTPUT ? f : 0u;
+          while (g) {
+            const int i = __ffs(g) - 1;
+            g &= g - 1;
+            atomicAdd(p.counts + (size_t)(sj + i) * p.C + cls, 1);
+          }
+        } else if (has_output) {
           // a6 output bus: lane i receives the output neurons (lanes) fired
           // in sample i; one add per (sample, class group of lanes)
           const uint32_t m = transpose32(kind == RK_OUTPUT ? f : 0u, lane);
@@ -892,68 +906,22 @@ void tc_fill_params(ranc_ctx* ctx, TickParams& p) {
 
 bool tc_multi_eligible(const ranc_ctx* ctx, int64_t num_ticks) {
   if (ctx->kernel_active != RANC_KERNEL_TC || ctx->shard_mode == RANC_SHARD_CORES || num_ticks < 2) return false;
-  if (ctx->stream_opt == 1 || getenv("RANC_DEBUG_TIMELINE") || ctx->net.tc_wide) return false;
+  if (ctx->stream_opt == 1 || getenv("RANC_DEBUG_TIMELINE") || ctx->net.tc_wide) return false;   // (_MULTI: kept)
   const int64_t total = (int64_t)ctx->G_loc * ((ctx->S + NT - 1) / NT);
   return total <= ctx->num_sms;   // one work item per CTA, one CTA per SM (cooperative launch)
 }
 
 // all ticks of a ranc_run_ticks call in one cooperative launch (small
 // batches: at most one (core, 64-sample tile) per SM)
-cudaError_t launch_tc_multi(ranc_ctx* ctx, TickParams p, int64_t num_ticks) {
-  const Compiled& n = ctx->net;
-  tc_fill_params(ctx, p);
-  const int grid = (int)((int64_t)ctx->G_loc * ((ctx->S + NT - 1) / NT));
-  const size_t smem = tc_smem_bytes(n);
-  const void* fn = p.wmajor ? (const void*)tick_tc_kernel<true, false, true, false>
-                            : (const void*)tick_tc_kernel<true, false, false, false>;
-  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-  int nt = (int)std::min<int64_t>(num_ticks, 1 << 30);
-  void* args[] = {&p, &nt};
-  return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kThreadsTC), args,
-                                     smem, ctx->stream);
-}
-
-cudaError_t launch_tick_tc(ranc_ctx* ctx, TickParams p) {
-  const Compiled& n = ctx->net;
-  tc_fill_params(ctx, p);
-  const int64_t total = (int64_t)ctx->G_loc * ((ctx->S + NT - 1) / NT);
-  const int grid = (int)std::min<int64_t>(total, ctx->num_sms);
-  const size_t smem = tc_smem_bytes(n);
-  static bool configured = false;
-  if (!configured) {
-    const void* fns[] = {(const void*)tick_tc_kernel<false, false, false, false>,
-                         (const void*)tick_tc_kernel<false, true, false, false>,
-                         (const void*)tick_tc_kernel<false, false, true, false>,
-                         (const void*)tick_tc_kernel<false, true, true, false>,
-                         (const void*)tick_tc_kernel<false, false, false, true>,
-                         (const void*)tick_tc_kernel<false, false, true, true>};
-    for (const void* f : fns) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    configured = true;
-  }
-  static const bool dbg_env = getenv("RANC_DEBUG_TIMELINE") != nullptr;
-  const bool dbg = dbg_env && !n.tc_wide;
-  constexpr int kDbg = 64 * 16 + 64 + 512;   // timeline, per-warp wait/total, per-CTA start/end
-  if (dbg && !ctx->d_dbg.p) dev_alloc(ctx, &ctx->d_dbg, kDbg * 8);
-  p.dbg = dbg ? (unsigned long long*)ctx->d_dbg.p : nullptr;
-  if (dbg) cudaMemsetAsync(ctx->d_dbg.p, 0, kDbg * 8, ctx->stream);
-  if (n.tc_wide && p.wmajor)   // wide weights: no timeline instrumentation
-    tick_tc_kernel<false, false, true, true><<<grid, kThreadsTC, smem, ctx->stream>>>(p, 1);
-  else if (n.tc_wide)
-    tick_tc_kernel<false, false, false, true><<<grid, kThreadsTC, smem, ctx->stream>>>(p, 1);
-  else if (dbg && p.wmajor)
-    tick_tc_kernel<false, true, true, false><<<grid, kThreadsTC, smem, ctx->stream>>>(p, 1);
-  else if (dbg)
-    tick_tc_kernel<false, true, false, false><<<grid, kThreadsTC, smem, ctx->stream>>>(p, 1);
-  else if (p.wmajor)
-    tick_tc_kernel<false, false, true, false><<<grid, kThreadsTC, smem, ctx->stream>>>(p, 1);
-  else
-    tick_tc_kernel<false, false, false, false><<<grid, kThreadsTC, smem, ctx->stream>>>(p, 1);
-  if (dbg) {
+// RANC_DEBUG_TIMELINE(_MULTI): per-tile stamps of CTA 0 (work items k < 64;
+// in a multi-tick launch k = tick), per-warp wait / total cycles, CTA end times
+constexpr int kDbg = 64 * 16 + 64 + 512;
+void dump_timeline(ranc_ctx* ctx, int64_t t, int grid) {
     static unsigned long long h[kDbg];
     cudaMemcpyAsync(h, ctx->d_dbg.p, sizeof h, cudaMemcpyDeviceToHost, ctx->stream);
     cudaStreamSynchronize(ctx->stream);
     const unsigned long long t0 = h[0];
-    fprintf(stderr, "timeline t=%lld grid=%d (cycles rel. to producer start)\n", (long long)p.t, grid);
+    fprintf(stderr, "timeline t=%lld grid=%d (cycles rel. to producer start)\n", (long long)t, grid);
     fprintf(stderr, "  k  prodW prodGo expFull expBempty expBfull mmaB mmaAccE mmaCommit | ew0: acc ld0 ld1 done | exp: cleared injected synced expanded\n");
     for (int k = 0; k < 64; ++k) {
       fprintf(stderr, "%3d", k);
@@ -975,6 +943,63 @@ cudaError_t launch_tick_tc(ranc_ctx* ctx, TickParams p) {
       if (h[64 * 16 + 64 + 2 * b + 1] + 20000 > e_max) fprintf(stderr, " %d", b);
     fprintf(stderr, "\n");
   }
+
+cudaError_t launch_tc_multi(ranc_ctx* ctx, TickParams p, int64_t num_ticks) {
+  const Compiled& n = ctx->net;
+  tc_fill_params(ctx, p);
+  const int grid = (int)((int64_t)ctx->G_loc * ((ctx->S + NT - 1) / NT));
+  const size_t smem = tc_smem_bytes(n);
+  static const bool dbg = getenv("RANC_DEBUG_TIMELINE_MULTI") != nullptr;
+  if (dbg && !ctx->d_dbg.p) dev_alloc(ctx, &ctx->d_dbg, kDbg * 8);
+  p.dbg = dbg ? (unsigned long long*)ctx->d_dbg.p : nullptr;
+  if (dbg) cudaMemsetAsync(ctx->d_dbg.p, 0, kDbg * 8, ctx->stream);
+  const void* fn = dbg ? (p.wmajor ? (const void*)tick_tc_kernel<true, true, true, false>
+                                   : (const void*)tick_tc_kernel<true, true, false, false>)
+                       : (p.wmajor ? (const void*)tick_tc_kernel<true, false, true, false>
+                                   : (const void*)tick_tc_kernel<true, false, false, false>);
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  int nt = (int)std::min<int64_t>(num_ticks, 1 << 30);
+  void* args[] = {&p, &nt};
+  const cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kThreadsTC), args, smem, ctx->stream);
+  if (dbg && e == cudaSuccess) dump_timeline(ctx, p.t, grid);
+  return e;
+}
+
+cudaError_t launch_tick_tc(ranc_ctx* ctx, TickParams p) {
+  const Compiled& n = ctx->net;
+  tc_fill_params(ctx, p);
+  const int64_t total = (int64_t)ctx->G_loc * ((ctx->S + NT - 1) / NT);
+  const int grid = (int)std::min<int64_t>(total, ctx->num_sms);
+  const size_t smem = tc_smem_bytes(n);
+  static bool configured = false;
+  if (!configured) {
+    const void* fns[] = {(const void*)tick_tc_kernel<false, false, false, false>,
+                         (const void*)tick_tc_kernel<false, true, false, false>,
+                         (const void*)tick_tc_kernel<false, false, true, false>,
+                         (const void*)tick_tc_kernel<false, true, true, false>,
+                         (const void*)tick_tc_kernel<false, false, false, true>,
+                         (const void*)tick_tc_kernel<false, false, true, true>};
+    for (const void* f : fns) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    configured = true;
+  }
+  static const bool dbg_env = getenv("RANC_DEBUG_TIMELINE") != nullptr;
+  const bool dbg = dbg_env && !n.tc_wide;
+  if (dbg && !ctx->d_dbg.p) dev_alloc(ctx, &ctx->d_dbg, kDbg * 8);
+  p.dbg = dbg ? (unsigned long long*)ctx->d_dbg.p : nullptr;
+  if (dbg) cudaMemsetAsync(ctx->d_dbg.p, 0, kDbg * 8, ctx->stream);
+  if (n.tc_wide && p.wmajor)   // wide weights: no timeline instrumentation
+    tick_tc_kernel<false, false, true, true><<<grid, kThreadsTC, smem, ctx->stream>>>(p, 1);
+  else if (n.tc_wide)
+    tick_tc_kernel<false, false, false, true><<<grid, kThreadsTC, smem, ctx->stream>>>(p, 1);
+  else if (dbg && p.wmajor)
+    tick_tc_kernel<false, true, true, false><<<grid, kThreadsTC, smem, ctx->stream>>>(p, 1);
+  else if (dbg)
+    tick_tc_kernel<false, true, false, false><<<grid, kThreadsTC, smem, ctx->stream>>>(p, 1);
+  else if (p.wmajor)
+    tick_tc_kernel<false, false, true, false><<<grid, kThreadsTC, smem, ctx->stream>>>(p, 1);
+  else
+    tick_tc_kernel<false, false, false, false><<<grid, kThreadsTC, smem, ctx->stream>>>(p, 1);
+  if (dbg) dump_timeline(ctx, p.t, grid);
   return cudaGetLastError();
 }
 
