@@ -152,6 +152,8 @@ struct ranc_ctx {
   int32_t sample_tile = 0;       // in use (set by ranc_run_ticks)
   int32_t sample_tile_opt = 0;   // RANC_OPT_SAMPLE_TILE, 0 = automatic
   int32_t input_decode = 1;      // RANC_OPT_INPUT_DECODE
+  int32_t pdl = 1;               // programmatic dependent launch of per-tick tensor-core launches
+                                 // (RANC_DEBUG_NO_PDL=1 disables it, for timing comparisons)
   int32_t stream_opt = 0;        // RANC_OPT_STREAM: 0 auto, 1 off, 2 on
   int32_t kernel = 0;            // RANC_OPT_KERNEL request: 0 auto, 1 popcount, 2 tensor core
   int32_t kernel_active = 1;     // latched at every reset (the potential layout depends on it)

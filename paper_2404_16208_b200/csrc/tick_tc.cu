@@ -258,6 +258,15 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
     ptx::mbar_init(&bars[WFREE], 1);
     ptx::fence_mbar_init();
   }
+  // programmatic dependent launch (per-tick launches): let the next tick's
+  // grid be scheduled now, so its CTAs start (launch, TMEM allocation,
+  // barrier set-up) as soon as this grid's CTAs leave their SMs; then wait
+  // until the previous tick's grid has completed and its writes (potentials,
+  // ring deposits, counts) are visible.  Both are no-ops without PDL.
+  if (!kMulti) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+  }
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
@@ -987,18 +996,29 @@ cudaError_t launch_tick_tc(ranc_ctx* ctx, TickParams p) {
   if (dbg && !ctx->d_dbg.p) dev_alloc(ctx, &ctx->d_dbg, kDbg * 8);
   p.dbg = dbg ? (unsigned long long*)ctx->d_dbg.p : nullptr;
   if (dbg) cudaMemsetAsync(ctx->d_dbg.p, 0, kDbg * 8, ctx->stream);
-  if (n.tc_wide && p.wmajor)   // wide weights: no timeline instrumentation
-    tick_tc_kernel<false, false, true, true><<<grid, kThreadsTC, smem, ctx->stream>>>(p, 1);
-  else if (n.tc_wide)
-    tick_tc_kernel<false, false, false, true><<<grid, kThreadsTC, smem, ctx->stream>>>(p, 1);
-  else if (dbg && p.wmajor)
-    tick_tc_kernel<false, true, true, false><<<grid, kThreadsTC, smem, ctx->stream>>>(p, 1);
-  else if (dbg)
-    tick_tc_kernel<false, true, false, false><<<grid, kThreadsTC, smem, ctx->stream>>>(p, 1);
-  else if (p.wmajor)
-    tick_tc_kernel<false, false, true, false><<<grid, kThreadsTC, smem, ctx->stream>>>(p, 1);
-  else
-    tick_tc_kernel<false, false, false, false><<<grid, kThreadsTC, smem, ctx->stream>>>(p, 1);
+  const void* fn = n.tc_wide ? (p.wmajor ? (const void*)tick_tc_kernel<false, false, true, true>   // wide: no timeline
+                                          : (const void*)tick_tc_kernel<false, false, false, true>)
+                   : dbg ? (p.wmajor ? (const void*)tick_tc_kernel<false, true, true, false>
+                                     : (const void*)tick_tc_kernel<false, true, false, false>)
+                         : (p.wmajor ? (const void*)tick_tc_kernel<false, false, true, false>
+                                     : (const void*)tick_tc_kernel<false, false, false, false>);
+  // programmatic dependent launch: consecutive tick launches overlap the
+  // next grid's start-up with this one's tail (griddepcontrol in the kernel)
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreadsTC);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  static const bool no_pdl = getenv("RANC_DEBUG_NO_PDL") != nullptr;
+  attr[0].val.programmaticStreamSerializationAllowed = (ctx->pdl && !no_pdl) ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int one = 1;
+  void* args[] = {&p, &one};
+  const cudaError_t e = cudaLaunchKernelExC(&cfg, fn, args);
+  if (e != cudaSuccess) return e;
   if (dbg) dump_timeline(ctx, p.t, grid);
   return cudaGetLastError();
 }
