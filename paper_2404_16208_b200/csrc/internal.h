@@ -52,6 +52,7 @@ struct TickParams {
   int32_t fresh;            // first tick after a reset: potentials start at init
   int32_t wmajor;           // tensor-core path: ring and decoded inputs word-major [..][W][Sr]
   int32_t any_route;        // some neuron routes (multi-tick tensor-core launch needs the grid barrier)
+  int32_t pot_items;        // multi-tick tensor-core launch: work items (potential tiles) per CTA, 1 or 2
   int32_t Kp;               // tensor-core path: K bytes per operand row (= 32*W)
   int64_t t;                // tick being executed
   int64_t raster_t0;        // first tick of the raster buffer

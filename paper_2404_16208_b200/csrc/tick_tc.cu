@@ -80,7 +80,9 @@ struct TcLayout {
 // [-128,127]); the two folded operands double the weight buffer and the
 // spike pipeline keeps 2 stages (NS_WIDE) to stay inside 227 KB
 constexpr int NS_WIDE = 2;
-__host__ __device__ inline TcLayout tc_layout(int Np, int Kp, int W, int WIp, int rmax, bool wide) {
+// pot_items: potential tiles kept on chip (multi-tick launch with up to two
+// work items per CTA: one region each)
+__host__ __device__ inline TcLayout tc_layout(int Np, int Kp, int W, int WIp, int rmax, bool wide, int pot_items = 1) {
   TcLayout L;
   L.w = 1024;
   uint32_t o = L.w + (uint32_t)Np * Kp * (wide ? 2u : 1u);
@@ -91,7 +93,7 @@ __host__ __device__ inline TcLayout tc_layout(int Np, int Kp, int W, int WIp, in
   o += 256 * 8;
   o = (o + 127) & ~127u;
   L.potbuf = o;                               // uint4 [NT/8][epilogue threads]: next tile's potentials
-  o += (NT / 8) * (32 * 8) * 16;           // = 4 chunks x 512 epilogue threads
+  o += (NT / 8) * (32 * 8) * 16 * (uint32_t)pot_items;   // = 4 chunks x 512 epilogue threads per item
   L.stage = (o + 1023) & ~1023u;
   uint32_t q = 0;
   L.b = q;     q += (uint32_t)NT * Kp;       // spikes as 0/1 bytes, canonical layout
@@ -208,7 +210,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + 8 * NBARS);
   const int Np = p.Npad, Kp = p.Kp, W = p.W, WIp = p.WIp;
-  const TcLayout L = tc_layout(Np, Kp, W, WIp, p.rmax, kWide);
+  const TcLayout L = tc_layout(Np, Kp, W, WIp, p.rmax, kWide, kMulti ? p.pot_items : 1);
   constexpr int NS = kWide ? NS_WIDE : ranc::NS;   // spike stages in use
   uint8_t* w_s = smem + L.w;
   const int Mh = Np >> 7;
@@ -370,9 +372,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
         tc::commit(&bars[BEMPTY0 + s]);
         tc::commit(&bars[ACCFULL0 + a]);
         stamp_k(k, 7);
-        // last tile of this core (in a multi-tick launch the next item is the
-        // same core again, except after the last tick)
-        if (k0 + 1 < nwork ? tile + 1 == nT : it + 1 == nticks) tc::commit(&bars[WFREE]);
+        // the next item (in a multi-tick launch: cyclically, the CTA's first
+        // item of the next tick) belongs to another core, or this is the end
+        const bool last_item = k0 + 1 == nwork;
+        const int next_cl = last_item ? lo / nT : (tile + 1 == nT ? cl + 1 : cl);
+        if ((last_item && it + 1 == nticks) || next_cl != cl) tc::commit(&bars[WFREE]);
       }
       __syncwarp();
     }
@@ -563,6 +567,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
     constexpr int kPass = 32 / kSub, kCh = kSub / 8;   // passes per half, chunks per pass
     uint4* pbuf = reinterpret_cast<uint4*>(smem + L.potbuf) + (threadIdx.x - 32 * kFirstEpi);
     constexpr int PB = 32 * kEpiWarps;   // uint4 stride between chunks in potbuf
+    constexpr int kItem = kPass * kCh * PB;   // uint4 per item region (multi-tick launch): 32 KB
     const bool load = active && !p.fresh;
     const bool sat16 = p.pot_lo == -32768 && p.pot_hi == 32767;
     const int one = 1 + (p.N >> 30);   // N <= 1024: 1 (see lif)
@@ -629,12 +634,14 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
           if (p.fresh && first) {
             // first tick after a reset: the pass inputs are the initial
             // potentials; pbuf is not refilled while this core's tiles run
-            // (the new potentials go to HBM, or to pbuf only after the
-            // single tile of a multi-tick launch has read it)
+            // (the new potentials go to HBM; a multi-tick launch fills each
+            // item's region below and keeps its potentials there)
             const uint32_t ii = ((uint32_t)init & 0xFFFFu) * 0x10001u;
             initv = make_uint4(ii, ii, ii, ii);
+            if (!kMulti) {
 #pragma unroll
-            for (int i = 0; i < kPass * kCh; ++i) pbuf[i * PB] = initv;
+              for (int i = 0; i < kPass * kCh; ++i) pbuf[i * PB] = initv;
+            }
           }
           kind = valid ? route_kind(rt.x) : RK_NONE;
           const bool lin = route_lin(rt.x);
@@ -670,6 +677,14 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
           out_scatter = __popc(__ballot_sync(0xFFFFFFFFu, kind == RK_OUTPUT && __ffs(out_peers) - 1 == lane)) > 8;
           prev_core = c;
         }
+        // this item's potential region: the multi-tick launch keeps one per
+        // item (pb) and prefetches the next item's into its own (pbn)
+        uint4* const pb = kMulti ? pbuf + k0 * kItem : pbuf;
+        uint4* const pbn = kMulti ? pb + kItem : pbuf;
+        if (kMulti && p.fresh && first) {
+#pragma unroll
+          for (int i = 0; i < kPass * kCh; ++i) pb[i * PB] = initv;
+        }
         if (kMulti) {   // ring slot of tick t + delay
           ring_off = ring_base + (size_t)((t + rdelay) & p.rp_mask) * slot_stride;
           warp_ring_off = warp_ring_base + (size_t)((t + warp_rdelay) & p.rp_mask) * slot_stride;
@@ -693,14 +708,14 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
           if (first && load) ptx::cp_async_wait<1>();   // this pass's group has landed
           uint4 cur[kCh];
 #pragma unroll
-          for (int i = 0; i < kCh; ++i) cur[i] = pbuf[(kCh * sb + i) * PB];
+          for (int i = 0; i < kCh; ++i) cur[i] = pb[(kCh * sb + i) * PB];
           if (first && load) {
             // request the same chunks of the next tile into the slots just read
             if (pf) {
               const char* nb = reinterpret_cast<const char*>(nsrc);
 #pragma unroll
               for (int i = 0; i < kCh; ++i)
-                ptx::cp_async16(pbuf + (kCh * sb + i) * PB, nb + (uint32_t)((kCh * sb + i) * chunk_bytes));
+                ptx::cp_async16(pbn + (kCh * sb + i) * PB, nb + (uint32_t)((kCh * sb + i) * chunk_bytes));
             }
             ptx::cp_async_commit();   // (possibly empty) group: keeps the wait_group 1 accounting
           }
@@ -715,7 +730,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
 #pragma unroll
           for (int cc = 0; cc < kCh; ++cc) {
             const uint4 o = make_uint4(outw[4 * cc + 0], outw[4 * cc + 1], outw[4 * cc + 2], outw[4 * cc + 3]);
-            if (!last) pbuf[(kCh * sb + cc) * PB] = o;   // kept on chip for the next tick
+            if (!last) pb[(kCh * sb + cc) * PB] = o;   // kept on chip for the next tick
             else POT_STORE(reinterpret_cast<char*>(dst) + (uint32_t)((kCh * sb + cc) * chunk_bytes), o);
           }
         }
@@ -917,11 +932,15 @@ bool tc_multi_eligible(const ranc_ctx* ctx, int64_t num_ticks) {
   if (ctx->kernel_active != RANC_KERNEL_TC || ctx->shard_mode == RANC_SHARD_CORES || num_ticks < 2) return false;
   if (ctx->stream_opt == 1 || getenv("RANC_DEBUG_TIMELINE") || ctx->net.tc_wide) return false;   // (_MULTI: kept)
   const int64_t total = (int64_t)ctx->G_loc * ((ctx->S + NT - 1) / NT);
-  return total <= ctx->num_sms;   // one work item per CTA, one CTA per SM (cooperative launch)
+  if (total <= ctx->num_sms) return true;   // one work item per CTA, one CTA per SM (cooperative launch)
+  // two work items per CTA: both potential tiles stay in shared memory
+  const Compiled& n = ctx->net;
+  return total <= 2 * (int64_t)ctx->num_sms && tc_layout(n.Npad, n.Kp, n.W, n.WIp, n.rmax, false, 2).total <= 227 * 1024;
 }
 
 // all ticks of a ranc_run_ticks call in one cooperative launch (small
-// batches: at most one (core, 64-sample tile) per SM)
+// batches: at most two (core, 64-sample tile) items per SM, their
+// potentials kept in shared memory between ticks)
 // RANC_DEBUG_TIMELINE(_MULTI): per-tile stamps of CTA 0 (work items k < 64;
 // in a multi-tick launch k = tick), per-warp wait / total cycles, CTA end times
 constexpr int kDbg = 64 * 16 + 64 + 512;
@@ -956,8 +975,10 @@ void dump_timeline(ranc_ctx* ctx, int64_t t, int grid) {
 cudaError_t launch_tc_multi(ranc_ctx* ctx, TickParams p, int64_t num_ticks) {
   const Compiled& n = ctx->net;
   tc_fill_params(ctx, p);
-  const int grid = (int)((int64_t)ctx->G_loc * ((ctx->S + NT - 1) / NT));
-  const size_t smem = tc_smem_bytes(n);
+  const int64_t total = (int64_t)ctx->G_loc * ((ctx->S + NT - 1) / NT);
+  p.pot_items = total <= ctx->num_sms ? 1 : 2;
+  const int grid = (int)((total + p.pot_items - 1) / p.pot_items);   // contiguous items: mostly the same core
+  const size_t smem = tc_layout(n.Npad, n.Kp, n.W, n.WIp, n.rmax, false, p.pot_items).total;
   static const bool dbg = getenv("RANC_DEBUG_TIMELINE_MULTI") != nullptr;
   if (dbg && !ctx->d_dbg.p) dev_alloc(ctx, &ctx->d_dbg, kDbg * 8);
   p.dbg = dbg ? (unsigned long long*)ctx->d_dbg.p : nullptr;

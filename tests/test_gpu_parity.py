@@ -485,6 +485,39 @@ def test_tc_multi_tick_launch(ranc, oracle_mod, stream):
         sim.close()
 
 
+@pytest.mark.parametrize("S", [1650, 1600])
+@pytest.mark.parametrize("ring", [1, 2])
+def test_tc_multi_tick_two_items_per_cta(ranc, oracle_mod, S, ring):
+    """More than 148 and at most 296 (core, tile) items: the multi-tick launch
+    keeps two potential tiles per CTA in shared memory (6 random 128x128
+    cores; S = 1650: 156 items, pairs of one core; S = 1600: 150 items, some
+    CTAs straddle two cores, a ragged last tile), in one call and resumed in
+    pieces."""
+    from workloads.gen import bernoulli_inputs, random_network
+    from workloads.rng import substream
+    net = random_network(7, 3, 2, 128, 128, 4, 3, I=64, wb=8)
+    net.weight[:] = np.maximum(net.weight, -127)   # int8 operand (the wide variant has no multi-tick launch)
+    inp = bernoulli_inputs(substream(17, "two-items"), S, 6, net.num_lines, 0.3)
+    T = 20
+    o = oracle_mod.Oracle(net, inp).run(T)
+    for pieces in ([T], [1, 6, T - 7]):
+        sim = ranc.Simulator(net)
+        sim.set_option(ranc.OPT_KERNEL, 2)
+        sim.set_option(ranc.OPT_RING_LAYOUT, ring)
+        sim.set_trace(ranc.TRACE_OUTPUT_EVENTS)
+        sim.load_inputs(inp)
+        l0 = sim.info()["kernel_launches"]
+        for k in pieces:
+            sim.run(k)
+        assert sim.info()["kernel_launches"] - l0 == len(pieces)   # one cooperative launch per call
+        assert np.array_equal(sim.outputs(), o.counts())
+        assert np.array_equal(sim.potentials(), o.potentials())
+        assert np.array_equal(sim.pending(), o.pending())
+        if len(pieces) == 1:
+            assert np.array_equal(sim.events(), o.events())
+        sim.close()
+
+
 def test_tc_multi_tick_corpus_and_vmm(ranc, oracle_mod):
     for seed in range(12):
         net, inp = corpus_case(seed)
