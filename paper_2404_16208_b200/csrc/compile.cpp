@@ -341,7 +341,10 @@ ranc_status validate_and_compile(const ranc_network_desc* d, Compiled* out, std:
     o.incoming.assign(G, 0);
     o.any_route = false;
     for (int c = 0; c < G; ++c)
-      for (int n = 0; n < N; ++n) o.any_route |= d->dest_kind[(size_t)c * N + n] == RK_ROUTE;
+      for (int n = 0; n < N; ++n) {
+        o.any_route |= d->dest_kind[(size_t)c * N + n] == RK_ROUTE;
+        o.any_output |= d->dest_kind[(size_t)c * N + n] == RK_OUTPUT;
+      }
     for (int c = 0; c < G; ++c)
       for (int n = 0; n < N; ++n)
         if (route_kind(o.route_tc[(size_t)c * Np + n].x) == RK_ROUTE) o.incoming[o.route_tc[(size_t)c * Np + n].y] = 1;

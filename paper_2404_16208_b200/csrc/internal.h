@@ -53,6 +53,7 @@ struct TickParams {
   int32_t wmajor;           // tensor-core path: ring and decoded inputs word-major [..][W][Sr]
   int32_t any_route;        // some neuron routes (multi-tick tensor-core launch needs the grid barrier)
   int32_t pot_items;        // multi-tick tensor-core launch: work items (potential tiles) per CTA, 1 or 2
+  int32_t out_planes;       // multi-tick tensor-core launch: bit-sliced per-thread output counters in shared memory
   int32_t Kp;               // tensor-core path: K bytes per operand row (= 32*W)
   int64_t t;                // tick being executed
   int64_t raster_t0;        // first tick of the raster buffer
@@ -93,6 +94,7 @@ struct Compiled {
   int32_t WIp = 0;              // WI rounded up to 4
   bool tc_ok = false;           // eligible for the tcgen05 kind::i8 path
   bool any_route = false;       // some neuron has dest_kind ROUTE
+  bool any_output = false;      // some neuron has dest_kind OUTPUT
   bool tc_wide = false;         // some |weight| > 127: Wfold split into lo/hi int8 operands [G][2][Npad*Kp]
   bool tc_wmajor = false;       // automatic ring layout: word-major when most routing neurons sit in
                                 // warps without a shared destination word (per-neuron routes)

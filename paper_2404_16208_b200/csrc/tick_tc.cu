@@ -72,7 +72,7 @@ enum Bar { FULL0 = 0, SEMPTY0 = 4, BFULL0 = 8, BEMPTY0 = 12, ACCFULL0 = 16, ACCE
            NBARS = 26 };
 
 struct TcLayout {
-  uint32_t w, runs, lut, potbuf, stage, b, raw, lines, stage_bytes, total;
+  uint32_t w, runs, lut, potbuf, cplanes, stage, b, raw, lines, stage_bytes, total;
 };
 
 // WIp: input-line row words (multiple of 4)
@@ -82,7 +82,10 @@ struct TcLayout {
 constexpr int NS_WIDE = 2;
 // pot_items: potential tiles kept on chip (multi-tick launch with up to two
 // work items per CTA: one region each)
-__host__ __device__ inline TcLayout tc_layout(int Np, int Kp, int W, int WIp, int rmax, bool wide, int pot_items = 1) {
+// cnt_planes: per-thread bit-sliced output-bus counters (multi-tick launch)
+constexpr int kCntPlanes = 8;   // counts < 256 between flushes
+__host__ __device__ inline TcLayout tc_layout(int Np, int Kp, int W, int WIp, int rmax, bool wide, int pot_items = 1,
+                                              bool cnt_planes = false) {
   TcLayout L;
   L.w = 1024;
   uint32_t o = L.w + (uint32_t)Np * Kp * (wide ? 2u : 1u);
@@ -94,6 +97,8 @@ __host__ __device__ inline TcLayout tc_layout(int Np, int Kp, int W, int WIp, in
   o = (o + 127) & ~127u;
   L.potbuf = o;                               // uint4 [NT/8][epilogue threads]: next tile's potentials
   o += (NT / 8) * (32 * 8) * 16 * (uint32_t)pot_items;   // = 4 chunks x 512 epilogue threads per item
+  L.cplanes = o;                              // u32 [items][kCntPlanes][512 epilogue threads]
+  if (cnt_planes) o += (uint32_t)pot_items * kCntPlanes * 512 * 4;
   L.stage = (o + 1023) & ~1023u;
   uint32_t q = 0;
   L.b = q;     q += (uint32_t)NT * Kp;       // spikes as 0/1 bytes, canonical layout
@@ -210,7 +215,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + 8 * NBARS);
   const int Np = p.Npad, Kp = p.Kp, W = p.W, WIp = p.WIp;
-  const TcLayout L = tc_layout(Np, Kp, W, WIp, p.rmax, kWide, kMulti ? p.pot_items : 1);
+  const TcLayout L = tc_layout(Np, Kp, W, WIp, p.rmax, kWide, kMulti ? p.pot_items : 1, kMulti && p.out_planes);
   constexpr int NS = kWide ? NS_WIDE : ranc::NS;   // spike stages in use
   uint8_t* w_s = smem + L.w;
   const int Mh = Np >> 7;
@@ -568,6 +573,15 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
     uint4* pbuf = reinterpret_cast<uint4*>(smem + L.potbuf) + (threadIdx.x - 32 * kFirstEpi);
     constexpr int PB = 32 * kEpiWarps;   // uint4 stride between chunks in potbuf
     constexpr int kItem = kPass * kCh * PB;   // uint4 per item region (multi-tick launch): 32 KB
+    // multi-tick launch: output-bus counts of this thread's 32 samples, bit-
+    // sliced (plane b = bit b of every sample's count), flushed every 255
+    // ticks and after the last one -- one add per (sample, neuron) per flush
+    // instead of one per spike
+    const bool planes = kMulti && p.out_planes;
+    uint32_t* const cpl = reinterpret_cast<uint32_t*>(smem + L.cplanes) + (threadIdx.x - 32 * kFirstEpi);
+    constexpr int kPl = kCntPlanes * 512;   // u32 per item
+    if (planes)
+      for (int i = 0; i < nwork * kCntPlanes; ++i) cpl[i * 512] = 0u;
     const bool load = active && !p.fresh;
     const bool sat16 = p.pot_lo == -32768 && p.pot_hi == 32767;
     const int one = 1 + (p.N >> 30);   // N <= 1024: 1 (see lif)
@@ -780,7 +794,29 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
             if ((m >> l) & 1u) atomicOr(p.ring + off + sj + lane, bit);
           }
         }
-        if (has_output && out_scatter) {
+        if (has_output && planes && out_scatter) {   // (few classes: the grouped adds below are cheaper)
+          uint32_t* const pl = cpl + k0 * kPl;
+          uint32_t carry = kind == RK_OUTPUT ? f : 0u;
+          for (int b = 0; b < kCntPlanes && carry; ++b) {   // ripple-carry add of one per fired sample
+            const uint32_t x = pl[b * 512];
+            pl[b * 512] = x ^ carry;
+            carry &= x;
+          }
+          if (kind == RK_OUTPUT && (last || (it + 1) % 255 == 0)) {
+            uint32_t v[kCntPlanes];
+#pragma unroll
+            for (int b = 0; b < kCntPlanes; ++b) {
+              v[b] = pl[b * 512];
+              pl[b * 512] = 0u;
+            }
+            for (int i = 0; i < 32; ++i) {
+              int cnt = 0;
+#pragma unroll
+              for (int b = 0; b < kCntPlanes; ++b) cnt |= (int)((v[b] >> i) & 1u) << b;
+              if (cnt) atomicAdd(p.counts + (size_t)(sj + i) * p.C + cls, cnt);
+            }
+          }
+        } else if (has_output && out_scatter) {
           // a6 output bus, many classes in the warp (e.g. VMM: one class per
           // neuron): each lane adds its own fired samples; the lanes' classes
           // are neighbouring words of one counts row, so a warp's add touches
@@ -978,7 +1014,9 @@ cudaError_t launch_tc_multi(ranc_ctx* ctx, TickParams p, int64_t num_ticks) {
   const int64_t total = (int64_t)ctx->G_loc * ((ctx->S + NT - 1) / NT);
   p.pot_items = total <= ctx->num_sms ? 1 : 2;
   const int grid = (int)((total + p.pot_items - 1) / p.pot_items);   // contiguous items: mostly the same core
-  const size_t smem = tc_layout(n.Npad, n.Kp, n.W, n.WIp, n.rmax, false, p.pot_items).total;
+  // bit-sliced output counters when the network has an output bus and they fit
+  p.out_planes = n.any_output && tc_layout(n.Npad, n.Kp, n.W, n.WIp, n.rmax, false, p.pot_items, true).total <= 227 * 1024;
+  const size_t smem = tc_layout(n.Npad, n.Kp, n.W, n.WIp, n.rmax, false, p.pot_items, p.out_planes).total;
   static const bool dbg = getenv("RANC_DEBUG_TIMELINE_MULTI") != nullptr;
   if (dbg && !ctx->d_dbg.p) dev_alloc(ctx, &ctx->d_dbg, kDbg * 8);
   p.dbg = dbg ? (unsigned long long*)ctx->d_dbg.p : nullptr;
