@@ -28,6 +28,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #include <string>
 #include <vector>
 
@@ -41,6 +43,16 @@ __host__ __device__ inline uint32_t route_kind(uint32_t x) { return x & 3u; }
 __host__ __device__ inline uint32_t route_lin(uint32_t x) { return (x >> 2) & 1u; }
 __host__ __device__ inline uint32_t route_delay(uint32_t x) { return (x >> 3) & 31u; }
 __host__ __device__ inline uint32_t route_axon(uint32_t x) { return (x >> 8) & 0x7FFu; }
+
+// Function attributes (cudaFuncSetAttribute) are per device: true the first
+// time `mask` sees the current device (contexts on several GPUs in one
+// process each configure their device's copy of a kernel).
+inline bool first_use_on_device(std::atomic<uint64_t>& mask) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  return !(mask.fetch_or(bit) & bit);
+}
 
 struct TickParams {
   int32_t G, S, N, Npad, A, W, E, Wn, C, T_in, WI, ST;

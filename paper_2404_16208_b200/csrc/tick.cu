@@ -463,11 +463,9 @@ __global__ void transpose_lines_kernel(const uint32_t* __restrict__ in, uint32_t
 
 template <int E>
 cudaError_t launch_one(const TickParams& p, dim3 grid, size_t smem, cudaStream_t st) {
-  static bool configured = false;
-  if (!configured) {
+  static std::atomic<uint64_t> configured{0};
+  if (first_use_on_device(configured))
     cudaFuncSetAttribute(tick_popc_kernel<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    configured = true;
-  }
   tick_popc_kernel<E><<<grid, kThreads, smem, st>>>(p);
   return cudaGetLastError();
 }

@@ -1039,8 +1039,8 @@ cudaError_t launch_tick_tc(ranc_ctx* ctx, TickParams p) {
   const int64_t total = (int64_t)ctx->G_loc * ((ctx->S + NT - 1) / NT);
   const int grid = (int)std::min<int64_t>(total, ctx->num_sms);
   const size_t smem = tc_smem_bytes(n);
-  static bool configured = false;
-  if (!configured) {
+  static std::atomic<uint64_t> configured{0};
+  if (first_use_on_device(configured)) {
     const void* fns[] = {(const void*)tick_tc_kernel<false, false, false, false>,
                          (const void*)tick_tc_kernel<false, true, false, false>,
                          (const void*)tick_tc_kernel<false, false, true, false>,
@@ -1048,7 +1048,6 @@ cudaError_t launch_tick_tc(ranc_ctx* ctx, TickParams p) {
                          (const void*)tick_tc_kernel<false, false, false, true>,
                          (const void*)tick_tc_kernel<false, false, true, true>};
     for (const void* f : fns) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    configured = true;
   }
   static const bool dbg_env = getenv("RANC_DEBUG_TIMELINE") != nullptr;
   const bool dbg = dbg_env && !n.tc_wide;
