@@ -630,6 +630,16 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       const bool pf = load && k0 + 1 < nwork;
       const uint4* nsrc = dst + tile_stride;
       const long long tw0 = dbg_on ? clock64() : 0;
+      // a new core's neuron parameters are requested before the accumulator
+      // wait, so their latency hides behind it (one tile per core, config 5)
+      short4 prm = make_short4(0, 0, 0, 0);
+      uint2 rt = make_uint2(0u, 0u);
+      int ini = 0;
+      if (active && c != prev_core) {
+        prm = p.prm[(size_t)c * Np + n];
+        rt = p.route[(size_t)c * Np + n];
+        ini = p.init[(size_t)c * Np + n];
+      }
       // one warp per lane quarter polls the accumulator barrier; the other
       // three wait on the quarter's named barrier (no issue slots spent)
       // back-off polling (measured best against the suspend-hint wait, a plain
@@ -641,10 +651,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       tc::fence_after();
       if (active) {
         if (c != prev_core) {
-          const short4 prm = p.prm[(size_t)c * Np + n];
-          const uint2 rt = p.route[(size_t)c * Np + n];
           leak = prm.x; pth = prm.y; nth = prm.z; rst = prm.w;
-          init = p.init[(size_t)c * Np + n];
+          init = ini;
           if (p.fresh && first) {
             // first tick after a reset: the pass inputs are the initial
             // potentials; pbuf is not refilled while this core's tiles run
