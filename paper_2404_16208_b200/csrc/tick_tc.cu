@@ -80,12 +80,15 @@ struct TcLayout {
 // [-128,127]); the two folded operands double the weight buffer and the
 // spike pipeline keeps 2 stages (NS_WIDE) to stay inside 227 KB
 constexpr int NS_WIDE = 2;
+// multi-tick launch: 3 spike stages (its ticks are a latency chain; the
+// freed 20 KB hold the bit-sliced output counters of two items)
+constexpr int NS_MULTI = 3;
 // pot_items: potential tiles kept on chip (multi-tick launch with up to two
 // work items per CTA: one region each)
 // cnt_planes: per-thread bit-sliced output-bus counters (multi-tick launch)
 constexpr int kCntPlanes = 8;   // counts < 256 between flushes
 __host__ __device__ inline TcLayout tc_layout(int Np, int Kp, int W, int WIp, int rmax, bool wide, int pot_items = 1,
-                                              bool cnt_planes = false) {
+                                              bool cnt_planes = false, bool multi = false) {
   TcLayout L;
   L.w = 1024;
   uint32_t o = L.w + (uint32_t)Np * Kp * (wide ? 2u : 1u);
@@ -107,7 +110,7 @@ __host__ __device__ inline TcLayout tc_layout(int Np, int Kp, int W, int WIp, in
   q = (q + 15) & ~15u;
   L.lines = q; q += (uint32_t)NT * (WIp > W ? WIp : W) * 4;  // input line rows or decoded words (TMA)
   L.stage_bytes = (q + 1023) & ~1023u;
-  L.total = L.stage + (wide ? NS_WIDE : NS) * L.stage_bytes;
+  L.total = L.stage + (wide ? NS_WIDE : multi ? NS_MULTI : NS) * L.stage_bytes;
   return L;
 }
 
@@ -215,8 +218,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + 8 * NBARS);
   const int Np = p.Npad, Kp = p.Kp, W = p.W, WIp = p.WIp;
-  const TcLayout L = tc_layout(Np, Kp, W, WIp, p.rmax, kWide, kMulti ? p.pot_items : 1, kMulti && p.out_planes);
-  constexpr int NS = kWide ? NS_WIDE : ranc::NS;   // spike stages in use
+  const TcLayout L = tc_layout(Np, Kp, W, WIp, p.rmax, kWide, kMulti ? p.pot_items : 1, kMulti && p.out_planes, kMulti);
+  constexpr int NS = kWide ? NS_WIDE : kMulti ? NS_MULTI : ranc::NS;   // spike stages in use
   uint8_t* w_s = smem + L.w;
   const int Mh = Np >> 7;
   const int nT = (p.S + NT - 1) / NT;
@@ -979,7 +982,8 @@ bool tc_multi_eligible(const ranc_ctx* ctx, int64_t num_ticks) {
   if (total <= ctx->num_sms) return true;   // one work item per CTA, one CTA per SM (cooperative launch)
   // two work items per CTA: both potential tiles stay in shared memory
   const Compiled& n = ctx->net;
-  return total <= 2 * (int64_t)ctx->num_sms && tc_layout(n.Npad, n.Kp, n.W, n.WIp, n.rmax, false, 2).total <= 227 * 1024;
+  return total <= 2 * (int64_t)ctx->num_sms &&
+         tc_layout(n.Npad, n.Kp, n.W, n.WIp, n.rmax, false, 2, false, true).total <= 227 * 1024;
 }
 
 // all ticks of a ranc_run_ticks call in one cooperative launch (small
@@ -1023,8 +1027,9 @@ cudaError_t launch_tc_multi(ranc_ctx* ctx, TickParams p, int64_t num_ticks) {
   p.pot_items = total <= ctx->num_sms ? 1 : 2;
   const int grid = (int)((total + p.pot_items - 1) / p.pot_items);   // contiguous items: mostly the same core
   // bit-sliced output counters when the network has an output bus and they fit
-  p.out_planes = n.any_output && tc_layout(n.Npad, n.Kp, n.W, n.WIp, n.rmax, false, p.pot_items, true).total <= 227 * 1024;
-  const size_t smem = tc_layout(n.Npad, n.Kp, n.W, n.WIp, n.rmax, false, p.pot_items, p.out_planes).total;
+  p.out_planes =
+      n.any_output && tc_layout(n.Npad, n.Kp, n.W, n.WIp, n.rmax, false, p.pot_items, true, true).total <= 227 * 1024;
+  const size_t smem = tc_layout(n.Npad, n.Kp, n.W, n.WIp, n.rmax, false, p.pot_items, p.out_planes, true).total;
   static const bool dbg = getenv("RANC_DEBUG_TIMELINE_MULTI") != nullptr;
   if (dbg && !ctx->d_dbg.p) dev_alloc(ctx, &ctx->d_dbg, kDbg * 8);
   p.dbg = dbg ? (unsigned long long*)ctx->d_dbg.p : nullptr;
