@@ -416,12 +416,34 @@ def run_ours(args, rank, world, local):
         dist.destroy_process_group()
 
 
+def _free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def relaunch_under_torchrun(args):
+    """`python bench.py --gpus N` outside torchrun: start the N ranks (one
+    process per GPU) with torch.distributed.run on this node and return its
+    exit code."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
     rank, world, local = dist_env()
     if args.impl == "reference":
-        run_reference(args, rank, world)
+        run_reference(args, rank, max(world, args.gpus))
         return
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(relaunch_under_torchrun(args))
+    if world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU")
     run_ours(args, rank, world, local)
 
 

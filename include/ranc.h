@@ -168,7 +168,9 @@ ranc_status ranc_read_trace(ranc_ctx* ctx, uint32_t kind, void* buf, size_t byte
 
 /* Runtime plumbing.  ranc_set_stream: use this cudaStream_t for all work
  * (e.g. torch.cuda.current_stream().cuda_stream); NULL restores the context's
- * own stream.  ranc_set_allocator: device allocations made from now on use
+ * own stream.  Switching synchronises the previous stream first, so work and
+ * stream-ordered allocations queued there never race the new stream.  Buffers
+ * of a user allocator are released only after the context stream has drained.  ranc_set_allocator: device allocations made from now on use
  * alloc(bytes, user) / dealloc(ptr, user) (e.g. the torch caching allocator);
  * must be called before ranc_load_inputs. */
 ranc_status ranc_set_stream(ranc_ctx* ctx, void* cuda_stream);
@@ -208,6 +210,13 @@ ranc_status ranc_set_allocator(ranc_ctx* ctx, void* (*alloc)(size_t, void*),
  * of one route hit one 128-byte line).  Takes effect at the next
  * ranc_load_inputs / ranc_reset_state.  Results are identical either way. */
 #define RANC_OPT_RING_LAYOUT 5
+/* RANC_OPT_DEBUG_FAULT (mutation tests only, "deliberately
+ * fault-injected parallel build (skip barrier) -> FAIL with located
+ * divergence"; CHANGES RESULTS): 0 (default) none; 1 the cooperative
+ * multi-tick launches skip their per-tick grid barrier (the tick barrier a7,
+ * P:70); 2 every route of delay >= 2 delivers one tick early (a wrong
+ * scheduler offset).  Parity tests must fail with either set. */
+#define RANC_OPT_DEBUG_FAULT 6
 ranc_status ranc_set_option(ranc_ctx* ctx, int option, int64_t value);
 
 /* Introspection of the compiled network and of the last run. */
@@ -246,16 +255,38 @@ ranc_status ranc_get_info(const ranc_ctx* ctx, ranc_info* info);
  *     ranc_load_inputs.  The readers (potentials, pending, outputs, trace)
  *     then cover the local cores only ([S][G_local]..., local output counts);
  *     ranc_get_info reports core_lo / cores_local.
- * ranc_gather_outputs: every rank calls it.  Sample mode: `root` receives the
- * class counts of all ranks concatenated in rank order ([sum S_local][C]).
- * Core mode: `root` receives the element-wise sum ([S][C]).  n is checked on
- * root only.  Synchronises.  Errors: RANC_E_NCCL, RANC_E_STATE, RANC_E_SIZE. */
+ * ranc_gather_outputs: every rank calls it, with the same n.  Sample mode:
+ * the ranks hold the contiguous shards of S_total = n / C samples (sizes
+ * differ by at most one, lower ranks first: rank r owns [r*b + min(r, m),
+ * ...) with b = S_total / world, m = S_total % world, and its
+ * ranc_inputs_desc.first_sample says so); every rank pads its counts to
+ * ceil(S_total / world) rows and ONE ncclGather delivers them to `root`, which
+ * receives the class counts of all samples in order ([S_total][C]) in
+ * counts_global (may be NULL off-root).  A rank whose shard differs returns
+ * RANC_E_SIZE naming both ranges.  Core mode: n = S*C; `root` receives the
+ * element-wise sum ([S][C]) of one ncclReduce.  Synchronises.
+ * Errors: RANC_E_NCCL, RANC_E_STATE, RANC_E_SIZE, RANC_E_ARG. */
 #define RANC_SHARD_SAMPLES 0
 #define RANC_SHARD_CORES 1
 ranc_status ranc_comm_init(ranc_ctx* ctx, const void* nccl_unique_id, int world, int rank, int mode);
 ranc_status ranc_gather_outputs(ranc_ctx* ctx, int32_t* counts_global, size_t n, int root);
 /* Fill a 128-byte buffer with a fresh ncclUniqueId (call on one rank). */
 ranc_status ranc_comm_unique_id(void* out128);
+
+/* Host-only planner of RANC_SHARD_CORES (no device needed; the same code
+ * ranc_comm_init runs): validates and compiles `net`, then reports rank
+ * `rank`'s band of cores [*core_lo, *core_lo + *cores_local) of `world` and
+ * its per-tick exchange lists.  send_counts[p] / recv_counts[p] (caller
+ * arrays of `world` entries) receive the list lengths; send_cores receives,
+ * peer by peer, the LOCAL ids of this rank's cores with a route into peer
+ * p's band (their fired bits are sent to p every tick, Alg. 1 l.15-20,
+ * P:102-110), recv_cores the GLOBAL ids of peer p's cores with a route into
+ * this band.  Capacities are in entries; too small -> RANC_E_SIZE (counts
+ * still written).  Errors as ranc_load_network, message via
+ * ranc_last_error(NULL). */
+ranc_status ranc_plan_core_shards(const ranc_network_desc* net, int world, int rank, int32_t* core_lo,
+                                  int32_t* cores_local, int32_t* send_counts, int32_t* recv_counts,
+                                  int32_t* send_cores, size_t send_cap, int32_t* recv_cores, size_t recv_cap);
 
 /* Loopback group: n contexts of this process (same device, same network)
  * act as the n ranks of a core-sharded run, exchanging spikes with device

@@ -22,6 +22,7 @@ OPT_INPUT_DECODE = 2
 OPT_KERNEL = 3
 OPT_STREAM = 4
 OPT_RING_LAYOUT = 5
+OPT_DEBUG_FAULT = 6   # mutation tests only (changes results)
 SHARD_SAMPLES = 0
 SHARD_CORES = 1
 
@@ -65,7 +66,7 @@ EXPORTS = [
     "ranc_read_outputs", "ranc_read_potentials", "ranc_read_pending", "ranc_set_trace", "ranc_read_trace",
     "ranc_set_stream", "ranc_set_allocator", "ranc_set_option", "ranc_get_info", "ranc_comm_init",
     "ranc_gather_outputs", "ranc_comm_unique_id", "ranc_comm_init_loopback", "ranc_run_ticks_loopback",
-    "ranc_last_error", "ranc_destroy",
+    "ranc_plan_core_shards", "ranc_last_error", "ranc_destroy",
 ]
 
 _lib = None
@@ -101,6 +102,9 @@ def load(path: str = LIB_PATH):
     L.ranc_comm_unique_id.argtypes = [vp]
     L.ranc_comm_init_loopback.argtypes = [C.POINTER(vp), C.c_int, C.c_int]
     L.ranc_run_ticks_loopback.argtypes = [C.POINTER(vp), C.c_int, C.c_int64]
+    i32p = C.POINTER(C.c_int32)
+    L.ranc_plan_core_shards.argtypes = [C.POINTER(NetworkDesc), C.c_int, C.c_int, i32p, i32p, i32p, i32p, i32p,
+                                        C.c_size_t, i32p, C.c_size_t]
     L.ranc_last_error.argtypes = [vp]
     L.ranc_last_error.restype = C.c_char_p
     L.ranc_destroy.argtypes = [vp]

@@ -19,6 +19,8 @@ thread_local std::string g_load_err;
 
 namespace ranc {
 
+void set_load_error(const std::string& m) { g_load_err = m; }
+
 ranc_status set_cuda_error(ranc_ctx* ctx, cudaError_t e, const char* where) {
   std::string m = std::string(where) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
   if (ctx) ctx->err = m;
@@ -50,9 +52,17 @@ ranc_status dev_alloc(ranc_ctx* ctx, DevBuf* b, size_t bytes) {
 void dev_free(ranc_ctx* ctx, DevBuf* b) {
   if (!b->p) return;
   // a buffer is released by the allocator that made it (network buffers are
-  // allocated before ranc_set_allocator may be called)
-  if (b->user) ctx->user_free(b->p, ctx->user);
-  else cudaFreeAsync(b->p, ctx->stream);
+  // allocated before ranc_set_allocator may be called).  A user allocator
+  // (e.g. torch's caching allocator) may hand the block to someone else at
+  // once, so the context's queued work that can still touch it must finish
+  // first; cudaFreeAsync is stream-ordered on the context stream, which every
+  // user of the buffer ran on (ranc_set_stream drains the previous stream).
+  if (b->user) {
+    cudaStreamSynchronize(ctx->stream);
+    ctx->user_free(b->p, ctx->user);
+  } else {
+    cudaFreeAsync(b->p, ctx->stream);
+  }
   ctx->device_bytes -= (int64_t)b->bytes;
   b->p = nullptr;
   b->bytes = 0;
@@ -100,7 +110,7 @@ void free_all(ranc_ctx* ctx) {
                     &ctx->d_nruns, &ctx->d_wflags_tc, &ctx->d_incoming, &ctx->d_word_runs, &ctx->d_pot, &ctx->d_ring, &ctx->d_counts, &ctx->d_lines,
                     &ctx->d_stage, &ctx->d_raster, &ctx->d_fired, &ctx->d_exports, &ctx->d_send, &ctx->d_recv,
                     &ctx->d_send_list, &ctx->d_recv_list, &ctx->d_dbg, &ctx->d_inw, &ctx->d_inslot,
-                    &ctx->d_slot_core, &ctx->d_spkin, &ctx->d_digest, &ctx->d_perm_dig};
+                    &ctx->d_slot_core, &ctx->d_spkin, &ctx->d_digest, &ctx->d_perm_dig, &ctx->d_gsend, &ctx->d_grecv};
   for (DevBuf* b : bufs) dev_free(ctx, b);
 }
 
@@ -396,8 +406,19 @@ ranc_status ranc_run_ticks_loopback(ranc_ctx* const* ctxs, int n, int64_t num_ti
       return RANC_E_STATE;
     }
   }
-  // one stream for the whole group (the exchange orders the members)
+  // one stream for the whole group (the exchange orders the members); work
+  // queued on the members' own streams (allocations, raster clears, input
+  // decode, ring / count resets) is ordered before it with events
   std::vector<cudaStream_t> saved(n);
+  for (int i = 1; i < n; ++i)
+    if (ctxs[i]->stream != ctxs[0]->stream) {
+      cudaEvent_t ev;
+      cudaError_t e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventRecord(ev, ctxs[i]->stream);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(ctxs[0]->stream, ev, 0);
+      if (e == cudaSuccess) e = cudaEventDestroy(ev);
+      if (e != cudaSuccess) return set_cuda_error(ctxs[i], e, "ranc_run_ticks_loopback (stream ordering)");
+    }
   for (int i = 0; i < n; ++i) {
     saved[i] = ctxs[i]->stream;
     ctxs[i]->stream = ctxs[0]->stream;
@@ -598,7 +619,14 @@ ranc_status ranc_read_trace(ranc_ctx* ctx, uint32_t kind, void* buf, size_t byte
 
 ranc_status ranc_set_stream(ranc_ctx* ctx, void* cuda_stream) {
   TRY(check_ctx(ctx));
-  ctx->stream = cuda_stream ? (cudaStream_t)cuda_stream : ctx->own_stream;
+  const cudaStream_t next = cuda_stream ? (cudaStream_t)cuda_stream : ctx->own_stream;
+  if (next != ctx->stream) {
+    // everything queued on the old stream (uploads, input decode, stream-
+    // ordered allocations and frees) completes before work on the new one
+    CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+    CK(cudaStreamSynchronize(ctx->stream), "ranc_set_stream (draining the previous stream)");
+  }
+  ctx->stream = next;
   return RANC_OK;
 }
 
@@ -658,6 +686,26 @@ ranc_status ranc_set_option(ranc_ctx* ctx, int option, int64_t value) {
       }
       ctx->ring_layout = (int32_t)value;  // takes effect at the next ranc_load_inputs / ranc_reset_state
       return RANC_OK;
+    case RANC_OPT_DEBUG_FAULT: {
+      if (value < 0 || value > 2) {
+        ctx->err = "debug fault must be 0 (none), 1 (skip the multi-tick grid barrier) or 2 (routes one tick early)";
+        return RANC_E_ARG;
+      }
+      ctx->fault = (int32_t)value;
+      // fault 2: every route of delay >= 2 delivers one tick early (a wrong
+      // scheduler offset); the compiled route words are re-uploaded
+      const Compiled& c = ctx->net;
+      CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+      auto early = [&](std::vector<uint2> v) {
+        if (value == 2)
+          for (uint2& r : v)
+            if (route_kind(r.x) == RK_ROUTE && route_delay(r.x) >= 2) r.x -= 1u << 3;
+        return v;
+      };
+      TRY(upload(ctx, &ctx->d_route, early(c.route)));
+      if (c.tc_ok) TRY(upload(ctx, &ctx->d_route_tc, early(c.route_tc)));
+      return sync(ctx, "ranc_set_option");
+    }
     default:
       ctx->err = "unknown option";
       return RANC_E_ARG;

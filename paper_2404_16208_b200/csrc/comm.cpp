@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -40,17 +41,16 @@ ranc_status nccl_err(ranc_ctx* ctx, ncclResult_t r, const char* where) {
 namespace ranc {
 
 // Row-band partition of the cores over `world` ranks and the export / import
-// lists of this rank (computed identically on every rank from the replicated
-// network).
-ranc_status setup_core_shards(ranc_ctx* ctx, int world, int rank) {
-  const Compiled& c = ctx->net;
-  if (ctx->have_inputs) {
-    ctx->err = "core-sharded communicators must be set up before ranc_load_inputs";
-    return RANC_E_STATE;
+// lists of `rank` (computed identically on every rank from the replicated
+// network; host only, so ranc_plan_core_shards can expose it without a GPU).
+ranc_status plan_core_shards(const Compiled& c, int world, int rank, CoreShardPlan* out, std::string* err) {
+  if (world < 1 || rank < 0 || rank >= world) {
+    *err = "bad world/rank (world=" + std::to_string(world) + ", rank=" + std::to_string(rank) + ")";
+    return RANC_E_ARG;
   }
   if (world > c.grid_h) {
-    ctx->err = "core-sharded mode needs at least one grid row per rank (grid_h=" + std::to_string(c.grid_h) +
-               ", world=" + std::to_string(world) + ")";
+    *err = "core-sharded mode needs at least one grid row per rank (grid_h=" + std::to_string(c.grid_h) +
+           ", world=" + std::to_string(world) + ")";
     return RANC_E_CONFIG;
   }
   auto row_lo = [&](int r) { return (int)((int64_t)r * c.grid_h / world); };
@@ -58,10 +58,10 @@ ranc_status setup_core_shards(ranc_ctx* ctx, int world, int rank) {
   for (int r = 0; r < world; ++r)
     for (int y = row_lo(r); y < row_lo(r + 1); ++y)
       for (int x = 0; x < c.grid_w; ++x) owner[y * c.grid_w + x] = r;
-  ctx->c_lo = row_lo(rank) * c.grid_w;
-  ctx->G_loc = (row_lo(rank + 1) - row_lo(rank)) * c.grid_w;
-  // needs[src core][dest rank]
-  std::vector<uint8_t> exports(c.G, 0);
+  out->c_lo = row_lo(rank) * c.grid_w;
+  out->G_loc = (row_lo(rank + 1) - row_lo(rank)) * c.grid_w;
+  // to[dest rank][src core]: some neuron of src routes to a core of dest rank
+  out->exports.assign(c.G, 0);
   std::vector<std::vector<uint8_t>> to(world, std::vector<uint8_t>(c.G, 0));
   for (int g = 0; g < c.G; ++g)
     for (int j = 0; j < c.N; ++j) {
@@ -69,25 +69,50 @@ ranc_status setup_core_shards(ranc_ctx* ctx, int world, int rank) {
       if (route_kind(rt.x) != RK_ROUTE) continue;
       const int dr = owner[rt.y];
       if (dr != owner[g]) {
-        exports[g] = 1;
+        out->exports[g] = 1;
         to[dr][g] = 1;
       }
     }
-  ctx->send_cores.assign(world, {});
-  ctx->recv_cores.assign(world, {});
+  out->send_cores.assign(world, {});
+  out->recv_cores.assign(world, {});
   for (int p = 0; p < world; ++p) {
     if (p == rank) continue;
     for (int g = 0; g < c.G; ++g) {
-      if (owner[g] == rank && to[p][g]) ctx->send_cores[p].push_back(g - ctx->c_lo);   // local id
-      if (owner[g] == p && to[rank][g]) ctx->recv_cores[p].push_back(g);              // global id
+      if (owner[g] == rank && to[p][g]) out->send_cores[p].push_back(g - out->c_lo);   // local id
+      if (owner[g] == p && to[rank][g]) out->recv_cores[p].push_back(g);              // global id
     }
   }
-  ranc_status s = dev_alloc(ctx, &ctx->d_exports, (size_t)c.G);
+  return RANC_OK;
+}
+
+ranc_status setup_core_shards(ranc_ctx* ctx, int world, int rank) {
+  const Compiled& c = ctx->net;
+  if (ctx->have_inputs) {
+    ctx->err = "core-sharded communicators must be set up before ranc_load_inputs";
+    return RANC_E_STATE;
+  }
+  CoreShardPlan plan;
+  ranc_status s = plan_core_shards(c, world, rank, &plan, &ctx->err);
   if (s) return s;
-  cudaError_t e = cudaMemcpyAsync(ctx->d_exports.p, exports.data(), c.G, cudaMemcpyHostToDevice, ctx->stream);
+  s = dev_alloc(ctx, &ctx->d_exports, (size_t)c.G);
+  if (s) return s;
+  cudaError_t e = cudaMemcpyAsync(ctx->d_exports.p, plan.exports.data(), c.G, cudaMemcpyHostToDevice, ctx->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
   if (e != cudaSuccess) return set_cuda_error(ctx, e, "setup_core_shards");
+  ctx->c_lo = plan.c_lo;
+  ctx->G_loc = plan.G_loc;
+  ctx->send_cores = std::move(plan.send_cores);
+  ctx->recv_cores = std::move(plan.recv_cores);
   return RANC_OK;
+}
+
+// undo setup_core_shards (a failed group set-up)
+void clear_core_shards(ranc_ctx* ctx) {
+  ctx->c_lo = 0;
+  ctx->G_loc = ctx->net.G;
+  ctx->send_cores.clear();
+  ctx->recv_cores.clear();
+  dev_free(ctx, &ctx->d_exports);
 }
 
 // Size the exchange buffers for S samples (called by ranc_load_inputs).
@@ -251,50 +276,59 @@ ranc_status ranc_gather_outputs(ranc_ctx* ctx, int32_t* counts_global, size_t n,
     if (e != cudaSuccess) return set_cuda_error(ctx, e, "reduce");
     return RANC_OK;
   }
-  // 1) every rank's sample count
-  DevBuf sizes;
-  {
-    ranc_status s = dev_alloc(ctx, &sizes, sizeof(int64_t) * (ctx->world + 1));
-    if (s) return s;
-  }
-  int64_t mine = ctx->S;
-  cudaMemcpyAsync((int64_t*)sizes.p + ctx->world, &mine, 8, cudaMemcpyHostToDevice, ctx->stream);
-  NK(ncclAllGather((int64_t*)sizes.p + ctx->world, sizes.p, 1, ncclInt64, comm, ctx->stream), "ncclAllGather");
-  std::vector<int64_t> hs(ctx->world);
-  cudaMemcpyAsync(hs.data(), sizes.p, 8 * ctx->world, cudaMemcpyDeviceToHost, ctx->stream);
-  cudaError_t e = cudaStreamSynchronize(ctx->stream);
-  dev_free(ctx, &sizes);
-  if (e != cudaSuccess) return set_cuda_error(ctx, e, "gather sizes");
-  int64_t total = 0;
-  for (int64_t v : hs) total += v;
-  if (ctx->rank == root && n != (size_t)(total * C)) {
-    ctx->err = "counts_global has " + std::to_string(n) + " elements, need (sum S_local)*C = " +
-               std::to_string(total * C);
+  // Sample mode: the shards are the contiguous partition of S_total = n / C
+  // samples (sizes differ by at most one, lower ranks first; the binding's
+  // shard_range), so every rank knows every shard size without a message.
+  // Each rank pads its counts to Smax rows and ONE ncclGather collects the
+  // [world][Smax][C] block on the root, which copies the S_r rows of each
+  // rank to the host.
+  if (C == 0) return RANC_OK;
+  if (n % (size_t)C) {
+    ctx->err = "counts_global has " + std::to_string(n) + " elements, not a multiple of C = " + std::to_string(C);
     return RANC_E_SIZE;
   }
-  if (C == 0) return RANC_OK;
-  // 2) point-to-point gather into a device buffer on the root
-  DevBuf all;
-  if (ctx->rank == root) {
-    ranc_status s = dev_alloc(ctx, &all, (size_t)total * C * 4);
+  const int64_t S_total = (int64_t)(n / C);
+  const int world = ctx->world;
+  auto shard_lo = [&](int r) {
+    const int64_t base = S_total / world, rem = S_total % world;
+    return r * base + std::min<int64_t>(r, rem);
+  };
+  const int64_t mine = shard_lo(ctx->rank + 1) - shard_lo(ctx->rank);
+  if (ctx->S != mine || ctx->first_sample != shard_lo(ctx->rank)) {
+    ctx->err = "rank " + std::to_string(ctx->rank) + " holds samples [" + std::to_string(ctx->first_sample) + ", " +
+               std::to_string(ctx->first_sample + ctx->S) + "), but the contiguous shard of " +
+               std::to_string(S_total) + " samples over " + std::to_string(world) + " ranks is [" +
+               std::to_string(shard_lo(ctx->rank)) + ", " + std::to_string(shard_lo(ctx->rank + 1)) + ")";
+    return RANC_E_SIZE;
+  }
+  if (ctx->rank == root && !counts_global) return RANC_E_ARG;
+  const int64_t Smax = (S_total + world - 1) / world;
+  const size_t chunk = (size_t)Smax * C;   // int32 elements per rank
+  if (ctx->d_gsend.bytes != chunk * 4) {
+    ranc_status s = dev_alloc(ctx, &ctx->d_gsend, chunk * 4);
     if (s) return s;
   }
-  NK(ncclGroupStart(), "ncclGroupStart");
-  if (ctx->rank == root) {
-    int64_t off = 0;
-    for (int r = 0; r < ctx->world; ++r) {
-      NK(ncclRecv((int32_t*)all.p + off * C, (size_t)hs[r] * C, ncclInt32, r, comm, ctx->stream), "ncclRecv");
-      off += hs[r];
+  if (ctx->rank == root && ctx->d_grecv.bytes != chunk * world * 4) {
+    ranc_status s = dev_alloc(ctx, &ctx->d_grecv, chunk * world * 4);
+    if (s) return s;
+  }
+  cudaError_t e = cudaMemcpyAsync(ctx->d_gsend.p, ctx->d_counts.p, (size_t)ctx->S * C * 4, cudaMemcpyDeviceToDevice,
+                                  ctx->stream);
+  if (e == cudaSuccess && (size_t)ctx->S * C < chunk)
+    e = cudaMemsetAsync((int32_t*)ctx->d_gsend.p + (size_t)ctx->S * C, 0, (chunk - (size_t)ctx->S * C) * 4,
+                        ctx->stream);
+  if (e != cudaSuccess) return set_cuda_error(ctx, e, "gather staging");
+  NK(ncclGather(ctx->d_gsend.p, ctx->rank == root ? ctx->d_grecv.p : nullptr, chunk, ncclInt32, root, comm,
+                ctx->stream),
+     "ncclGather");
+  if (ctx->rank == root)
+    for (int r = 0; r < world && e == cudaSuccess; ++r) {
+      const int64_t lo = shard_lo(r), rows = shard_lo(r + 1) - lo;
+      if (rows)
+        e = cudaMemcpyAsync(counts_global + (size_t)lo * C, (const int32_t*)ctx->d_grecv.p + (size_t)r * chunk,
+                            (size_t)rows * C * 4, cudaMemcpyDeviceToHost, ctx->stream);
     }
-  }
-  NK(ncclSend(ctx->d_counts.p, (size_t)ctx->S * C, ncclInt32, root, comm, ctx->stream), "ncclSend");
-  NK(ncclGroupEnd(), "ncclGroupEnd");
-  if (ctx->rank == root) {
-    if (!counts_global) return RANC_E_ARG;
-    cudaMemcpyAsync(counts_global, all.p, (size_t)total * C * 4, cudaMemcpyDeviceToHost, ctx->stream);
-  }
-  e = cudaStreamSynchronize(ctx->stream);
-  dev_free(ctx, &all);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
   if (e != cudaSuccess) return set_cuda_error(ctx, e, "gather");
   return RANC_OK;
 }
@@ -317,17 +351,62 @@ ranc_status ranc_comm_init_loopback(ranc_ctx* const* ctxs, int n, int mode) {
       return RANC_E_ARG;
     }
   }
+  // set every member up before any of them joins the group; on failure the
+  // members set up so far are rolled back and nothing is left half-sharded
+  for (int i = 0; i < n; ++i) {
+    ranc_status st = setup_core_shards(ctxs[i], n, i);
+    if (st) {
+      if (i > 0) ctxs[0]->err = ctxs[i]->err;
+      for (int j = 0; j < i; ++j) clear_core_shards(ctxs[j]);
+      return st;
+    }
+  }
   ranc_group* g = new ranc_group();
   g->ctxs.assign(ctxs, ctxs + n);
   for (int i = 0; i < n; ++i) {
-    ranc_status st = setup_core_shards(ctxs[i], n, i);
-    if (st) return st;
     ctxs[i]->world = n;
     ctxs[i]->rank = i;
     ctxs[i]->shard_mode = RANC_SHARD_CORES;
     ctxs[i]->group = g;
   }
   return RANC_OK;
+}
+
+ranc_status ranc_plan_core_shards(const ranc_network_desc* net, int world, int rank, int32_t* core_lo,
+                                  int32_t* cores_local, int32_t* send_counts, int32_t* recv_counts,
+                                  int32_t* send_cores, size_t send_cap, int32_t* recv_cores, size_t recv_cap) {
+  static thread_local std::string perr;
+  if (!net || !core_lo || !cores_local || !send_counts || !recv_counts) return RANC_E_ARG;
+  Compiled c;
+  std::string err;
+  ranc_status s = validate_and_compile(net, &c, &err);
+  if (s == RANC_OK) {
+    CoreShardPlan plan;
+    s = plan_core_shards(c, world, rank, &plan, &err);
+    if (s == RANC_OK) {
+      size_t ns = 0, nr = 0;
+      for (int p = 0; p < world; ++p) {
+        send_counts[p] = (int32_t)plan.send_cores[p].size();
+        recv_counts[p] = (int32_t)plan.recv_cores[p].size();
+        ns += plan.send_cores[p].size();
+        nr += plan.recv_cores[p].size();
+      }
+      *core_lo = plan.c_lo;
+      *cores_local = plan.G_loc;
+      if (ns > send_cap || nr > recv_cap || (ns && !send_cores) || (nr && !recv_cores)) {
+        err = "list buffers too small: need " + std::to_string(ns) + " send and " + std::to_string(nr) +
+              " receive entries";
+        s = RANC_E_SIZE;
+      } else {
+        for (int p = 0; p < world; ++p) {
+          for (int32_t v : plan.send_cores[p]) *send_cores++ = v;
+          for (int32_t v : plan.recv_cores[p]) *recv_cores++ = v;
+        }
+      }
+    }
+  }
+  set_load_error(err);
+  return s;
 }
 
 void ranc_comm_destroy_internal(ranc_ctx* ctx) {

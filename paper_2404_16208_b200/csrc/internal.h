@@ -67,6 +67,8 @@ struct TickParams {
   int32_t pot_items;        // multi-tick tensor-core launch: work items (potential tiles) per CTA, 1 or 2
   int32_t out_planes;       // multi-tick tensor-core launch: bit-sliced per-thread output counters in shared memory
   int32_t Kp;               // tensor-core path: K bytes per operand row (= 32*W)
+  int32_t fault;            // RANC_OPT_DEBUG_FAULT (mutation tests): 1 = skip the grid barrier of
+                            // cooperative multi-tick launches
   int64_t t;                // tick being executed
   int64_t raster_t0;        // first tick of the raster buffer
   const uint8_t* wfold;     // tensor-core path: [G][Npad*Kp] canonical-layout int8
@@ -189,6 +191,7 @@ struct ranc_ctx {
   std::vector<std::vector<int32_t>> send_cores, recv_cores;  // per peer: local / global core ids
   std::vector<int64_t> send_off, recv_off;                   // per peer, in u32 words
   ranc::DevBuf d_fired, d_exports, d_send, d_recv, d_send_list, d_recv_list, d_recv_peer;
+  ranc::DevBuf d_gsend, d_grecv;   // sample-sharded gather: padded shard, root's [world][Smax][C]
   int64_t n_send_words = 0, n_recv_words = 0, n_recv_rows = 0;
   int64_t exchange_bytes = 0;    // bytes sent per tick (introspection)
   ranc::DevBuf d_dbg;            // RANC_DEBUG_TIMELINE
@@ -199,6 +202,7 @@ struct ranc_ctx {
   int32_t perm_dig_kernel = 0;   // kernel whose axon order d_perm_dig holds
   int32_t n_inslots = 0;
   bool inw_valid = false;
+  int32_t fault = 0;             // RANC_OPT_DEBUG_FAULT (mutation tests only)
 };
 
 struct ranc_group {
@@ -208,7 +212,15 @@ struct ranc_group {
 namespace ranc {
 enum { RANC_KERNEL_AUTO = 0, RANC_KERNEL_POPC = 1, RANC_KERNEL_TC = 2 };
 // comm.cpp
+struct CoreShardPlan {
+  int32_t c_lo = 0, G_loc = 0;                   // this rank's cores [c_lo, c_lo + G_loc)
+  std::vector<uint8_t> exports;                  // [G] core has a route into another rank's band
+  std::vector<std::vector<int32_t>> send_cores;  // per peer: local ids of the cores whose fired bits it needs
+  std::vector<std::vector<int32_t>> recv_cores;  // per peer: global ids of the peer's cores routing here
+};
+ranc_status plan_core_shards(const Compiled& c, int world, int rank, CoreShardPlan* out, std::string* err);
 ranc_status setup_core_shards(ranc_ctx* ctx, int world, int rank);
+void clear_core_shards(ranc_ctx* ctx);
 ranc_status alloc_exchange(ranc_ctx* ctx);
 ranc_status exchange_nccl(ranc_ctx* ctx, int64_t t);
 ranc_status exchange_loopback(ranc_group* g, int64_t t);
@@ -237,4 +249,5 @@ cudaError_t launch_stream(ranc_ctx* ctx, int64_t num_ticks);
 ranc_status dev_alloc(ranc_ctx* ctx, DevBuf* b, size_t bytes);
 void dev_free(ranc_ctx* ctx, DevBuf* b);
 ranc_status set_cuda_error(ranc_ctx* ctx, cudaError_t e, const char* where);
+void set_load_error(const std::string& m);   // the thread-local message of ranc_last_error(NULL)
 }  // namespace ranc

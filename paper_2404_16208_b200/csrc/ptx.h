@@ -108,6 +108,12 @@ __device__ __forceinline__ void cp_async_wait() {
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
+// the same for global memory: generic-proxy writes (e.g. other CTAs' ring
+// deposits, ordered before this thread by a grid barrier) become visible to
+// this thread's subsequent async-proxy reads (cp.async.bulk)
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
 
 }  // namespace ptx
 }  // namespace ranc

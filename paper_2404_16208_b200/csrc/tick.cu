@@ -272,7 +272,7 @@ __global__ void __launch_bounds__(kThreads, 1) tick_stream_kernel(TickParams p, 
       popc_tile<E, true>(p, w % p.G_loc, w / p.G_loc, smem, phase, res + j * tile_elems);
     p.fresh = 0;
     ++p.t;
-    grid.sync();
+    if (p.fault != 1) grid.sync();   // (RANC_OPT_DEBUG_FAULT 1: the mutation test's missing barrier)
   }
   int j = 0;
   for (int w = blockIdx.x; w < items; w += gridDim.x, ++j) {
@@ -396,7 +396,7 @@ __global__ void __launch_bounds__(kThreads, (E <= 12 ? 4 : (E <= 16 ? 3 : 2)))
         }
       }
     }
-    grid.sync();   // a7: tick t's deliveries are visible to tick t+1's row reads
+    if (p.fault != 1) grid.sync();   // a7: tick t's deliveries are visible to tick t+1's row reads
   }
   if (has_n)
     for (int s = 0; s < ns; ++s) p.pot[((size_t)cl * p.S + s0 + s) * p.Npad + n] = pot_s[s * p.Npad + n];
@@ -602,6 +602,7 @@ TickParams make_params(ranc_ctx* ctx) {
   p.wfold = (const uint8_t*)ctx->d_wfold.p;
   p.t = ctx->now;
   p.fresh = ctx->fresh ? 1 : 0;
+  p.fault = ctx->fault;
   return p;
 }
 

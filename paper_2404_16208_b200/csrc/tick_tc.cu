@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
   // one (core, tile) and its potentials), so its ticks need no barrier and
   // the roles' mbarrier pipelines overlap consecutive ticks.
   auto tick_barrier = [&]() {
-    if (kMulti && p.any_route) cg::this_grid().sync();
+    if (kMulti && p.any_route && p.fault != 1) cg::this_grid().sync();
   };
   // pipeline waits: sleeping (issue slots left to the working warps) in the
   // throughput kernel; spinning in the multi-tick kernel, whose ticks are a
@@ -340,6 +340,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       __syncwarp();
     }
     tick_barrier();
+    // the next tick's ring rows were written through the generic proxy
+    // (other CTAs' atomicOr deposits, this CTA's clears Rp ticks ago) and are
+    // read below with cp.async.bulk (async proxy): order the two proxies
+    // after the grid barrier (per-tick launches: the kernel boundary does)
+    if (kMulti) ptx::fence_proxy_async_global();
     }
   } else if (warp == mma_warp) {
     // ------------------------------------------------------------ MMA issuer
@@ -897,9 +902,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
 __global__ void decode_inputs_kernel(const uint32_t* __restrict__ lines, uint32_t* __restrict__ inw,
                                      const int32_t* __restrict__ slot_core, const int2* __restrict__ runs,
                                      const int32_t* __restrict__ word_runs, int S, int Sr, int W, int WIp,
-                                     int rmax, int wmajor) {
+                                     int rmax, int wmajor, int n_slots, int slot0, int t0) {
   extern __shared__ int2 dec_sm[];
-  const int slot = blockIdx.y, t = blockIdx.z, n_slots = gridDim.y;
+  const int slot = slot0 + blockIdx.y, t = t0 + blockIdx.z;
   const int c = slot_core[slot];
   int2* rs = dec_sm;
   int32_t* wr = reinterpret_cast<int32_t*>(dec_sm + rmax);
@@ -937,17 +942,25 @@ cudaError_t decode_inputs_tc(ranc_ctx* ctx) {
   const Compiled& n = ctx->net;
   const int64_t words = (int64_t)ctx->S * n.W;
   if (words == 0 || ctx->n_inslots == 0 || ctx->T_in == 0) return cudaSuccess;
-  if (words > INT32_MAX || ctx->T_in > 65535 || ctx->n_inslots > 65535) return cudaErrorInvalidValue;
+  if (words > INT32_MAX) return cudaErrorInvalidValue;
   const int threads = 256;
-  const dim3 grid((unsigned)((words + threads * 4 - 1) / (threads * 4)), (unsigned)ctx->n_inslots,
-                  (unsigned)ctx->T_in);
   const size_t smem = (size_t)n.rmax * sizeof(int2) + (size_t)n.W * sizeof(int32_t);
-  decode_inputs_kernel<<<grid, threads, smem, ctx->stream>>>(
-      (const uint32_t*)ctx->d_lines.p, (uint32_t*)ctx->d_inw.p, (const int32_t*)ctx->d_slot_core.p,
-      (const int2*)ctx->d_runs.p, (const int32_t*)ctx->d_word_runs.p, (int)ctx->S, (int)ctx->Sr, n.W, n.WIp,
-      n.rmax, ctx->ring_wmajor ? 1 : 0);
-  ctx->launches++;
-  return cudaGetLastError();
+  // grid.y / grid.z are limited to 65535: long input streams and many input
+  // slots are decoded in chunks
+  constexpr int kMaxYZ = 65535;
+  for (int t0 = 0; t0 < ctx->T_in; t0 += kMaxYZ)
+    for (int s0 = 0; s0 < ctx->n_inslots; s0 += kMaxYZ) {
+      const dim3 grid((unsigned)((words + threads * 4 - 1) / (threads * 4)),
+                      (unsigned)std::min(kMaxYZ, ctx->n_inslots - s0), (unsigned)std::min(kMaxYZ, ctx->T_in - t0));
+      decode_inputs_kernel<<<grid, threads, smem, ctx->stream>>>(
+          (const uint32_t*)ctx->d_lines.p, (uint32_t*)ctx->d_inw.p, (const int32_t*)ctx->d_slot_core.p,
+          (const int2*)ctx->d_runs.p, (const int32_t*)ctx->d_word_runs.p, (int)ctx->S, (int)ctx->Sr, n.W, n.WIp,
+          n.rmax, ctx->ring_wmajor ? 1 : 0, ctx->n_inslots, s0, t0);
+      ctx->launches++;
+      const cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) return e;
+    }
+  return cudaSuccess;
 }
 
 int tc_tile() { return NT; }

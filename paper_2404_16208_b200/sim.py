@@ -70,13 +70,17 @@ class Simulator:
         """stream: a torch.cuda.Stream, an int cudaStream_t, or None."""
         ptr = getattr(stream, "cuda_stream", stream)
         self._ck(self.lib.ranc_set_stream(self.h, C.c_void_p(ptr) if ptr else None))
+        self._stream = stream if hasattr(stream, "cuda_stream") else None
 
     def use_torch_allocator(self):
         import torch
 
         dev = self.device
+        stream = getattr(self, "_stream", None)   # blocks belong to the context's stream
 
         def _alloc(nbytes, _user):
+            if stream is not None:
+                return torch.cuda.caching_allocator_alloc(int(nbytes), device=dev, stream=stream)
             return torch.cuda.caching_allocator_alloc(int(nbytes), device=dev)
 
         def _free(ptr, _user):
@@ -217,13 +221,36 @@ class Simulator:
         _check(sims[0].lib, sims[0].lib.ranc_run_ticks_loopback(arr, len(sims), int(ticks)), sims[0].h)
 
     def gather_outputs(self, total_samples: int, root: int = 0, rank: int = 0):
-        """Sample mode: [sum S_local][C] concatenated in rank order; core mode:
-        pass total_samples = S, returns the [S][C] sum.  None off-root."""
+        """Sample mode: the [total_samples][C] counts of all ranks' contiguous
+        shards (one ncclGather); core mode: pass total_samples = S, returns the
+        [S][C] sum.  None off-root.  Every rank passes the same total."""
         C_ = int(self.net.num_classes)
-        out = np.zeros((total_samples, C_), np.int32) if rank == root else np.zeros((1,), np.int32)
-        n = out.size if rank == root else 0
-        self._ck(self.lib.ranc_gather_outputs(self.h, out.ctypes.data, n, int(root)))
-        return out if rank == root else None
+        out = np.zeros((total_samples, C_), np.int32) if rank == root else None
+        self._ck(self.lib.ranc_gather_outputs(self.h, out.ctypes.data if out is not None else None,
+                                              total_samples * C_, int(root)))
+        return out
+
+    @staticmethod
+    def plan_core_shards(net, world: int, rank: int) -> dict:
+        """Host-only core-sharded plan (ranc_plan_core_shards; no GPU needed):
+        this rank's core band and, per peer, the local ids of the cores it
+        sends fired bits of and the global ids of the peer cores it receives."""
+        lib = L.load()
+        desc, keep = make_network_desc(net)
+        i32 = C.c_int32
+        lo, gl = i32(), i32()
+        sc, rc = (i32 * world)(), (i32 * world)()
+        cap = int(net.G) * world
+        sl, rl = (i32 * max(cap, 1))(), (i32 * max(cap, 1))()
+        _check(lib, lib.ranc_plan_core_shards(C.byref(desc), int(world), int(rank), C.byref(lo), C.byref(gl), sc, rc,
+                                              sl, cap, rl, cap))
+        send, recv, a, b = [], [], 0, 0
+        for p in range(world):
+            send.append(list(sl[a:a + sc[p]]))
+            recv.append(list(rl[b:b + rc[p]]))
+            a += sc[p]
+            b += rc[p]
+        return {"core_lo": lo.value, "cores_local": gl.value, "send": send, "recv": recv}
 
     # -- lifetime -----------------------------------------------------------
     def close(self):

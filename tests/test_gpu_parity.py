@@ -581,3 +581,34 @@ def test_digest_core_sharded_shards_add_up(ranc, oracle_mod, kernel):
     for t in range(T):
         o.run(1)
         assert np.array_equal(total[t], o.digest()), f"tick {t}"
+
+
+# ---- mutation tests (a fault-injected parallel build must FAIL
+# with a located divergence; RANC_OPT_DEBUG_FAULT) -------------------------------
+
+
+@pytest.mark.parametrize("fault,variant", [(0, "tc_multi"), (1, "tc_multi"), (0, "popc_stream"), (1, "popc_stream"),
+                                           (2, "tc"), (2, "popc")])
+def test_fault_injection_is_caught(ranc, fault, variant):
+    from verify import first_divergence, verdict
+    net, inp = config2(S=130 if variant.startswith("tc") else 48)
+    T = net.meta["T"]
+    sim = ranc.Simulator(net)
+    sim.set_option(ranc.OPT_KERNEL, 2 if variant.startswith("tc") else 1)
+    sim.set_option(ranc.OPT_STREAM, 2 if variant.endswith(("multi", "stream")) else 1)
+    sim.set_option(ranc.OPT_DEBUG_FAULT, fault)
+    sim.set_trace(ranc.TRACE_SPIKE_RASTER)
+    sim.load_inputs(inp)
+    l0 = sim.info()["kernel_launches"]
+    div = first_divergence(sim, net, inp, T)
+    launches = sim.info()["kernel_launches"] - l0
+    sim.close()
+    if variant.endswith(("multi", "stream")):
+        assert launches == 1, "the barrier fault needs the one-launch (grid barrier) path"
+    msg = verdict(div)
+    if fault == 0:
+        assert div is None, msg
+    else:
+        assert div is not None, f"fault {fault} on {variant} was NOT detected"
+        assert msg.startswith("FAIL: first divergence at tick") and div["tick"] >= 1, msg
+        print(msg)

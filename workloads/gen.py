@@ -547,3 +547,32 @@ CONFIGS = {
     4: config4,
     5: config5,
 }
+
+
+def envelope_case(seed):
+    """Configurable-envelope corpus (configurable axons and
+    neurons per core and bitwidths): A and N beyond 256 up to the ABI's 1024,
+    weights over the FULL range of 13..16 bits, potential widths down to 2
+    and 3 bits (saturating almost every tick), K 1..4, D up to 15.  Sizes are
+    bounded so the serial oracle finishes in seconds."""
+    r = substream(seed, "envelope-shape")
+    A = int([513, 1000, 1024, 256, 700, 33][int(r.ints(1, 0, 5)[0])])
+    N = int([257, 1000, 1024, 256, 300, 64][int(r.ints(1, 0, 5)[0])])
+    wb = int(r.ints(1, 13, 16)[0])
+    pb = int([2, 3, 5, 16][int(r.ints(1, 0, 3)[0])])
+    K = int(r.ints(1, 1, 4)[0])
+    D = int(r.ints(1, 1, 15)[0])
+    big = A * N > 300000
+    gw = 1 if big else int(r.ints(1, 1, 2)[0])
+    gh = int(r.ints(1, 1, 2)[0])
+    S = int(r.ints(1, 1, 12 if big else 40)[0])
+    dens = [0.1, 0.5, 1.0][int(r.ints(1, 0, 2)[0])]
+    net = random_network(7000 + seed, gw, gh, A, N, K, D, C=5, I=max(1, A // 2), density=dens,
+                         pb=pb, wb=wb, lb=min(wb, 10), tb=16, rb=min(pb, 12))
+    net.name = f"envelope-{seed}-A{A}-N{N}-wb{wb}-pb{pb}"
+    # the extremes of the weight range on some synapses of every core
+    lo, hi = -(1 << (wb - 1)), (1 << (wb - 1)) - 1
+    net.weight[:, 0, :] = lo
+    net.weight[:, min(1, N - 1), :] = hi
+    inp = random_inputs(7000 + seed, net, S, 8, p=[0.05, 0.2, 0.5][int(r.ints(1, 0, 2)[0])])
+    return net, inp
