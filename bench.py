@@ -66,6 +66,11 @@ WORKLOADS = {
     "vmm256": (_vmm("vmm256"), 1000, "samples"),
     "vmm1024": (_vmm("vmm1024"), 1000, "samples"),
     "config5": (_cfg(5), 64, "cores"),
+    # the same mesh with uniformly random (global) destinations
+    "config5g": (_cfg(5, variant="global"), 64, "cores"),
+    # TrueNorth Ref. as the paper ran it: every tick's work
+    # on the 4096-core mesh "but with no spikes" (no drive, nothing fires)
+    "config5z": (_cfg(5, drive=False), 64, "cores"),
     # streaming: the config-3 net fed one image per tick,
     # 10000 images in 10003 ticks, one sample (10010 ticks)
     "stream": (lambda S: __import__("workloads.gen", fromlist=["x"]).config3_stream(10000), 1, "samples"),
@@ -228,6 +233,42 @@ def build_workload(args):
     return net, inp, mode
 
 
+def issue_roofline(ctr, tick_ms, peaks):
+    """The second limit of the tick kernel (report both
+    fractions): issued warp instructions of one launch (ncu
+    smsp__inst_executed.sum, profiles/counters.json) over the live mean launch
+    time, against 4 issue slots per clock per SM x 148 SMs at the max SM clock."""
+    if not ctr or not ctr.get("inst_executed"):
+        return None
+    peak = 4 * 148 * peaks.get("sm_max_mhz", 1965.0) * 1e6
+    ach = ctr["inst_executed"] / (tick_ms / 1e3)
+    return {"bound": "issue", "achieved": ach, "peak": peak, "unit": "warp-inst/s", "frac": ach / peak,
+            "inst_per_launch": ctr["inst_executed"], "ncu_issue_active_pct": ctr.get("issue_active_pct"),
+            "note": "ncu smsp__inst_executed.sum of one launch (profiles/counters.json) / mean launch time (CUDA "
+                    "events); peak = 4 warp-instructions/clk/SM x 148 SMs x sm_max_mhz"}
+
+
+def int_roofline(net, info, G_loc, S_local, tick_ms, kname):
+    """Algorithmic integer work of the synaptic integration: ceil(A/32) x N
+    AND+POPC words per (core, sample) per tick (DESIGN 7), against the
+    measured POPC rate of this B200 (profiles/r01_int_peaks.json).  On the
+    tensor-core path the same work runs as int8 MMAs (2 A N ops per
+    core-tick) against the 4.5 POPS dense int8 nominal."""
+    words = ((net.axons + 31) // 32) * net.neurons * G_loc * S_local
+    try:
+        popc = json.load(open(os.path.join(ROOT, "profiles", "r01_int_peaks.json")))["popc_per_s"]
+    except Exception:
+        popc = 4.5253e12
+    if info["kernel"] == 1:
+        ach = words / (tick_ms / 1e3)
+        return {"bound": "alu (POPC)", "achieved": ach, "peak": popc, "unit": "POPC words/s", "frac": ach / popc,
+                "note": "ceil(A/32) x N words per core-tick; peak = measured POPC rate (profiles/r01_int_peaks.json)"}
+    ops = 2.0 * net.axons * net.neurons * G_loc * S_local
+    ach = ops / (tick_ms / 1e3)
+    return {"bound": "tensor (int8)", "achieved": ach, "peak": 4.5e15, "unit": "int8 op/s", "frac": ach / 4.5e15,
+            "note": "2 A N MMA ops per core-tick (the integration as int8 MMAs); peak = 4.5 POPS dense int8 nominal"}
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
@@ -357,7 +398,7 @@ def run_ours(args, rank, world, local):
     if rank == 0:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
             os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
-        hbm = peaks.get("hbm_gbs", 6650.0)
+        hbm = peaks.get("hbm_gbs", 6650.0)   # (the recipe's fallback when MEASURED_PEAKS.json is absent)
         S_local = hi - lo
         bpt = alg_bytes_per_core_tick(net)
         alg_bytes = bpt * G_loc * S_local
@@ -365,10 +406,14 @@ def run_ours(args, rank, world, local):
         info = sim.info()
         kname = ("tick_tc_kernel" if info["kernel"] == 2 else
                  "tick_stream_kernel" if launches == args.steps else "tick_popc_kernel")
-        traffic = None   # measured DRAM bytes per launch (ncu --set full), when profiled for this workload
-        tpath = os.path.join(ROOT, "profiles", "traffic.json")
-        if os.path.exists(tpath) and S_local == args.samples:
-            traffic = json.load(open(tpath)).get(kname, {}).get(net.name)
+        # per-launch ncu counters of this kernel on this workload (profiles/counters.json,
+        # tools/profile_all.sh + tools/ncu_summary.py counters), when profiled
+        ctr = None
+        cpath = os.path.join(ROOT, "profiles", "counters.json")
+        wl_key = args.workload + ("_popc" if args.kernel == "popc" else "")
+        if os.path.exists(cpath) and S_local == args.samples:
+            ctr = json.load(open(cpath)).get(kname, {}).get(wl_key)
+        traffic = ctr["dram_bytes"] if ctr else None
         state_gb = (2 * net.neurons * net.G + 4 * info["ring_rows"] * info["ring_words"] * net.G) * args.samples / 1e9
         line = {
             "metric": METRIC if args.workload == "config3" else f"simulated core-ticks/sec & samples/sec, {net.name}",
@@ -399,6 +444,8 @@ def run_ours(args, rank, world, local):
             "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(inp.line_bits.nbytes),
                     "d2h_bytes_per_step": int(counts.nbytes)},
             "clocks": clk.summary(),
+            "roofline_issue": issue_roofline(ctr, tick_ms, peaks),
+            "roofline_int": int_roofline(net, info, G_loc, S_local, tick_ms, kname),
         }
         if not args.no_cpu_baseline and world == 1:
             cores = max(1, min(host_cores(), 32))

@@ -116,7 +116,11 @@ ranc_status ranc_load_network(const ranc_network_desc* net, int cuda_device, ran
 /* Copy the input stream to the device and reset the simulation state:
  * potentials = initial_potential, scheduler rings empty, class counts 0,
  * tick = 0 (Alg. 1 l.1).  Stream-ordered; the host array is staged
- * before the call returns.  Errors: RANC_E_ARG/RANGE/SIZE/CUDA/OOM. */
+ * before the call returns.  From page-locked (pinned) host memory the copy
+ * runs on the context's copy stream into one of two staging buffers, so it
+ * overlaps work still queued on the context stream (a running batch) and the
+ * call returns as soon as the copy is done; from pageable memory the call
+ * waits for the context stream.  Errors: RANC_E_ARG/RANGE/SIZE/CUDA/OOM. */
 ranc_status ranc_load_inputs(ranc_ctx* ctx, const ranc_inputs_desc* in);
 
 /* Reset the state exactly as ranc_load_inputs does, keeping the inputs

@@ -106,9 +106,9 @@ ranc_status sync(ranc_ctx* ctx, const char* where) {
 
 void free_all(ranc_ctx* ctx) {
   DevBuf* bufs[] = {&ctx->d_xp, &ctx->d_wp, &ctx->d_pword, &ctx->d_prm, &ctx->d_route, &ctx->d_inl,
-                    &ctx->d_has_in, &ctx->d_init, &ctx->d_wfold, &ctx->d_route_tc, &ctx->d_runs,
+                    &ctx->d_has_in, &ctx->d_init, &ctx->d_wfold, &ctx->d_wcomp, &ctx->d_route_tc, &ctx->d_runs,
                     &ctx->d_nruns, &ctx->d_wflags_tc, &ctx->d_incoming, &ctx->d_word_runs, &ctx->d_pot, &ctx->d_ring, &ctx->d_counts, &ctx->d_lines,
-                    &ctx->d_stage, &ctx->d_raster, &ctx->d_fired, &ctx->d_exports, &ctx->d_send, &ctx->d_recv,
+                    &ctx->d_stage, &ctx->d_stage2, &ctx->d_raster, &ctx->d_fired, &ctx->d_exports, &ctx->d_send, &ctx->d_recv,
                     &ctx->d_send_list, &ctx->d_recv_list, &ctx->d_dbg, &ctx->d_inw, &ctx->d_inslot,
                     &ctx->d_slot_core, &ctx->d_spkin, &ctx->d_digest, &ctx->d_perm_dig, &ctx->d_gsend, &ctx->d_grecv};
   for (DevBuf* b : bufs) dev_free(ctx, b);
@@ -216,6 +216,7 @@ ranc_status ranc_load_network(const ranc_network_desc* net, int cuda_device, ran
   if (!s) s = upload(ctx, &ctx->d_has_in, c.has_in);
   if (!s) s = upload(ctx, &ctx->d_init, c.init);
   if (!s && c.tc_ok) s = upload(ctx, &ctx->d_wfold, c.wfold);
+  if (!s && c.tc_ok) s = upload(ctx, &ctx->d_wcomp, c.wcomp);
   if (!s && c.tc_ok) s = upload(ctx, &ctx->d_route_tc, c.route_tc);
   if (!s && c.tc_ok) s = upload(ctx, &ctx->d_runs, c.runs);
   if (!s && c.tc_ok) s = upload(ctx, &ctx->d_nruns, c.nruns);
@@ -262,12 +263,14 @@ ranc_status ranc_load_inputs(ranc_ctx* ctx, const ranc_inputs_desc* in) {
   if (S != ctx->S || !ctx->d_pot.p) {
     // room for either potential layout: [G][S][Npad] or [G][nT][Npad][NT]
     TRY(dev_alloc(ctx, &ctx->d_pot, (size_t)ctx->G_loc * Sr * c.Npad * sizeof(int16_t)));
+    // padding rows (samples >= S of the popcount layout) are never written;
+    // zero them once so readback copies no uninitialised bytes (initcheck)
+    CK(cudaMemsetAsync(ctx->d_pot.p, 0, ctx->d_pot.bytes, ctx->stream), "potential buffer clear");
     TRY(dev_alloc(ctx, &ctx->d_ring, (size_t)c.Rp * ctx->G_loc * Sr * c.W * sizeof(uint32_t)));
     TRY(dev_alloc(ctx, &ctx->d_counts, (size_t)S * c.C * sizeof(int32_t)));
   }
   const size_t dev_line_words = (size_t)in->num_input_ticks * Sr * c.WIp;
   if (ctx->d_lines.bytes != dev_line_words * sizeof(uint32_t)) TRY(dev_alloc(ctx, &ctx->d_lines, dev_line_words * 4));
-  if (ctx->d_stage.bytes != line_words * sizeof(uint32_t)) TRY(dev_alloc(ctx, &ctx->d_stage, line_words * 4));
   ctx->inw_valid = false;
   ctx->S = S;
   ctx->Sr = Sr;
@@ -276,12 +279,46 @@ ranc_status ranc_load_inputs(ranc_ctx* ctx, const ranc_inputs_desc* in) {
   TRY(alloc_exchange(ctx));
   if (line_words) {
     // H2D into a staging buffer, then a device transpose to [T_in][S][WI].
-    // The host buffer must stay valid until the call returns: from pageable
-    // memory the copy is staged before return; from pinned memory we wait.
-    CK(cudaMemcpyAsync(ctx->d_stage.p, in->line_bits, line_words * 4, cudaMemcpyHostToDevice, ctx->stream),
-       "ranc_load_inputs H2D");
-    CK(transpose_lines(ctx, (const uint32_t*)ctx->d_stage.p), "transpose_lines");
-    CK(cudaStreamSynchronize(ctx->stream), "ranc_load_inputs sync");
+    // The host buffer is borrowed for the call only.  From pinned memory the
+    // copy runs on a copy stream into one of two staging buffers, so it
+    // overlaps the batch still queued on the context stream (which waits for
+    // it with an event), and the call returns when the copy is done -- not
+    // when the previous batch is.  From pageable memory: copy, transpose, sync.
+    cudaPointerAttributes at{};
+    const bool pinned = cudaPointerGetAttributes(&at, in->line_bits) == cudaSuccess && at.type == cudaMemoryTypeHost;
+    cudaGetLastError();   // (a pageable pointer may leave an error behind on old drivers)
+    if (pinned) {
+      if (!ctx->copy_stream) {
+        CK(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking), "copy stream");
+        CK(cudaEventCreateWithFlags(&ctx->ev_copied, cudaEventDisableTiming), "copy event");
+        for (cudaEvent_t& e : ctx->ev_stage_free) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "copy event");
+        CK(cudaEventRecord(ctx->ev_stage_free[0], ctx->stream), "copy event");
+        CK(cudaEventRecord(ctx->ev_stage_free[1], ctx->stream), "copy event");
+      }
+      const int f = ctx->stage_flip;
+      DevBuf* st = f ? &ctx->d_stage2 : &ctx->d_stage;
+      if (st->bytes != line_words * sizeof(uint32_t)) {
+        CK(cudaStreamSynchronize(ctx->copy_stream), "copy stream");
+        TRY(dev_alloc(ctx, st, line_words * 4));   // stream-ordered on the context stream:
+        CK(cudaEventRecord(ctx->ev_stage_free[f], ctx->stream), "ranc_load_inputs");   // (ordered below)
+      }
+      // the transpose that last read this staging buffer has run
+      CK(cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_stage_free[f], 0), "ranc_load_inputs");
+      CK(cudaMemcpyAsync(st->p, in->line_bits, line_words * 4, cudaMemcpyHostToDevice, ctx->copy_stream),
+         "ranc_load_inputs H2D");
+      CK(cudaEventRecord(ctx->ev_copied, ctx->copy_stream), "ranc_load_inputs");
+      CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_copied, 0), "ranc_load_inputs");
+      CK(transpose_lines(ctx, (const uint32_t*)st->p), "transpose_lines");
+      CK(cudaEventRecord(ctx->ev_stage_free[f], ctx->stream), "ranc_load_inputs");
+      ctx->stage_flip ^= 1;
+      CK(cudaEventSynchronize(ctx->ev_copied), "ranc_load_inputs H2D");
+    } else {
+      if (ctx->d_stage.bytes != line_words * sizeof(uint32_t)) TRY(dev_alloc(ctx, &ctx->d_stage, line_words * 4));
+      CK(cudaMemcpyAsync(ctx->d_stage.p, in->line_bits, line_words * 4, cudaMemcpyHostToDevice, ctx->stream),
+         "ranc_load_inputs H2D");
+      CK(transpose_lines(ctx, (const uint32_t*)ctx->d_stage.p), "transpose_lines");
+      CK(cudaStreamSynchronize(ctx->stream), "ranc_load_inputs sync");
+    }
   }
   ctx->have_inputs = true;
   return ranc_reset_state(ctx);
@@ -739,8 +776,14 @@ void ranc_destroy(ranc_ctx* ctx) {
   cudaSetDevice(ctx->device);
   ranc_comm_destroy_internal(ctx);
   cudaStreamSynchronize(ctx->stream);
+  if (ctx->copy_stream) cudaStreamSynchronize(ctx->copy_stream);
   free_all(ctx);
   cudaStreamSynchronize(ctx->stream);
+  if (ctx->copy_stream) {
+    cudaStreamDestroy(ctx->copy_stream);
+    cudaEventDestroy(ctx->ev_copied);
+    for (cudaEvent_t e : ctx->ev_stage_free) cudaEventDestroy(e);
+  }
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;
 }

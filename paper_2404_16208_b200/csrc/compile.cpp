@@ -414,6 +414,37 @@ ranc_status validate_and_compile(const ranc_network_desc* d, Compiled* out, std:
           }
       }
     }
+    // compact crossbar (int8 weights only): what Wfold is made of, 7x smaller,
+    // expanded into the canonical operand on chip by the tick kernel when
+    // every work item is a new core (few sample tiles per core, config 5):
+    //   xbits u32 [W][Npad]  connection bits in the tensor-core axon order
+    //   tsel  u32 [Kp/4]     axon types of four consecutive axons as byte-
+    //                        permute selector nibbles (type t -> byte t)
+    //   wq    u32 [Npad]     the K <= 4 int8 weights of neuron n, byte t = w[n][t]
+    if (!o.tc_wide) {
+      o.comp_bytes = (int32_t)((size_t)W * o.Npad * 4 + (size_t)o.Kp + (size_t)o.Npad * 4);
+      o.wcomp.assign((size_t)G * o.comp_bytes, 0);
+      for (int c = 0; c < G; ++c) {
+        uint8_t* base = &o.wcomp[(size_t)c * o.comp_bytes];
+        uint32_t* xb = reinterpret_cast<uint32_t*>(base);
+        uint32_t* tsel = reinterpret_cast<uint32_t*>(base + (size_t)W * o.Npad * 4);
+        uint32_t* wq = reinterpret_cast<uint32_t*>(base + (size_t)W * o.Npad * 4 + o.Kp);
+        const int32_t* perm = &o.perm_tc[(size_t)c * A];
+        const int32_t* inv = &o.inv_tc[(size_t)c * A];
+        const uint8_t* ty = d->axon_type + (size_t)c * A;
+        for (int ap = 0; ap < A; ++ap) tsel[ap >> 2] |= (uint32_t)ty[perm[ap]] << (4 * (ap & 3));
+        for (int n = 0; n < N; ++n) {
+          const size_t cn = (size_t)c * N + n;
+          const uint32_t* src = d->crossbar + cn * W;
+          for (int a = 0; a < A; ++a)
+            if ((src[a >> 5] >> (a & 31)) & 1u) {
+              const int ap = inv[a];
+              xb[(size_t)(ap >> 5) * o.Npad + n] |= 1u << (ap & 31);
+            }
+          for (int k = 0; k < K; ++k) wq[n] |= (uint32_t)(uint8_t)(int8_t)d->weight[cn * K + k] << (8 * k);
+        }
+      }
+    }
   }
   return RANC_OK;
 }

@@ -72,6 +72,8 @@ struct TickParams {
   int64_t t;                // tick being executed
   int64_t raster_t0;        // first tick of the raster buffer
   const uint8_t* wfold;     // tensor-core path: [G][Npad*Kp] canonical-layout int8
+  const uint8_t* wcomp;     // tensor-core path: [G][comp] compact crossbar, expanded on chip
+  int32_t comp;             // bytes per core of wcomp when the compact form is in use, else 0
   const int2* runs;         // tensor-core path: input runs [G][rmax]
   const int32_t* word_runs; // [G][W]: runs overlapping ring word w: first | count << 16
   const uint32_t* inw;      // decoded inputs [T_in][n_inslots][Sr][W] or [..][W][Sr] (the ring's layout), or nullptr
@@ -113,6 +115,8 @@ struct Compiled {
   bool tc_wmajor = false;       // automatic ring layout: word-major when most routing neurons sit in
                                 // warps without a shared destination word (per-neuron routes)
   std::vector<int8_t> wfold;    // [G][Npad*Kp] canonical operand layout, tensor-core axon order
+  std::vector<uint8_t> wcomp;   // [G][comp_bytes] compact crossbar (int8 weights only, compile.cpp)
+  int32_t comp_bytes = 0;       // bytes per core of wcomp (0: no compact form)
   std::vector<int32_t> perm_tc, inv_tc;   // tensor-core axon order (sorted by input line)
   std::vector<uint2> route_tc;  // route words with tensor-core destination axons
   std::vector<int2> runs;       // [G][rmax] input runs: x = a'start | len<<16, y = first line
@@ -155,11 +159,17 @@ struct ranc_ctx {
   std::string err;
   ranc::Compiled net;
   // device: compiled network
-  ranc::DevBuf d_xp, d_wp, d_pword, d_prm, d_route, d_inl, d_has_in, d_init, d_wfold, d_route_tc, d_runs, d_nruns, d_wflags_tc, d_incoming,
+  ranc::DevBuf d_xp, d_wp, d_pword, d_prm, d_route, d_inl, d_has_in, d_init, d_wfold, d_wcomp, d_route_tc, d_runs, d_nruns, d_wflags_tc, d_incoming,
       d_word_runs;
   int num_sms = 148;
   // device: state
   ranc::DevBuf d_pot, d_ring, d_counts, d_lines, d_stage, d_raster;
+  // inputs from pinned host memory: H2D on a copy stream into one of two
+  // staging buffers, overlapping the work already queued on the context stream
+  ranc::DevBuf d_stage2;
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_copied = nullptr, ev_stage_free[2] = {nullptr, nullptr};
+  int stage_flip = 0;
   bool fresh = false;            // no tick since the last reset: d_pot is stale, potentials = init
   int64_t S = 0, first_sample = 0;
   int64_t Sr = 0;                // S rounded up to 64

@@ -69,10 +69,10 @@ constexpr int kSub = 16;               // samples per TMEM load / LIF pass of an
 static_assert(kExpThreads == 2 * NT, "spike stage maps thread -> (sample, 16-bit half)");
 
 enum Bar { FULL0 = 0, SEMPTY0 = 4, BFULL0 = 8, BEMPTY0 = 12, ACCFULL0 = 16, ACCEMPTY0 = 20, WFULL = 24, WFREE = 25,
-           NBARS = 26 };
+           CFULL0 = 26, CFREE0 = 28, WFULL1 = 30, WFREE1 = 31, NBARS = 32 };
 
 struct TcLayout {
-  uint32_t w, runs, lut, potbuf, cplanes, stage, b, raw, lines, stage_bytes, total;
+  uint32_t w, runs, lut, potbuf, cplanes, comp, stage, b, raw, lines, stage_bytes, total;
 };
 
 // WIp: input-line row words (multiple of 4)
@@ -83,15 +83,20 @@ constexpr int NS_WIDE = 2;
 // multi-tick launch: 3 spike stages (its ticks are a latency chain; the
 // freed 20 KB hold the bit-sliced output counters of two items)
 constexpr int NS_MULTI = 3;
+// compact-crossbar launch: two expanded operand buffers (the next core's is
+// expanded while the current one is multiplied) leave room for 2 stages
+constexpr int NS_COMP = 2;
 // pot_items: potential tiles kept on chip (multi-tick launch with up to two
 // work items per CTA: one region each)
 // cnt_planes: per-thread bit-sliced output-bus counters (multi-tick launch)
 constexpr int kCntPlanes = 8;   // counts < 256 between flushes
+// comp: bytes per core of the compact crossbar (two staging buffers and two
+// expanded operand buffers), 0 = not used
 __host__ __device__ inline TcLayout tc_layout(int Np, int Kp, int W, int WIp, int rmax, bool wide, int pot_items = 1,
-                                              bool cnt_planes = false, bool multi = false) {
+                                              bool cnt_planes = false, bool multi = false, uint32_t comp = 0) {
   TcLayout L;
   L.w = 1024;
-  uint32_t o = L.w + (uint32_t)Np * Kp * (wide ? 2u : 1u);
+  uint32_t o = L.w + (uint32_t)Np * Kp * (wide || comp ? 2u : 1u);
   L.runs = o;                                 // int2 [rmax] + int32 [W] of the current core
   o += (uint32_t)rmax * 8 + (uint32_t)W * 4;
   o = (o + 15) & ~15u;
@@ -102,6 +107,9 @@ __host__ __device__ inline TcLayout tc_layout(int Np, int Kp, int W, int WIp, in
   o += (NT / 8) * (32 * 8) * 16 * (uint32_t)pot_items;   // = 4 chunks x 512 epilogue threads per item
   L.cplanes = o;                              // u32 [items][kCntPlanes][512 epilogue threads]
   if (cnt_planes) o += (uint32_t)pot_items * kCntPlanes * 512 * 4;
+  o = (o + 127) & ~127u;
+  L.comp = o;                                 // u8 [2][comp]: compact crossbars of the next cores (TMA)
+  o += 2 * comp;
   L.stage = (o + 1023) & ~1023u;
   uint32_t q = 0;
   L.b = q;     q += (uint32_t)NT * Kp;       // spikes as 0/1 bytes, canonical layout
@@ -110,7 +118,7 @@ __host__ __device__ inline TcLayout tc_layout(int Np, int Kp, int W, int WIp, in
   q = (q + 15) & ~15u;
   L.lines = q; q += (uint32_t)NT * (WIp > W ? WIp : W) * 4;  // input line rows or decoded words (TMA)
   L.stage_bytes = (q + 1023) & ~1023u;
-  L.total = L.stage + (wide ? NS_WIDE : multi ? NS_MULTI : NS) * L.stage_bytes;
+  L.total = L.stage + (wide ? NS_WIDE : multi ? NS_MULTI : comp ? NS_COMP : NS) * L.stage_bytes;
   return L;
 }
 
@@ -205,8 +213,11 @@ __device__ __forceinline__ uint32_t lif(const uint4 (&cur)[NE / 8], const uint32
 // carries its own layout's code)
 // kWide: weights split into lo/hi int8 operands, two MMAs and two TMEM
 // accumulators per tile, acc = acc_lo + 128 * acc_hi in the epilogue
-template <bool kMulti, bool kDebug, bool kWm, bool kWide>
+// kComp: the compact crossbar (p.comp bytes per core) is staged by TMA and
+// expanded on chip into two alternating operand buffers
+template <bool kMulti, bool kDebug, bool kWm, bool kWide, bool kComp = false>
 __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams p, const int nticks_arg) {
+  static_assert(!kComp || (!kMulti && !kWide), "the compact crossbar is a per-tick int8 launch");
   const int nticks = kMulti ? nticks_arg : 1;
   // kDebug: the RANC_DEBUG_TIMELINE instrumentation (a separate instantiation,
   // so that the product kernel issues none of it)
@@ -218,8 +229,16 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + 8 * NBARS);
   const int Np = p.Npad, Kp = p.Kp, W = p.W, WIp = p.WIp;
-  const TcLayout L = tc_layout(Np, Kp, W, WIp, p.rmax, kWide, kMulti ? p.pot_items : 1, kMulti && p.out_planes, kMulti);
-  constexpr int NS = kWide ? NS_WIDE : kMulti ? NS_MULTI : ranc::NS;   // spike stages in use
+  const TcLayout L = tc_layout(Np, Kp, W, WIp, p.rmax, kWide, kMulti ? p.pot_items : 1, kMulti && p.out_planes, kMulti,
+                               kComp ? (uint32_t)p.comp : 0u);
+  // compact crossbar (p.comp > 0, per-tick int8 launches with few tiles per
+  // core): the producer stages each core's 7x smaller crossbar bits, axon
+  // types and weights (two buffers), the spike warps expand them into the
+  // canonical operand w_s, so the operand costs ~10 KB of HBM per core
+  // instead of 64 KB
+  constexpr bool comp = kComp;
+  const uint32_t wbuf_bytes = (uint32_t)Np * Kp;   // one expanded operand (kComp: two, alternating per core)
+  constexpr int NS = kWide ? NS_WIDE : kMulti ? NS_MULTI : kComp ? NS_COMP : ranc::NS;   // spike stages in use
   uint8_t* w_s = smem + L.w;
   const int Mh = Np >> 7;
   const int nT = (p.S + NT - 1) / NT;
@@ -266,6 +285,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
     }
     ptx::mbar_init(&bars[WFULL], 1);
     ptx::mbar_init(&bars[WFREE], 1);
+    ptx::mbar_init(&bars[WFULL1], 1);
+    ptx::mbar_init(&bars[WFREE1], 1);
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&bars[CFULL0 + i], 1);
+      ptx::mbar_init(&bars[CFREE0 + i], 1);
+    }
     ptx::fence_mbar_init();
   }
   // programmatic dependent launch (per-tick launches): let the next tick's
@@ -298,11 +323,23 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       const int s = k % NS, u = k / NS;
       if (c != prev_core) {
         ++jw;
-        if (jw > 0) wait(&bars[WFREE], (jw - 1) & 1);
-        if (lane == 0) {
-          const uint32_t wb = (uint32_t)Np * Kp * (kWide ? 2u : 1u);   // wide: [lo | hi]
-          ptx::mbar_arrive_expect_tx(&bars[WFULL], wb);
-          ptx::bulk_g2s(w_s, p.wfold + (size_t)c * wb, wb, &bars[WFULL]);
+        if (comp) {
+          // compact crossbar into staging buffer jw & 1 once the spike warps
+          // have expanded the core that used it before
+          const int cs = jw & 1, cu = jw >> 1;
+          if (jw >= 2) wait(&bars[CFREE0 + cs], (cu - 1) & 1);
+          if (lane == 0) {
+            ptx::mbar_arrive_expect_tx(&bars[CFULL0 + cs], (uint32_t)p.comp);
+            ptx::bulk_g2s(smem + L.comp + cs * p.comp, p.wcomp + (size_t)c * p.comp, (uint32_t)p.comp,
+                          &bars[CFULL0 + cs]);
+          }
+        } else {
+          if (jw > 0) wait(&bars[WFREE], (jw - 1) & 1);
+          if (lane == 0) {
+            const uint32_t wb = (uint32_t)Np * Kp * (kWide ? 2u : 1u);   // wide: [lo | hi]
+            ptx::mbar_arrive_expect_tx(&bars[WFULL], wb);
+            ptx::bulk_g2s(w_s, p.wfold + (size_t)c * wb, wb, &bars[WFULL]);
+          }
         }
         prev_core = c;
       }
@@ -361,9 +398,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       const int a = k % NA, ua = k / NA;
       if (c != prev_core) {
         ++jw;
-        wait(&bars[WFULL], jw & 1);
+        if (comp) wait(&bars[(jw & 1) ? WFULL1 : WFULL], (jw >> 1) & 1);
+        else wait(&bars[WFULL], jw & 1);
         prev_core = c;
       }
+      const uint8_t* w_cur = w_s + (comp ? (uint32_t)(jw & 1) * wbuf_bytes : 0u);
       wait(&bars[BFULL0 + s], u & 1);
       if (lane == 0) stamp_k(k, 5);
       wait(&bars[ACCEMPTY0 + a], (ua & 1) ^ 1);
@@ -374,7 +413,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
         const uint32_t acc = tmem + a * acc_stride;
         for (int hh = 0; hh < Mh; ++hh)
           for (int kk = 0; kk < Kp / 32; ++kk) {
-            const uint64_t ad = tc::smem_desc(ptx::smem_u32(w_s + hh * 2048 + kk * 2 * lbo_a), lbo_a, 128);
+            const uint64_t ad = tc::smem_desc(ptx::smem_u32(w_cur + hh * 2048 + kk * 2 * lbo_a), lbo_a, 128);
             const uint64_t bd = tc::smem_desc(ptx::smem_u32(b_s + kk * 2 * lbo_b), lbo_b, 128);
             tc::mma_i8(acc + hh * NT, ad, bd, id, kk > 0 ? 1u : 0u);
             if (kWide) {
@@ -389,7 +428,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
         // item of the next tick) belongs to another core, or this is the end
         const bool last_item = k0 + 1 == nwork;
         const int next_cl = last_item ? lo / nT : (tile + 1 == nT ? cl + 1 : cl);
-        if ((last_item && it + 1 == nticks) || next_cl != cl) tc::commit(&bars[WFREE]);
+        if ((last_item && it + 1 == nticks) || next_cl != cl)
+          tc::commit(&bars[comp && (jw & 1) ? WFREE1 : WFREE]);
       }
       __syncwarp();
     }
@@ -579,6 +619,68 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
     static_assert(NT == 64 && kSub == 16, "two 32-sample halves, two passes each");
     constexpr int kPass = 32 / kSub, kCh = kSub / 8;   // passes per half, chunks per pass
     uint4* pbuf = reinterpret_cast<uint4*>(smem + L.potbuf) + (threadIdx.x - 32 * kFirstEpi);
+    // word-major rings (scattered routes, e.g. config 5) want the ring to stay
+    // in L2 next to the potential stream: there the potentials may be loaded
+    // and stored evict-first (RANC_WM_EVICT_FIRST builds, an experiment)
+#ifdef RANC_WM_EVICT_FIRST
+    constexpr bool kEvictFirstPot = kWm;
+#else
+    constexpr bool kEvictFirstPot = false;
+#endif
+    const uint64_t pot_pol = kEvictFirstPot ? ptx::policy_evict_first() : 0ull;
+    auto pot_load = [&](void* d, const void* g) {
+      if (kEvictFirstPot) ptx::cp_async16_hint(d, g, pot_pol);
+      else ptx::cp_async16(d, g);
+    };
+    // kComp: the 16 epilogue warps expand the compact crossbar of the NEXT
+    // core into the other operand buffer before they wait for this item's
+    // accumulator (they wait there anyway), so the MMAs of the next core
+    // never wait for an operand load.  Byte (n, a') = conn ? w[n][type(a')]
+    // : 0 is one byte permute per four axons: the selector nibble is the
+    // axon's type (a byte of wq) or, for a missing connection, 4 + type (a
+    // byte of the zero second operand; the table lut[16 + bits]).  The
+    // buffer refilled last held core jw - 1, whose MMAs completed before
+    // this warp passed that core's last accumulator barrier.
+    int jw_e = -1;
+    uint32_t* const lutc = reinterpret_cast<uint32_t*>(smem + L.lut) + 16;
+    if (comp && threadIdx.x - 32 * kFirstEpi < 16) {
+      // selector bit 2 of nibble j set iff bit j of b is clear (a missing
+      // connection selects a zero byte); ordered by the first expansion's bar 3
+      const int b = threadIdx.x - 32 * kFirstEpi;
+      uint32_t z = 0u;
+      for (int j = 0; j < 4; ++j)
+        if (!((b >> j) & 1)) z |= 4u << (4 * j);
+      lutc[b] = z;
+    }
+    auto expand_core = [&](int cglob) {
+      (void)cglob;
+      ++jw_e;
+      const int cs = jw_e & 1, cu = jw_e >> 1;   // staging buffer = operand buffer = jw_e & 1
+      ptx::mbar_wait(&bars[CFULL0 + cs], cu & 1);
+      const uint8_t* cb = smem + L.comp + cs * p.comp;
+      const uint32_t* xb = reinterpret_cast<const uint32_t*>(cb);                          // [W][Np]
+      const uint32_t* tsel = reinterpret_cast<const uint32_t*>(cb + (size_t)W * Np * 4);     // [Kp/4]
+      const uint32_t* wq = reinterpret_cast<const uint32_t*>(cb + (size_t)W * Np * 4 + Kp);  // [Np]
+      uint8_t* const w_dst = w_s + (uint32_t)cs * wbuf_bytes;
+      const int et512 = threadIdx.x - 32 * kFirstEpi;
+      const int nq = Np * (Kp / 16);   // 16-byte chunks: chunk q = (K chunk q / Np, neuron q % Np)
+#pragma unroll 2
+      for (int q = et512; q < nq; q += 32 * kEpiWarps) {
+        const int nn = q % Np, kc = q / Np;
+        const uint32_t b16 = xb[(size_t)(kc >> 1) * Np + nn] >> (16 * (kc & 1));
+        const uint32_t wv = wq[nn];
+        const uint4 sel = *reinterpret_cast<const uint4*>(tsel + kc * 4);
+        *reinterpret_cast<uint4*>(w_dst + tc::operand_offset((uint32_t)nn, (uint32_t)(16 * kc), (uint32_t)Np)) =
+            make_uint4(__byte_perm(wv, 0u, lutc[b16 & 15u] | sel.x), __byte_perm(wv, 0u, lutc[(b16 >> 4) & 15u] | sel.y),
+                       __byte_perm(wv, 0u, lutc[(b16 >> 8) & 15u] | sel.z), __byte_perm(wv, 0u, lutc[(b16 >> 12) & 15u] | sel.w));
+      }
+      ptx::fence_proxy_async_smem();   // generic writes -> the tensor core's (async proxy) reads
+      named_sync(3, 32 * kEpiWarps);
+      if (et512 == 0) {
+        ptx::mbar_arrive(&bars[cs ? WFULL1 : WFULL]);
+        ptx::mbar_arrive(&bars[CFREE0 + cs]);
+      }
+    };
     constexpr int PB = 32 * kEpiWarps;   // uint4 stride between chunks in potbuf
     constexpr int kItem = kPass * kCh * PB;   // uint4 per item region (multi-tick launch): 32 KB
     // multi-tick launch: output-bus counts of this thread's 32 samples, bit-
@@ -605,13 +707,27 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       for (int sb = 0; sb < kPass; ++sb) {
 #pragma unroll
         for (int i = 0; i < kCh; ++i)
-          ptx::cp_async16(pbuf + (kCh * sb + i) * PB, dst + (size_t)(kCh * sb + i) * Np);
+          pot_load(pbuf + (kCh * sb + i) * PB, dst + (size_t)(kCh * sb + i) * Np);
         ptx::cp_async_commit();
       }
     }
     long long dbg_wait = 0;
     const long long dbg_t0 = dbg_on ? clock64() : 0;
     const int cl0 = cl, tile0 = tile;
+    // neuron parameters of the next work item's core (prefetched one item ahead)
+    short4 nprm = make_short4(0, 0, 0, 0);
+    uint2 nrt = make_uint2(0u, 0u);
+    int nini = 0;
+    if (active && nwork > 0) {
+      const size_t nc = (size_t)(p.c_lo + cl0) * Np + n;
+      nprm = p.prm[nc];
+      nrt = p.route[nc];
+      nini = p.init[nc];
+    }
+    if (comp && nwork > 0) {
+      named_sync(3, 32 * kEpiWarps);   // lutc is written
+      expand_core(p.c_lo + cl0);
+    }
     // this thread's TMEM lane and column offset (the stage adds a * acc_stride)
     const uint32_t tmem_lane_base = tmem + ((uint32_t)(q * 32) << 16) + h * NT + jj * 32;
     // chunk c of this thread's 32 samples sits c * Np * 16 bytes after chunk 0
@@ -638,15 +754,21 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       const bool pf = load && k0 + 1 < nwork;
       const uint4* nsrc = dst + tile_stride;
       const long long tw0 = dbg_on ? clock64() : 0;
-      // a new core's neuron parameters are requested before the accumulator
-      // wait, so their latency hides behind it (one tile per core, config 5)
-      short4 prm = make_short4(0, 0, 0, 0);
-      uint2 rt = make_uint2(0u, 0u);
-      int ini = 0;
-      if (active && c != prev_core) {
-        prm = p.prm[(size_t)c * Np + n];
-        rt = p.route[(size_t)c * Np + n];
-        ini = p.init[(size_t)c * Np + n];
+      // a new core's neuron parameters were requested a whole work item
+      // ahead (one tile per core at config 5: the loads would otherwise stall
+      // the epilogue at every item); prefetch the next item's now
+      const short4 prm = nprm;
+      const uint2 rt = nrt;
+      const int ini = nini;
+      {
+        const int ncl = (k0 + 1 == nwork) ? cl0 : (tile + 1 == nT ? cl + 1 : cl);
+        if (active && ncl != cl) {
+          const size_t nc = (size_t)(p.c_lo + ncl) * Np + n;
+          nprm = p.prm[nc];
+          nrt = p.route[nc];
+          nini = p.init[nc];
+        }
+        if (comp && k0 + 1 < nwork && ncl != cl) expand_core(p.c_lo + ncl);
       }
       // one warp per lane quarter polls the accumulator barrier; the other
       // three wait on the quarter's named barrier (no issue slots spent)
@@ -745,7 +867,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
               const char* nb = reinterpret_cast<const char*>(nsrc);
 #pragma unroll
               for (int i = 0; i < kCh; ++i)
-                ptx::cp_async16(pbn + (kCh * sb + i) * PB, nb + (uint32_t)((kCh * sb + i) * chunk_bytes));
+                pot_load(pbn + (kCh * sb + i) * PB, nb + (uint32_t)((kCh * sb + i) * chunk_bytes));
             }
             ptx::cp_async_commit();   // (possibly empty) group: keeps the wait_group 1 accounting
           }
@@ -761,6 +883,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
           for (int cc = 0; cc < kCh; ++cc) {
             const uint4 o = make_uint4(outw[4 * cc + 0], outw[4 * cc + 1], outw[4 * cc + 2], outw[4 * cc + 3]);
             if (!last) pb[(kCh * sb + cc) * PB] = o;   // kept on chip for the next tick
+            else if (kEvictFirstPot) ptx::st16_cs(reinterpret_cast<char*>(dst) + (uint32_t)((kCh * sb + cc) * chunk_bytes), o);
             else POT_STORE(reinterpret_cast<char*>(dst) + (uint32_t)((kCh * sb + cc) * chunk_bytes), o);
           }
         }
@@ -982,6 +1105,8 @@ void tc_fill_params(ranc_ctx* ctx, TickParams& p) {
   p.n_inslots = ctx->n_inslots;
   p.nruns = (const int32_t*)ctx->d_nruns.p;
   p.rmax = n.rmax;
+  p.wcomp = (const uint8_t*)ctx->d_wcomp.p;
+  p.comp = 0;
   p.wmajor = ctx->ring_wmajor ? 1 : 0;
   p.any_route = n.any_route ? 1 : 0;
 }
@@ -1064,7 +1189,18 @@ cudaError_t launch_tick_tc(ranc_ctx* ctx, TickParams p) {
   tc_fill_params(ctx, p);
   const int64_t total = (int64_t)ctx->G_loc * ((ctx->S + NT - 1) / NT);
   const int grid = (int)std::min<int64_t>(total, ctx->num_sms);
-  const size_t smem = tc_smem_bytes(n);
+  // compact crossbar when most work items start a new core (<= 4 sample
+  // tiles per core, e.g. config 5's 64 samples): the 64 KB operand of every
+  // core would otherwise be re-read from HBM every tick.  RANC_DEBUG_WCOMP=0/1
+  // forces it off / on (timing comparisons).
+  static const int wcomp_env = getenv("RANC_DEBUG_WCOMP") ? atoi(getenv("RANC_DEBUG_WCOMP")) : -1;
+  const int64_t nT = (ctx->S + NT - 1) / NT;
+  const bool comp = !n.tc_wide && n.comp_bytes > 0 && ctx->d_wcomp.p && (wcomp_env >= 0 ? wcomp_env == 1 : nT <= 4) &&
+                    tc_layout(n.Npad, n.Kp, n.W, n.WIp, n.rmax, false, 1, false, false, (uint32_t)n.comp_bytes).total <=
+                        227 * 1024;
+  p.comp = comp ? n.comp_bytes : 0;
+  const size_t smem =
+      tc_layout(n.Npad, n.Kp, n.W, n.WIp, n.rmax, n.tc_wide, 1, false, false, (uint32_t)p.comp).total;
   static std::atomic<uint64_t> configured{0};
   if (first_use_on_device(configured)) {
     const void* fns[] = {(const void*)tick_tc_kernel<false, false, false, false>,
@@ -1072,7 +1208,11 @@ cudaError_t launch_tick_tc(ranc_ctx* ctx, TickParams p) {
                          (const void*)tick_tc_kernel<false, false, true, false>,
                          (const void*)tick_tc_kernel<false, true, true, false>,
                          (const void*)tick_tc_kernel<false, false, false, true>,
-                         (const void*)tick_tc_kernel<false, false, true, true>};
+                         (const void*)tick_tc_kernel<false, false, true, true>,
+                         (const void*)tick_tc_kernel<false, false, false, false, true>,
+                         (const void*)tick_tc_kernel<false, true, false, false, true>,
+                         (const void*)tick_tc_kernel<false, false, true, false, true>,
+                         (const void*)tick_tc_kernel<false, true, true, false, true>};
     for (const void* f : fns) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   }
   static const bool dbg_env = getenv("RANC_DEBUG_TIMELINE") != nullptr;
@@ -1082,6 +1222,10 @@ cudaError_t launch_tick_tc(ranc_ctx* ctx, TickParams p) {
   if (dbg) cudaMemsetAsync(ctx->d_dbg.p, 0, kDbg * 8, ctx->stream);
   const void* fn = n.tc_wide ? (p.wmajor ? (const void*)tick_tc_kernel<false, false, true, true>   // wide: no timeline
                                           : (const void*)tick_tc_kernel<false, false, false, true>)
+                   : comp ? (dbg ? (p.wmajor ? (const void*)tick_tc_kernel<false, true, true, false, true>
+                                             : (const void*)tick_tc_kernel<false, true, false, false, true>)
+                                 : (p.wmajor ? (const void*)tick_tc_kernel<false, false, true, false, true>
+                                             : (const void*)tick_tc_kernel<false, false, false, false, true>))
                    : dbg ? (p.wmajor ? (const void*)tick_tc_kernel<false, true, true, false>
                                      : (const void*)tick_tc_kernel<false, true, false, false>)
                          : (p.wmajor ? (const void*)tick_tc_kernel<false, false, true, false>

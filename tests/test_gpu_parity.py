@@ -591,7 +591,10 @@ def test_digest_core_sharded_shards_add_up(ranc, oracle_mod, kernel):
                                            (2, "tc"), (2, "popc")])
 def test_fault_injection_is_caught(ranc, fault, variant):
     from verify import first_divergence, verdict
-    net, inp = config2(S=130 if variant.startswith("tc") else 48)
+    if fault == 2:   # early delivery needs delays >= 2: the D = 15 random mesh
+        net, inp = config5(S=40, T=20, grid=6)
+    else:            # the missing barrier: the 5-core net's cross-core deposits
+        net, inp = config2(S=130 if variant.startswith("tc") else 48)
     T = net.meta["T"]
     sim = ranc.Simulator(net)
     sim.set_option(ranc.OPT_KERNEL, 2 if variant.startswith("tc") else 1)

@@ -3,6 +3,8 @@
 
   python tools/ncu_summary.py full gpurun_out/prof.ncu-rep        # key metrics of a --set full capture
   python tools/ncu_summary.py launches gpurun_out/launches.csv    # per-kernel launch-time shares
+  python tools/ncu_summary.py counters OUT.json REP...            # merge per-launch counters into OUT.json
+      (REP named prof_<tag>_<workload>.ncu-rep; bench.py reads profiles/counters.json)
 """
 import csv
 import io
@@ -78,6 +80,45 @@ def launches(path):
     return "\n".join(out)
 
 
+def counters(out_json, reps):
+    """Per (kernel, workload) counters of one launch: DRAM bytes, issued warp
+    instructions, issue-slot utilisation, duration and SM clock."""
+    import json
+    import os
+    import re
+    db = json.load(open(out_json)) if os.path.exists(out_json) else {}
+    for rep in reps:
+        wl = re.sub(r"^prof_[^_]+_", "", os.path.basename(rep).replace(".ncu-rep", ""))
+        raw = list(csv.reader(io.StringIO(ncu("-i", rep, "--page", "raw", "--csv"))))
+        if len(raw) < 3:
+            continue
+        h = raw[0]
+        d = dict(zip(h, raw[2]))
+
+        scale = {"byte": 1, "kbyte": 1e3, "mbyte": 1e6, "gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6,
+                 "msecond": 1e-3, "second": 1, "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "hz": 1, "khz": 1e3, "mhz": 1e6,
+                 "ghz": 1e9, "cycle/second": 1, "cycle/nsecond": 1e9, "cycle/usecond": 1e6, "inst": 1, "%": 1}
+
+        def f(k):   # value in base units (bytes, seconds, Hz)
+            try:
+                return float(d[k].replace(",", "")) * scale.get(raw[1][h.index(k)].strip().lower(), 1)
+            except (KeyError, ValueError):
+                return None
+        name = d.get("Kernel Name", "?")
+        kname = "tick_tc_kernel" if "tick_tc" in name else name.split("<")[0].split("(")[0].split("::")[-1]
+        dur_ns = (f("gpu__time_duration.sum") or 0) * 1e9
+        db.setdefault(kname, {})[wl] = {
+            "kernel": name[:160], "dram_bytes": (f("dram__bytes_read.sum") or 0) + (f("dram__bytes_write.sum") or 0),
+            "inst_executed": f("smsp__inst_executed.sum"),
+            "issue_active_pct": f("sm__inst_issued.avg.pct_of_peak_sustained_active"),
+            "duration_ns": dur_ns, "sm_hz": f("smsp__cycles_elapsed.avg.per_second")}
+    json.dump(db, open(out_json, "w"), indent=1, sort_keys=True)
+    return json.dumps(db, indent=1, sort_keys=True)
+
+
 if __name__ == "__main__":
     mode, path = sys.argv[1], sys.argv[2]
-    print(full(path) if mode == "full" else launches(path))
+    if mode == "counters":
+        print(counters(path, sys.argv[3:]))
+    else:
+        print(full(path) if mode == "full" else launches(path))

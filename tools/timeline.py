@@ -1,13 +1,22 @@
-"""Print the TC kernel's per-tile pipeline timeline of CTA 0 (debug aid)."""
+"""Print the TC kernel's per-tile pipeline timeline of CTA 0 (debug aid).
+
+  python tools/timeline.py [config3|config5|config5g] [S] [ticks]
+"""
 import os
 import sys
 
 os.environ["RANC_DEBUG_TIMELINE"] = "1"
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2404_16208_b200 import Simulator  # noqa: E402
-from workloads.gen import config3  # noqa: E402
+from workloads import gen  # noqa: E402
 
-net, inp = config3(S=int(sys.argv[1]) if len(sys.argv) > 1 else 10000)
+wl = sys.argv[1] if len(sys.argv) > 1 else "config3"
+S = int(sys.argv[2]) if len(sys.argv) > 2 else (64 if wl.startswith("config5") else 10000)
+if wl == "config3":
+    net, inp = gen.config3(S=S)
+else:
+    net, inp = gen.config5(S=S, T=10, variant="global" if wl == "config5g" else "local")
 sim = Simulator(net)
+sim.set_option(3, 2)
 sim.load_inputs(inp)
-sim.run(int(sys.argv[2]) if len(sys.argv) > 2 else 3)
+sim.run(int(sys.argv[3]) if len(sys.argv) > 3 else 3)
