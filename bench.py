@@ -81,6 +81,9 @@ WORKLOADS = {
     # config 3 with weights / leaks / thresholds x16 (13-bit weights, beyond
     # int8): the tensor-core wide-weight variant (two int8 operands)
     "config3w": (lambda S: __import__("workloads.gen", fromlist=["x"]).config3_wide(S=S), 10000, "samples"),
+    # cores beyond 256 x 256 (configurable axons / neurons):
+    # 4x4 mesh of 512-axon x 1024-neuron cores, tensor cores in neuron groups
+    "bigcore": (lambda S: __import__("workloads.gen", fromlist=["x"]).bigcore(S=S), 4096, "samples"),
 }
 
 
@@ -233,7 +236,7 @@ def build_workload(args):
     return net, inp, mode
 
 
-def issue_roofline(ctr, tick_ms, peaks):
+def issue_roofline(ctr, launch_ms, peaks):
     """The second limit of the tick kernel (report both
     fractions): issued warp instructions of one launch (ncu
     smsp__inst_executed.sum, profiles/counters.json) over the live mean launch
@@ -241,7 +244,7 @@ def issue_roofline(ctr, tick_ms, peaks):
     if not ctr or not ctr.get("inst_executed"):
         return None
     peak = 4 * 148 * peaks.get("sm_max_mhz", 1965.0) * 1e6
-    ach = ctr["inst_executed"] / (tick_ms / 1e3)
+    ach = ctr["inst_executed"] / (launch_ms / 1e3)
     return {"bound": "issue", "achieved": ach, "peak": peak, "unit": "warp-inst/s", "frac": ach / peak,
             "inst_per_launch": ctr["inst_executed"], "ncu_issue_active_pct": ctr.get("issue_active_pct"),
             "note": "ncu smsp__inst_executed.sum of one launch (profiles/counters.json) / mean launch time (CUDA "
@@ -412,8 +415,12 @@ def run_ours(args, rank, world, local):
         cpath = os.path.join(ROOT, "profiles", "counters.json")
         wl_key = args.workload + ("_popc" if args.kernel == "popc" else "")
         if os.path.exists(cpath) and S_local == args.samples:
-            ctr = json.load(open(cpath)).get(kname, {}).get(wl_key)
-        traffic = ctr["dram_bytes"] if ctr else None
+            for kn, per_wl in json.load(open(cpath)).items():
+                if kn.startswith(kname[:12]) and wl_key in per_wl:
+                    ctr = per_wl[wl_key]
+        # a multi-tick (cooperative) launch runs all T ticks of a step
+        ticks_per_launch = T if launches == args.steps else 1
+        traffic = ctr["dram_bytes"] / ticks_per_launch if ctr else None
         state_gb = (2 * net.neurons * net.G + 4 * info["ring_rows"] * info["ring_words"] * net.G) * args.samples / 1e9
         line = {
             "metric": METRIC if args.workload == "config3" else f"simulated core-ticks/sec & samples/sec, {net.name}",
@@ -444,7 +451,7 @@ def run_ours(args, rank, world, local):
             "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(inp.line_bits.nbytes),
                     "d2h_bytes_per_step": int(counts.nbytes)},
             "clocks": clk.summary(),
-            "roofline_issue": issue_roofline(ctr, tick_ms, peaks),
+            "roofline_issue": issue_roofline(ctr, tick_ms * ticks_per_launch, peaks),
             "roofline_int": int_roofline(net, info, G_loc, S_local, tick_ms, kname),
         }
         if not args.no_cpu_baseline and world == 1:

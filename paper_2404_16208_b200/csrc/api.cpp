@@ -106,7 +106,7 @@ ranc_status sync(ranc_ctx* ctx, const char* where) {
 
 void free_all(ranc_ctx* ctx) {
   DevBuf* bufs[] = {&ctx->d_xp, &ctx->d_wp, &ctx->d_pword, &ctx->d_prm, &ctx->d_route, &ctx->d_inl,
-                    &ctx->d_has_in, &ctx->d_init, &ctx->d_wfold, &ctx->d_wcomp, &ctx->d_route_tc, &ctx->d_runs,
+                    &ctx->d_has_in, &ctx->d_init, &ctx->d_wfold, &ctx->d_route_tc, &ctx->d_runs,
                     &ctx->d_nruns, &ctx->d_wflags_tc, &ctx->d_incoming, &ctx->d_word_runs, &ctx->d_pot, &ctx->d_ring, &ctx->d_counts, &ctx->d_lines,
                     &ctx->d_stage, &ctx->d_stage2, &ctx->d_raster, &ctx->d_fired, &ctx->d_exports, &ctx->d_send, &ctx->d_recv,
                     &ctx->d_send_list, &ctx->d_recv_list, &ctx->d_dbg, &ctx->d_inw, &ctx->d_inslot,
@@ -216,7 +216,6 @@ ranc_status ranc_load_network(const ranc_network_desc* net, int cuda_device, ran
   if (!s) s = upload(ctx, &ctx->d_has_in, c.has_in);
   if (!s) s = upload(ctx, &ctx->d_init, c.init);
   if (!s && c.tc_ok) s = upload(ctx, &ctx->d_wfold, c.wfold);
-  if (!s && c.tc_ok) s = upload(ctx, &ctx->d_wcomp, c.wcomp);
   if (!s && c.tc_ok) s = upload(ctx, &ctx->d_route_tc, c.route_tc);
   if (!s && c.tc_ok) s = upload(ctx, &ctx->d_runs, c.runs);
   if (!s && c.tc_ok) s = upload(ctx, &ctx->d_nruns, c.nruns);
@@ -710,8 +709,8 @@ ranc_status ranc_set_option(ranc_ctx* ctx, int option, int64_t value) {
         ctx->err = "kernel variant must be 0 (auto), 1 (popcount) or 2 (tensor core)";
         return RANC_E_ARG;
       }
-      if (value == RANC_KERNEL_TC && !ctx->net.tc_ok) {
-        ctx->err = "network is outside the tensor-core envelope (|w| <= 16383, Npad*32*ceil(A/32) <= 64 KB)";
+      if (value == RANC_KERNEL_TC && (!ctx->net.tc_ok || tc_smem_bytes(ctx->net) > 227 * 1024)) {
+        ctx->err = "network is outside the tensor-core envelope (<= 1024 neurons and <= 512 axons, whose operands and stages fit 227 KB of shared memory)";
         return RANC_E_CONFIG;
       }
       ctx->kernel = (int32_t)value;  // takes effect at the next ranc_load_inputs / ranc_reset_state

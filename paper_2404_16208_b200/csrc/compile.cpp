@@ -264,16 +264,21 @@ ranc_status validate_and_compile(const ranc_network_desc* d, Compiled* out, std:
     }
   }
   // tensor-core eligibility: Wfold of one core fits the 64 KB shared-memory
-  // operand budget (<= 256 neurons) and the folded weights fit int8, or, split
-  // as w = 128*hi + lo (lo in [0,127], hi in [-128,127]), 15 bits; the kernel's
-  // shared-memory layout is checked against 227 KB when the path is chosen
+  // operand budget (<= 256 neurons); the folded weights fit int8, or, split as
+  // w = 256*hi + lo (lo the unsigned low byte, hi in [-128,127]), any 16-bit
+  // weight (the validated range); the kernel's shared-memory layout is
+  // checked against 227 KB when the path is chosen
+  // Larger cores (N <= 1024, A <= 512) run as neuron groups of grp_rows rows
+  // (256 when the axons fit 256 and the padded neurons are whole groups of
+  // 256, else 128), one 64 KB operand per group.
   {
-    bool ok = o.Npad <= 256 && (size_t)o.Npad * o.Kp <= 65536;
+    const bool single = o.Npad <= 256 && (size_t)o.Npad * o.Kp <= 65536;
+    bool ok = single || o.Kp <= 512;
+    o.tc_grp = !single;
+    o.grp_rows = single ? o.Npad : ((o.Kp <= 256 && o.Npad % 256 == 0) ? 256 : 128);
     bool wide = false;
-    for (size_t i = 0; ok && i < (size_t)G * N * K; ++i) {
-      if (d->weight[i] < -127 || d->weight[i] > 127) wide = true;
-      if (d->weight[i] < -16384 || d->weight[i] > 16383) ok = false;
-    }
+    for (size_t i = 0; ok && i < (size_t)G * N * K; ++i)
+      if (d->weight[i] < -128 || d->weight[i] > 127) wide = true;
     o.tc_ok = ok;
     o.tc_wide = ok && wide;
   }
@@ -390,59 +395,31 @@ ranc_status validate_and_compile(const ranc_network_desc* d, Compiled* out, std:
       o.tc_wmajor = 3 * scattered > 2 * (int64_t)G * N;
     }
     // folded weights in the canonical operand layout (tc.h)
-    // (wide weights: [lo | hi] per core, w = 128*hi + lo)
-    const size_t per = (size_t)o.Npad * o.Kp, parts = o.tc_wide ? 2 : 1;
-    o.wfold.assign((size_t)G * parts * per, 0);
+    // (wide weights: [lo | hi] per core, w = 256*hi + lo, lo unsigned)
+    // per core: Npad / grp_rows groups, each [parts][grp_rows * Kp] in the
+    // canonical layout of grp_rows rows (one group = the whole core unless tc_grp)
+    const size_t GS = (size_t)o.grp_rows, per = GS * o.Kp, parts = o.tc_wide ? 2 : 1;
+    o.wfold.assign((size_t)G * parts * o.Npad * o.Kp, 0);
     for (int c = 0; c < G; ++c) {
       const int32_t* inv = &o.inv_tc[(size_t)c * A];
       const uint8_t* ty = d->axon_type + (size_t)c * A;
-      int8_t* dst = &o.wfold[(size_t)c * parts * per];
+      int8_t* const core_dst = &o.wfold[(size_t)c * parts * o.Npad * o.Kp];
       for (int n = 0; n < N; ++n) {
         const size_t cn = (size_t)c * N + n;
         const uint32_t* src = d->crossbar + cn * W;
         for (int a = 0; a < A; ++a)
           if ((src[a >> 5] >> (a & 31)) & 1u) {
             const int w = d->weight[cn * K + ty[a]];
-            const size_t off = tc_operand_offset((uint32_t)n, (uint32_t)inv[a], (uint32_t)o.Npad);
+            int8_t* const dst = core_dst + (size_t)(n / GS) * parts * per;
+            const size_t off = tc_operand_offset((uint32_t)(n % GS), (uint32_t)inv[a], (uint32_t)GS);
             if (!o.tc_wide) {
               dst[off] = (int8_t)w;
             } else {
-              const int hi = w >> 7;   // floor(w / 128): arithmetic shift
-              dst[off] = (int8_t)(w - 128 * hi);
+              const int hi = w >> 8;   // floor(w / 256): arithmetic shift, in [-128, 127]
+              dst[off] = (int8_t)(uint8_t)(w - 256 * hi);   // low byte, read as u8 by the MMA
               dst[per + off] = (int8_t)hi;
             }
           }
-      }
-    }
-    // compact crossbar (int8 weights only): what Wfold is made of, 7x smaller,
-    // expanded into the canonical operand on chip by the tick kernel when
-    // every work item is a new core (few sample tiles per core, config 5):
-    //   xbits u32 [W][Npad]  connection bits in the tensor-core axon order
-    //   tsel  u32 [Kp/4]     axon types of four consecutive axons as byte-
-    //                        permute selector nibbles (type t -> byte t)
-    //   wq    u32 [Npad]     the K <= 4 int8 weights of neuron n, byte t = w[n][t]
-    if (!o.tc_wide) {
-      o.comp_bytes = (int32_t)((size_t)W * o.Npad * 4 + (size_t)o.Kp + (size_t)o.Npad * 4);
-      o.wcomp.assign((size_t)G * o.comp_bytes, 0);
-      for (int c = 0; c < G; ++c) {
-        uint8_t* base = &o.wcomp[(size_t)c * o.comp_bytes];
-        uint32_t* xb = reinterpret_cast<uint32_t*>(base);
-        uint32_t* tsel = reinterpret_cast<uint32_t*>(base + (size_t)W * o.Npad * 4);
-        uint32_t* wq = reinterpret_cast<uint32_t*>(base + (size_t)W * o.Npad * 4 + o.Kp);
-        const int32_t* perm = &o.perm_tc[(size_t)c * A];
-        const int32_t* inv = &o.inv_tc[(size_t)c * A];
-        const uint8_t* ty = d->axon_type + (size_t)c * A;
-        for (int ap = 0; ap < A; ++ap) tsel[ap >> 2] |= (uint32_t)ty[perm[ap]] << (4 * (ap & 3));
-        for (int n = 0; n < N; ++n) {
-          const size_t cn = (size_t)c * N + n;
-          const uint32_t* src = d->crossbar + cn * W;
-          for (int a = 0; a < A; ++a)
-            if ((src[a >> 5] >> (a & 31)) & 1u) {
-              const int ap = inv[a];
-              xb[(size_t)(ap >> 5) * o.Npad + n] |= 1u << (ap & 31);
-            }
-          for (int k = 0; k < K; ++k) wq[n] |= (uint32_t)(uint8_t)(int8_t)d->weight[cn * K + k] << (8 * k);
-        }
       }
     }
   }

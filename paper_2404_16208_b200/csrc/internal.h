@@ -67,13 +67,12 @@ struct TickParams {
   int32_t pot_items;        // multi-tick tensor-core launch: work items (potential tiles) per CTA, 1 or 2
   int32_t out_planes;       // multi-tick tensor-core launch: bit-sliced per-thread output counters in shared memory
   int32_t Kp;               // tensor-core path: K bytes per operand row (= 32*W)
+  int32_t grp_rows;         // tensor-core path: rows per neuron group (Compiled::grp_rows)
   int32_t fault;            // RANC_OPT_DEBUG_FAULT (mutation tests): 1 = skip the grid barrier of
                             // cooperative multi-tick launches
   int64_t t;                // tick being executed
   int64_t raster_t0;        // first tick of the raster buffer
   const uint8_t* wfold;     // tensor-core path: [G][Npad*Kp] canonical-layout int8
-  const uint8_t* wcomp;     // tensor-core path: [G][comp] compact crossbar, expanded on chip
-  int32_t comp;             // bytes per core of wcomp when the compact form is in use, else 0
   const int2* runs;         // tensor-core path: input runs [G][rmax]
   const int32_t* word_runs; // [G][W]: runs overlapping ring word w: first | count << 16
   const uint32_t* inw;      // decoded inputs [T_in][n_inslots][Sr][W] or [..][W][Sr] (the ring's layout), or nullptr
@@ -109,14 +108,14 @@ struct Compiled {
   int32_t Kp = 0;               // 32 * W
   int32_t WIp = 0;              // WI rounded up to 4
   bool tc_ok = false;           // eligible for the tcgen05 kind::i8 path
+  bool tc_grp = false;          // tensor-core path in neuron groups (Npad > 256 or Npad*Kp > 64 KB)
+  int32_t grp_rows = 0;         // rows per neuron group (Npad unless tc_grp: 256 or 128)
   bool any_route = false;       // some neuron has dest_kind ROUTE
   bool any_output = false;      // some neuron has dest_kind OUTPUT
-  bool tc_wide = false;         // some |weight| > 127: Wfold split into lo/hi int8 operands [G][2][Npad*Kp]
+  bool tc_wide = false;         // some weight outside [-128,127]: Wfold split w = 256*hi + lo, [G][2][Npad*Kp] (u8 lo, s8 hi)
   bool tc_wmajor = false;       // automatic ring layout: word-major when most routing neurons sit in
                                 // warps without a shared destination word (per-neuron routes)
   std::vector<int8_t> wfold;    // [G][Npad*Kp] canonical operand layout, tensor-core axon order
-  std::vector<uint8_t> wcomp;   // [G][comp_bytes] compact crossbar (int8 weights only, compile.cpp)
-  int32_t comp_bytes = 0;       // bytes per core of wcomp (0: no compact form)
   std::vector<int32_t> perm_tc, inv_tc;   // tensor-core axon order (sorted by input line)
   std::vector<uint2> route_tc;  // route words with tensor-core destination axons
   std::vector<int2> runs;       // [G][rmax] input runs: x = a'start | len<<16, y = first line
@@ -159,7 +158,7 @@ struct ranc_ctx {
   std::string err;
   ranc::Compiled net;
   // device: compiled network
-  ranc::DevBuf d_xp, d_wp, d_pword, d_prm, d_route, d_inl, d_has_in, d_init, d_wfold, d_wcomp, d_route_tc, d_runs, d_nruns, d_wflags_tc, d_incoming,
+  ranc::DevBuf d_xp, d_wp, d_pword, d_prm, d_route, d_inl, d_has_in, d_init, d_wfold, d_route_tc, d_runs, d_nruns, d_wflags_tc, d_incoming,
       d_word_runs;
   int num_sms = 148;
   // device: state

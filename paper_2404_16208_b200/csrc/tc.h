@@ -36,16 +36,17 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo_bytes
   return d;
 }
 
-// instruction descriptor, kind::i8: D s32, A s8 (signed weights), B u8 (0/1 spikes),
-// both K-major, M x N.
-__host__ __device__ constexpr uint32_t idesc_i8(uint32_t M, uint32_t N) {
-  return (2u << 4)            // c_format = S32
-         | (1u << 7)          // a_format = signed int8
-         | (0u << 10)         // b_format = unsigned int8
-         | (0u << 15)         // a_major = K
-         | (0u << 16)         // b_major = K
-         | ((N >> 3) << 17)   // n_dim
-         | ((M >> 4) << 24);  // m_dim
+// instruction descriptor, kind::i8: D s32, A s8 (signed weights; a_signed =
+// false: u8, the low byte of a 16-bit weight split), B u8 (0/1 spikes), both
+// K-major, M x N.
+__host__ __device__ constexpr uint32_t idesc_i8(uint32_t M, uint32_t N, bool a_signed = true) {
+  return (2u << 4)                      // c_format = S32
+         | ((a_signed ? 1u : 0u) << 7)  // a_format: signed / unsigned int8
+         | (0u << 10)                   // b_format = unsigned int8
+         | (0u << 15)                   // a_major = K
+         | (0u << 16)                   // b_major = K
+         | ((N >> 3) << 17)             // n_dim
+         | ((M >> 4) << 24);            // m_dim
 }
 
 __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,

@@ -69,34 +69,35 @@ constexpr int kSub = 16;               // samples per TMEM load / LIF pass of an
 static_assert(kExpThreads == 2 * NT, "spike stage maps thread -> (sample, 16-bit half)");
 
 enum Bar { FULL0 = 0, SEMPTY0 = 4, BFULL0 = 8, BEMPTY0 = 12, ACCFULL0 = 16, ACCEMPTY0 = 20, WFULL = 24, WFREE = 25,
-           CFULL0 = 26, CFREE0 = 28, WFULL1 = 30, WFREE1 = 31, NBARS = 32 };
+           NBARS = 26 };
 
 struct TcLayout {
-  uint32_t w, runs, lut, potbuf, cplanes, comp, stage, b, raw, lines, stage_bytes, total;
+  uint32_t w, runs, lut, potbuf, cplanes, stage, b, raw, lines, stage_bytes, total;
 };
 
 // WIp: input-line row words (multiple of 4)
-// wide: weights beyond int8 are split w = 128*hi + lo (lo in [0,127], hi in
-// [-128,127]); the two folded operands double the weight buffer and the
+// wide: weights beyond int8 are split w = 256*hi + lo (lo the unsigned low
+// byte, hi in [-128,127]); the two folded operands double the weight buffer and the
 // spike pipeline keeps 2 stages (NS_WIDE) to stay inside 227 KB
 constexpr int NS_WIDE = 2;
 // multi-tick launch: 3 spike stages (its ticks are a latency chain; the
 // freed 20 KB hold the bit-sliced output counters of two items)
 constexpr int NS_MULTI = 3;
-// compact-crossbar launch: two expanded operand buffers (the next core's is
-// expanded while the current one is multiplied) leave room for 2 stages
-constexpr int NS_COMP = 2;
+// neuron-group launch (cores of more than 256 neurons or more than 256
+// axons): one spike stage feeds several groups' MMAs, and a B stage holds up
+// to 512 axons, so 2 stages
+constexpr int NS_GRP = 2;
 // pot_items: potential tiles kept on chip (multi-tick launch with up to two
 // work items per CTA: one region each)
 // cnt_planes: per-thread bit-sliced output-bus counters (multi-tick launch)
 constexpr int kCntPlanes = 8;   // counts < 256 between flushes
-// comp: bytes per core of the compact crossbar (two staging buffers and two
-// expanded operand buffers), 0 = not used
-__host__ __device__ inline TcLayout tc_layout(int Np, int Kp, int W, int WIp, int rmax, bool wide, int pot_items = 1,
-                                              bool cnt_planes = false, bool multi = false, uint32_t comp = 0) {
+// wrows: operand rows held in shared memory (Npad, or the group size of a
+// neuron-group launch, grp)
+__host__ __device__ inline TcLayout tc_layout(int wrows, int Kp, int W, int WIp, int rmax, bool wide, int pot_items = 1,
+                                              bool cnt_planes = false, bool multi = false, bool grp = false) {
   TcLayout L;
   L.w = 1024;
-  uint32_t o = L.w + (uint32_t)Np * Kp * (wide || comp ? 2u : 1u);
+  uint32_t o = L.w + (uint32_t)wrows * Kp * (wide ? 2u : 1u);
   L.runs = o;                                 // int2 [rmax] + int32 [W] of the current core
   o += (uint32_t)rmax * 8 + (uint32_t)W * 4;
   o = (o + 15) & ~15u;
@@ -107,9 +108,6 @@ __host__ __device__ inline TcLayout tc_layout(int Np, int Kp, int W, int WIp, in
   o += (NT / 8) * (32 * 8) * 16 * (uint32_t)pot_items;   // = 4 chunks x 512 epilogue threads per item
   L.cplanes = o;                              // u32 [items][kCntPlanes][512 epilogue threads]
   if (cnt_planes) o += (uint32_t)pot_items * kCntPlanes * 512 * 4;
-  o = (o + 127) & ~127u;
-  L.comp = o;                                 // u8 [2][comp]: compact crossbars of the next cores (TMA)
-  o += 2 * comp;
   L.stage = (o + 1023) & ~1023u;
   uint32_t q = 0;
   L.b = q;     q += (uint32_t)NT * Kp;       // spikes as 0/1 bytes, canonical layout
@@ -118,7 +116,7 @@ __host__ __device__ inline TcLayout tc_layout(int Np, int Kp, int W, int WIp, in
   q = (q + 15) & ~15u;
   L.lines = q; q += (uint32_t)NT * (WIp > W ? WIp : W) * 4;  // input line rows or decoded words (TMA)
   L.stage_bytes = (q + 1023) & ~1023u;
-  L.total = L.stage + (wide ? NS_WIDE : multi ? NS_MULTI : comp ? NS_COMP : NS) * L.stage_bytes;
+  L.total = L.stage + (grp ? NS_GRP : wide ? NS_WIDE : multi ? NS_MULTI : NS) * L.stage_bytes;
   return L;
 }
 
@@ -211,13 +209,17 @@ __device__ __forceinline__ uint32_t lif(const uint4 (&cur)[NE / 8], const uint32
 // registers between ticks (stored once, after the last tick).
 // kWm: word-major scheduler rings (compile-time, so each instantiation only
 // carries its own layout's code)
-// kWide: weights split into lo/hi int8 operands, two MMAs and two TMEM
-// accumulators per tile, acc = acc_lo + 128 * acc_hi in the epilogue
-// kComp: the compact crossbar (p.comp bytes per core) is staged by TMA and
-// expanded on chip into two alternating operand buffers
-template <bool kMulti, bool kDebug, bool kWm, bool kWide, bool kComp = false>
+// kWide: 16-bit weights split into a u8 low byte and an s8 high byte, two MMAs and two TMEM
+// accumulators per tile, acc = acc_lo + 256 * acc_hi in the epilogue
+// kGrp: cores of up to 1024 neurons / 512 axons.  The neurons are processed in
+// groups of p.grp_rows (256 or 128) rows: per (core, sample tile) work item
+// the spike operand is built once and multiplied with each group's Wfold
+// (loaded in turn into the one operand buffer), every group filling its own
+// accumulator stage and being retired by the epilogue like a work item of
+// its own (a sub-item).  Per-tick launches only.
+template <bool kMulti, bool kDebug, bool kWm, bool kWide, bool kGrp = false>
 __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams p, const int nticks_arg) {
-  static_assert(!kComp || (!kMulti && !kWide), "the compact crossbar is a per-tick int8 launch");
+  static_assert(!kGrp || !kMulti, "neuron groups are a per-tick launch");
   const int nticks = kMulti ? nticks_arg : 1;
   // kDebug: the RANC_DEBUG_TIMELINE instrumentation (a separate instantiation,
   // so that the product kernel issues none of it)
@@ -229,18 +231,14 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + 8 * NBARS);
   const int Np = p.Npad, Kp = p.Kp, W = p.W, WIp = p.WIp;
-  const TcLayout L = tc_layout(Np, Kp, W, WIp, p.rmax, kWide, kMulti ? p.pot_items : 1, kMulti && p.out_planes, kMulti,
-                               kComp ? (uint32_t)p.comp : 0u);
-  // compact crossbar (p.comp > 0, per-tick int8 launches with few tiles per
-  // core): the producer stages each core's 7x smaller crossbar bits, axon
-  // types and weights (two buffers), the spike warps expand them into the
-  // canonical operand w_s, so the operand costs ~10 KB of HBM per core
-  // instead of 64 KB
-  constexpr bool comp = kComp;
-  const uint32_t wbuf_bytes = (uint32_t)Np * Kp;   // one expanded operand (kComp: two, alternating per core)
-  constexpr int NS = kWide ? NS_WIDE : kMulti ? NS_MULTI : kComp ? NS_COMP : ranc::NS;   // spike stages in use
+  // operand rows per sub-item and sub-items (neuron groups) per work item
+  const int GS = kGrp ? p.grp_rows : Np;
+  const int nGrp = kGrp ? Np / GS : 1;
+  const TcLayout L =
+      tc_layout(GS, Kp, W, WIp, p.rmax, kWide, kMulti ? p.pot_items : 1, kMulti && p.out_planes, kMulti, kGrp);
+  constexpr int NS = kGrp ? NS_GRP : kWide ? NS_WIDE : kMulti ? NS_MULTI : ranc::NS;   // spike stages in use
   uint8_t* w_s = smem + L.w;
-  const int Mh = Np >> 7;
+  const int Mh = GS >> 7;
   const int nT = (p.S + NT - 1) / NT;
   const int total = p.G_loc * nT;
   const int lo = (int)((int64_t)blockIdx.x * total / gridDim.x);
@@ -285,12 +283,6 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
     }
     ptx::mbar_init(&bars[WFULL], 1);
     ptx::mbar_init(&bars[WFREE], 1);
-    ptx::mbar_init(&bars[WFULL1], 1);
-    ptx::mbar_init(&bars[WFREE1], 1);
-    for (int i = 0; i < 2; ++i) {
-      ptx::mbar_init(&bars[CFULL0 + i], 1);
-      ptx::mbar_init(&bars[CFREE0 + i], 1);
-    }
     ptx::fence_mbar_init();
   }
   // programmatic dependent launch (per-tick launches): let the next tick's
@@ -321,25 +313,13 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       const int k = it * nwork + k0;                 // pipeline index (barrier phases)
       const int c = p.c_lo + cl;
       const int s = k % NS, u = k / NS;
-      if (c != prev_core) {
+      if (!kGrp && c != prev_core) {
         ++jw;
-        if (comp) {
-          // compact crossbar into staging buffer jw & 1 once the spike warps
-          // have expanded the core that used it before
-          const int cs = jw & 1, cu = jw >> 1;
-          if (jw >= 2) wait(&bars[CFREE0 + cs], (cu - 1) & 1);
-          if (lane == 0) {
-            ptx::mbar_arrive_expect_tx(&bars[CFULL0 + cs], (uint32_t)p.comp);
-            ptx::bulk_g2s(smem + L.comp + cs * p.comp, p.wcomp + (size_t)c * p.comp, (uint32_t)p.comp,
-                          &bars[CFULL0 + cs]);
-          }
-        } else {
-          if (jw > 0) wait(&bars[WFREE], (jw - 1) & 1);
-          if (lane == 0) {
-            const uint32_t wb = (uint32_t)Np * Kp * (kWide ? 2u : 1u);   // wide: [lo | hi]
-            ptx::mbar_arrive_expect_tx(&bars[WFULL], wb);
-            ptx::bulk_g2s(w_s, p.wfold + (size_t)c * wb, wb, &bars[WFULL]);
-          }
+        if (jw > 0) wait(&bars[WFREE], (jw - 1) & 1);
+        if (lane == 0) {
+          const uint32_t wb = (uint32_t)Np * Kp * (kWide ? 2u : 1u);   // wide: [lo | hi]
+          ptx::mbar_arrive_expect_tx(&bars[WFULL], wb);
+          ptx::bulk_g2s(w_s, p.wfold + (size_t)c * wb, wb, &bars[WFULL]);
         }
         prev_core = c;
       }
@@ -375,6 +355,20 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
           ptx::bulk_g2s(st + L.lines, p.lines + ((size_t)t * p.Sr + s0) * WIp, line_bytes, &bars[FULL0 + s]);
       }
       __syncwarp();
+      if (kGrp) {
+        // the groups' operands in turn, each once the MMAs of the previous
+        // one have read the buffer (Wfold per core: nGrp blocks of wb bytes)
+        const uint32_t wb = (uint32_t)GS * Kp * (kWide ? 2u : 1u);
+        for (int g = 0; g < nGrp; ++g) {
+          ++jw;
+          if (jw > 0) wait(&bars[WFREE], (jw - 1) & 1);
+          if (lane == 0) {
+            ptx::mbar_arrive_expect_tx(&bars[WFULL], wb);
+            ptx::bulk_g2s(w_s, p.wfold + ((size_t)c * nGrp + g) * wb, wb, &bars[WFULL]);
+          }
+          __syncwarp();
+        }
+      }
     }
     tick_barrier();
     // the next tick's ring rows were written through the generic proxy
@@ -387,7 +381,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
     // ------------------------------------------------------------ MMA issuer
     // convergent warp loop; one elected thread issues the tcgen05 operations
     const uint32_t id = tc::idesc_i8(128, NT);
-    const uint32_t lbo_a = (uint32_t)Np * 16, lbo_b = (uint32_t)NT * 16;   // tc.h layout
+    // wide weights: w = 256*hi + lo, lo the UNSIGNED low byte, hi signed
+    const uint32_t id_lo = kWide ? tc::idesc_i8(128, NT, false) : id;
+    const uint32_t lbo_a = (uint32_t)GS * 16, lbo_b = (uint32_t)NT * 16;   // tc.h layout
     int prev_core = -1, jw = -1;
     for (int it = 0; it < nticks; ++it) {
     int cl = lo / nT, tile = lo - (lo / nT) * nT;
@@ -395,16 +391,20 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       const int k = it * nwork + k0;
       const int c = cl;
       const int s = k % NS, u = k / NS;
-      const int a = k % NA, ua = k / NA;
-      if (c != prev_core) {
+      if (!kGrp && c != prev_core) {
         ++jw;
-        if (comp) wait(&bars[(jw & 1) ? WFULL1 : WFULL], (jw >> 1) & 1);
-        else wait(&bars[WFULL], jw & 1);
+        wait(&bars[WFULL], jw & 1);
         prev_core = c;
       }
-      const uint8_t* w_cur = w_s + (comp ? (uint32_t)(jw & 1) * wbuf_bytes : 0u);
       wait(&bars[BFULL0 + s], u & 1);
       if (lane == 0) stamp_k(k, 5);
+      for (int g = 0; g < nGrp; ++g) {
+      const int j = k * nGrp + g;          // sub-item: accumulator ring index
+      const int a = j % NA, ua = j / NA;
+      if (kGrp) {   // every group is a new operand
+        ++jw;
+        wait(&bars[WFULL], jw & 1);
+      }
       wait(&bars[ACCEMPTY0 + a], (ua & 1) ^ 1);
       tc::fence_after();
       if (lane == 0) {
@@ -413,25 +413,26 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
         const uint32_t acc = tmem + a * acc_stride;
         for (int hh = 0; hh < Mh; ++hh)
           for (int kk = 0; kk < Kp / 32; ++kk) {
-            const uint64_t ad = tc::smem_desc(ptx::smem_u32(w_cur + hh * 2048 + kk * 2 * lbo_a), lbo_a, 128);
+            const uint64_t ad = tc::smem_desc(ptx::smem_u32(w_s + hh * 2048 + kk * 2 * lbo_a), lbo_a, 128);
             const uint64_t bd = tc::smem_desc(ptx::smem_u32(b_s + kk * 2 * lbo_b), lbo_b, 128);
-            tc::mma_i8(acc + hh * NT, ad, bd, id, kk > 0 ? 1u : 0u);
+            tc::mma_i8(acc + hh * NT, ad, bd, id_lo, kk > 0 ? 1u : 0u);
             if (kWide) {
-              const uint64_t ah = tc::smem_desc(ptx::smem_u32(w_s + Np * Kp + hh * 2048 + kk * 2 * lbo_a), lbo_a, 128);
+              const uint64_t ah = tc::smem_desc(ptx::smem_u32(w_s + GS * Kp + hh * 2048 + kk * 2 * lbo_a), lbo_a, 128);
               tc::mma_i8(acc + (Mh + hh) * NT, ah, bd, id, kk > 0 ? 1u : 0u);
             }
           }
-        tc::commit(&bars[BEMPTY0 + s]);
+        if (g + 1 == nGrp) tc::commit(&bars[BEMPTY0 + s]);
         tc::commit(&bars[ACCFULL0 + a]);
         stamp_k(k, 7);
         // the next item (in a multi-tick launch: cyclically, the CTA's first
         // item of the next tick) belongs to another core, or this is the end
+        // (neuron groups: every sub-item has its own operand)
         const bool last_item = k0 + 1 == nwork;
         const int next_cl = last_item ? lo / nT : (tile + 1 == nT ? cl + 1 : cl);
-        if ((last_item && it + 1 == nticks) || next_cl != cl)
-          tc::commit(&bars[comp && (jw & 1) ? WFREE1 : WFREE]);
+        if (kGrp || (last_item && it + 1 == nticks) || next_cl != cl) tc::commit(&bars[WFREE]);
       }
       __syncwarp();
+      }
     }
     tick_barrier();
     }
@@ -601,10 +602,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
     const int ew = warp - kFirstEpi;
     const int q = warp & 3;
     const int h = (ew >> 2) & 1, jj = ew >> 3;
-    const int n = h * 128 + q * 32 + lane;
+    // neuron of this thread in group g: n0 + g * GS (one group unless kGrp)
+    const int n0 = h * 128 + q * 32 + lane;
+    int n = n0;
     const bool active = h < Mh;
-    const bool valid = active && n < p.N;
-    int prev_core = -1;
+    bool valid = active && n < p.N;
+    int prev_core = -1;   // key of the parameters in registers: core (* nGrp + group)
     int leak = 0, pth = 0, nth = 0, rst = 0, init = 0, bf = 0, bn = 0, linmul = 0;
     uint32_t kind = RK_NONE, cls = 0, axbit = 0, out_lanes = 0, out_peers = 0;
     bool route_here = false, exporting = false, block_route = false, block_identity = false, has_output = false;
@@ -619,68 +622,6 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
     static_assert(NT == 64 && kSub == 16, "two 32-sample halves, two passes each");
     constexpr int kPass = 32 / kSub, kCh = kSub / 8;   // passes per half, chunks per pass
     uint4* pbuf = reinterpret_cast<uint4*>(smem + L.potbuf) + (threadIdx.x - 32 * kFirstEpi);
-    // word-major rings (scattered routes, e.g. config 5) want the ring to stay
-    // in L2 next to the potential stream: there the potentials may be loaded
-    // and stored evict-first (RANC_WM_EVICT_FIRST builds, an experiment)
-#ifdef RANC_WM_EVICT_FIRST
-    constexpr bool kEvictFirstPot = kWm;
-#else
-    constexpr bool kEvictFirstPot = false;
-#endif
-    const uint64_t pot_pol = kEvictFirstPot ? ptx::policy_evict_first() : 0ull;
-    auto pot_load = [&](void* d, const void* g) {
-      if (kEvictFirstPot) ptx::cp_async16_hint(d, g, pot_pol);
-      else ptx::cp_async16(d, g);
-    };
-    // kComp: the 16 epilogue warps expand the compact crossbar of the NEXT
-    // core into the other operand buffer before they wait for this item's
-    // accumulator (they wait there anyway), so the MMAs of the next core
-    // never wait for an operand load.  Byte (n, a') = conn ? w[n][type(a')]
-    // : 0 is one byte permute per four axons: the selector nibble is the
-    // axon's type (a byte of wq) or, for a missing connection, 4 + type (a
-    // byte of the zero second operand; the table lut[16 + bits]).  The
-    // buffer refilled last held core jw - 1, whose MMAs completed before
-    // this warp passed that core's last accumulator barrier.
-    int jw_e = -1;
-    uint32_t* const lutc = reinterpret_cast<uint32_t*>(smem + L.lut) + 16;
-    if (comp && threadIdx.x - 32 * kFirstEpi < 16) {
-      // selector bit 2 of nibble j set iff bit j of b is clear (a missing
-      // connection selects a zero byte); ordered by the first expansion's bar 3
-      const int b = threadIdx.x - 32 * kFirstEpi;
-      uint32_t z = 0u;
-      for (int j = 0; j < 4; ++j)
-        if (!((b >> j) & 1)) z |= 4u << (4 * j);
-      lutc[b] = z;
-    }
-    auto expand_core = [&](int cglob) {
-      (void)cglob;
-      ++jw_e;
-      const int cs = jw_e & 1, cu = jw_e >> 1;   // staging buffer = operand buffer = jw_e & 1
-      ptx::mbar_wait(&bars[CFULL0 + cs], cu & 1);
-      const uint8_t* cb = smem + L.comp + cs * p.comp;
-      const uint32_t* xb = reinterpret_cast<const uint32_t*>(cb);                          // [W][Np]
-      const uint32_t* tsel = reinterpret_cast<const uint32_t*>(cb + (size_t)W * Np * 4);     // [Kp/4]
-      const uint32_t* wq = reinterpret_cast<const uint32_t*>(cb + (size_t)W * Np * 4 + Kp);  // [Np]
-      uint8_t* const w_dst = w_s + (uint32_t)cs * wbuf_bytes;
-      const int et512 = threadIdx.x - 32 * kFirstEpi;
-      const int nq = Np * (Kp / 16);   // 16-byte chunks: chunk q = (K chunk q / Np, neuron q % Np)
-#pragma unroll 2
-      for (int q = et512; q < nq; q += 32 * kEpiWarps) {
-        const int nn = q % Np, kc = q / Np;
-        const uint32_t b16 = xb[(size_t)(kc >> 1) * Np + nn] >> (16 * (kc & 1));
-        const uint32_t wv = wq[nn];
-        const uint4 sel = *reinterpret_cast<const uint4*>(tsel + kc * 4);
-        *reinterpret_cast<uint4*>(w_dst + tc::operand_offset((uint32_t)nn, (uint32_t)(16 * kc), (uint32_t)Np)) =
-            make_uint4(__byte_perm(wv, 0u, lutc[b16 & 15u] | sel.x), __byte_perm(wv, 0u, lutc[(b16 >> 4) & 15u] | sel.y),
-                       __byte_perm(wv, 0u, lutc[(b16 >> 8) & 15u] | sel.z), __byte_perm(wv, 0u, lutc[(b16 >> 12) & 15u] | sel.w));
-      }
-      ptx::fence_proxy_async_smem();   // generic writes -> the tensor core's (async proxy) reads
-      named_sync(3, 32 * kEpiWarps);
-      if (et512 == 0) {
-        ptx::mbar_arrive(&bars[cs ? WFULL1 : WFULL]);
-        ptx::mbar_arrive(&bars[CFREE0 + cs]);
-      }
-    };
     constexpr int PB = 32 * kEpiWarps;   // uint4 stride between chunks in potbuf
     constexpr int kItem = kPass * kCh * PB;   // uint4 per item region (multi-tick launch): 32 KB
     // multi-tick launch: output-bus counts of this thread's 32 samples, bit-
@@ -707,7 +648,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       for (int sb = 0; sb < kPass; ++sb) {
 #pragma unroll
         for (int i = 0; i < kCh; ++i)
-          pot_load(pbuf + (kCh * sb + i) * PB, dst + (size_t)(kCh * sb + i) * Np);
+          ptx::cp_async16(pbuf + (kCh * sb + i) * PB, dst + (size_t)(kCh * sb + i) * Np);
         ptx::cp_async_commit();
       }
     }
@@ -718,15 +659,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
     short4 nprm = make_short4(0, 0, 0, 0);
     uint2 nrt = make_uint2(0u, 0u);
     int nini = 0;
-    if (active && nwork > 0) {
+    if (!kMulti && active && nwork > 0) {
       const size_t nc = (size_t)(p.c_lo + cl0) * Np + n;
       nprm = p.prm[nc];
       nrt = p.route[nc];
       nini = p.init[nc];
-    }
-    if (comp && nwork > 0) {
-      named_sync(3, 32 * kEpiWarps);   // lutc is written
-      expand_core(p.c_lo + cl0);
     }
     // this thread's TMEM lane and column offset (the stage adds a * acc_stride)
     const uint32_t tmem_lane_base = tmem + ((uint32_t)(q * 32) << 16) + h * NT + jj * 32;
@@ -748,27 +685,41 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
     dst = dst0;
     for (int k0 = 0; k0 < nwork; ++k0, dst += tile_stride) {
       const int k = it * nwork + k0;
-      const int c = p.c_lo + cl;
-      const int a = k % NA, ua = k / NA;
       const int s0 = tile * NT, ns = min(NT, p.S - s0);
-      const bool pf = load && k0 + 1 < nwork;
-      const uint4* nsrc = dst + tile_stride;
+      const int ncl = (k0 + 1 == nwork) ? cl0 : (tile + 1 == nT ? cl + 1 : cl);   // next item's core
+      for (int g = 0; g < nGrp; ++g) {
+      const int j = k * nGrp + g;   // sub-item (neuron group g of item k): accumulator ring index
+      const int c = p.c_lo + cl;
+      const int key = kGrp ? c * nGrp + g : c;
+      const int a = j % NA, ua = j / NA;
+      n = n0 + g * GS;
+      valid = active && n < p.N;
+      uint4* const dsub = dst + g * GS;   // this group's rows of the potential tile
+      const bool pf = load && (g + 1 < nGrp || k0 + 1 < nwork);
+      const uint4* nsrc = g + 1 < nGrp ? dsub + GS : dst + tile_stride;
       const long long tw0 = dbg_on ? clock64() : 0;
       // a new core's neuron parameters were requested a whole work item
       // ahead (one tile per core at config 5: the loads would otherwise stall
       // the epilogue at every item); prefetch the next item's now
-      const short4 prm = nprm;
-      const uint2 rt = nrt;
-      const int ini = nini;
-      {
-        const int ncl = (k0 + 1 == nwork) ? cl0 : (tile + 1 == nT ? cl + 1 : cl);
-        if (active && ncl != cl) {
-          const size_t nc = (size_t)(p.c_lo + ncl) * Np + n;
+      // (the multi-tick launch, at most two items per CTA, loads them in place)
+      short4 prm = nprm;
+      uint2 rt = nrt;
+      int ini = nini;
+      if (kMulti && active && key != prev_core) {
+        const size_t nc = (size_t)c * Np + n;
+        prm = p.prm[nc];
+        rt = p.route[nc];
+        ini = p.init[nc];
+      }
+      if (!kMulti && active) {
+        const int nkc = g + 1 < nGrp ? cl : ncl;            // next sub-item: core, neuron
+        const int nkn = g + 1 < nGrp ? n + GS : n0;
+        if (nkc != cl || nkn != n) {
+          const size_t nc = (size_t)(p.c_lo + nkc) * Np + nkn;
           nprm = p.prm[nc];
           nrt = p.route[nc];
           nini = p.init[nc];
         }
-        if (comp && k0 + 1 < nwork && ncl != cl) expand_core(p.c_lo + ncl);
       }
       // one warp per lane quarter polls the accumulator barrier; the other
       // three wait on the quarter's named barrier (no issue slots spent)
@@ -780,7 +731,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       if (lane == 0 && ew == 0) stamp_k(k, 8);
       tc::fence_after();
       if (active) {
-        if (c != prev_core) {
+        if (key != prev_core) {
           leak = prm.x; pth = prm.y; nth = prm.z; rst = prm.w;
           init = ini;
           if (p.fresh && first) {
@@ -827,7 +778,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
           out_peers = __match_any_sync(0xFFFFFFFFu, kind == RK_OUTPUT ? cls : 0xFFFFFFFFu);
           // more than 8 class groups: per-lane adds (see the output bus below)
           out_scatter = __popc(__ballot_sync(0xFFFFFFFFu, kind == RK_OUTPUT && __ffs(out_peers) - 1 == lane)) > 8;
-          prev_core = c;
+          prev_core = key;
         }
         // this item's potential region: the multi-tick launch keeps one per
         // item (pb) and prefetches the next item's into its own (pbn)
@@ -847,12 +798,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
         for (int sb = 0; sb < kPass; ++sb) {
           uint32_t acc[kSub];
           tc::ld16(acc_addr + sb * kSub, acc);
-          if (kWide) {   // acc = lo + 128 * hi (exact in int32)
+          if (kWide) {   // acc = lo + 256 * hi (exact in int32: |acc| < 2^26 for A <= 1024)
             uint32_t hi[kSub];
             tc::ld16(acc_addr + Mh * NT + sb * kSub, hi);
             tc::wait_ld();
 #pragma unroll
-            for (int i = 0; i < kSub; ++i) acc[i] += hi[i] << 7;
+            for (int i = 0; i < kSub; ++i) acc[i] += hi[i] << 8;
           }
           // this pass's potentials are in pbuf: prefetched a tile ago
           // (cp.async), kept from the previous tick (multi-tick launch), or
@@ -867,7 +818,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
               const char* nb = reinterpret_cast<const char*>(nsrc);
 #pragma unroll
               for (int i = 0; i < kCh; ++i)
-                pot_load(pbn + (kCh * sb + i) * PB, nb + (uint32_t)((kCh * sb + i) * chunk_bytes));
+                ptx::cp_async16(pbn + (kCh * sb + i) * PB, nb + (uint32_t)((kCh * sb + i) * chunk_bytes));
             }
             ptx::cp_async_commit();   // (possibly empty) group: keeps the wait_group 1 accounting
           }
@@ -883,8 +834,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
           for (int cc = 0; cc < kCh; ++cc) {
             const uint4 o = make_uint4(outw[4 * cc + 0], outw[4 * cc + 1], outw[4 * cc + 2], outw[4 * cc + 3]);
             if (!last) pb[(kCh * sb + cc) * PB] = o;   // kept on chip for the next tick
-            else if (kEvictFirstPot) ptx::st16_cs(reinterpret_cast<char*>(dst) + (uint32_t)((kCh * sb + cc) * chunk_bytes), o);
-            else POT_STORE(reinterpret_cast<char*>(dst) + (uint32_t)((kCh * sb + cc) * chunk_bytes), o);
+            else POT_STORE(reinterpret_cast<char*>(dsub) + (uint32_t)((kCh * sb + cc) * chunk_bytes), o);
           }
         }
         // a5 / a6: route or count the spikes of real samples
@@ -994,6 +944,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       __syncwarp();
       if (lane == 0 && ew == 0) stamp_k(k, 11);
       if (lane == 0) ptx::mbar_arrive(&bars[ACCEMPTY0 + a]);
+      }
       if (++tile == nT) {
         tile = 0;
         ++cl;
@@ -1088,7 +1039,9 @@ cudaError_t decode_inputs_tc(ranc_ctx* ctx) {
 
 int tc_tile() { return NT; }
 
-size_t tc_smem_bytes(const Compiled& n) { return tc_layout(n.Npad, n.Kp, n.W, n.WIp, n.rmax, n.tc_wide).total; }
+size_t tc_smem_bytes(const Compiled& n) {
+  return tc_layout(n.grp_rows, n.Kp, n.W, n.WIp, n.rmax, n.tc_wide, 1, false, false, n.tc_grp).total;
+}
 
 namespace {
 
@@ -1105,8 +1058,7 @@ void tc_fill_params(ranc_ctx* ctx, TickParams& p) {
   p.n_inslots = ctx->n_inslots;
   p.nruns = (const int32_t*)ctx->d_nruns.p;
   p.rmax = n.rmax;
-  p.wcomp = (const uint8_t*)ctx->d_wcomp.p;
-  p.comp = 0;
+  p.grp_rows = n.grp_rows;
   p.wmajor = ctx->ring_wmajor ? 1 : 0;
   p.any_route = n.any_route ? 1 : 0;
 }
@@ -1115,7 +1067,8 @@ void tc_fill_params(ranc_ctx* ctx, TickParams& p) {
 
 bool tc_multi_eligible(const ranc_ctx* ctx, int64_t num_ticks) {
   if (ctx->kernel_active != RANC_KERNEL_TC || ctx->shard_mode == RANC_SHARD_CORES || num_ticks < 2) return false;
-  if (ctx->stream_opt == 1 || getenv("RANC_DEBUG_TIMELINE") || ctx->net.tc_wide) return false;   // (_MULTI: kept)
+  if (ctx->stream_opt == 1 || getenv("RANC_DEBUG_TIMELINE") || ctx->net.tc_wide || ctx->net.tc_grp)
+    return false;   // (_MULTI: kept)
   const int64_t total = (int64_t)ctx->G_loc * ((ctx->S + NT - 1) / NT);
   if (total <= ctx->num_sms) return true;   // one work item per CTA, one CTA per SM (cooperative launch)
   // two work items per CTA: both potential tiles stay in shared memory
@@ -1189,18 +1142,7 @@ cudaError_t launch_tick_tc(ranc_ctx* ctx, TickParams p) {
   tc_fill_params(ctx, p);
   const int64_t total = (int64_t)ctx->G_loc * ((ctx->S + NT - 1) / NT);
   const int grid = (int)std::min<int64_t>(total, ctx->num_sms);
-  // compact crossbar when most work items start a new core (<= 4 sample
-  // tiles per core, e.g. config 5's 64 samples): the 64 KB operand of every
-  // core would otherwise be re-read from HBM every tick.  RANC_DEBUG_WCOMP=0/1
-  // forces it off / on (timing comparisons).
-  static const int wcomp_env = getenv("RANC_DEBUG_WCOMP") ? atoi(getenv("RANC_DEBUG_WCOMP")) : -1;
-  const int64_t nT = (ctx->S + NT - 1) / NT;
-  const bool comp = !n.tc_wide && n.comp_bytes > 0 && ctx->d_wcomp.p && (wcomp_env >= 0 ? wcomp_env == 1 : nT <= 4) &&
-                    tc_layout(n.Npad, n.Kp, n.W, n.WIp, n.rmax, false, 1, false, false, (uint32_t)n.comp_bytes).total <=
-                        227 * 1024;
-  p.comp = comp ? n.comp_bytes : 0;
-  const size_t smem =
-      tc_layout(n.Npad, n.Kp, n.W, n.WIp, n.rmax, n.tc_wide, 1, false, false, (uint32_t)p.comp).total;
+  const size_t smem = tc_smem_bytes(n);
   static std::atomic<uint64_t> configured{0};
   if (first_use_on_device(configured)) {
     const void* fns[] = {(const void*)tick_tc_kernel<false, false, false, false>,
@@ -1210,22 +1152,22 @@ cudaError_t launch_tick_tc(ranc_ctx* ctx, TickParams p) {
                          (const void*)tick_tc_kernel<false, false, false, true>,
                          (const void*)tick_tc_kernel<false, false, true, true>,
                          (const void*)tick_tc_kernel<false, false, false, false, true>,
-                         (const void*)tick_tc_kernel<false, true, false, false, true>,
                          (const void*)tick_tc_kernel<false, false, true, false, true>,
-                         (const void*)tick_tc_kernel<false, true, true, false, true>};
+                         (const void*)tick_tc_kernel<false, false, false, true, true>,
+                         (const void*)tick_tc_kernel<false, false, true, true, true>};
     for (const void* f : fns) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   }
   static const bool dbg_env = getenv("RANC_DEBUG_TIMELINE") != nullptr;
-  const bool dbg = dbg_env && !n.tc_wide;
+  const bool dbg = dbg_env && !n.tc_wide && !n.tc_grp;
   if (dbg && !ctx->d_dbg.p) dev_alloc(ctx, &ctx->d_dbg, kDbg * 8);
   p.dbg = dbg ? (unsigned long long*)ctx->d_dbg.p : nullptr;
   if (dbg) cudaMemsetAsync(ctx->d_dbg.p, 0, kDbg * 8, ctx->stream);
-  const void* fn = n.tc_wide ? (p.wmajor ? (const void*)tick_tc_kernel<false, false, true, true>   // wide: no timeline
+  const void* fn = n.tc_grp ? (n.tc_wide ? (p.wmajor ? (const void*)tick_tc_kernel<false, false, true, true, true>
+                                                      : (const void*)tick_tc_kernel<false, false, false, true, true>)
+                                         : (p.wmajor ? (const void*)tick_tc_kernel<false, false, true, false, true>
+                                                      : (const void*)tick_tc_kernel<false, false, false, false, true>))
+                   : n.tc_wide ? (p.wmajor ? (const void*)tick_tc_kernel<false, false, true, true>   // wide: no timeline
                                           : (const void*)tick_tc_kernel<false, false, false, true>)
-                   : comp ? (dbg ? (p.wmajor ? (const void*)tick_tc_kernel<false, true, true, false, true>
-                                             : (const void*)tick_tc_kernel<false, true, false, false, true>)
-                                 : (p.wmajor ? (const void*)tick_tc_kernel<false, false, true, false, true>
-                                             : (const void*)tick_tc_kernel<false, false, false, false, true>))
                    : dbg ? (p.wmajor ? (const void*)tick_tc_kernel<false, true, true, false>
                                      : (const void*)tick_tc_kernel<false, true, false, false>)
                          : (p.wmajor ? (const void*)tick_tc_kernel<false, false, true, false>

@@ -132,3 +132,45 @@ def test_envelope_multi_tick_calls(ranc, oracle_mod):
         assert np.array_equal(sim.outputs(), o.counts()), net.name
         assert np.array_equal(sim.pending(), o.pending()), net.name
         sim.close()
+
+
+@pytest.mark.parametrize("kernel", ["tc", "popc"])
+@pytest.mark.parametrize("A,N", [(512, 1024), (256, 1024), (300, 257), (512, 128)])
+def test_bigcore_every_tick(ranc, oracle_mod, kernel, A, N):
+    """Cores beyond 256 x 256: on the tensor cores they run as
+    neuron groups (256 rows when A <= 256 and Npad % 256 == 0, else 128);
+    full state against the oracle after every tick, 70 samples (a ragged
+    second tile)."""
+    from workloads.gen import bigcore
+    net, inp = bigcore(S=70, T=8, A=A, N=N, grid=2)
+    sim = ranc.Simulator(net)
+    sim.set_option(ranc.OPT_KERNEL, 2 if kernel == "tc" else 1)
+    sim.set_trace(ranc.TRACE_SPIKE_RASTER)
+    sim.load_inputs(inp)
+    assert sim.info()["kernel"] == (2 if kernel == "tc" else 1)
+    o = oracle_mod.Oracle(net, inp)
+    for t in range(8):
+        sim.run(1)
+        o.run(1)
+        where = f"{net.name} tick {t}"
+        assert np.array_equal(sim.potentials(), o.potentials()), where + " potentials"
+        assert np.array_equal(sim.raster()[0], o.fired()), where + " fired"
+        assert np.array_equal(sim.pending(), o.pending()), where + " pending"
+        assert np.array_equal(sim.outputs(), o.counts()), where + " counts"
+    sim.close()
+
+
+def test_bigcore_full_size_digests(ranc):
+    """The bench's big-core workload (16 cores of 512 axons x 1024 neurons,
+    4096 samples, 20 ticks) on the tensor cores in neuron groups: per-tick
+    digests of one sample from each of 16 tiles spread over the batch."""
+    from workloads.gen import bigcore
+    net, inp = bigcore()
+    T = net.meta["T"]
+    d, cnt, pot, info = gpu_digests(ranc, net, inp, T)
+    assert info["kernel"] == 2
+    idx = np.array([64 * k * 4 + (k * 13) % 64 for k in range(16)])
+    (ref_d, ref_c, ref_p), = oracle_digests([(net, inp, idx, T)])
+    check_digests("bigcore", d, ref_d, idx)
+    assert np.array_equal(cnt[idx], ref_c)
+    assert np.array_equal(pot[idx], ref_p)

@@ -267,19 +267,23 @@ def test_ring_layout_switch_at_reset(ranc, oracle_mod):
 
 
 def test_tc_envelope_rejects_wide_weights(ranc):
-    """|w| <= 127: one int8 operand; |w| <= 16383: the lo/hi split (wide
-    variant); beyond 15 bits the tensor-core path is refused."""
+    """Weights of any valid width run on the tensor cores (-128..127: one s8
+    operand; 16-bit: w = 256*hi + lo, a u8 and an s8 operand), and cores of up
+    to 1024 neurons and 512 axons (neuron groups); more axons are refused."""
     from workloads.gen import random_network
     net = random_network(3, 2, 1, 64, 64, 4, 3, wb=16)
-    net.weight[:] = np.clip(net.weight, -16384, 16383)
-    net.weight[0, 0, 0] = 1000
+    net.weight[0, 0, :2] = [-32768, 32767]
     sim = ranc.Simulator(net)
-    sim.set_option(ranc.OPT_KERNEL, 2)   # 15-bit weights: accepted
+    sim.set_option(ranc.OPT_KERNEL, 2)   # 16-bit weights: accepted
     sim.close()
-    net.weight[0, 0, 1] = 20000
+    net = random_network(3, 1, 1, 64, 300, 4, 3, wb=16)
+    sim = ranc.Simulator(net)
+    sim.set_option(ranc.OPT_KERNEL, 2)   # > 256 neurons: neuron groups
+    sim.close()
+    net = random_network(3, 1, 1, 600, 64, 4, 3, wb=16)
     sim = ranc.Simulator(net)
     with pytest.raises(ranc.RancError) as ei:
-        sim.set_option(ranc.OPT_KERNEL, 2)
+        sim.set_option(ranc.OPT_KERNEL, 2)   # > 512 axons: popcount only
     assert ei.value.code == "RANC_E_CONFIG"
     sim.close()
 
@@ -287,13 +291,13 @@ def test_tc_envelope_rejects_wide_weights(ranc):
 @pytest.mark.parametrize("seed", range(4))
 @pytest.mark.parametrize("wk", ["tc", "tc_wm"])
 def test_wide_weights_every_tick(ranc, oracle_mod, seed, wk):
-    """Weights beyond int8 (wb 10..15, full range, incl. the extremes and
-    multiples of 128) on the tensor-core path: w = 128*hi + lo, two MMAs, two
+    """Weights beyond int8 (wb 10..16, full range, incl. the extremes and
+    multiples of 128 / 256) on the tensor-core path: w = 256*hi + lo, two MMAs, two
     TMEM accumulators; full state against the oracle every tick, 70 samples
     (a ragged second tile)."""
     from workloads.gen import bernoulli_inputs, random_network
     from workloads.rng import substream
-    wb = 10 + seed + (seed == 3)                 # 10, 11, 12, 15 bits
+    wb = [10, 12, 15, 16][seed]
     net = random_network(100 + seed, 3, 2, 256, 256, 4, 3, wb=wb, I=64)
     lo, hi = -(1 << (wb - 1)), (1 << (wb - 1)) - 1
     net.weight[0, :4, :] = [[lo, hi, -128, 128], [127, -127, 0, -129], [255, -256, 384, -385], [lo, lo, hi, hi]]

@@ -576,3 +576,29 @@ def envelope_case(seed):
     net.weight[:, min(1, N - 1), :] = hi
     inp = random_inputs(7000 + seed, net, S, 8, p=[0.05, 0.2, 0.5][int(r.ints(1, 0, 2)[0])])
     return net, inp
+
+
+def bigcore(seed=1006, S=4096, T=20, A=512, N=1024, grid=4):
+    """Cores beyond the paper's 256x256 (configurable axons / neurons, P:42,
+    P:362): a grid x grid mesh of A-axon, N-neuron cores with the perf
+    parameter recipe, random routes inside the mesh (D = 15), Bernoulli(0.1)
+    inputs on A/2 lines for T_in = T ticks."""
+    rng = substream(seed, "bigcore")
+    net = _blank(grid, grid, A, N, 4, 15, 10, A // 2, name=f"bigcore-{grid}x{grid}-A{A}-N{N}")
+    perf_params(net, rng, density=0.5)
+    G = net.G
+    il = rng.ints(G * A, 0, A // 2 - 1).reshape(G, A)
+    net.input_line[:] = np.where(rng.bernoulli(G * A, 0.5).reshape(G, A), il, -1)
+    u = rng.ints(G * N, 0, 99).reshape(G, N)
+    kind = np.where(u < 60, KIND_ROUTE, np.where(u < 70, KIND_OUTPUT, KIND_NONE))
+    net.dest_kind[:] = kind
+    x = (np.arange(G) % grid)[:, None]
+    y = (np.arange(G) // grid)[:, None]
+    route = kind == KIND_ROUTE
+    net.dest_dx[:] = np.where(route, rng.ints(G * N, 0, grid - 1).reshape(G, N) - x, 0)
+    net.dest_dy[:] = np.where(route, rng.ints(G * N, 0, grid - 1).reshape(G, N) - y, 0)
+    net.dest_axon[:] = rng.ints(G * N, 0, A - 1).reshape(G, N)
+    net.dest_delay[:] = rng.ints(G * N, 1, 15).reshape(G, N)
+    net.out_class[:] = (np.arange(N) % 10)[None, :]
+    net.meta.update(T=T)
+    return net, bernoulli_inputs(substream(seed + 1000, "bigcore-inputs"), S, T, A // 2, 0.1)
