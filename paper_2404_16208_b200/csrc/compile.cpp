@@ -400,6 +400,10 @@ ranc_status validate_and_compile(const ranc_network_desc* d, Compiled* out, std:
     // canonical layout of grp_rows rows (one group = the whole core unless tc_grp)
     const size_t GS = (size_t)o.grp_rows, per = GS * o.Kp, parts = o.tc_wide ? 2 : 1;
     o.wfold.assign((size_t)G * parts * o.Npad * o.Kp, 0);
+    // a 128-row core whose wide spike stages (512 axons) do not fit four deep
+    // runs as one neuron group (the grouped launch keeps 2 stages); its
+    // operand layout is the same
+    if (!o.tc_grp && tc_smem_bytes(o) > 227 * 1024 && o.Npad == 128) o.tc_grp = true;
     for (int c = 0; c < G; ++c) {
       const int32_t* inv = &o.inv_tc[(size_t)c * A];
       const uint8_t* ty = d->axon_type + (size_t)c * A;
