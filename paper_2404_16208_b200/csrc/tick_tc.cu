@@ -244,6 +244,21 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
   const int lo = (int)((int64_t)blockIdx.x * total / gridDim.x);
   const int hi = (int)((int64_t)(blockIdx.x + 1) * total / gridDim.x);
   const int nwork = hi - lo;
+  // Serpentine order (per-tick launches, p.serp): odd ticks walk the CTA's
+  // items backwards, so a tick starts on the items whose potentials, ring
+  // rows and operands the previous tick touched last and are still in L2.
+  // Items of one tick are independent, so the order is invisible.
+  const bool rev = !kMulti && p.serp && (p.t & 1);
+  const int first_idx = rev ? hi - 1 : lo;
+  auto adv = [&](int& cl_, int& tile_) {   // the next item in walking order
+    if (!rev) {
+      if (++tile_ == nT) { tile_ = 0; ++cl_; }
+    } else if (--tile_ < 0) {
+      tile_ = nT - 1;
+      --cl_;
+    }
+  };
+  auto next_cl_of = [&](int cl_, int tile_) { return !rev ? (tile_ + 1 == nT ? cl_ + 1 : cl_) : (tile_ == 0 ? cl_ - 1 : cl_); };
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // TMEM columns per accumulator stage (wide: the hi accumulator follows the lo one)
   const uint32_t acc_stride = (uint32_t)Mh * NT * (kWide ? 2u : 1u);
@@ -308,8 +323,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
     for (int it = 0; it < nticks; ++it) {
     const int64_t t = p.t + it;
     const int cur = (int)(t & p.rp_mask);
-    int cl = lo / nT, tile = lo - (lo / nT) * nT;   // work item lo + k, advanced incrementally
-    for (int k0 = 0; k0 < nwork; ++k0, tile = (tile + 1 == nT) ? (++cl, 0) : tile + 1) {
+    int cl = first_idx / nT, tile = first_idx - (first_idx / nT) * nT;   // advanced incrementally
+    for (int k0 = 0; k0 < nwork; ++k0, adv(cl, tile)) {
       const int k = it * nwork + k0;                 // pipeline index (barrier phases)
       const int c = p.c_lo + cl;
       const int s = k % NS, u = k / NS;
@@ -386,8 +401,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
     const uint32_t lbo_a = (uint32_t)GS * 16, lbo_b = (uint32_t)NT * 16;   // tc.h layout
     int prev_core = -1, jw = -1;
     for (int it = 0; it < nticks; ++it) {
-    int cl = lo / nT, tile = lo - (lo / nT) * nT;
-    for (int k0 = 0; k0 < nwork; ++k0, tile = (tile + 1 == nT) ? (++cl, 0) : tile + 1) {
+    int cl = first_idx / nT, tile = first_idx - (first_idx / nT) * nT;
+    for (int k0 = 0; k0 < nwork; ++k0, adv(cl, tile)) {
       const int k = it * nwork + k0;
       const int c = cl;
       const int s = k % NS, u = k / NS;
@@ -428,7 +443,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
         // item of the next tick) belongs to another core, or this is the end
         // (neuron groups: every sub-item has its own operand)
         const bool last_item = k0 + 1 == nwork;
-        const int next_cl = last_item ? lo / nT : (tile + 1 == nT ? cl + 1 : cl);
+        const int next_cl = last_item ? first_idx / nT : next_cl_of(cl, tile);
         if (kGrp || (last_item && it + 1 == nticks) || next_cl != cl) tc::commit(&bars[WFREE]);
       }
       __syncwarp();
@@ -448,8 +463,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
     for (int it = 0; it < nticks; ++it) {
     const int64_t t = p.t + it;
     const int cur = (int)(t & p.rp_mask);
-    int cl = lo / nT, tile = lo - (lo / nT) * nT;
-    for (int k0 = 0; k0 < nwork; ++k0, tile = (tile + 1 == nT) ? (++cl, 0) : tile + 1) {
+    int cl = first_idx / nT, tile = first_idx - (first_idx / nT) * nT;
+    for (int k0 = 0; k0 < nwork; ++k0, adv(cl, tile)) {
       const int k = it * nwork + k0;
       const int c = p.c_lo + cl;
       const int s = k % NS, u = k / NS;
@@ -640,8 +655,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
     // work item idx = cl * nT + tile, advanced incrementally (no divisions);
     // its potential tile is pot + idx * tile_stride (pot_tile); this warp's
     // chunks start at chunk 4*jj
-    int cl = lo / nT, tile = lo - (lo / nT) * nT;
+    int cl = first_idx / nT, tile = first_idx - (first_idx / nT) * nT;
     const size_t tile_stride = (size_t)Np * NT / 8;   // uint4 per potential tile
+    const ptrdiff_t dstep = rev ? -(ptrdiff_t)tile_stride : (ptrdiff_t)tile_stride;   // to the next item's tile
     uint4* dst = pot_tile(p, cl, tile, nT, n) + (size_t)(4 * jj) * Np;
     if (load && nwork > 0) {
 #pragma unroll
@@ -683,10 +699,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
     cl = cl0;
     tile = tile0;
     dst = dst0;
-    for (int k0 = 0; k0 < nwork; ++k0, dst += tile_stride) {
+    for (int k0 = 0; k0 < nwork; ++k0, dst += dstep) {
       const int k = it * nwork + k0;
       const int s0 = tile * NT, ns = min(NT, p.S - s0);
-      const int ncl = (k0 + 1 == nwork) ? cl0 : (tile + 1 == nT ? cl + 1 : cl);   // next item's core
+      const int ncl = (k0 + 1 == nwork) ? cl0 : next_cl_of(cl, tile);   // next item's core
       for (int g = 0; g < nGrp; ++g) {
       const int j = k * nGrp + g;   // sub-item (neuron group g of item k): accumulator ring index
       const int c = p.c_lo + cl;
@@ -696,7 +712,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       valid = active && n < p.N;
       uint4* const dsub = dst + g * GS;   // this group's rows of the potential tile
       const bool pf = load && (g + 1 < nGrp || k0 + 1 < nwork);
-      const uint4* nsrc = g + 1 < nGrp ? dsub + GS : dst + tile_stride;
+      const uint4* nsrc = g + 1 < nGrp ? dsub + GS : dst + dstep;
       const long long tw0 = dbg_on ? clock64() : 0;
       // a new core's neuron parameters were requested a whole work item
       // ahead (one tile per core at config 5: the loads would otherwise stall
@@ -945,10 +961,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       if (lane == 0 && ew == 0) stamp_k(k, 11);
       if (lane == 0) ptx::mbar_arrive(&bars[ACCEMPTY0 + a]);
       }
-      if (++tile == nT) {
-        tile = 0;
-        ++cl;
-      }
+      adv(cl, tile);
     }
     tick_barrier();
     }
@@ -1143,6 +1156,8 @@ cudaError_t launch_tick_tc(ranc_ctx* ctx, TickParams p) {
   const int64_t total = (int64_t)ctx->G_loc * ((ctx->S + NT - 1) / NT);
   const int grid = (int)std::min<int64_t>(total, ctx->num_sms);
   const size_t smem = tc_smem_bytes(n);
+  static const bool no_serp = getenv("RANC_DEBUG_NO_SERP") != nullptr;   // (timing comparisons)
+  p.serp = no_serp ? 0 : 1;
   static std::atomic<uint64_t> configured{0};
   if (first_use_on_device(configured)) {
     const void* fns[] = {(const void*)tick_tc_kernel<false, false, false, false>,
