@@ -214,8 +214,12 @@ ranc_status ranc_set_allocator(ranc_ctx* ctx, void* (*alloc)(size_t, void*),
  * own destination word (e.g. the random mesh of config 5), else sample-major
  * (layered MNIST nets deposit whole words together); 1 sample-major
  * [Rp][G][S][W]; 2 word-major [Rp][G][W][S] (a warp's deposits for 32 samples
- * of one route hit one 128-byte line).  Takes effect at the next
- * ranc_load_inputs / ranc_reset_state.  Results are identical either way. */
+ * of one route hit one 128-byte line); 3 pull scheduler: no ring -- every
+ * tick each neuron's fired bits are published to a history of Rp ticks and
+ * every core gathers its axons' sources (fired at t - delay) from it
+ * (RANC_E_CONFIG when neuron groups or core sharding are in use).  Takes
+ * effect at the next ranc_load_inputs / ranc_reset_state.  Results are
+ * identical either way. */
 #define RANC_OPT_RING_LAYOUT 5
 /* RANC_OPT_DEBUG_FAULT (mutation tests only, "deliberately
  * fault-injected parallel build (skip barrier) -> FAIL with located

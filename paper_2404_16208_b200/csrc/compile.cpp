@@ -394,6 +394,42 @@ ranc_status validate_and_compile(const ranc_network_desc* d, Compiled* out, std:
             ++scattered;
       o.tc_wmajor = 3 * scattered > 2 * (int64_t)G * N;
     }
+    // Pull scheduler (RANC_OPT_RING_LAYOUT 3): for every destination core and
+    // tensor-core axon a', the routing neurons that feed it -- the
+    // destination gathers their fired bits of tick t - delay from a history
+    // of fired bitmaps instead of receiving deposits into a ring.
+    //   pull_base [G+1]            first entry of core c
+    //   pull_ent  [entries]        src core | src neuron << 16 | delay << 26, sorted by a'
+    //   pull_aoff [G][Kp + 8] u16  entries of axon a' of core c: [aoff[a'], aoff[a'+1]) after pull_base[c]
+    {
+      std::vector<std::vector<std::pair<int, uint32_t>>> in(G);   // (a', entry)
+      for (int c = 0; c < G; ++c)
+        for (int n = 0; n < N; ++n) {
+          const uint2 r = o.route_tc[(size_t)c * Np + n];
+          if (route_kind(r.x) != RK_ROUTE) continue;
+          in[r.y].push_back({(int)route_axon(r.x),
+                             (uint32_t)c | ((uint32_t)n << 16) | (route_delay(r.x) << 26)});
+        }
+      o.pull_base.assign(G + 1, 0);
+      o.pull_aoff.assign((size_t)G * (o.Kp + 8), 0);
+      o.pull_emax = 0;
+      o.pull_ent.clear();
+      for (int c = 0; c < G; ++c) {
+        std::stable_sort(in[c].begin(), in[c].end(),
+                         [](const std::pair<int, uint32_t>& x, const std::pair<int, uint32_t>& y) { return x.first < y.first; });
+        o.pull_base[c] = (uint32_t)o.pull_ent.size();
+        o.pull_emax = std::max<int32_t>(o.pull_emax, (int32_t)in[c].size());
+        uint16_t* aoff = &o.pull_aoff[(size_t)c * (o.Kp + 8)];
+        size_t e = 0;
+        for (int ap = 0; ap <= o.Kp; ++ap) {
+          aoff[ap] = (uint16_t)std::min<size_t>(e, 65535);
+          while (ap < o.Kp && e < in[c].size() && in[c][e].first == ap) ++e;
+        }
+        for (auto& pe : in[c]) o.pull_ent.push_back(pe.second);
+      }
+      o.pull_base[G] = (uint32_t)o.pull_ent.size();
+      if (o.pull_ent.empty()) o.pull_ent.push_back(0u);   // (a valid device buffer)
+    }
     // folded weights in the canonical operand layout (tc.h)
     // (wide weights: [lo | hi] per core, w = 256*hi + lo, lo unsigned)
     // per core: Npad / grp_rows groups, each [parts][grp_rows * Kp] in the

@@ -100,6 +100,14 @@ struct TickParams {
   const uint8_t* wflags;    // [G][Npad/32] per-warp flags (bit 0: block route), or nullptr
   const uint8_t* incoming;  // [G] 1 if any neuron of the network routes to the core (its ring can be non-zero)
   uint32_t* spkin;          // RANC_TRACE_STATE_DIGEST: [S][G_loc][W] axon spikes integrated this tick, or nullptr
+  // pull scheduler (tensor-core path, RANC_OPT_RING_LAYOUT 3): fired-bit
+  // history u32 [Rp][G_loc][nT][Npad][2] (slot t & (Rp-1); word j = samples
+  // 32j..32j+31 of the tile) and the per-core source lists (Compiled::pull_*)
+  uint32_t* hist;
+  const uint32_t* pull_ent;
+  const uint32_t* pull_base;
+  const uint16_t* pull_aoff;
+  int32_t pull_emax;
 };
 
 // Host copy of the compiled network.
@@ -123,6 +131,10 @@ struct Compiled {
   std::vector<int32_t> nruns;   // [G]
   std::vector<int32_t> word_runs;  // [G][W] first run | count << 16 (runs overlapping word w)
   std::vector<uint8_t> incoming;   // [G] 1 if some neuron routes to the core
+  std::vector<uint32_t> pull_base; // [G+1] pull scheduler: first source entry of core c (compile.cpp)
+  std::vector<uint32_t> pull_ent;  // src core | src neuron << 16 | delay << 26, per core sorted by axon a'
+  std::vector<uint16_t> pull_aoff; // [G][Kp + 8] per-axon entry offsets relative to pull_base[c]
+  int32_t pull_emax = 0;           // most source entries of one core
   std::vector<uint8_t> wflags_tc;  // [G][Npad/32] bit 0: all routing neurons of the warp share one
                                    // (dest core, ring word, delay) in the tensor-core axon order
   int32_t rmax = 0;
@@ -207,6 +219,9 @@ struct ranc_ctx {
   ranc::DevBuf d_dbg;            // RANC_DEBUG_TIMELINE
   // tensor-core path: input decode (once per ranc_load_inputs)
   ranc::DevBuf d_inw, d_inslot, d_slot_core;
+  // tensor-core path: pull scheduler (latched at reset, RANC_OPT_RING_LAYOUT 3)
+  ranc::DevBuf d_hist, d_pull_ent, d_pull_base, d_pull_aoff;
+  bool ring_pull = false;
   // RANC_TRACE_STATE_DIGEST
   ranc::DevBuf d_spkin, d_digest, d_perm_dig;
   int32_t perm_dig_kernel = 0;   // kernel whose axon order d_perm_dig holds
@@ -248,6 +263,7 @@ int pieces_template(int E);
 // tick_tc.cu
 int tc_tile();
 size_t tc_smem_bytes(const Compiled& n);
+size_t tc_smem_bytes_pull(const Compiled& n);
 cudaError_t launch_tick_tc(ranc_ctx* ctx, TickParams p);
 cudaError_t decode_inputs_tc(ranc_ctx* ctx);
 bool stream_eligible(ranc_ctx* ctx, int64_t num_ticks);

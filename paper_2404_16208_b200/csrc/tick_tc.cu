@@ -72,7 +72,7 @@ enum Bar { FULL0 = 0, SEMPTY0 = 4, BFULL0 = 8, BEMPTY0 = 12, ACCFULL0 = 16, ACCE
            NBARS = 26 };
 
 struct TcLayout {
-  uint32_t w, runs, lut, potbuf, cplanes, stage, b, raw, lines, stage_bytes, total;
+  uint32_t w, runs, lut, potbuf, cplanes, pmask, stage, b, raw, lines, pull, paoff, stage_bytes, total;
 };
 
 // WIp: input-line row words (multiple of 4)
@@ -94,7 +94,8 @@ constexpr int kCntPlanes = 8;   // counts < 256 between flushes
 // wrows: operand rows held in shared memory (Npad, or the group size of a
 // neuron-group launch, grp)
 __host__ __device__ inline TcLayout tc_layout(int wrows, int Kp, int W, int WIp, int rmax, bool wide, int pot_items = 1,
-                                              bool cnt_planes = false, bool multi = false, bool grp = false) {
+                                              bool cnt_planes = false, bool multi = false, bool grp = false,
+                                              int pull_emax = -1) {
   TcLayout L;
   L.w = 1024;
   uint32_t o = L.w + (uint32_t)wrows * Kp * (wide ? 2u : 1u);
@@ -108,6 +109,9 @@ __host__ __device__ inline TcLayout tc_layout(int wrows, int Kp, int W, int WIp,
   o += (NT / 8) * (32 * 8) * 16 * (uint32_t)pot_items;   // = 4 chunks x 512 epilogue threads per item
   L.cplanes = o;                              // u32 [items][kCntPlanes][512 epilogue threads]
   if (cnt_planes) o += (uint32_t)pot_items * kCntPlanes * 512 * 4;
+  o = (o + 15) & ~15u;
+  L.pmask = o;                                // pull scheduler: u64 [Kp] gathered spike masks per axon
+  if (pull_emax >= 0) o += (uint32_t)Kp * 8;
   L.stage = (o + 1023) & ~1023u;
   uint32_t q = 0;
   L.b = q;     q += (uint32_t)NT * Kp;       // spikes as 0/1 bytes, canonical layout
@@ -115,6 +119,12 @@ __host__ __device__ inline TcLayout tc_layout(int wrows, int Kp, int W, int WIp,
   L.raw = q;   q += (uint32_t)NT * W * 4;    // scheduler rows due now (TMA)
   q = (q + 15) & ~15u;
   L.lines = q; q += (uint32_t)NT * (WIp > W ? WIp : W) * 4;  // input line rows or decoded words (TMA)
+  q = (q + 15) & ~15u;
+  L.paoff = q;                                // pull: u16 [Kp + 8] per-axon source offsets (TMA)
+  if (pull_emax >= 0) q += (uint32_t)(Kp + 8) * 2;
+  q = (q + 15) & ~15u;
+  L.pull = q;                                 // pull: u64 [emax] gathered source words (cp.async)
+  if (pull_emax >= 0) q += (uint32_t)pull_emax * 8;
   L.stage_bytes = (q + 1023) & ~1023u;
   L.total = L.stage + (grp ? NS_GRP : wide ? NS_WIDE : multi ? NS_MULTI : NS) * L.stage_bytes;
   return L;
@@ -217,9 +227,16 @@ __device__ __forceinline__ uint32_t lif(const uint4 (&cur)[NE / 8], const uint32
 // (loaded in turn into the one operand buffer), every group filling its own
 // accumulator stage and being retired by the epilogue like a work item of
 // its own (a sub-item).  Per-tick launches only.
-template <bool kMulti, bool kDebug, bool kWm, bool kWide, bool kGrp = false>
+// kPull: the pull scheduler (word-major networks, per-tick launches): every
+// tick the epilogue writes each neuron's fired bits to a history of Rp ticks,
+// and the producer gathers each axon's sources from it (one 8-byte cp.async
+// per source: its fired bits of tick t - delay for the 64 samples of the
+// tile); the spike stage ORs them per axon and transposes them into the
+// staged ring-word layout.  No deposits, no ring, no clears.
+template <bool kMulti, bool kDebug, bool kWm, bool kWide, bool kGrp = false, bool kPull = false>
 __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams p, const int nticks_arg) {
   static_assert(!kGrp || !kMulti, "neuron groups are a per-tick launch");
+  static_assert(!kPull || (!kMulti && kWm && !kGrp), "the pull scheduler is a per-tick word-major launch");
   const int nticks = kMulti ? nticks_arg : 1;
   // kDebug: the RANC_DEBUG_TIMELINE instrumentation (a separate instantiation,
   // so that the product kernel issues none of it)
@@ -234,8 +251,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
   // operand rows per sub-item and sub-items (neuron groups) per work item
   const int GS = kGrp ? p.grp_rows : Np;
   const int nGrp = kGrp ? Np / GS : 1;
-  const TcLayout L =
-      tc_layout(GS, Kp, W, WIp, p.rmax, kWide, kMulti ? p.pot_items : 1, kMulti && p.out_planes, kMulti, kGrp);
+  const TcLayout L = tc_layout(GS, Kp, W, WIp, p.rmax, kWide, kMulti ? p.pot_items : 1, kMulti && p.out_planes,
+                               kMulti, kGrp, kPull ? p.pull_emax : -1);
   constexpr int NS = kGrp ? NS_GRP : kWide ? NS_WIDE : kMulti ? NS_MULTI : ranc::NS;   // spike stages in use
   uint8_t* w_s = smem + L.w;
   const int Mh = GS >> 7;
@@ -287,7 +304,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
   if (warp == mma_warp) tc::alloc(tmem_holder, tcols < 32 ? 32 : tcols);
   if (threadIdx.x == 0) {
     for (int i = 0; i < NS; ++i) {
-      ptx::mbar_init(&bars[FULL0 + i], 1);
+      ptx::mbar_init(&bars[FULL0 + i], kPull ? 33 : 1);   // pull: + one cp.async arrival per producer lane
       ptx::mbar_init(&bars[SEMPTY0 + i], 1);
       ptx::mbar_init(&bars[BFULL0 + i], 1);
       ptx::mbar_init(&bars[BEMPTY0 + i], 1);
@@ -328,16 +345,6 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       const int k = it * nwork + k0;                 // pipeline index (barrier phases)
       const int c = p.c_lo + cl;
       const int s = k % NS, u = k / NS;
-      if (!kGrp && c != prev_core) {
-        ++jw;
-        if (jw > 0) wait(&bars[WFREE], (jw - 1) & 1);
-        if (lane == 0) {
-          const uint32_t wb = (uint32_t)Np * Kp * (kWide ? 2u : 1u);   // wide: [lo | hi]
-          ptx::mbar_arrive_expect_tx(&bars[WFULL], wb);
-          ptx::bulk_g2s(w_s, p.wfold + (size_t)c * wb, wb, &bars[WFULL]);
-        }
-        prev_core = c;
-      }
       if (lane == 0) stamp_k(k, 0);
       wait(&bars[SEMPTY0 + s], (u & 1) ^ 1);
       if (lane == 0) {
@@ -347,9 +354,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
         const bool inject = t < p.T_in && p.nruns[c] > 0;
         // decoded inputs: the tile's input words in ring-row layout; else the raw line rows
         const int slot = p.inw ? p.inslot[cl] : -1;
-        const uint32_t ring_bytes = p.incoming[c] ? (uint32_t)NT * W * 4 : 0u;
+        const uint32_t ring_bytes = (!kPull && p.incoming[c]) ? (uint32_t)NT * W * 4 : 0u;
         const uint32_t line_bytes = !inject ? 0u : (p.inw ? (uint32_t)NT * W * 4 : (uint32_t)NT * WIp * 4);
-        ptx::mbar_arrive_expect_tx(&bars[FULL0 + s], ring_bytes + line_bytes);
+        const uint32_t aoff_bytes = kPull ? (uint32_t)(Kp + 8) * 2 : 0u;
+        ptx::mbar_arrive_expect_tx(&bars[FULL0 + s], ring_bytes + line_bytes + aoff_bytes);
+        if (kPull)
+          ptx::bulk_g2s(st + L.paoff, p.pull_aoff + (size_t)c * (Kp + 8), aoff_bytes, &bars[FULL0 + s]);
         // ring rows and decoded inputs: sample-major [..][Sr][W] is one bulk
         // copy per tile, staged [NT][W]; word-major [..][W][Sr] one copy of
         // the tile's 64 samples per ring word, staged [W][NT]
@@ -369,7 +379,52 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
         else if (inject)
           ptx::bulk_g2s(st + L.lines, p.lines + ((size_t)t * p.Sr + s0) * WIp, line_bytes, &bars[FULL0 + s]);
       }
+      if (kPull) {
+        // gather: the fired bits (tick t - delay, this tile's 64 samples) of
+        // every source of every axon of core c, in the core's source order
+        uint8_t* st = smem + L.stage + s * L.stage_bytes;
+        const uint32_t base = p.pull_base[c], cnt = p.pull_base[c + 1] - base;
+        const size_t slot_stride = (size_t)p.G_loc * nT * Np * 2;   // u32 per history slot
+        // entries are loaded in batches of kPer per lane (independent loads:
+        // one L2 latency per batch, not per entry), then the copies issued
+        constexpr int kPer = 8;
+        for (uint32_t e0 = 0; e0 < cnt; e0 += 32 * kPer) {
+          uint32_t ents[kPer];
+#pragma unroll
+          for (int i = 0; i < kPer; ++i) {
+            const uint32_t e = e0 + i * 32 + lane;
+            ents[i] = e < cnt ? __ldg(p.pull_ent + base + e) : 0u;
+          }
+#pragma unroll
+          for (int i = 0; i < kPer; ++i) {
+            const uint32_t e = e0 + i * 32 + lane;
+            if (e < cnt) {
+              const uint32_t ent = ents[i];
+              const int sc = (int)(ent & 0xFFFFu) - p.c_lo, sn = (int)((ent >> 16) & 0x3FFu), d = (int)(ent >> 26);
+              const uint32_t* src = p.hist + (size_t)((t - d) & p.rp_mask) * slot_stride +
+                                    (((size_t)sc * nT + tile) * Np + sn) * 2;
+              ptx::cp_async8(st + L.pull + e * 8, src);
+            }
+          }
+        }
+        ptx::cp_async_mbar_arrive_noinc(&bars[FULL0 + s]);
+      }
       __syncwarp();
+      // a new core's operand, once the previous core's MMAs have read the
+      // buffer.  Issued AFTER this item's ring rows / gathers, so that their
+      // latency overlaps the previous item's MMAs instead of following them
+      // (one tile per core at config 5: every item waits here).
+      if (!kGrp && c != prev_core) {
+        ++jw;
+        if (jw > 0) wait(&bars[WFREE], (jw - 1) & 1);
+        if (lane == 0) {
+          const uint32_t wb = (uint32_t)Np * Kp * (kWide ? 2u : 1u);   // wide: [lo | hi]
+          ptx::mbar_arrive_expect_tx(&bars[WFULL], wb);
+          ptx::bulk_g2s(w_s, p.wfold + (size_t)c * wb, wb, &bars[WFULL]);
+        }
+        prev_core = c;
+        __syncwarp();
+      }
       if (kGrp) {
         // the groups' operands in turn, each once the MMAs of the previous
         // one have read the buffer (Wfold per core: nGrp blocks of wb bytes)
@@ -479,7 +534,27 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       // staged rows: raw[sm * W + w] (sample-major) or raw[w * NT + sm]
       // (word-major) = ring word w of sample s0 + sm
       constexpr bool wm = kWm;
-      if (p.incoming[c]) {
+      if (kPull) {
+        // a1 (pull scheduler): the spikes due now on axon a' are the OR of its
+        // sources' fired bits of tick t - delay (idempotent OR, G11);
+        // then each 32-axon x 32-sample block is bit-transposed into the
+        // staged ring-word layout raw[w * NT + sample]
+        const uint64_t* gat = reinterpret_cast<const uint64_t*>(st + L.pull);
+        const uint16_t* aoff = reinterpret_cast<const uint16_t*>(st + L.paoff);
+        uint64_t* msk = reinterpret_cast<uint64_t*>(smem + L.pmask);
+        for (int ap = et; ap < Kp; ap += kExpThreads) {
+          uint64_t m = 0;
+          for (int e = aoff[ap], e1 = aoff[ap + 1]; e < e1; ++e) m |= gat[e];
+          msk[ap] = m;
+        }
+        named_sync(2, kExpThreads);
+        for (int b = et >> 5; b < 2 * W; b += kExpWarps) {
+          const int w = b >> 1, hf = b & 1;
+          const uint32_t x = (uint32_t)(msk[32 * w + lane] >> (32 * hf));
+          raw[w * NT + 32 * hf + lane] = transpose32(x, lane);
+        }
+        named_sync(2, kExpThreads);
+      } else if (p.incoming[c]) {
         // only the words that hold spikes need clearing
         if (!wm) {
           uint32_t* row = p.ring + (((size_t)cur * p.G_loc + cl) * p.Sr + s0) * W;
@@ -857,7 +932,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
         const int sj = s0 + jj * 32;          // first sample of this warp's half
         const int lim = ns - jj * 32;
         const uint32_t f = lim >= 32 ? fired : (lim > 0 ? fired & ((1u << lim) - 1u) : 0u);
-        if (block_identity) {
+        if (kPull) {
+          // a5 (pull scheduler): publish this neuron's fired bits of tick t
+          // for the 32 samples of this half; destinations gather them
+          p.hist[(((((size_t)(t & p.rp_mask) * p.G_loc + cl) * nT + tile) * Np + n) << 1) + jj] = valid ? f : 0u;
+        } else if (block_identity) {
           // every routing lane l of this warp deposits bit l of one ring
           // word: a 32x32 bit transpose turns the per-lane sample masks into
           // per-sample deposit words, one RED per (sample, word) issued by
@@ -1056,6 +1135,11 @@ size_t tc_smem_bytes(const Compiled& n) {
   return tc_layout(n.grp_rows, n.Kp, n.W, n.WIp, n.rmax, n.tc_wide, 1, false, false, n.tc_grp).total;
 }
 
+// shared memory of the pull-scheduler launch (word-major, per-tick, no groups)
+size_t tc_smem_bytes_pull(const Compiled& n) {
+  return tc_layout(n.grp_rows, n.Kp, n.W, n.WIp, n.rmax, n.tc_wide, 1, false, false, false, n.pull_emax).total;
+}
+
 namespace {
 
 void tc_fill_params(ranc_ctx* ctx, TickParams& p) {
@@ -1073,6 +1157,11 @@ void tc_fill_params(ranc_ctx* ctx, TickParams& p) {
   p.rmax = n.rmax;
   p.grp_rows = n.grp_rows;
   p.wmajor = ctx->ring_wmajor ? 1 : 0;
+  p.hist = (uint32_t*)ctx->d_hist.p;
+  p.pull_ent = (const uint32_t*)ctx->d_pull_ent.p;
+  p.pull_base = (const uint32_t*)ctx->d_pull_base.p;
+  p.pull_aoff = (const uint16_t*)ctx->d_pull_aoff.p;
+  p.pull_emax = n.pull_emax;
   p.any_route = n.any_route ? 1 : 0;
 }
 
@@ -1080,7 +1169,7 @@ void tc_fill_params(ranc_ctx* ctx, TickParams& p) {
 
 bool tc_multi_eligible(const ranc_ctx* ctx, int64_t num_ticks) {
   if (ctx->kernel_active != RANC_KERNEL_TC || ctx->shard_mode == RANC_SHARD_CORES || num_ticks < 2) return false;
-  if (ctx->stream_opt == 1 || getenv("RANC_DEBUG_TIMELINE") || ctx->net.tc_wide || ctx->net.tc_grp)
+  if (ctx->stream_opt == 1 || getenv("RANC_DEBUG_TIMELINE") || ctx->net.tc_wide || ctx->net.tc_grp || ctx->ring_pull)
     return false;   // (_MULTI: kept)
   const int64_t total = (int64_t)ctx->G_loc * ((ctx->S + NT - 1) / NT);
   if (total <= ctx->num_sms) return true;   // one work item per CTA, one CTA per SM (cooperative launch)
@@ -1155,7 +1244,7 @@ cudaError_t launch_tick_tc(ranc_ctx* ctx, TickParams p) {
   tc_fill_params(ctx, p);
   const int64_t total = (int64_t)ctx->G_loc * ((ctx->S + NT - 1) / NT);
   const int grid = (int)std::min<int64_t>(total, ctx->num_sms);
-  const size_t smem = tc_smem_bytes(n);
+  const size_t smem = ctx->ring_pull ? tc_smem_bytes_pull(n) : tc_smem_bytes(n);
   static const bool no_serp = getenv("RANC_DEBUG_NO_SERP") != nullptr;   // (timing comparisons)
   p.serp = no_serp ? 0 : 1;
   static std::atomic<uint64_t> configured{0};
@@ -1169,7 +1258,10 @@ cudaError_t launch_tick_tc(ranc_ctx* ctx, TickParams p) {
                          (const void*)tick_tc_kernel<false, false, false, false, true>,
                          (const void*)tick_tc_kernel<false, false, true, false, true>,
                          (const void*)tick_tc_kernel<false, false, false, true, true>,
-                         (const void*)tick_tc_kernel<false, false, true, true, true>};
+                         (const void*)tick_tc_kernel<false, false, true, true, true>,
+                         (const void*)tick_tc_kernel<false, false, true, true, false, true>,
+                         (const void*)tick_tc_kernel<false, true, true, false, false, true>,
+                         (const void*)tick_tc_kernel<false, false, true, false, false, true>};
     for (const void* f : fns) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   }
   static const bool dbg_env = getenv("RANC_DEBUG_TIMELINE") != nullptr;
@@ -1177,7 +1269,11 @@ cudaError_t launch_tick_tc(ranc_ctx* ctx, TickParams p) {
   if (dbg && !ctx->d_dbg.p) dev_alloc(ctx, &ctx->d_dbg, kDbg * 8);
   p.dbg = dbg ? (unsigned long long*)ctx->d_dbg.p : nullptr;
   if (dbg) cudaMemsetAsync(ctx->d_dbg.p, 0, kDbg * 8, ctx->stream);
-  const void* fn = n.tc_grp ? (n.tc_wide ? (p.wmajor ? (const void*)tick_tc_kernel<false, false, true, true, true>
+  const bool pull = ctx->ring_pull;
+  const void* fn = pull ? (n.tc_wide ? (const void*)tick_tc_kernel<false, false, true, true, false, true>
+                                     : dbg ? (const void*)tick_tc_kernel<false, true, true, false, false, true>
+                                           : (const void*)tick_tc_kernel<false, false, true, false, false, true>)
+                   : n.tc_grp ? (n.tc_wide ? (p.wmajor ? (const void*)tick_tc_kernel<false, false, true, true, true>
                                                       : (const void*)tick_tc_kernel<false, false, false, true, true>)
                                          : (p.wmajor ? (const void*)tick_tc_kernel<false, false, true, false, true>
                                                       : (const void*)tick_tc_kernel<false, false, false, false, true>))

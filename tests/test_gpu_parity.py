@@ -21,9 +21,10 @@ def ranc():
 # "tc": tensor-core kernel, sample-major scheduler rings; "tc_wm": word-major
 # rings (RANC_OPT_RING_LAYOUT = 2); "tc_gather": word-major rings and the
 # per-tick input-run gather instead of the load-time input decode
-# (RANC_OPT_INPUT_DECODE = 0)
-KERNELS = {"popc": 1, "tc": 2, "tc_wm": 2, "tc_gather": 2}
-RING = {"tc": 1, "tc_wm": 2, "tc_gather": 2}
+# (RANC_OPT_INPUT_DECODE = 0); "tc_pull": the pull scheduler (layout 3: fired-
+# bit history gathered by the destinations)
+KERNELS = {"popc": 1, "tc": 2, "tc_wm": 2, "tc_gather": 2, "tc_pull": 2}
+RING = {"tc": 1, "tc_wm": 2, "tc_gather": 2, "tc_pull": 3}
 
 
 def make_sim(ranc, net, kernel, **kw):
@@ -42,7 +43,7 @@ def make_sim(ranc, net, kernel, **kw):
     return sim
 
 
-@pytest.fixture(params=["popc", "tc", "tc_wm", "tc_gather"])
+@pytest.fixture(params=["popc", "tc", "tc_wm", "tc_gather", "tc_pull"])
 def kernel(request):
     return request.param
 

@@ -1,6 +1,6 @@
 """Print the TC kernel's per-tile pipeline timeline of CTA 0 (debug aid).
 
-  python tools/timeline.py [config3|config5|config5g] [S] [ticks]
+  python tools/timeline.py [config3|config5|config5g] [S] [ticks] [ring layout 0-3]
 """
 import os
 import sys
@@ -18,5 +18,7 @@ else:
     net, inp = gen.config5(S=S, T=10, variant="global" if wl == "config5g" else "local")
 sim = Simulator(net)
 sim.set_option(3, 2)
+if len(sys.argv) > 4:
+    sim.set_option(5, int(sys.argv[4]))
 sim.load_inputs(inp)
 sim.run(int(sys.argv[3]) if len(sys.argv) > 3 else 3)
