@@ -7,8 +7,10 @@ Each variant is checked against the oracle at the end (bit-exact), so a run
 that the sanitizer lets through is also a parity run.  Variants: popc (per-tick
 popcount launches), popc_stream (cooperative one-launch streaming kernel),
 tc (per-tick tcgen05 kernel, sample-major rings), tc_wm (word-major rings),
-tc_multi (cooperative multi-tick tcgen05 launch), tc_wide (lo/hi int8 split),
-loopback (core-sharded group of 2 with the exchange kernels), digest.
+tc_multi (cooperative multi-tick tcgen05 launch, neighbourhood barrier),
+tc_wide (16-bit weights: u8/s8 split), tc_pull (pull scheduler), tc_grp
+(neuron groups), loopback (core-sharded group of 2 with the exchange
+kernels), digest.
 """
 from __future__ import annotations
 
@@ -46,7 +48,8 @@ def main(argv):
         check(sim, net, inp, T, what)
         sim.close()
 
-    variants = argv or ["popc", "popc_stream", "tc", "tc_wm", "tc_multi", "tc_wide", "loopback", "digest"]
+    variants = argv or ["popc", "popc_stream", "tc", "tc_wm", "tc_multi", "tc_wide", "tc_pull", "tc_grp",
+                        "loopback", "digest"]
     net2, inp2 = config2(S=70)
     T2 = net2.meta["T"]
     mesh, mesh_in = config5(S=3, T=6, grid=6)
@@ -69,6 +72,13 @@ def main(argv):
             for f in ("weight_bits", "leak_bits", "threshold_bits", "reset_bits"):
                 setattr(w, f, getattr(w, f) + 7)
             run(w, mesh_in, 6, 2, 1, ring=2, what=v)
+        elif v == "tc_pull":
+            run(mesh, mesh_in, 6, 2, 1, ring=3, what=v)
+        elif v == "tc_grp":
+            from workloads.gen import bigcore
+            for A, N in ((512, 1024), (256, 512)):
+                big, big_in = bigcore(S=70, T=4, A=A, N=N, grid=2)
+                run(big, big_in, 4, 2, 1, what=f"{v}_A{A}_N{N}")
         elif v == "loopback":
             sims = [r.Simulator(mesh) for _ in range(2)]
             for s in sims:
