@@ -123,3 +123,21 @@ def test_null_args(lib):
     assert lib.ranc_load_network(None, 0, ctypes.byref(h)) == 1
     assert b"NULL" in lib.ranc_last_error(None)
     lib.ranc_destroy(None)
+
+
+def test_plain_c99_consumer(lib, tmp_path):
+    """The header is plain C99: a consumer compiled with gcc -std=c99
+    -pedantic -Werror and linked to libranc.so runs the host-only entry
+    points (core-shard planner, located validation error, NULL arguments, no
+    CPU fallback) -- tests/c/consumer.c."""
+    import subprocess
+    from paper_2404_16208_b200 import _lib
+    exe = str(tmp_path / "consumer")
+    libdir = os.path.dirname(_lib.LIB_PATH)
+    cc = ["gcc", "-std=c99", "-pedantic", "-Wall", "-Werror", "-I" + os.path.join(ROOT, "include"),
+          os.path.join(ROOT, "tests", "c", "consumer.c"), "-o", exe, "-L" + libdir, "-l:libranc.so",
+          "-Wl,-rpath," + libdir]
+    r = subprocess.run(cc, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
