@@ -191,12 +191,13 @@ ranc_status ranc_set_allocator(ranc_ctx* ctx, void* (*alloc)(size_t, void*),
  * RANC_OPT_KERNEL: 0 automatic (tensor core when the network is eligible,
  * unless S < 64 and cores x S <= 592, where the popcount path's streaming
  * launch is faster), 1 popcount, 2 tensor core (see ranc_info.kernel).
- * Tensor-core eligibility: N <= 1024 neurons and A <= 512 axons (cores with
+ * Tensor-core eligibility: N <= 1024 neurons and A <= 1024 axons (cores with
  * more than 256 neurons or 32*ceil(A/32)*Npad > 64 KB run in neuron groups
- * of 256 or 128 rows, one Wfold operand each), weights of any valid width
- * (-128..127: one s8 operand; 16-bit: w = 256*hi + lo, a u8 low byte and an
- * s8 high byte, two MMAs), and the kernel's shared memory within 227 KB;
- * otherwise RANC_E_CONFIG for value 2. */
+ * of 256 or 128 rows, one Wfold operand each, split into K chunks of 512
+ * axons beyond 512), weights of any valid width (-128..127: one s8 operand;
+ * 16-bit: w = 256*hi + lo, a u8 low byte and an s8 high byte, two MMAs),
+ * and the kernel's shared memory within 227 KB (16-bit weights: up to 512
+ * axons); otherwise RANC_E_CONFIG for value 2. */
 #define RANC_OPT_SAMPLE_TILE 1
 #define RANC_OPT_INPUT_DECODE 2
 /* RANC_OPT_STREAM (streaming mode: one long stream of inputs,

@@ -268,12 +268,12 @@ ranc_status validate_and_compile(const ranc_network_desc* d, Compiled* out, std:
   // w = 256*hi + lo (lo the unsigned low byte, hi in [-128,127]), any 16-bit
   // weight (the validated range); the kernel's shared-memory layout is
   // checked against 227 KB when the path is chosen
-  // Larger cores (N <= 1024, A <= 512) run as neuron groups of grp_rows rows
+  // Larger cores (N <= 1024, A <= 1024) run as neuron groups of grp_rows rows
   // (256 when the axons fit 256 and the padded neurons are whole groups of
   // 256, else 128), one 64 KB operand per group.
   {
     const bool single = o.Npad <= 256 && (size_t)o.Npad * o.Kp <= 65536;
-    bool ok = single || o.Kp <= 512;
+    bool ok = single || o.Kp <= 1024;   // beyond 512 axons: K chunks of 512 within a group
     o.tc_grp = !single;
     o.grp_rows = single ? o.Npad : ((o.Kp <= 256 && o.Npad % 256 == 0) ? 256 : 128);
     bool wide = false;
@@ -450,14 +450,17 @@ ranc_status validate_and_compile(const ranc_network_desc* d, Compiled* out, std:
         for (int a = 0; a < A; ++a)
           if ((src[a >> 5] >> (a & 31)) & 1u) {
             const int w = d->weight[cn * K + ty[a]];
-            int8_t* const dst = core_dst + (size_t)(n / GS) * parts * per;
-            const size_t off = tc_operand_offset((uint32_t)(n % GS), (uint32_t)inv[a], (uint32_t)GS);
+            // K chunk kc of 512 axons (one chunk unless Kp > 512): its own
+            // canonical block of KSc columns, [lo | hi] parts
+            const int ap = inv[a], kc = ap / 512, ksc = std::min(512, o.Kp - kc * 512);
+            int8_t* const dst = core_dst + (size_t)(n / GS) * parts * per + (size_t)kc * 512 * GS * parts;
+            const size_t off = tc_operand_offset((uint32_t)(n % GS), (uint32_t)(ap - kc * 512), (uint32_t)GS);
             if (!o.tc_wide) {
               dst[off] = (int8_t)w;
             } else {
               const int hi = w >> 8;   // floor(w / 256): arithmetic shift, in [-128, 127]
               dst[off] = (int8_t)(uint8_t)(w - 256 * hi);   // low byte, read as u8 by the MMA
-              dst[per + off] = (int8_t)hi;
+              dst[(size_t)GS * ksc + off] = (int8_t)hi;
             }
           }
       }

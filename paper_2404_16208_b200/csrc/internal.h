@@ -68,6 +68,7 @@ struct TickParams {
   int32_t out_planes;       // multi-tick tensor-core launch: bit-sliced per-thread output counters in shared memory
   int32_t Kp;               // tensor-core path: K bytes per operand row (= 32*W)
   int32_t grp_rows;         // tensor-core path: rows per neuron group (Compiled::grp_rows)
+  int32_t grp_ns;           // neuron-group launch: spike stages (2, or 1 beyond 512 axons)
   int32_t serp;             // tensor-core per-tick launches: odd ticks walk each CTA's items backwards
   int32_t fault;            // RANC_OPT_DEBUG_FAULT (mutation tests): 1 = skip the grid barrier of
                             // cooperative multi-tick launches

@@ -87,6 +87,10 @@ constexpr int NS_MULTI = 3;
 // axons): one spike stage feeds several groups' MMAs, and a B stage holds up
 // to 512 axons, so 2 stages
 constexpr int NS_GRP = 2;
+// neuron groups beyond 512 axons: the group's operand is split into K chunks
+// of 512 axons (one 64 KB buffer load each, accumulated in TMEM) and the
+// 64 KB spike stage is single (TickParams::grp_ns = 1)
+constexpr int kKChunk = 512;
 // pot_items: potential tiles kept on chip (multi-tick launch with up to two
 // work items per CTA: one region each)
 // cnt_planes: per-thread bit-sliced output-bus counters (multi-tick launch)
@@ -94,11 +98,13 @@ constexpr int kCntPlanes = 8;   // counts < 256 between flushes
 // wrows: operand rows held in shared memory (Npad, or the group size of a
 // neuron-group launch, grp)
 __host__ __device__ inline TcLayout tc_layout(int wrows, int Kp, int W, int WIp, int rmax, bool wide, int pot_items = 1,
-                                              bool cnt_planes = false, bool multi = false, bool grp = false,
+                                              bool cnt_planes = false, bool multi = false, int grp = 0,
                                               int pull_emax = -1) {
+  // grp: spike stages of a neuron-group launch (0: not grouped); its operand
+  // buffer holds one K chunk of at most kKChunk axons
   TcLayout L;
   L.w = 1024;
-  uint32_t o = L.w + (uint32_t)wrows * Kp * (wide ? 2u : 1u);
+  uint32_t o = L.w + (uint32_t)wrows * (grp ? (Kp < kKChunk ? Kp : kKChunk) : Kp) * (wide ? 2u : 1u);
   L.runs = o;                                 // int2 [rmax] + int32 [W] of the current core
   o += (uint32_t)rmax * 8 + (uint32_t)W * 4;
   o = (o + 15) & ~15u;
@@ -126,7 +132,7 @@ __host__ __device__ inline TcLayout tc_layout(int wrows, int Kp, int W, int WIp,
   L.pull = q;                                 // pull: u64 [emax] gathered source words (cp.async)
   if (pull_emax >= 0) q += (uint32_t)pull_emax * 8;
   L.stage_bytes = (q + 1023) & ~1023u;
-  L.total = L.stage + (grp ? NS_GRP : wide ? NS_WIDE : multi ? NS_MULTI : NS) * L.stage_bytes;
+  L.total = L.stage + (grp ? grp : wide ? NS_WIDE : multi ? NS_MULTI : NS) * L.stage_bytes;
   return L;
 }
 
@@ -252,8 +258,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
   const int GS = kGrp ? p.grp_rows : Np;
   const int nGrp = kGrp ? Np / GS : 1;
   const TcLayout L = tc_layout(GS, Kp, W, WIp, p.rmax, kWide, kMulti ? p.pot_items : 1, kMulti && p.out_planes,
-                               kMulti, kGrp, kPull ? p.pull_emax : -1);
-  constexpr int NS = kGrp ? NS_GRP : kWide ? NS_WIDE : kMulti ? NS_MULTI : ranc::NS;   // spike stages in use
+                               kMulti, kGrp ? p.grp_ns : 0, kPull ? p.pull_emax : -1);
+  constexpr int NS = kGrp ? NS_GRP : kWide ? NS_WIDE : kMulti ? NS_MULTI : ranc::NS;   // spike stages (at most)
+  const int nsr = kGrp ? p.grp_ns : NS;   // spike stages in use
+  const int nK = kGrp ? (Kp + kKChunk - 1) / kKChunk : 1;   // K chunks of a group's operand
   uint8_t* w_s = smem + L.w;
   const int Mh = GS >> 7;
   const int nT = (p.S + NT - 1) / NT;
@@ -344,7 +352,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
     for (int k0 = 0; k0 < nwork; ++k0, adv(cl, tile)) {
       const int k = it * nwork + k0;                 // pipeline index (barrier phases)
       const int c = p.c_lo + cl;
-      const int s = k % NS, u = k / NS;
+      const int s = k % nsr, u = k / nsr;
       if (lane == 0) stamp_k(k, 0);
       wait(&bars[SEMPTY0 + s], (u & 1) ^ 1);
       if (lane == 0) {
@@ -426,18 +434,24 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
         __syncwarp();
       }
       if (kGrp) {
-        // the groups' operands in turn, each once the MMAs of the previous
-        // one have read the buffer (Wfold per core: nGrp blocks of wb bytes)
-        const uint32_t wb = (uint32_t)GS * Kp * (kWide ? 2u : 1u);
-        for (int g = 0; g < nGrp; ++g) {
-          ++jw;
-          if (jw > 0) wait(&bars[WFREE], (jw - 1) & 1);
-          if (lane == 0) {
-            ptx::mbar_arrive_expect_tx(&bars[WFULL], wb);
-            ptx::bulk_g2s(w_s, p.wfold + ((size_t)c * nGrp + g) * wb, wb, &bars[WFULL]);
+        // the groups' operands in turn (K chunk by K chunk beyond 512 axons),
+        // each once the MMAs of the previous one have read the buffer
+        // (Wfold per core: nGrp blocks of gb bytes; chunk kc of a block at
+        // kc * 512 * GS * parts, [lo | hi] parts of KSc columns each)
+        const uint32_t parts = kWide ? 2u : 1u, gb = (uint32_t)GS * Kp * parts;
+        for (int g = 0; g < nGrp; ++g)
+          for (int kc = 0; kc < nK; ++kc) {
+            const uint32_t ksc = (uint32_t)min(kKChunk, Kp - kc * kKChunk);
+            const uint32_t wb = (uint32_t)GS * ksc * parts;
+            ++jw;
+            if (jw > 0) wait(&bars[WFREE], (jw - 1) & 1);
+            if (lane == 0) {
+              ptx::mbar_arrive_expect_tx(&bars[WFULL], wb);
+              ptx::bulk_g2s(w_s, p.wfold + ((size_t)c * nGrp + g) * gb + (size_t)kc * kKChunk * GS * parts, wb,
+                            &bars[WFULL]);
+            }
+            __syncwarp();
           }
-          __syncwarp();
-        }
       }
     }
     tick_barrier();
@@ -460,7 +474,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
     for (int k0 = 0; k0 < nwork; ++k0, adv(cl, tile)) {
       const int k = it * nwork + k0;
       const int c = cl;
-      const int s = k % NS, u = k / NS;
+      const int s = k % nsr, u = k / nsr;
       if (!kGrp && c != prev_core) {
         ++jw;
         wait(&bars[WFULL], jw & 1);
@@ -471,37 +485,42 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       for (int g = 0; g < nGrp; ++g) {
       const int j = k * nGrp + g;          // sub-item: accumulator ring index
       const int a = j % NA, ua = j / NA;
-      if (kGrp) {   // every group is a new operand
+      wait(&bars[ACCEMPTY0 + a], (ua & 1) ^ 1);
+      for (int kc = 0; kc < nK; ++kc) {
+      const int ksc = kGrp ? min(kKChunk, Kp - kc * kKChunk) : Kp;   // axons of this operand chunk
+      if (kGrp) {   // every group (K chunk) is a new operand
         ++jw;
         wait(&bars[WFULL], jw & 1);
       }
-      wait(&bars[ACCEMPTY0 + a], (ua & 1) ^ 1);
       tc::fence_after();
       if (lane == 0) {
         stamp_k(k, 6);
         const uint8_t* b_s = smem + L.stage + s * L.stage_bytes + L.b;
         const uint32_t acc = tmem + a * acc_stride;
+        const int kk0 = kc * (kKChunk / 32);   // K step of the spike operand
         for (int hh = 0; hh < Mh; ++hh)
-          for (int kk = 0; kk < Kp / 32; ++kk) {
+          for (int kk = 0; kk < ksc / 32; ++kk) {
+            const uint32_t accum = (kc > 0 || kk > 0) ? 1u : 0u;
             const uint64_t ad = tc::smem_desc(ptx::smem_u32(w_s + hh * 2048 + kk * 2 * lbo_a), lbo_a, 128);
-            const uint64_t bd = tc::smem_desc(ptx::smem_u32(b_s + kk * 2 * lbo_b), lbo_b, 128);
-            tc::mma_i8(acc + hh * NT, ad, bd, id_lo, kk > 0 ? 1u : 0u);
+            const uint64_t bd = tc::smem_desc(ptx::smem_u32(b_s + (kk0 + kk) * 2 * lbo_b), lbo_b, 128);
+            tc::mma_i8(acc + hh * NT, ad, bd, id_lo, accum);
             if (kWide) {
-              const uint64_t ah = tc::smem_desc(ptx::smem_u32(w_s + GS * Kp + hh * 2048 + kk * 2 * lbo_a), lbo_a, 128);
-              tc::mma_i8(acc + (Mh + hh) * NT, ah, bd, id, kk > 0 ? 1u : 0u);
+              const uint64_t ah = tc::smem_desc(ptx::smem_u32(w_s + GS * ksc + hh * 2048 + kk * 2 * lbo_a), lbo_a, 128);
+              tc::mma_i8(acc + (Mh + hh) * NT, ah, bd, id, accum);
             }
           }
-        if (g + 1 == nGrp) tc::commit(&bars[BEMPTY0 + s]);
-        tc::commit(&bars[ACCFULL0 + a]);
+        if (g + 1 == nGrp && kc + 1 == nK) tc::commit(&bars[BEMPTY0 + s]);
+        if (kc + 1 == nK) tc::commit(&bars[ACCFULL0 + a]);
         stamp_k(k, 7);
         // the next item (in a multi-tick launch: cyclically, the CTA's first
         // item of the next tick) belongs to another core, or this is the end
-        // (neuron groups: every sub-item has its own operand)
+        // (neuron groups: every sub-item / K chunk has its own operand)
         const bool last_item = k0 + 1 == nwork;
         const int next_cl = last_item ? first_idx / nT : next_cl_of(cl, tile);
         if (kGrp || (last_item && it + 1 == nticks) || next_cl != cl) tc::commit(&bars[WFREE]);
       }
       __syncwarp();
+      }
       }
     }
     tick_barrier();
@@ -522,7 +541,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
     for (int k0 = 0; k0 < nwork; ++k0, adv(cl, tile)) {
       const int k = it * nwork + k0;
       const int c = p.c_lo + cl;
-      const int s = k % NS, u = k / NS;
+      const int s = k % nsr, u = k / nsr;
       const int s0 = tile * NT, ns = min(NT, p.S - s0);
       uint8_t* st = smem + L.stage + s * L.stage_bytes;
       uint32_t* raw = reinterpret_cast<uint32_t*>(st + L.raw);
@@ -1131,13 +1150,15 @@ cudaError_t decode_inputs_tc(ranc_ctx* ctx) {
 
 int tc_tile() { return NT; }
 
+int grp_stages(const Compiled& n) { return !n.tc_grp ? 0 : n.Kp > kKChunk ? 1 : NS_GRP; }
+
 size_t tc_smem_bytes(const Compiled& n) {
-  return tc_layout(n.grp_rows, n.Kp, n.W, n.WIp, n.rmax, n.tc_wide, 1, false, false, n.tc_grp).total;
+  return tc_layout(n.grp_rows, n.Kp, n.W, n.WIp, n.rmax, n.tc_wide, 1, false, false, grp_stages(n)).total;
 }
 
 // shared memory of the pull-scheduler launch (word-major, per-tick, no groups)
 size_t tc_smem_bytes_pull(const Compiled& n) {
-  return tc_layout(n.grp_rows, n.Kp, n.W, n.WIp, n.rmax, n.tc_wide, 1, false, false, false, n.pull_emax).total;
+  return tc_layout(n.grp_rows, n.Kp, n.W, n.WIp, n.rmax, n.tc_wide, 1, false, false, 0, n.pull_emax).total;
 }
 
 namespace {
@@ -1156,6 +1177,7 @@ void tc_fill_params(ranc_ctx* ctx, TickParams& p) {
   p.nruns = (const int32_t*)ctx->d_nruns.p;
   p.rmax = n.rmax;
   p.grp_rows = n.grp_rows;
+  p.grp_ns = grp_stages(n);
   p.wmajor = ctx->ring_wmajor ? 1 : 0;
   p.hist = (uint32_t*)ctx->d_hist.p;
   p.pull_ent = (const uint32_t*)ctx->d_pull_ent.p;

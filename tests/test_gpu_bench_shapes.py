@@ -135,7 +135,8 @@ def test_envelope_multi_tick_calls(ranc, oracle_mod):
 
 
 @pytest.mark.parametrize("kernel", ["tc", "popc"])
-@pytest.mark.parametrize("A,N", [(512, 1024), (256, 1024), (300, 257), (512, 128)])
+@pytest.mark.parametrize("A,N", [(512, 1024), (256, 1024), (300, 257), (512, 128), (1024, 1024), (700, 300),
+                                 (1024, 128)])
 def test_bigcore_every_tick(ranc, oracle_mod, kernel, A, N):
     """Cores beyond 256 x 256: on the tensor cores they run as
     neuron groups (256 rows when A <= 256 and Npad % 256 == 0, else 128);
