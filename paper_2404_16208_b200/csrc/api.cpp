@@ -762,7 +762,7 @@ ranc_status ranc_set_option(ranc_ctx* ctx, int option, int64_t value) {
         return RANC_E_ARG;
       }
       if (value == RANC_KERNEL_TC && (!ctx->net.tc_ok || tc_smem_bytes(ctx->net) > 227 * 1024)) {
-        ctx->err = "network is outside the tensor-core envelope (<= 1024 neurons and axons, whose operands and stages fit 227 KB of shared memory; 16-bit weights: <= 512 axons)";
+        ctx->err = "network is outside the tensor-core envelope (<= 1024 neurons and axons, whose operands and stages fit 227 KB of shared memory; 16-bit weights on the widest cores do not)";
         return RANC_E_CONFIG;
       }
       ctx->kernel = (int32_t)value;  // takes effect at the next ranc_load_inputs / ranc_reset_state

@@ -271,7 +271,7 @@ def test_tc_envelope_rejects_wide_weights(ranc):
     """Weights of any valid width run on the tensor cores (-128..127: one s8
     operand; 16-bit: w = 256*hi + lo, a u8 and an s8 operand), and cores of up
     to 1024 neurons and axons (neuron groups, K chunks of 512 axons); 16-bit
-    weights beyond 512 axons do not fit the shared memory and are refused."""
+    weights on 1024 axons do not fit the shared memory and are refused."""
     from workloads.gen import random_network
     net = random_network(3, 2, 1, 64, 64, 4, 3, wb=16)
     net.weight[0, 0, :2] = [-32768, 32767]
@@ -286,10 +286,10 @@ def test_tc_envelope_rejects_wide_weights(ranc):
     sim = ranc.Simulator(net)
     sim.set_option(ranc.OPT_KERNEL, 2)   # > 512 axons: K chunks of 512
     sim.close()
-    net = random_network(3, 1, 1, 600, 64, 4, 3, wb=16)
+    net = random_network(3, 1, 1, 1024, 64, 4, 3, wb=16)
     sim = ranc.Simulator(net)
     with pytest.raises(ranc.RancError) as ei:
-        sim.set_option(ranc.OPT_KERNEL, 2)   # > 512 axons and 16-bit weights: beyond 227 KB, popcount only
+        sim.set_option(ranc.OPT_KERNEL, 2)   # 1024 axons and 16-bit weights: beyond 227 KB, popcount only
     assert ei.value.code == "RANC_E_CONFIG"
     sim.close()
 
