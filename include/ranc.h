@@ -197,7 +197,7 @@ ranc_status ranc_set_allocator(ranc_ctx* ctx, void* (*alloc)(size_t, void*),
  * axons beyond 512), weights of any valid width (-128..127: one s8 operand;
  * 16-bit: w = 256*hi + lo, a u8 low byte and an s8 high byte, two MMAs),
  * and the kernel's shared memory within 227 KB (16-bit weights on more than
- * ~700 axons do not fit); otherwise RANC_E_CONFIG for value 2. */
+ * ~800 axons do not fit); otherwise RANC_E_CONFIG for value 2. */
 #define RANC_OPT_SAMPLE_TILE 1
 #define RANC_OPT_INPUT_DECODE 2
 /* RANC_OPT_STREAM (streaming mode: one long stream of inputs,
