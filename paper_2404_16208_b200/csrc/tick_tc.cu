@@ -273,7 +273,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
   // items backwards, so a tick starts on the items whose potentials, ring
   // rows and operands the previous tick touched last and are still in L2.
   // Items of one tick are independent, so the order is invisible.
-  const bool rev = !kMulti && p.serp && (p.t & 1);
+  // (word-major instantiations only: on the layered nets' sample-major path
+  // the reverse walk buys no L2 hits and its branches cost the issue-bound
+  // epilogue ~1.5 %, measured)
+  const bool rev = !kMulti && kWm && p.serp && (p.t & 1);
   const int first_idx = rev ? hi - 1 : lo;
   auto adv = [&](int& cl_, int& tile_) {   // the next item in walking order
     if (!rev) {
