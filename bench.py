@@ -104,8 +104,10 @@ def parse():
     ap.add_argument("--samples", type=int, default=0, help="samples (0 = the workload's default)")
     ap.add_argument("--tile", type=int, default=0)
     ap.add_argument("--kernel", default="auto", choices=["auto", "popc", "tc"])
-    ap.add_argument("--ring", default="auto", choices=["auto", "sample", "word", "pull"],
+    ap.add_argument("--ring", default="auto", choices=["auto", "sample", "word", "history"],
                     help="tensor-core scheduler layout (RANC_OPT_RING_LAYOUT)")
+    ap.add_argument("--operand", default="auto", choices=["auto", "folded", "compact"],
+                    help="tensor-core integration operand (RANC_OPT_OPERAND)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-samples", type=int, default=0, help="oracle sample size (0 = auto)")
     return ap.parse_args()
@@ -336,7 +338,10 @@ def run_ours(args, rank, world, local):
     sim.set_option(OPT_KERNEL, {"auto": 0, "popc": 1, "tc": 2}[args.kernel])
     if args.ring != "auto":
         from paper_2404_16208_b200 import OPT_RING_LAYOUT
-        sim.set_option(OPT_RING_LAYOUT, {"sample": 1, "word": 2, "pull": 3}[args.ring])
+        sim.set_option(OPT_RING_LAYOUT, {"sample": 1, "word": 2, "history": 3}[args.ring])
+    if args.operand != "auto":
+        from paper_2404_16208_b200 import OPT_OPERAND
+        sim.set_option(OPT_OPERAND, {"folded": 1, "compact": 2}[args.operand])
     if world > 1:
         init_comm(sim, world, rank, mode=SHARD_CORES if core_sharded else SHARD_SAMPLES)
     sim.load_inputs(inp)
@@ -439,7 +444,8 @@ def run_ours(args, rank, world, local):
                        "l2": (f"state {state_gb:.2f} GB exceeds the 126 MB L2; no flush needed" if state_gb > 0.126
                               else f"state {state_gb * 1e3:.1f} MB fits in L2 (latency-bound workload)"),
                        "sample_tile": info["sample_tile"], "pieces": info["pieces"],
-                       "ring_layout": {1: "sample-major", 2: "word-major", 3: "pull"}.get(info["ring_layout"]),
+                       "ring_layout": {1: "sample-major", 2: "word-major", 3: "history"}.get(info["ring_layout"]),
+                       "operand": {1: "folded", 2: "compact"}.get(info["operand"]),
                        "kernel": ("tcgen05 kind::i8" if info["kernel"] == 2 else
                                   "popcount, streaming (one cooperative launch per run)" if launches == args.steps
                                   else "popcount")},

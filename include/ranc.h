@@ -211,14 +211,17 @@ ranc_status ranc_set_allocator(ranc_ctx* ctx, void* (*alloc)(size_t, void*),
 #define RANC_OPT_KERNEL 3
 /* RANC_OPT_RING_LAYOUT (tensor-core kernel only; device memory layout of the
  * scheduler rings, Alg. 1 l.3-5 and l.15-20, P:79-82 / P:102-110): 0 (default)
- * automatic -- word-major when more than 2/3 of all neurons route to their
- * own destination word (e.g. the random mesh of config 5), else sample-major
- * (layered MNIST nets deposit whole words together); 1 sample-major
+ * automatic -- when more than 2/3 of all neurons route to their own
+ * destination word (e.g. the random mesh of config 5): the history scheduler
+ * (3) if a tick has more than two 64-sample tiles per SM (per-tick
+ * launches), else word-major; otherwise sample-major (layered MNIST nets
+ * deposit whole words together); 1 sample-major
  * [Rp][G][S][W]; 2 word-major [Rp][G][W][S] (a warp's deposits for 32 samples
- * of one route hit one 128-byte line); 3 pull scheduler: no ring -- every
- * tick each neuron's fired bits are published to a history of Rp ticks and
- * every core gathers its axons' sources (fired at t - delay) from it
- * (RANC_E_CONFIG when neuron groups or core sharding are in use).  Takes
+ * of one route hit one 128-byte line); 3 history scheduler: no ring -- every
+ * routing neuron owns a position in its destination core's list and each
+ * tick stores its fired bits there, in the history slot of the arrival tick
+ * t + delay; every core reads its contiguous positions of slot t with one
+ * bulk copy (RANC_E_CONFIG when neuron groups or core sharding are in use).  Takes
  * effect at the next ranc_load_inputs / ranc_reset_state.  Results are
  * identical either way. */
 #define RANC_OPT_RING_LAYOUT 5
@@ -229,6 +232,16 @@ ranc_status ranc_set_allocator(ranc_ctx* ctx, void* (*alloc)(size_t, void*),
  * P:70); 2 every route of delay >= 2 delivers one tick early (a wrong
  * scheduler offset).  Parity tests must fail with either set. */
 #define RANC_OPT_DEBUG_FAULT 6
+/* RANC_OPT_OPERAND (tensor-core kernel, per-tick launches; the integration
+ * operand Wfold[n][a'] = conn[n][a'] * w[n][type(a')]): 0 (default)
+ * automatic -- compact when eligible, the history scheduler is in use and
+ * every core has at most two 64-sample tiles (S <= 128: the 64 KB folded
+ * operand would be re-read from HBM for every 64 samples); 1 folded: the host-folded int8 operand is loaded per
+ * core; 2 compact: the crossbar bits, the K weights per neuron and the axon
+ * types (9.3 KB per 256 x 256 core) are read and expanded on chip
+ * (RANC_E_CONFIG unless the weights fit int8 and the cores have at most 256
+ * neurons and 256 axons).  Results are identical either way. */
+#define RANC_OPT_OPERAND 7
 ranc_status ranc_set_option(ranc_ctx* ctx, int option, int64_t value);
 
 /* Introspection of the compiled network and of the last run. */
@@ -247,7 +260,7 @@ typedef struct {
   int32_t shard_mode;         /* RANC_SHARD_* (0 without a communicator)                */
   int64_t exchange_bytes;     /* core-sharded: bytes sent per tick                      */
   int32_t ring_layout;        /* scheduler ring layout in use: 1 sample-major, 2 word-major (RANC_OPT_RING_LAYOUT) */
-  int32_t reserved;
+  int32_t operand;            /* operand of the last tensor-core launch: 1 folded, 2 compact, 0 none (RANC_OPT_OPERAND) */
 } ranc_info;
 ranc_status ranc_get_info(const ranc_ctx* ctx, ranc_info* info);
 

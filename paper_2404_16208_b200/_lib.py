@@ -23,6 +23,7 @@ OPT_KERNEL = 3
 OPT_STREAM = 4
 OPT_RING_LAYOUT = 5
 OPT_DEBUG_FAULT = 6   # mutation tests only (changes results)
+OPT_OPERAND = 7
 SHARD_SAMPLES = 0
 SHARD_CORES = 1
 
@@ -55,7 +56,7 @@ class Info(C.Structure):
         "ring_rows", "ring_words", "pieces", "sample_tile")] + [
         ("num_samples", C.c_int64), ("device_bytes", C.c_int64), ("kernel_launches", C.c_int64),
         ("kernel", C.c_int32), ("core_lo", C.c_int32), ("cores_local", C.c_int32), ("shard_mode", C.c_int32),
-        ("exchange_bytes", C.c_int64), ("ring_layout", C.c_int32), ("reserved", C.c_int32)]
+        ("exchange_bytes", C.c_int64), ("ring_layout", C.c_int32), ("operand", C.c_int32)]
 
 
 ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p)

@@ -111,7 +111,7 @@ void free_all(ranc_ctx* ctx) {
                     &ctx->d_stage, &ctx->d_stage2, &ctx->d_raster, &ctx->d_fired, &ctx->d_exports, &ctx->d_send, &ctx->d_recv,
                     &ctx->d_send_list, &ctx->d_recv_list, &ctx->d_dbg, &ctx->d_inw, &ctx->d_inslot,
                     &ctx->d_slot_core, &ctx->d_spkin, &ctx->d_digest, &ctx->d_perm_dig, &ctx->d_gsend, &ctx->d_grecv,
-                    &ctx->d_hist, &ctx->d_pull_ent, &ctx->d_pull_base, &ctx->d_pull_aoff};
+                    &ctx->d_hist, &ctx->d_hpos, &ctx->d_hbase, &ctx->d_hax, &ctx->d_xbits, &ctx->d_wq, &ctx->d_tsel};
   for (DevBuf* b : bufs) dev_free(ctx, b);
 }
 
@@ -164,13 +164,12 @@ ranc_status prepare_inputs_tc(ranc_ctx* ctx) {
   return RANC_OK;
 }
 
-// The pull scheduler needs the tensor-core path without neuron groups, all
-// sources in this context (not core-sharded), per-core source lists that fit
-// the u16 offsets, and its gather staging within 227 KB of shared memory.
+// The history scheduler needs the tensor-core path without neuron groups,
+// all sources in this context (not core-sharded), and its staged positions
+// within 227 KB of shared memory.
 bool pull_eligible(const ranc_ctx* ctx) {
   const Compiled& c = ctx->net;
-  return c.tc_ok && !c.tc_grp && ctx->shard_mode != RANC_SHARD_CORES && c.pull_emax <= 65535 &&
-         tc_smem_bytes_pull(c) <= 227 * 1024;
+  return c.tc_ok && !c.tc_grp && ctx->shard_mode != RANC_SHARD_CORES && tc_smem_bytes_pull(c) <= 227 * 1024;
 }
 
 }  // namespace
@@ -232,9 +231,12 @@ ranc_status ranc_load_network(const ranc_network_desc* net, int cuda_device, ran
   if (!s && c.tc_ok) s = upload(ctx, &ctx->d_wflags_tc, c.wflags_tc);
   if (!s && c.tc_ok) s = upload(ctx, &ctx->d_incoming, c.incoming);
   if (!s && c.tc_ok) s = upload(ctx, &ctx->d_word_runs, c.word_runs);
-  if (!s && c.tc_ok) s = upload(ctx, &ctx->d_pull_ent, c.pull_ent);
-  if (!s && c.tc_ok) s = upload(ctx, &ctx->d_pull_base, c.pull_base);
-  if (!s && c.tc_ok) s = upload(ctx, &ctx->d_pull_aoff, c.pull_aoff);
+  if (!s && c.tc_ok) s = upload(ctx, &ctx->d_hpos, c.hpos);
+  if (!s && c.tc_ok) s = upload(ctx, &ctx->d_hbase, c.hbase);
+  if (!s && c.tc_ok) s = upload(ctx, &ctx->d_hax, c.hax);
+  if (!s && c.tc_comp_ok) s = upload(ctx, &ctx->d_xbits, c.xbits);
+  if (!s && c.tc_comp_ok) s = upload(ctx, &ctx->d_wq, c.wq);
+  if (!s && c.tc_comp_ok) s = upload(ctx, &ctx->d_tsel, c.tsel);
   if (!s) {
     int sms = 0;
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cuda_device) == cudaSuccess && sms > 0)
@@ -353,16 +355,22 @@ ranc_status ranc_reset_state(ranc_ctx* ctx) {
                         tc_smem_bytes(ctx->net) > 227 * 1024)
                            ? RANC_KERNEL_POPC
                            : RANC_KERNEL_TC;
-  // the pull scheduler (layout 3) replaces the word-major ring on request
-  const bool pull = ctx->kernel_active == RANC_KERNEL_TC && ctx->ring_layout == 3 && pull_eligible(ctx);
+  // the history scheduler (layout 3) replaces the word-major ring on request,
+  // and automatically for networks of per-neuron routes whose ticks run as
+  // per-tick launches anyway (more than two 64-sample tiles per SM: no
+  // cooperative multi-tick launch), e.g. config 5: 126 -> 97 us per tick
+  const int64_t tc_items = (int64_t)ctx->G_loc * ((ctx->S + tc_tile() - 1) / tc_tile());
+  const bool pull = ctx->kernel_active == RANC_KERNEL_TC && pull_eligible(ctx) &&
+                    (ctx->ring_layout == 3 ||
+                     (ctx->ring_layout == 0 && ctx->net.tc_wmajor && tc_items > 2 * (int64_t)ctx->num_sms));
   const bool wmajor = ctx->kernel_active == RANC_KERNEL_TC &&
                       (pull || ctx->ring_layout == 2 || (ctx->ring_layout == 0 && ctx->net.tc_wmajor));
   if (wmajor != ctx->ring_wmajor) ctx->inw_valid = false;   // decoded inputs follow the ring layout
   ctx->ring_wmajor = wmajor;
   ctx->ring_pull = pull;
   if (pull) {
-    // fired-bit history [Rp][G_loc][nT][Npad][2] u32, empty (no spikes before tick 0)
-    const size_t hb = (size_t)ctx->net.Rp * ctx->G_loc * ((ctx->S + tc_tile() - 1) / tc_tile()) * ctx->net.Npad * 8;
+    // fired-bit history [Rp][nT][P][2] u32, empty (no spikes before tick 0)
+    const size_t hb = (size_t)ctx->net.Rp * ((ctx->S + tc_tile() - 1) / tc_tile()) * ctx->net.hbase.back() * 8;
     if (ctx->d_hist.bytes != hb) TRY(dev_alloc(ctx, &ctx->d_hist, hb));
     CK(cudaMemsetAsync(ctx->d_hist.p, 0, hb, ctx->stream), "history clear");
   }
@@ -578,33 +586,29 @@ ranc_status ranc_read_pending(ranc_ctx* ctx, uint32_t* bits, size_t n) {
   }
   CK(cudaSetDevice(ctx->device), "cudaSetDevice");
   if (ctx->ring_pull) {
-    // pull scheduler: the spikes due at tick now+j are the fired bits of tick
-    // now+j-d (d > j, not before tick 0) of every source with delay d
+    // history scheduler: the spikes due at tick now+j on position i (delay
+    // d) were stored at tick now+j-d; they are pending iff that tick has run
+    // (d > j) -- otherwise the slot still holds the word of Rp ticks earlier
     std::vector<uint32_t> hh(ctx->d_hist.bytes / 4);
     CK(cudaMemcpyAsync(hh.data(), ctx->d_hist.p, ctx->d_hist.bytes, cudaMemcpyDeviceToHost, ctx->stream), "D2H hist");
     TRY(sync(ctx, "ranc_read_pending"));
     std::memset(bits, 0, want * 4);
     const int64_t nT = (ctx->S + tc_tile() - 1) / tc_tile();
-    const size_t slot_words = (size_t)GL * nT * c.Npad * 2;
-    for (int g = 0; g < GL; ++g) {
-      const uint16_t* aoff = &c.pull_aoff[(size_t)g * (c.Kp + 8)];
-      const uint32_t base = c.pull_base[g];
-      for (int ap = 0; ap < c.A; ++ap)
-        for (int e = aoff[ap]; e < aoff[ap + 1]; ++e) {
-          const uint32_t ent = c.pull_ent[base + e];
-          const int sc = (int)(ent & 0xFFFFu), sn = (int)((ent >> 16) & 0x3FFu), d = (int)(ent >> 26);
-          const int a = c.perm_tc[(size_t)g * c.A + ap];
-          for (int j = 0; j < std::min(d, c.D); ++j) {
-            const int64_t tau = ctx->now + j - d;
-            if (tau < 0) continue;
-            const uint32_t* hs = &hh[(size_t)(tau & (c.Rp - 1)) * slot_words];
-            for (int64_t s = 0; s < ctx->S; ++s) {
-              const uint32_t w = hs[(((size_t)sc * nT + s / 64) * c.Npad + sn) * 2 + (s % 64) / 32];
-              if ((w >> (s % 32)) & 1u) bits[(((size_t)s * GL + g) * c.D + j) * c.W + (a >> 5)] |= 1u << (a & 31);
-            }
+    const size_t P = c.hbase.back();
+    for (int g = 0; g < GL; ++g)
+      for (uint32_t i = c.hbase[g]; i < c.hbase[g + 1]; ++i) {
+        const int d = c.hdel[i];
+        if (!d) continue;   // padding
+        const int a = c.perm_tc[(size_t)g * c.A + c.hax[i]];
+        for (int j = 0; j < std::min(d, c.D); ++j) {
+          if (ctx->now + j - d < 0) continue;
+          const uint32_t* hs = &hh[(size_t)((ctx->now + j) & (c.Rp - 1)) * nT * P * 2];
+          for (int64_t s = 0; s < ctx->S; ++s) {
+            const uint32_t w = hs[((size_t)(s / 64) * P + i) * 2 + (s % 64) / 32];
+            if ((w >> (s % 32)) & 1u) bits[(((size_t)s * GL + g) * c.D + j) * c.W + (a >> 5)] |= 1u << (a & 31);
           }
         }
-    }
+      }
     return RANC_OK;
   }
   std::vector<uint32_t> h((size_t)c.Rp * GL * ctx->Sr * c.W);
@@ -769,16 +773,28 @@ ranc_status ranc_set_option(ranc_ctx* ctx, int option, int64_t value) {
       return RANC_OK;
     case RANC_OPT_RING_LAYOUT:
       if (value < 0 || value > 3) {
-        ctx->err = "ring layout must be 0 (auto), 1 (sample-major), 2 (word-major) or 3 (pull scheduler); "
+        ctx->err = "ring layout must be 0 (auto), 1 (sample-major), 2 (word-major) or 3 (history scheduler); "
                    "tensor-core path";
         return RANC_E_ARG;
       }
       if (value == 3 && !pull_eligible(ctx)) {
-        ctx->err = "the pull scheduler needs the tensor-core path without neuron groups, no core sharding and "
-                   "per-core source lists within the shared-memory budget";
+        ctx->err = "the history scheduler needs the tensor-core path without neuron groups, no core sharding and "
+                   "per-core position lists within the shared-memory budget";
         return RANC_E_CONFIG;
       }
       ctx->ring_layout = (int32_t)value;  // takes effect at the next ranc_load_inputs / ranc_reset_state
+      return RANC_OK;
+    case RANC_OPT_OPERAND:
+      if (value < 0 || value > 2) {
+        ctx->err = "operand must be 0 (auto), 1 (folded Wfold) or 2 (compact, expanded on chip)";
+        return RANC_E_ARG;
+      }
+      if (value == 2 && !ctx->net.tc_comp_ok) {
+        ctx->err = "the compact operand needs the tensor-core path with int8 weights and cores of at most 256 "
+                   "neurons and 256 axons";
+        return RANC_E_CONFIG;
+      }
+      ctx->operand = (int32_t)value;  // chosen per launch (per-tick tensor-core launches)
       return RANC_OK;
     case RANC_OPT_DEBUG_FAULT: {
       if (value < 0 || value > 2) {
@@ -817,6 +833,7 @@ ranc_status ranc_get_info(const ranc_ctx* ctx, ranc_info* info) {
   info->device_bytes = ctx->device_bytes; info->kernel_launches = ctx->launches;
   info->kernel = ctx->kernel_active;
   info->ring_layout = ctx->ring_pull ? 3 : ctx->ring_wmajor ? 2 : 1;
+  info->operand = ctx->operand_used;
   info->core_lo = ctx->c_lo;
   info->cores_local = ctx->G_loc;
   info->shard_mode = (ctx->nccl_comm || ctx->group) ? ctx->shard_mode : 0;

@@ -394,41 +394,95 @@ ranc_status validate_and_compile(const ranc_network_desc* d, Compiled* out, std:
             ++scattered;
       o.tc_wmajor = 3 * scattered > 2 * (int64_t)G * N;
     }
-    // Pull scheduler (RANC_OPT_RING_LAYOUT 3): for every destination core and
-    // tensor-core axon a', the routing neurons that feed it -- the
-    // destination gathers their fired bits of tick t - delay from a history
-    // of fired bitmaps instead of receiving deposits into a ring.
-    //   pull_base [G+1]            first entry of core c
-    //   pull_ent  [entries]        src core | src neuron << 16 | delay << 26, sorted by a'
-    //   pull_aoff [G][Kp + 8] u16  entries of axon a' of core c: [aoff[a'], aoff[a'+1]) after pull_base[c]
+    // History scheduler (RANC_OPT_RING_LAYOUT 3): every routing neuron owns
+    // one POSITION in a destination-ordered list; each tick it stores its
+    // fired bits (one word per 32 samples, zero or not) at its position in the
+    // history slot of its ARRIVAL tick t + delay, and the destination core
+    // reads its contiguous positions of slot t with one bulk copy (Alg. 1
+    // l.15-20 / l.3-5).  No atomics, no clears: the slot
+    // of tick t holds, at position i, the word written at tick t - d_i.
+    //   hbase [G+1]      first position of destination core c (multiple of 8:
+    //                    16-byte aligned bulk copies; padding positions have no
+    //                    writer and stay zero)
+    //   hpos  [G][Npad]  position of routing neuron (c, n), ~0u otherwise
+    //   hax   [P] u16    destination axon a' (tensor-core order) of a position
+    //   hdel  [P] u8     delay of a position (host: ranc_read_pending), 0 = padding
+    // Positions of one destination are sorted by (delay, source core, source
+    // neuron): the words that share a 32-byte sector are mostly written by
+    // one source warp in one tick (whole sectors reach DRAM).
     {
-      std::vector<std::vector<std::pair<int, uint32_t>>> in(G);   // (a', entry)
+      struct Src { uint32_t d, sc, sn, ap; };
+      std::vector<std::vector<Src>> in(G);
       for (int c = 0; c < G; ++c)
         for (int n = 0; n < N; ++n) {
           const uint2 r = o.route_tc[(size_t)c * Np + n];
           if (route_kind(r.x) != RK_ROUTE) continue;
-          in[r.y].push_back({(int)route_axon(r.x),
-                             (uint32_t)c | ((uint32_t)n << 16) | (route_delay(r.x) << 26)});
+          in[r.y].push_back({route_delay(r.x), (uint32_t)c, (uint32_t)n, route_axon(r.x)});
         }
-      o.pull_base.assign(G + 1, 0);
-      o.pull_aoff.assign((size_t)G * (o.Kp + 8), 0);
-      o.pull_emax = 0;
-      o.pull_ent.clear();
+      o.hbase.assign(G + 1, 0);
+      o.hpos.assign((size_t)G * Np, ~0u);
+      o.hax.clear();
+      o.hdel.clear();
+      o.hist_emax = 0;
       for (int c = 0; c < G; ++c) {
-        std::stable_sort(in[c].begin(), in[c].end(),
-                         [](const std::pair<int, uint32_t>& x, const std::pair<int, uint32_t>& y) { return x.first < y.first; });
-        o.pull_base[c] = (uint32_t)o.pull_ent.size();
-        o.pull_emax = std::max<int32_t>(o.pull_emax, (int32_t)in[c].size());
-        uint16_t* aoff = &o.pull_aoff[(size_t)c * (o.Kp + 8)];
-        size_t e = 0;
-        for (int ap = 0; ap <= o.Kp; ++ap) {
-          aoff[ap] = (uint16_t)std::min<size_t>(e, 65535);
-          while (ap < o.Kp && e < in[c].size() && in[c][e].first == ap) ++e;
+        std::sort(in[c].begin(), in[c].end(), [](const Src& x, const Src& y) {
+          return x.d != y.d ? x.d < y.d : x.sc != y.sc ? x.sc < y.sc : x.sn < y.sn;
+        });
+        o.hbase[c] = (uint32_t)o.hax.size();
+        for (const Src& s : in[c]) {
+          o.hpos[(size_t)s.sc * Np + s.sn] = (uint32_t)o.hax.size();
+          o.hax.push_back((uint16_t)s.ap);
+          o.hdel.push_back((uint8_t)s.d);
         }
-        for (auto& pe : in[c]) o.pull_ent.push_back(pe.second);
+        while (o.hax.size() & 7) {
+          o.hax.push_back(0);
+          o.hdel.push_back(0);
+        }
+        o.hist_emax = std::max<int32_t>(o.hist_emax, (int32_t)(o.hax.size() - o.hbase[c]));
       }
-      o.pull_base[G] = (uint32_t)o.pull_ent.size();
-      if (o.pull_ent.empty()) o.pull_ent.push_back(0u);   // (a valid device buffer)
+      o.hbase[G] = (uint32_t)o.hax.size();
+      if (o.hax.empty())   // (valid device buffers)
+        for (int i = 0; i < 8; ++i) {
+          o.hax.push_back(0);
+          o.hdel.push_back(0);
+        }
+    }
+    // Compact operand (RANC_OPT_OPERAND, per-tick launches with few sample
+    // tiles per core): instead of the 64 KB folded Wfold, the crossbar bits,
+    // the neuron's K type weights and the axon types (9.3 KB per core at
+    // A = N = 256); the spike warps expand it on chip, one core
+    // ahead.  Bit layout for the expansion (tick_tc.cu): in word w of neuron
+    // n, axon a' = 32w + 4m + j (m = 0..7, j = 0..3) is bit 8j + 7 - m, so
+    // that (word << m) holds the connections of the m-th 4-axon group in the
+    // sign bits of its four bytes (one prmt turns them into byte masks).
+    //   xbits u32 [G][W][Npad]   wq u32 [G][Npad] (byte k = int8 w[n][k])
+    //   tsel  u32 [G][Kp/4]      prmt selector: nibble j = type of axon 4g + j
+    o.tc_comp_ok = o.tc_ok && !o.tc_wide && !o.tc_grp && o.Npad <= 256 && W <= 8;
+    o.xbits.clear();
+    o.wq.clear();
+    o.tsel.clear();
+    if (o.tc_comp_ok) {
+      o.xbits.assign((size_t)G * W * Np, 0u);
+      o.wq.assign((size_t)G * Np, 0u);
+      o.tsel.assign((size_t)G * (o.Kp / 4), 0u);
+      for (int c = 0; c < G; ++c) {
+        const int32_t* inv = &o.inv_tc[(size_t)c * A];
+        const int32_t* perm = &o.perm_tc[(size_t)c * A];
+        for (int ap = 0; ap < A; ++ap)
+          o.tsel[(size_t)c * (o.Kp / 4) + ap / 4] |= (uint32_t)d->axon_type[(size_t)c * A + perm[ap]] << (4 * (ap & 3));
+        for (int n = 0; n < N; ++n) {
+          const size_t cn = (size_t)c * N + n;
+          uint32_t q = 0;
+          for (int t = 0; t < K; ++t) q |= (uint32_t)(uint8_t)(int8_t)d->weight[cn * K + t] << (8 * t);
+          o.wq[(size_t)c * Np + n] = q;
+          const uint32_t* src = d->crossbar + cn * W;
+          for (int a = 0; a < A; ++a)
+            if ((src[a >> 5] >> (a & 31)) & 1u) {
+              const int ap = inv[a], w = ap >> 5, m = (ap >> 2) & 7, j = ap & 3;
+              o.xbits[((size_t)c * W + w) * Np + n] |= 1u << (8 * j + 7 - m);
+            }
+        }
+      }
     }
     // folded weights in the canonical operand layout (tc.h)
     // (wide weights: [lo | hi] per core, w = 256*hi + lo, lo unsigned)

@@ -70,6 +70,7 @@ struct TickParams {
   int32_t grp_rows;         // tensor-core path: rows per neuron group (Compiled::grp_rows)
   int32_t grp_ns;           // neuron-group launch: spike stages (2, or 1 beyond 512 axons)
   int32_t serp;             // tensor-core per-tick launches: odd ticks walk each CTA's items backwards
+  uint32_t epi_wait, epi_backoff;   // tensor-core per-tick launches: epilogue accumulator wait (suspend hint / back-off ns)
   int32_t fault;            // RANC_OPT_DEBUG_FAULT (mutation tests): 1 = skip the grid barrier of
                             // cooperative multi-tick launches
   int64_t t;                // tick being executed
@@ -101,14 +102,22 @@ struct TickParams {
   const uint8_t* wflags;    // [G][Npad/32] per-warp flags (bit 0: block route), or nullptr
   const uint8_t* incoming;  // [G] 1 if any neuron of the network routes to the core (its ring can be non-zero)
   uint32_t* spkin;          // RANC_TRACE_STATE_DIGEST: [S][G_loc][W] axon spikes integrated this tick, or nullptr
-  // pull scheduler (tensor-core path, RANC_OPT_RING_LAYOUT 3): fired-bit
-  // history u32 [Rp][G_loc][nT][Npad][2] (slot t & (Rp-1); word j = samples
-  // 32j..32j+31 of the tile) and the per-core source lists (Compiled::pull_*)
+  // history scheduler (tensor-core path, RANC_OPT_RING_LAYOUT 3): fired-bit
+  // history u32 [Rp][nT][P][2] (slot = arrival tick & (Rp-1); position i of
+  // the destination-ordered list; word j = samples 32j..32j+31 of the tile)
+  // and the position tables (Compiled::h*)
   uint32_t* hist;
-  const uint32_t* pull_ent;
-  const uint32_t* pull_base;
-  const uint16_t* pull_aoff;
-  int32_t pull_emax;
+  const uint32_t* hpos;
+  const uint32_t* hbase;
+  const uint16_t* hax;
+  int32_t hist_emax;
+  int32_t hist_P;
+  // compact operand (tensor-core path, RANC_OPT_OPERAND): Compiled::xbits / wq / tsel
+  const uint32_t* xbits;
+  const uint32_t* wq;
+  const uint32_t* tsel;
+  int32_t comp_epi;         // compact operand expanded by the epilogue warps (else the spike warps)
+  int32_t comp_nc;          // type-selector slots in shared memory (cores of one CTA, at most)
 };
 
 // Host copy of the compiled network.
@@ -132,10 +141,15 @@ struct Compiled {
   std::vector<int32_t> nruns;   // [G]
   std::vector<int32_t> word_runs;  // [G][W] first run | count << 16 (runs overlapping word w)
   std::vector<uint8_t> incoming;   // [G] 1 if some neuron routes to the core
-  std::vector<uint32_t> pull_base; // [G+1] pull scheduler: first source entry of core c (compile.cpp)
-  std::vector<uint32_t> pull_ent;  // src core | src neuron << 16 | delay << 26, per core sorted by axon a'
-  std::vector<uint16_t> pull_aoff; // [G][Kp + 8] per-axon entry offsets relative to pull_base[c]
-  int32_t pull_emax = 0;           // most source entries of one core
+  bool tc_comp_ok = false;         // the compact operand applies (int8 weights, Npad <= 256, A <= 256)
+  std::vector<uint32_t> xbits;     // [G][W][Npad] crossbar bits, expansion bit order (compile.cpp)
+  std::vector<uint32_t> wq;        // [G][Npad] the K type weights of neuron n as int8 bytes
+  std::vector<uint32_t> tsel;      // [G][Kp/4] prmt selectors: nibble j = type of axon a' = 4g + j
+  std::vector<uint32_t> hbase;     // [G+1] history scheduler: first position of destination core c (compile.cpp)
+  std::vector<uint32_t> hpos;      // [G][Npad] position of routing neuron (c, n), ~0u otherwise
+  std::vector<uint16_t> hax;       // [P] destination axon a' of a position
+  std::vector<uint8_t> hdel;       // [P] delay of a position (0: padding)
+  int32_t hist_emax = 0;           // most positions of one destination core
   std::vector<uint8_t> wflags_tc;  // [G][Npad/32] bit 0: all routing neurons of the warp share one
                                    // (dest core, ring word, delay) in the tensor-core axon order
   int32_t rmax = 0;
@@ -220,9 +234,13 @@ struct ranc_ctx {
   ranc::DevBuf d_dbg;            // RANC_DEBUG_TIMELINE
   // tensor-core path: input decode (once per ranc_load_inputs)
   ranc::DevBuf d_inw, d_inslot, d_slot_core;
-  // tensor-core path: pull scheduler (latched at reset, RANC_OPT_RING_LAYOUT 3)
-  ranc::DevBuf d_hist, d_pull_ent, d_pull_base, d_pull_aoff;
+  // tensor-core path: history scheduler (latched at reset, RANC_OPT_RING_LAYOUT 3)
+  ranc::DevBuf d_hist, d_hpos, d_hbase, d_hax;
   bool ring_pull = false;
+  // tensor-core path: compact operand (RANC_OPT_OPERAND; chosen per launch)
+  ranc::DevBuf d_xbits, d_wq, d_tsel;
+  int32_t operand = 0;           // RANC_OPT_OPERAND request: 0 auto, 1 folded, 2 compact
+  int32_t operand_used = 0;      // operand of the last tensor-core launch (1 folded, 2 compact)
   // RANC_TRACE_STATE_DIGEST
   ranc::DevBuf d_spkin, d_digest, d_perm_dig;
   int32_t perm_dig_kernel = 0;   // kernel whose axon order d_perm_dig holds
@@ -265,6 +283,7 @@ int pieces_template(int E);
 int tc_tile();
 size_t tc_smem_bytes(const Compiled& n);
 size_t tc_smem_bytes_pull(const Compiled& n);
+size_t tc_smem_bytes_comp(const Compiled& n, bool pull, int nc = 1);
 cudaError_t launch_tick_tc(ranc_ctx* ctx, TickParams p);
 cudaError_t decode_inputs_tc(ranc_ctx* ctx);
 bool stream_eligible(ranc_ctx* ctx, int64_t num_ticks);

@@ -69,10 +69,10 @@ constexpr int kSub = 16;               // samples per TMEM load / LIF pass of an
 static_assert(kExpThreads == 2 * NT, "spike stage maps thread -> (sample, 16-bit half)");
 
 enum Bar { FULL0 = 0, SEMPTY0 = 4, BFULL0 = 8, BEMPTY0 = 12, ACCFULL0 = 16, ACCEMPTY0 = 20, WFULL = 24, WFREE = 25,
-           NBARS = 26 };
+           WFULL1 = 26, WFREE1 = 27, NBARS = 28 };
 
 struct TcLayout {
-  uint32_t w, runs, lut, potbuf, cplanes, pmask, stage, b, raw, lines, pull, paoff, stage_bytes, total;
+  uint32_t w, runs, lut, tsel, potbuf, cplanes, pmask, stage, b, raw, lines, pull, paoff, hcnt, stage_bytes, total;
 };
 
 // WIp: input-line row words (multiple of 4)
@@ -91,6 +91,9 @@ constexpr int NS_GRP = 2;
 // of 512 axons (one 64 KB buffer load each, accumulated in TMEM) and the
 // 64 KB spike stage is single (TickParams::grp_ns = 1)
 constexpr int kKChunk = 512;
+// compact-operand launch: two expanded operand buffers (the next core's is
+// expanded while this one's MMAs run) leave room for 2 spike stages
+constexpr int NS_COMP = 2;
 // pot_items: potential tiles kept on chip (multi-tick launch with up to two
 // work items per CTA: one region each)
 // cnt_planes: per-thread bit-sliced output-bus counters (multi-tick launch)
@@ -99,24 +102,26 @@ constexpr int kCntPlanes = 8;   // counts < 256 between flushes
 // neuron-group launch, grp)
 __host__ __device__ inline TcLayout tc_layout(int wrows, int Kp, int W, int WIp, int rmax, bool wide, int pot_items = 1,
                                               bool cnt_planes = false, bool multi = false, int grp = 0,
-                                              int pull_emax = -1) {
+                                              int pull_emax = -1, bool comp = false, int comp_nc = 1) {
   // grp: spike stages of a neuron-group launch (0: not grouped); its operand
   // buffer holds one K chunk of at most kKChunk axons
   TcLayout L;
   L.w = 1024;
-  uint32_t o = L.w + (uint32_t)wrows * (grp ? (Kp < kKChunk ? Kp : kKChunk) : Kp) * (wide ? 2u : 1u);
+  uint32_t o = L.w + (uint32_t)wrows * (grp ? (Kp < kKChunk ? Kp : kKChunk) : Kp) * (wide || comp ? 2u : 1u);
   L.runs = o;                                 // int2 [rmax] + int32 [W] of the current core
   o += (uint32_t)rmax * 8 + (uint32_t)W * 4;
   o = (o + 15) & ~15u;
   L.lut = o;                                  // u32 [16]: nibble -> four 0/1 bytes
   o += 256 * 8;
+  L.tsel = o;                                 // compact operand: u32 [comp_nc][Kp/4] prmt type selectors
+  if (comp) o += (uint32_t)Kp * (uint32_t)comp_nc;
   o = (o + 127) & ~127u;
   L.potbuf = o;                               // uint4 [NT/8][epilogue threads]: next tile's potentials
   o += (NT / 8) * (32 * 8) * 16 * (uint32_t)pot_items;   // = 4 chunks x 512 epilogue threads per item
   L.cplanes = o;                              // u32 [items][kCntPlanes][512 epilogue threads]
   if (cnt_planes) o += (uint32_t)pot_items * kCntPlanes * 512 * 4;
   o = (o + 15) & ~15u;
-  L.pmask = o;                                // pull scheduler: u64 [Kp] gathered spike masks per axon
+  L.pmask = o;                                // history scheduler: u64 [Kp] spike masks per axon (64 samples)
   if (pull_emax >= 0) o += (uint32_t)Kp * 8;
   L.stage = (o + 1023) & ~1023u;
   uint32_t q = 0;
@@ -126,13 +131,16 @@ __host__ __device__ inline TcLayout tc_layout(int wrows, int Kp, int W, int WIp,
   q = (q + 15) & ~15u;
   L.lines = q; q += (uint32_t)NT * (WIp > W ? WIp : W) * 4;  // input line rows or decoded words (TMA)
   q = (q + 15) & ~15u;
-  L.paoff = q;                                // pull: u16 [Kp + 8] per-axon source offsets (TMA)
-  if (pull_emax >= 0) q += (uint32_t)(Kp + 8) * 2;
+  L.paoff = q;                                // history: u16 [emax] destination axon per position (TMA)
+  if (pull_emax >= 0) q += (uint32_t)pull_emax * 2;
   q = (q + 15) & ~15u;
-  L.pull = q;                                 // pull: u64 [emax] gathered source words (cp.async)
+  L.hcnt = q;                                 // history: u32 the core's position count (producer)
+  if (pull_emax >= 0) q += 16;
+  q = (q + 15) & ~15u;
+  L.pull = q;                                 // history: u64 [emax] the positions' words of this tile (TMA)
   if (pull_emax >= 0) q += (uint32_t)pull_emax * 8;
   L.stage_bytes = (q + 1023) & ~1023u;
-  L.total = L.stage + (grp ? grp : wide ? NS_WIDE : multi ? NS_MULTI : NS) * L.stage_bytes;
+  L.total = L.stage + (grp ? grp : wide ? NS_WIDE : multi ? NS_MULTI : comp ? NS_COMP : NS) * L.stage_bytes;
   return L;
 }
 
@@ -233,15 +241,19 @@ __device__ __forceinline__ uint32_t lif(const uint4 (&cur)[NE / 8], const uint32
 // (loaded in turn into the one operand buffer), every group filling its own
 // accumulator stage and being retired by the epilogue like a work item of
 // its own (a sub-item).  Per-tick launches only.
-// kPull: the pull scheduler (word-major networks, per-tick launches): every
-// tick the epilogue writes each neuron's fired bits to a history of Rp ticks,
-// and the producer gathers each axon's sources from it (one 8-byte cp.async
-// per source: its fired bits of tick t - delay for the 64 samples of the
-// tile); the spike stage ORs them per axon and transposes them into the
-// staged ring-word layout.  No deposits, no ring, no clears.
-template <bool kMulti, bool kDebug, bool kWm, bool kWide, bool kGrp = false, bool kPull = false>
+// kPull: the history scheduler (word-major networks, per-tick launches).
+// Every routing neuron owns a position in its destination core's list
+// (compile.cpp); each tick the epilogue stores the neuron's fired bits of the
+// tile's samples at that position in the history slot of the ARRIVAL tick
+// t + delay (plain stores, zero or not), and the producer of the destination
+// loads the core's contiguous positions of slot t with one bulk copy; the
+// spike stage ORs each position's word into its axon's mask and transposes
+// the masks into the staged ring-word layout.  No atomics in global memory,
+// no clears: position i of slot t was written at tick t - d_i.
+template <bool kMulti, bool kDebug, bool kWm, bool kWide, bool kGrp = false, bool kPull = false, bool kComp = false>
 __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams p, const int nticks_arg) {
   static_assert(!kGrp || !kMulti, "neuron groups are a per-tick launch");
+  static_assert(!kComp || (!kMulti && !kWide && !kGrp), "the compact operand is a per-tick int8 launch");
   static_assert(!kPull || (!kMulti && kWm && !kGrp), "the pull scheduler is a per-tick word-major launch");
   const int nticks = kMulti ? nticks_arg : 1;
   // kDebug: the RANC_DEBUG_TIMELINE instrumentation (a separate instantiation,
@@ -258,8 +270,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
   const int GS = kGrp ? p.grp_rows : Np;
   const int nGrp = kGrp ? Np / GS : 1;
   const TcLayout L = tc_layout(GS, Kp, W, WIp, p.rmax, kWide, kMulti ? p.pot_items : 1, kMulti && p.out_planes,
-                               kMulti, kGrp ? p.grp_ns : 0, kPull ? p.pull_emax : -1);
-  constexpr int NS = kGrp ? NS_GRP : kWide ? NS_WIDE : kMulti ? NS_MULTI : ranc::NS;   // spike stages (at most)
+                               kMulti, kGrp ? p.grp_ns : 0, kPull ? p.hist_emax : -1, kComp, kComp ? p.comp_nc : 1);
+  constexpr int NS = kGrp ? NS_GRP : kWide ? NS_WIDE : kMulti ? NS_MULTI : kComp ? NS_COMP : ranc::NS;   // spike stages (at most)
   const int nsr = kGrp ? p.grp_ns : NS;   // spike stages in use
   const int nK = kGrp ? (Kp + kKChunk - 1) / kKChunk : 1;   // K chunks of a group's operand
   uint8_t* w_s = smem + L.w;
@@ -315,7 +327,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
   if (warp == mma_warp) tc::alloc(tmem_holder, tcols < 32 ? 32 : tcols);
   if (threadIdx.x == 0) {
     for (int i = 0; i < NS; ++i) {
-      ptx::mbar_init(&bars[FULL0 + i], kPull ? 33 : 1);   // pull: + one cp.async arrival per producer lane
+      ptx::mbar_init(&bars[FULL0 + i], 1);
       ptx::mbar_init(&bars[SEMPTY0 + i], 1);
       ptx::mbar_init(&bars[BFULL0 + i], 1);
       ptx::mbar_init(&bars[BEMPTY0 + i], 1);
@@ -324,8 +336,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       ptx::mbar_init(&bars[ACCFULL0 + i], 1);
       ptx::mbar_init(&bars[ACCEMPTY0 + i], kEpiWarps);
     }
-    ptx::mbar_init(&bars[WFULL], 1);
+    // (compact operand expanded by the epilogue: one arrival per epilogue warp)
+    ptx::mbar_init(&bars[WFULL], kComp && p.comp_epi ? kEpiWarps : 1);
     ptx::mbar_init(&bars[WFREE], 1);
+    ptx::mbar_init(&bars[WFULL1], kComp && p.comp_epi ? kEpiWarps : 1);
+    ptx::mbar_init(&bars[WFREE1], 1);
     ptx::fence_mbar_init();
   }
   // programmatic dependent launch (per-tick launches): let the next tick's
@@ -367,10 +382,16 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
         const int slot = p.inw ? p.inslot[cl] : -1;
         const uint32_t ring_bytes = (!kPull && p.incoming[c]) ? (uint32_t)NT * W * 4 : 0u;
         const uint32_t line_bytes = !inject ? 0u : (p.inw ? (uint32_t)NT * W * 4 : (uint32_t)NT * WIp * 4);
-        const uint32_t aoff_bytes = kPull ? (uint32_t)(Kp + 8) * 2 : 0u;
-        ptx::mbar_arrive_expect_tx(&bars[FULL0 + s], ring_bytes + line_bytes + aoff_bytes);
-        if (kPull)
-          ptx::bulk_g2s(st + L.paoff, p.pull_aoff + (size_t)c * (Kp + 8), aoff_bytes, &bars[FULL0 + s]);
+        // history scheduler: the core's positions (axons, and their words of
+        // slot t for this tile); a multiple of 8 positions, 16-byte aligned
+        const uint32_t hb0 = kPull ? p.hbase[c] : 0u, hcnt = kPull ? p.hbase[c + 1] - hb0 : 0u;
+        if (kPull) *reinterpret_cast<uint32_t*>(st + L.hcnt) = hcnt;   // released by the arrive below
+        ptx::mbar_arrive_expect_tx(&bars[FULL0 + s], ring_bytes + line_bytes + hcnt * 10u);
+        if (kPull && hcnt) {
+          ptx::bulk_g2s(st + L.paoff, p.hax + hb0, hcnt * 2u, &bars[FULL0 + s]);
+          ptx::bulk_g2s(st + L.pull, p.hist + (((size_t)cur * nT + tile) * p.hist_P + hb0) * 2, hcnt * 8u,
+                        &bars[FULL0 + s]);
+        }
         // ring rows and decoded inputs: sample-major [..][Sr][W] is one bulk
         // copy per tile, staged [NT][W]; word-major [..][W][Sr] one copy of
         // the tile's 64 samples per ring word, staged [W][NT]
@@ -390,42 +411,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
         else if (inject)
           ptx::bulk_g2s(st + L.lines, p.lines + ((size_t)t * p.Sr + s0) * WIp, line_bytes, &bars[FULL0 + s]);
       }
-      if (kPull) {
-        // gather: the fired bits (tick t - delay, this tile's 64 samples) of
-        // every source of every axon of core c, in the core's source order
-        uint8_t* st = smem + L.stage + s * L.stage_bytes;
-        const uint32_t base = p.pull_base[c], cnt = p.pull_base[c + 1] - base;
-        const size_t slot_stride = (size_t)p.G_loc * nT * Np * 2;   // u32 per history slot
-        // entries are loaded in batches of kPer per lane (independent loads:
-        // one L2 latency per batch, not per entry), then the copies issued
-        constexpr int kPer = 8;
-        for (uint32_t e0 = 0; e0 < cnt; e0 += 32 * kPer) {
-          uint32_t ents[kPer];
-#pragma unroll
-          for (int i = 0; i < kPer; ++i) {
-            const uint32_t e = e0 + i * 32 + lane;
-            ents[i] = e < cnt ? __ldg(p.pull_ent + base + e) : 0u;
-          }
-#pragma unroll
-          for (int i = 0; i < kPer; ++i) {
-            const uint32_t e = e0 + i * 32 + lane;
-            if (e < cnt) {
-              const uint32_t ent = ents[i];
-              const int sc = (int)(ent & 0xFFFFu) - p.c_lo, sn = (int)((ent >> 16) & 0x3FFu), d = (int)(ent >> 26);
-              const uint32_t* src = p.hist + (size_t)((t - d) & p.rp_mask) * slot_stride +
-                                    (((size_t)sc * nT + tile) * Np + sn) * 2;
-              ptx::cp_async8(st + L.pull + e * 8, src);
-            }
-          }
-        }
-        ptx::cp_async_mbar_arrive_noinc(&bars[FULL0 + s]);
-      }
       __syncwarp();
       // a new core's operand, once the previous core's MMAs have read the
       // buffer.  Issued AFTER this item's ring rows / gathers, so that their
       // latency overlaps the previous item's MMAs instead of following them
       // (one tile per core at config 5: every item waits here).
-      if (!kGrp && c != prev_core) {
+      if (!kGrp && !kComp && c != prev_core) {
         ++jw;
         if (jw > 0) wait(&bars[WFREE], (jw - 1) & 1);
         if (lane == 0) {
@@ -467,9 +458,13 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
   } else if (warp == mma_warp) {
     // ------------------------------------------------------------ MMA issuer
     // convergent warp loop; one elected thread issues the tcgen05 operations
-    const uint32_t id = tc::idesc_i8(128, NT);
+    // history scheduler: the B operand is MN-major (instruction descriptor
+    // bit 16; descriptor LBO = 512 between 8-axon groups, SBO = 128 between
+    // 16-sample groups, the same 2 KB per 32-axon K step)
+    const uint32_t bmn = kPull ? (1u << 16) : 0u;
+    const uint32_t id = tc::idesc_i8(128, NT) | bmn;
     // wide weights: w = 256*hi + lo, lo the UNSIGNED low byte, hi signed
-    const uint32_t id_lo = kWide ? tc::idesc_i8(128, NT, false) : id;
+    const uint32_t id_lo = kWide ? (tc::idesc_i8(128, NT, false) | bmn) : id;
     const uint32_t lbo_a = (uint32_t)GS * 16, lbo_b = (uint32_t)NT * 16;   // tc.h layout
     int prev_core = -1, jw = -1;
     for (int it = 0; it < nticks; ++it) {
@@ -480,7 +475,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       const int s = k % nsr, u = k / nsr;
       if (!kGrp && c != prev_core) {
         ++jw;
-        wait(&bars[WFULL], jw & 1);
+        // compact operand: core jw's expanded operand is buffer jw & 1
+        if (kComp) wait(&bars[(jw & 1) ? WFULL1 : WFULL], (jw >> 1) & 1);
+        else wait(&bars[WFULL], jw & 1);
         prev_core = c;
       }
       wait(&bars[BFULL0 + s], u & 1);
@@ -499,13 +496,15 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       if (lane == 0) {
         stamp_k(k, 6);
         const uint8_t* b_s = smem + L.stage + s * L.stage_bytes + L.b;
+        const uint8_t* a_s = kComp ? w_s + (jw & 1) * (uint32_t)(GS * Kp) : w_s;
         const uint32_t acc = tmem + a * acc_stride;
         const int kk0 = kc * (kKChunk / 32);   // K step of the spike operand
         for (int hh = 0; hh < Mh; ++hh)
           for (int kk = 0; kk < ksc / 32; ++kk) {
             const uint32_t accum = (kc > 0 || kk > 0) ? 1u : 0u;
-            const uint64_t ad = tc::smem_desc(ptx::smem_u32(w_s + hh * 2048 + kk * 2 * lbo_a), lbo_a, 128);
-            const uint64_t bd = tc::smem_desc(ptx::smem_u32(b_s + (kk0 + kk) * 2 * lbo_b), lbo_b, 128);
+            const uint64_t ad = tc::smem_desc(ptx::smem_u32(a_s + hh * 2048 + kk * 2 * lbo_a), lbo_a, 128);
+            const uint64_t bd = kPull ? tc::smem_desc(ptx::smem_u32(b_s + (kk0 + kk) * 2048), 512, 128)
+                                      : tc::smem_desc(ptx::smem_u32(b_s + (kk0 + kk) * 2 * lbo_b), lbo_b, 128);
             tc::mma_i8(acc + hh * NT, ad, bd, id_lo, accum);
             if (kWide) {
               const uint64_t ah = tc::smem_desc(ptx::smem_u32(w_s + GS * ksc + hh * 2048 + kk * 2 * lbo_a), lbo_a, 128);
@@ -520,7 +519,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
         // (neuron groups: every sub-item / K chunk has its own operand)
         const bool last_item = k0 + 1 == nwork;
         const int next_cl = last_item ? first_idx / nT : next_cl_of(cl, tile);
-        if (kGrp || (last_item && it + 1 == nticks) || next_cl != cl) tc::commit(&bars[WFREE]);
+        if (kGrp || (last_item && it + 1 == nticks) || next_cl != cl) tc::commit(&bars[(kComp && (jw & 1)) ? WFREE1 : WFREE]);
       }
       __syncwarp();
       }
@@ -536,7 +535,75 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
     // so the lookups never conflict
     uint32_t* lut = reinterpret_cast<uint32_t*>(smem + L.lut);
     for (int b = et; b < 16; b += kExpThreads) lut[b] = tc::nib2bytes((uint32_t)b);
+    if (kPull)   // the per-axon masks start (and stay between items) zero
+      for (int i = et; i < 2 * Kp; i += kExpThreads) reinterpret_cast<uint32_t*>(smem + L.pmask)[i] = 0u;
     named_sync(2, kExpThreads);
+    // kComp: the spike warps expand each core's compact operand (crossbar
+    // bits, type weights, axon types) into Wfold[n][a'] = conn * w[n][type(a')]
+    // in the canonical layout, into operand buffer j & 1 for the
+    // CTA's j-th core, one core ahead of the MMAs; the compact operand of the
+    // core after that is prefetched into registers meanwhile (L2 evict_last:
+    // every core's operand is read again next tick).
+    uint32_t cx[2][8], cw[2] = {0u, 0u}, cts = 0u;
+    const uint64_t pol_keep = kComp ? ptx::policy_evict_last() : 0ull;
+    int ncores = 0, jcore = 0;
+    const int core0 = first_idx / nT, core_dir = rev ? -1 : 1;
+    if (kComp && !p.comp_epi && nwork > 0) ncores = abs((rev ? lo : hi - 1) / nT - core0) + 1;
+    auto comp_load = [&](int j) {   // registers <- the compact operand of the CTA's j-th core
+      if (j >= ncores) return;
+      const int cg = p.c_lo + core0 + core_dir * j;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int nn = et + 128 * h;
+#pragma unroll
+        for (int w = 0; w < 8; ++w)
+          cx[h][w] = (nn < Np && w < W) ? ptx::ldg_hint(p.xbits + ((size_t)cg * W + w) * Np + nn, pol_keep) : 0u;
+        cw[h] = nn < Np ? ptx::ldg_hint(p.wq + (size_t)cg * Np + nn, pol_keep) : 0u;
+      }
+      if (et < (Kp >> 2)) cts = ptx::ldg_hint(p.tsel + (size_t)cg * (Kp >> 2) + et, pol_keep);
+    };
+    auto comp_expand = [&](int j) {   // operand buffer j & 1 <- the j-th core's expanded operand
+      const int b = j & 1;
+      if (j >= 2) wait(&bars[b ? WFREE1 : WFREE], ((j >> 1) - 1) & 1);   // core j - 2's MMAs are done
+      if (et == 0 && j > 0) stamp_k(j - 1, 12);   // (timeline: slots 12 / 13 = expansion start / end)
+      uint32_t* ts = reinterpret_cast<uint32_t*>(smem + L.tsel);
+      if (et < (Kp >> 2)) ts[et] = cts;
+      named_sync(2, kExpThreads);
+      uint4* const abuf = reinterpret_cast<uint4*>(w_s + b * (uint32_t)(Np * Kp));
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int nn = et + 128 * h;
+        if (nn >= Np) break;   // Np = 128 or 256: warp-uniform
+        const uint32_t wv = cw[h];
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+          if (w >= W) break;
+          // chunk kc = 2w + (m >> 2) (16 axons) of row nn sits at (kc * Np + nn) * 16
+          // bytes (tc.h); byte j of word m: axon 32w + 4m + j, its connection bit
+          // is the sign of byte j of (x << m), its weight byte selected by type
+          const uint32_t x = cx[h][w];
+          const uint4 s0 = reinterpret_cast<const uint4*>(ts)[2 * w];
+          const uint4 s1 = reinterpret_cast<const uint4*>(ts)[2 * w + 1];
+          const uint32_t sel[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+          uint32_t o[8];
+#pragma unroll
+          for (int m = 0; m < 8; ++m) o[m] = ptx::prmt(x << m, 0u, 0xBA98u) & ptx::prmt(wv, 0u, sel[m]);
+          abuf[(2 * w) * Np + nn] = make_uint4(o[0], o[1], o[2], o[3]);
+          abuf[(2 * w + 1) * Np + nn] = make_uint4(o[4], o[5], o[6], o[7]);
+        }
+      }
+      ptx::fence_proxy_async_smem();   // generic writes -> the tensor core's (async proxy) reads
+      named_sync(2, kExpThreads);
+      if (et == 0) {
+        ptx::mbar_arrive(&bars[b ? WFULL1 : WFULL]);
+        if (j > 0) stamp_k(j - 1, 13);
+      }
+    };
+    if (kComp && ncores > 0) {
+      comp_load(0);
+      comp_expand(0);
+      comp_load(1);
+    }
     for (int it = 0; it < nticks; ++it) {
     const int64_t t = p.t + it;
     const int cur = (int)(t & p.rp_mask);
@@ -557,25 +624,92 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       // (word-major) = ring word w of sample s0 + sm
       constexpr bool wm = kWm;
       if (kPull) {
-        // a1 (pull scheduler): the spikes due now on axon a' are the OR of its
-        // sources' fired bits of tick t - delay (idempotent OR, G11);
-        // then each 32-axon x 32-sample block is bit-transposed into the
-        // staged ring-word layout raw[w * NT + sample]
-        const uint64_t* gat = reinterpret_cast<const uint64_t*>(st + L.pull);
-        const uint16_t* aoff = reinterpret_cast<const uint16_t*>(st + L.paoff);
-        uint64_t* msk = reinterpret_cast<uint64_t*>(smem + L.pmask);
+        // a1 (history scheduler): the spikes due now on axon a' are the OR of
+        // the words its sources stored for tick t (idempotent OR, P:158,
+        // G11), collected in the per-axon 64-sample masks msk (zero between
+        // items: the B emission below clears what it reads).  The B operand
+        // is MN-major (per axon, 64 contiguous sample bytes), so the masks
+        // become operand bytes without a bit transpose.
+        const uint2* gat = reinterpret_cast<const uint2*>(st + L.pull);
+        const uint16_t* hax = reinterpret_cast<const uint16_t*>(st + L.paoff);
+        uint32_t* msk = reinterpret_cast<uint32_t*>(smem + L.pmask);
+        const int hcnt = (int)*reinterpret_cast<const uint32_t*>(st + L.hcnt);
+        for (int e = et; e < hcnt; e += kExpThreads) {
+          const uint2 v = gat[e];
+          if (v.x | v.y) {
+            const int ap = hax[e];
+            if (v.x) atomicOr(msk + 2 * ap, v.x);
+            if (v.y) atomicOr(msk + 2 * ap + 1, v.y);
+          }
+        }
+        // a2: external inputs as ring words raw[w * NT + sample] (decoded at
+        // load, or gathered from the line runs), bit-transposed into msk
+        const bool inj = t < p.T_in && p.nruns[c] > 0;
+        if (inj) {
+          if (p.inw) {
+            for (int i = et; i < NT * W; i += kExpThreads) raw[i] = lines[i];
+          } else {
+            int2* runs = reinterpret_cast<int2*>(smem + L.runs);
+            int32_t* wr = reinterpret_cast<int32_t*>(smem + L.runs + (uint32_t)p.rmax * 8);
+            if (c != runs_core) {
+              named_sync(2, kExpThreads);
+              for (int i = et; i < p.nruns[c]; i += kExpThreads) runs[i] = p.runs[(size_t)c * p.rmax + i];
+              for (int i = et; i < W; i += kExpThreads) wr[i] = p.word_runs[(size_t)c * W + i];
+              named_sync(2, kExpThreads);
+              runs_core = c;
+            }
+            for (int i = et; i < NT * W; i += kExpThreads) {
+              const int w = i / NT, sm = i % NT;
+              uint32_t acc = 0u;
+              const int32_t fr = wr[w];
+              const uint32_t* lr = lines + sm * WIp;
+              for (int r = fr & 0xFFFF; r < (fr & 0xFFFF) + (fr >> 16); ++r) {
+                const int2 rn = runs[r];
+                const int ap = rn.x & 0xFFFF, len = rn.x >> 16, ln = rn.y;
+                const int lw = ln >> 5, lb = ln & 31;
+                uint32_t x = lr[lw] >> lb;
+                if (lb + len > 32) x |= lr[lw + 1] << (32 - lb);
+                if (len < 32) x &= (1u << len) - 1u;
+                const int off = ap - 32 * w;
+                acc |= off >= 0 ? (x << off) : (x >> (-off));
+              }
+              raw[i] = acc;
+            }
+          }
+          named_sync(2, kExpThreads);
+          for (int b = et >> 5; b < 2 * W; b += kExpWarps) {
+            const int w = b >> 1, hf = b & 1;
+            const uint32_t x = transpose32(raw[w * NT + 32 * hf + lane], lane);
+            if (x) atomicOr(msk + 2 * (32 * w + lane) + hf, x);
+          }
+        }
+        named_sync(2, kExpThreads);
+        if (p.spkin)   // RANC_TRACE_STATE_DIGEST: the axon spikes integrated this tick
+          for (int b = et >> 5; b < 2 * W; b += kExpWarps) {
+            const int w = b >> 1, hf = b & 1, sm = 32 * hf + lane;
+            const uint32_t y = transpose32(msk[2 * (32 * w + lane) + hf], lane);
+            if (sm < ns) p.spkin[((size_t)(s0 + sm) * p.G_loc + cl) * W + w] = y;
+          }
+        wait(&bars[BEMPTY0 + s], (u & 1) ^ 1);
+        if (et == 0) stamp_k(k, 3);
+        // MN-major B: axon a', samples 16g..16g+15 at (a'/8)*512 + g*128 + (a'%8)*16
+        // (tcgen05 MN-major core matrices: LBO = 512 between 8-axon groups,
+        // SBO = 128 between 16-sample groups); samples >= ns get no spikes
+        uint8_t* b_s = st + L.b;
+        const uint64_t keep = ns >= 64 ? ~0ull : ((1ull << ns) - 1ull);
         for (int ap = et; ap < Kp; ap += kExpThreads) {
-          uint64_t m = 0;
-          for (int e = aoff[ap], e1 = aoff[ap + 1]; e < e1; ++e) m |= gat[e];
-          msk[ap] = m;
+          uint2* mp = reinterpret_cast<uint2*>(msk) + ap;
+          const uint2 mv = *mp;
+          *mp = make_uint2(0u, 0u);
+          const uint64_t m = (((uint64_t)mv.y << 32) | mv.x) & keep;
+          uint8_t* bd = b_s + (ap >> 3) * 512 + (ap & 7) * 16;
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            const uint32_t h16 = (uint32_t)(m >> (16 * g));
+            *reinterpret_cast<uint4*>(bd + g * 128) =
+                make_uint4(lut[h16 & 15u], lut[(h16 >> 4) & 15u], lut[(h16 >> 8) & 15u], lut[(h16 >> 12) & 15u]);
+          }
         }
-        named_sync(2, kExpThreads);
-        for (int b = et >> 5; b < 2 * W; b += kExpWarps) {
-          const int w = b >> 1, hf = b & 1;
-          const uint32_t x = (uint32_t)(msk[32 * w + lane] >> (32 * hf));
-          raw[w * NT + 32 * hf + lane] = transpose32(x, lane);
-        }
-        named_sync(2, kExpThreads);
       } else if (p.incoming[c]) {
         // only the words that hold spikes need clearing
         if (!wm) {
@@ -593,7 +727,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
         // no neuron routes here: the ring stays zero and was not loaded
         for (int i = et; i < NT * W; i += kExpThreads) raw[i] = 0u;
       }
-      if (et == 0) stamp_k(k, 12);
+      if (et == 0 && !kComp) stamp_k(k, 12);
+      if (!kPull) {
       // a2: external inputs.  Thread <-> (sample, ring word): OR in the line
       // runs overlapping that word (no atomics: every word has one owner)
       if (t < p.T_in && p.nruns[c] > 0 && p.inw) {
@@ -646,7 +781,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
           const int w = wm ? i / NT : i % W, sm = wm ? i % NT : i / W;
           if (sm < ns) p.spkin[((size_t)(s0 + sm) * p.G_loc + cl) * W + w] = raw[i];
         }
-      if (et == 0) stamp_k(k, 13);
+      if (et == 0 && !kComp) stamp_k(k, 13);
       named_sync(2, kExpThreads);
       if (et == 0) stamp_k(k, 14);
       // bits -> 0/1 bytes, canonical K-major operand (rows = samples);
@@ -696,6 +831,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
           for (int w = 0; w < W; ++w) emit(w, rcol[w * NT]);
         }
       }
+      }   // !kPull
       if (et == 0) stamp_k(k, 15);
       ptx::fence_proxy_async_smem();
       named_sync(2, kExpThreads);
@@ -703,6 +839,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
         stamp_k(k, 4);
         ptx::mbar_arrive(&bars[BFULL0 + s]);
         ptx::mbar_arrive(&bars[SEMPTY0 + s]);   // raw/lines of this stage are consumed
+      }
+      if (kComp && !p.comp_epi && k0 + 1 < nwork && next_cl_of(cl, tile) != cl) {   // the next item starts a new core
+        comp_expand(++jcore);
+        comp_load(jcore + 1);
       }
     }
     tick_barrier();
@@ -765,6 +905,65 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
         ptx::cp_async_commit();
       }
     }
+    // kComp && p.comp_epi: the epilogue warps expand the compact operands
+    // (see the spike stage for the bit layout): the CTA's cores'
+    // type selectors are staged once; core j is expanded into buffer j & 1
+    // as soon as the last accumulator of core j - 2 (whose MMAs read that
+    // buffer) has been taken, from registers prefetched a core earlier (the
+    // epilogue waits for accumulators anyway: the work leaves the spike
+    // warps' per-item chain).  Thread -> (neuron xn, words xq + tpn * i).
+    const bool cepi = kComp && p.comp_epi;
+    const int et512 = threadIdx.x - 32 * kFirstEpi;
+    const int xcore0 = first_idx / nT, xdir = rev ? -1 : 1;
+    const int xnc = cepi && nwork > 0 ? abs((rev ? lo : hi - 1) / nT - xcore0) + 1 : 0;
+    const int tpn = 512 / Np, xn = et512 & (Np - 1), xq = et512 / Np;   // (Np = 128 or 256)
+    uint32_t ex[4] = {0u, 0u, 0u, 0u}, ewq = 0u;
+    int xj = 0;   // the next core to expand
+    const uint64_t xpol = cepi ? ptx::policy_evict_last() : 0ull;
+    auto xload = [&](int j) {   // registers <- the compact operand of the CTA's j-th core
+      if (j >= xnc) return;
+      const int cg = p.c_lo + xcore0 + xdir * j;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int w = xq + tpn * i;
+        ex[i] = w < W ? ptx::ldg_hint(p.xbits + ((size_t)cg * W + w) * Np + xn, xpol) : 0u;
+      }
+      ewq = ptx::ldg_hint(p.wq + (size_t)cg * Np + xn, xpol);
+    };
+    auto xexpand = [&](int j) {   // operand buffer j & 1 <- this thread's part of core j
+      const int b = j & 1;
+      const uint4* ts = reinterpret_cast<const uint4*>(smem + L.tsel + (uint32_t)j * Kp);
+      uint4* const abuf = reinterpret_cast<uint4*>(w_s + b * (uint32_t)(Np * Kp));
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int w = xq + tpn * i;
+        if (w < W) {
+          const uint4 s0 = ts[2 * w], s1 = ts[2 * w + 1];
+          const uint32_t sel[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+          uint32_t o[8];
+#pragma unroll
+          for (int m = 0; m < 8; ++m) o[m] = ptx::prmt(ex[i] << m, 0u, 0xBA98u) & ptx::prmt(ewq, 0u, sel[m]);
+          abuf[(2 * w) * Np + xn] = make_uint4(o[0], o[1], o[2], o[3]);
+          abuf[(2 * w + 1) * Np + xn] = make_uint4(o[4], o[5], o[6], o[7]);
+        }
+      }
+      ptx::fence_proxy_async_smem();   // generic writes -> the tensor core's (async proxy) reads
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&bars[b ? WFULL1 : WFULL]);
+    };
+    if (cepi && xnc > 0) {
+      uint32_t* ts = reinterpret_cast<uint32_t*>(smem + L.tsel);
+      const int kq = Kp >> 2;
+      for (int i = et512; i < xnc * kq; i += 32 * kEpiWarps)
+        ts[i] = __ldg(p.tsel + (size_t)(p.c_lo + xcore0 + xdir * (i / kq)) * kq + i % kq);
+      named_sync(3, 32 * kEpiWarps);
+      xload(0);
+      xexpand(0);
+      xload(1);
+      xexpand(1);
+      xload(2);
+      xj = 2;
+    }
     long long dbg_wait = 0;
     const long long dbg_t0 = dbg_on ? clock64() : 0;
     const int cl0 = cl, tile0 = tile;
@@ -772,11 +971,13 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
     short4 nprm = make_short4(0, 0, 0, 0);
     uint2 nrt = make_uint2(0u, 0u);
     int nini = 0;
+    uint32_t nhp = 0u, hpos = 0u;   // history scheduler: this neuron's position
     if (!kMulti && active && nwork > 0) {
       const size_t nc = (size_t)(p.c_lo + cl0) * Np + n;
       nprm = p.prm[nc];
       nrt = p.route[nc];
       nini = p.init[nc];
+      if (kPull) nhp = p.hpos[nc];
     }
     // this thread's TMEM lane and column offset (the stage adds a * acc_stride)
     const uint32_t tmem_lane_base = tmem + ((uint32_t)(q * 32) << 16) + h * NT + jj * 32;
@@ -818,6 +1019,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       short4 prm = nprm;
       uint2 rt = nrt;
       int ini = nini;
+      const uint32_t hp = nhp;
       if (kMulti && active && key != prev_core) {
         const size_t nc = (size_t)c * Np + n;
         prm = p.prm[nc];
@@ -832,6 +1034,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
           nprm = p.prm[nc];
           nrt = p.route[nc];
           nini = p.init[nc];
+          if (kPull) nhp = p.hpos[nc];
         }
       }
       // one warp per lane quarter polls the accumulator barrier; the other
@@ -839,7 +1042,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       // back-off polling (measured best against the suspend-hint wait, a plain
       // spin and a per-quarter named barrier)
       if (spin) ptx::mbar_wait(&bars[ACCFULL0 + a], ua & 1);
-      else ptx::mbar_wait_backoff(&bars[ACCFULL0 + a], ua & 1, 128);
+      else if (p.epi_wait) ptx::mbar_wait_sleep(&bars[ACCFULL0 + a], ua & 1, p.epi_wait);
+      else ptx::mbar_wait_backoff(&bars[ACCFULL0 + a], ua & 1, p.epi_backoff);
       if (dbg_on && blockIdx.x == 0) dbg_wait += clock64() - tw0;
       if (lane == 0 && ew == 0) stamp_k(k, 8);
       tc::fence_after();
@@ -847,6 +1051,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
         if (key != prev_core) {
           leak = prm.x; pth = prm.y; nth = prm.z; rst = prm.w;
           init = ini;
+          hpos = hp;
           if (p.fresh && first) {
             // first tick after a reset: the pass inputs are the initial
             // potentials; pbuf is not refilled while this core's tiles run
@@ -955,9 +1160,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
         const int lim = ns - jj * 32;
         const uint32_t f = lim >= 32 ? fired : (lim > 0 ? fired & ((1u << lim) - 1u) : 0u);
         if (kPull) {
-          // a5 (pull scheduler): publish this neuron's fired bits of tick t
-          // for the 32 samples of this half; destinations gather them
-          p.hist[(((((size_t)(t & p.rp_mask) * p.G_loc + cl) * nT + tile) * Np + n) << 1) + jj] = valid ? f : 0u;
+          // a5 (history scheduler): store this neuron's fired bits of the 32
+          // samples of this half at its position in the slot of tick t + delay
+          if (route_here) p.hist[((((size_t)((t + rdelay) & p.rp_mask)) * nT + tile) * p.hist_P + hpos) * 2 + jj] = f;
         } else if (block_identity) {
           // every routing lane l of this warp deposits bit l of one ring
           // word: a 32x32 bit transpose turns the per-lane sample masks into
@@ -1061,6 +1266,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       __syncwarp();
       if (lane == 0 && ew == 0) stamp_k(k, 11);
       if (lane == 0) ptx::mbar_arrive(&bars[ACCEMPTY0 + a]);
+      // the last item of core xj - 2: its buffer is free for core xj
+      if (cepi && xj < xnc && (k0 + 1 == nwork || ncl != cl)) {
+        xexpand(xj);
+        xload(++xj);
+      }
       }
       adv(cl, tile);
     }
@@ -1161,7 +1371,14 @@ size_t tc_smem_bytes(const Compiled& n) {
 
 // shared memory of the pull-scheduler launch (word-major, per-tick, no groups)
 size_t tc_smem_bytes_pull(const Compiled& n) {
-  return tc_layout(n.grp_rows, n.Kp, n.W, n.WIp, n.rmax, n.tc_wide, 1, false, false, 0, n.pull_emax).total;
+  return tc_layout(n.grp_rows, n.Kp, n.W, n.WIp, n.rmax, n.tc_wide, 1, false, false, 0, n.hist_emax).total;
+}
+
+// shared memory of the compact-operand launch (two expanded operand buffers;
+// the type selectors of `nc` cores)
+size_t tc_smem_bytes_comp(const Compiled& n, bool pull, int nc) {
+  return tc_layout(n.grp_rows, n.Kp, n.W, n.WIp, n.rmax, false, 1, false, false, 0, pull ? n.hist_emax : -1, true, nc)
+      .total;
 }
 
 namespace {
@@ -1183,10 +1400,14 @@ void tc_fill_params(ranc_ctx* ctx, TickParams& p) {
   p.grp_ns = grp_stages(n);
   p.wmajor = ctx->ring_wmajor ? 1 : 0;
   p.hist = (uint32_t*)ctx->d_hist.p;
-  p.pull_ent = (const uint32_t*)ctx->d_pull_ent.p;
-  p.pull_base = (const uint32_t*)ctx->d_pull_base.p;
-  p.pull_aoff = (const uint16_t*)ctx->d_pull_aoff.p;
-  p.pull_emax = n.pull_emax;
+  p.hpos = (const uint32_t*)ctx->d_hpos.p;
+  p.hbase = (const uint32_t*)ctx->d_hbase.p;
+  p.hax = (const uint16_t*)ctx->d_hax.p;
+  p.hist_emax = n.hist_emax;
+  p.hist_P = (int32_t)n.hbase.back();
+  p.xbits = (const uint32_t*)ctx->d_xbits.p;
+  p.wq = (const uint32_t*)ctx->d_wq.p;
+  p.tsel = (const uint32_t*)ctx->d_tsel.p;
   p.any_route = n.any_route ? 1 : 0;
 }
 
@@ -1243,6 +1464,7 @@ cudaError_t launch_tc_multi(ranc_ctx* ctx, TickParams p, int64_t num_ticks) {
   tc_fill_params(ctx, p);
   const int64_t total = (int64_t)ctx->G_loc * ((ctx->S + NT - 1) / NT);
   p.pot_items = total <= ctx->num_sms ? 1 : 2;
+  ctx->operand_used = 1;
   const int grid = (int)((total + p.pot_items - 1) / p.pot_items);   // contiguous items: mostly the same core
   // bit-sliced output counters when the network has an output bus and they fit
   p.out_planes =
@@ -1269,9 +1491,32 @@ cudaError_t launch_tick_tc(ranc_ctx* ctx, TickParams p) {
   tc_fill_params(ctx, p);
   const int64_t total = (int64_t)ctx->G_loc * ((ctx->S + NT - 1) / NT);
   const int grid = (int)std::min<int64_t>(total, ctx->num_sms);
-  const size_t smem = ctx->ring_pull ? tc_smem_bytes_pull(n) : tc_smem_bytes(n);
+  // compact operand: requested, or automatic with at most two sample tiles
+  // per core (the folded operand would be re-read for every 64 samples)
+  const int64_t nT = (ctx->S + NT - 1) / NT;
+  // (automatic: with the history scheduler, whose spike stage leaves the
+  // spike warps room for the expansion; measured on config 5)
+  // the expansion runs in the epilogue warps when the type selectors of a
+  // CTA's cores fit the shared memory (else in the spike warps);
+  // RANC_DEBUG_COMP_SPIKE=1 forces the spike warps (timing comparisons)
+  static const bool comp_spike = getenv("RANC_DEBUG_COMP_SPIKE") != nullptr;
+  const int comp_nc = (int)((total + grid - 1) / grid / nT) + 2;   // cores of one CTA, at most
+  p.comp_epi = !comp_spike && tc_smem_bytes_comp(n, ctx->ring_pull, comp_nc) <= 227 * 1024 &&
+               (n.Npad == 128 || n.Npad == 256);
+  p.comp_nc = p.comp_epi ? comp_nc : 1;
+  const bool comp = n.tc_comp_ok && (ctx->operand == 2 || (ctx->operand == 0 && nT <= 2 && ctx->ring_pull)) &&
+                    tc_smem_bytes_comp(n, ctx->ring_pull, p.comp_nc) <= 227 * 1024;
+  ctx->operand_used = comp ? 2 : 1;
+  const size_t smem = comp ? tc_smem_bytes_comp(n, ctx->ring_pull, p.comp_nc)
+                           : ctx->ring_pull ? tc_smem_bytes_pull(n) : tc_smem_bytes(n);
   static const bool no_serp = getenv("RANC_DEBUG_NO_SERP") != nullptr;   // (timing comparisons)
   p.serp = no_serp ? 0 : 1;
+  // epilogue accumulator wait (timing experiments): RANC_DEBUG_EPI_WAIT = suspend-hint ns
+  // (0: polling with back-off), RANC_DEBUG_EPI_BACKOFF = back-off ns
+  static const char* ew = getenv("RANC_DEBUG_EPI_WAIT");
+  static const char* eb = getenv("RANC_DEBUG_EPI_BACKOFF");
+  p.epi_wait = ew ? (uint32_t)atoi(ew) : 0u;
+  p.epi_backoff = eb ? (uint32_t)atoi(eb) : 128u;
   static std::atomic<uint64_t> configured{0};
   if (first_use_on_device(configured)) {
     const void* fns[] = {(const void*)tick_tc_kernel<false, false, false, false>,
@@ -1286,16 +1531,24 @@ cudaError_t launch_tick_tc(ranc_ctx* ctx, TickParams p) {
                          (const void*)tick_tc_kernel<false, false, true, true, true>,
                          (const void*)tick_tc_kernel<false, false, true, true, false, true>,
                          (const void*)tick_tc_kernel<false, true, true, false, false, true>,
-                         (const void*)tick_tc_kernel<false, false, true, false, false, true>};
+                         (const void*)tick_tc_kernel<false, false, true, false, false, true>,
+                         (const void*)tick_tc_kernel<false, false, false, false, false, false, true>,
+                         (const void*)tick_tc_kernel<false, false, true, false, false, false, true>,
+                         (const void*)tick_tc_kernel<false, false, true, false, false, true, true>,
+                         (const void*)tick_tc_kernel<false, true, true, false, false, true, true>};
     for (const void* f : fns) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   }
   static const bool dbg_env = getenv("RANC_DEBUG_TIMELINE") != nullptr;
-  const bool dbg = dbg_env && !n.tc_wide && !n.tc_grp;
+  const bool dbg = dbg_env && !n.tc_wide && !n.tc_grp && (!comp || ctx->ring_pull);
   if (dbg && !ctx->d_dbg.p) dev_alloc(ctx, &ctx->d_dbg, kDbg * 8);
   p.dbg = dbg ? (unsigned long long*)ctx->d_dbg.p : nullptr;
   if (dbg) cudaMemsetAsync(ctx->d_dbg.p, 0, kDbg * 8, ctx->stream);
   const bool pull = ctx->ring_pull;
-  const void* fn = pull ? (n.tc_wide ? (const void*)tick_tc_kernel<false, false, true, true, false, true>
+  const void* fn = comp ? (pull ? (dbg ? (const void*)tick_tc_kernel<false, true, true, false, false, true, true>
+                                       : (const void*)tick_tc_kernel<false, false, true, false, false, true, true>)
+                                : p.wmajor ? (const void*)tick_tc_kernel<false, false, true, false, false, false, true>
+                                           : (const void*)tick_tc_kernel<false, false, false, false, false, false, true>)
+                   : pull ? (n.tc_wide ? (const void*)tick_tc_kernel<false, false, true, true, false, true>
                                      : dbg ? (const void*)tick_tc_kernel<false, true, true, false, false, true>
                                            : (const void*)tick_tc_kernel<false, false, true, false, false, true>)
                    : n.tc_grp ? (n.tc_wide ? (p.wmajor ? (const void*)tick_tc_kernel<false, false, true, true, true>

@@ -95,7 +95,7 @@ class Simulator:
     def info(self) -> dict:
         i = L.Info()
         self._ck(self.lib.ranc_get_info(self.h, C.byref(i)))
-        return {f: getattr(i, f) for f, _ in L.Info._fields_ if f != "reserved"}
+        return {f: getattr(i, f) for f, _ in L.Info._fields_}
 
     # -- the four calls of the north star -------------------------------------
     def load_inputs(self, inputs):

@@ -62,15 +62,19 @@ def test_config3_one_sample_per_tile_every_tick(ranc):
     assert cnt.sum() > 0
 
 
+@pytest.mark.parametrize("ring", [0, 2])
 @pytest.mark.parametrize("variant", ["local", "global"])
-def test_config5_full_mesh_every_tick(ranc, variant):
+def test_config5_full_mesh_every_tick(ranc, variant, ring):
     """Config 5 as benchmarked: the 64x64 mesh (4096 cores, D = 15), S = 64,
-    word-major rings and per-tick launches; 100 ticks, samples 0 and 63 (the
-    first and last lane of the 64-sample tile) replayed by the oracle."""
+    per-tick launches -- the automatic layout (history scheduler, compact
+    operand expanded on chip) and the word-major ring (folded operand); 100
+    ticks, samples 0 and 63 (the first and last lane of the 64-sample tile)
+    replayed by the oracle."""
     T = 100
     net, inp = config5(S=64, T=T, variant=variant)
-    d, cnt, pot, info = gpu_digests(ranc, net, inp, T)
-    assert info["kernel"] == 2 and info["ring_layout"] == 2
+    d, cnt, pot, info = gpu_digests(ranc, net, inp, T, ring=ring)
+    assert info["kernel"] == 2
+    assert (info["ring_layout"], info["operand"]) == ((3, 2) if ring == 0 else (2, 1))
     idx = np.array([0, 63])
     (ref_d, ref_c, ref_p), = oracle_digests([(net, inp, idx, T)])
     check_digests(f"config5-{variant}", d, ref_d, idx)

@@ -21,10 +21,14 @@ def ranc():
 # "tc": tensor-core kernel, sample-major scheduler rings; "tc_wm": word-major
 # rings (RANC_OPT_RING_LAYOUT = 2); "tc_gather": word-major rings and the
 # per-tick input-run gather instead of the load-time input decode
-# (RANC_OPT_INPUT_DECODE = 0); "tc_pull": the pull scheduler (layout 3: fired-
-# bit history gathered by the destinations)
-KERNELS = {"popc": 1, "tc": 2, "tc_wm": 2, "tc_gather": 2, "tc_pull": 2}
-RING = {"tc": 1, "tc_wm": 2, "tc_gather": 2, "tc_pull": 3}
+# (RANC_OPT_INPUT_DECODE = 0); "tc_pull": the history scheduler (layout 3:
+# destination-ordered fired-bit history).  Operand: "tc" forces the folded
+# Wfold (RANC_OPT_OPERAND = 1), "tc_comp" the compact operand expanded on
+# chip (2); the others take the automatic choice (compact for the few-tile
+# batches of these tests when the network is eligible).
+KERNELS = {"popc": 1, "tc": 2, "tc_wm": 2, "tc_gather": 2, "tc_pull": 2, "tc_comp": 2, "tc_pull_gather": 2}
+RING = {"tc": 1, "tc_wm": 2, "tc_gather": 2, "tc_pull": 3, "tc_comp": 1, "tc_pull_gather": 3}
+OPERAND = {"tc": 1, "tc_comp": 2}
 
 
 def make_sim(ranc, net, kernel, **kw):
@@ -32,8 +36,9 @@ def make_sim(ranc, net, kernel, **kw):
     if kernel in RING:
         try:
             sim.set_option(ranc.OPT_KERNEL, KERNELS[kernel])
-            sim.set_option(ranc.OPT_INPUT_DECODE, 0 if kernel == "tc_gather" else 1)
+            sim.set_option(ranc.OPT_INPUT_DECODE, 0 if kernel in ("tc_gather", "tc_pull_gather") else 1)
             sim.set_option(ranc.OPT_RING_LAYOUT, RING[kernel])
+            sim.set_option(ranc.OPT_OPERAND, OPERAND.get(kernel, 0))
         except ranc.RancError as e:
             sim.close()
             assert e.code == "RANC_E_CONFIG"
@@ -43,7 +48,7 @@ def make_sim(ranc, net, kernel, **kw):
     return sim
 
 
-@pytest.fixture(params=["popc", "tc", "tc_wm", "tc_gather", "tc_pull"])
+@pytest.fixture(params=["popc", "tc", "tc_wm", "tc_gather", "tc_pull", "tc_comp"])
 def kernel(request):
     return request.param
 
@@ -62,6 +67,8 @@ def per_tick(ranc, oracle_mod, net, inp, T, tile=None, kernel=None):
     for t in range(T):
         sim.run(1)
         o.run(1)
+        if t == 0 and kernel in OPERAND:
+            assert sim.info()["operand"] == OPERAND[kernel]
         where = f"{net.name} tick {t}"
         assert np.array_equal(sim.potentials(), o.potentials()), where + " potentials"
         assert np.array_equal(sim.raster()[0], o.fired()), where + " fired"
@@ -104,6 +111,19 @@ def test_tiny_every_tick(ranc, oracle_mod, seed, kernel):
 def test_corpus_every_tick(ranc, oracle_mod, seed, kernel):
     net, inp = corpus_case(seed)
     per_tick(ranc, oracle_mod, net, inp, 12, kernel=kernel)
+
+
+@pytest.mark.parametrize("seed", range(0, 40, 3))
+def test_history_scheduler_gathered_inputs(ranc, oracle_mod, seed):
+    """The history scheduler with per-tick input gathering (no load-time
+    decode): input words transposed into the per-axon masks (a2)."""
+    net, inp = corpus_case(seed)
+    per_tick(ranc, oracle_mod, net, inp, 12, kernel="tc_pull_gather")
+
+
+def test_history_scheduler_gathered_inputs_config2(ranc, oracle_mod):
+    net, inp = config2(S=130)
+    final_state(ranc, oracle_mod, net, inp, 17, kernel="tc_pull_gather")
 
 
 @pytest.mark.parametrize("tile", [1, 3, 64])
@@ -263,7 +283,18 @@ def test_ring_layout_switch_at_reset(ranc, oracle_mod):
     sim = ranc.Simulator(net5)
     sim.set_option(ranc.OPT_KERNEL, 2)
     sim.load_inputs(inp5)
-    assert sim.info()["ring_layout"] == 2
+    assert sim.info()["ring_layout"] == 2   # 64 items: the multi-tick launch keeps the ring
+    sim.close()
+    # more than two 64-sample tiles per SM: the history scheduler, and the
+    # compact operand on its per-tick launches
+    net5, inp5 = config5(S=64, T=4, grid=20)
+    sim = ranc.Simulator(net5)
+    sim.set_option(ranc.OPT_KERNEL, 2)
+    sim.load_inputs(inp5).run(2)
+    assert (sim.info()["ring_layout"], sim.info()["operand"]) == (3, 2)
+    o = oracle_mod.Oracle(net5, inp5).run(2)
+    assert np.array_equal(sim.potentials(), o.potentials())
+    assert np.array_equal(sim.pending(), o.pending())
     sim.close()
 
 

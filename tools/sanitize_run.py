@@ -8,9 +8,10 @@ that the sanitizer lets through is also a parity run.  Variants: popc (per-tick
 popcount launches), popc_stream (cooperative one-launch streaming kernel),
 tc (per-tick tcgen05 kernel, sample-major rings), tc_wm (word-major rings),
 tc_multi (cooperative multi-tick tcgen05 launch, neighbourhood barrier),
-tc_wide (16-bit weights: u8/s8 split), tc_pull (pull scheduler), tc_grp
-(neuron groups), loopback (core-sharded group of 2 with the exchange
-kernels), digest.
+tc_wide (16-bit weights: u8/s8 split), tc_pull (history scheduler with the
+compact operand), tc_pull_fold (history scheduler, folded operand), tc_comp
+(compact operand, sample-major rings, input injection), tc_grp (neuron
+groups), loopback (core-sharded group of 2 with the exchange kernels), digest.
 """
 from __future__ import annotations
 
@@ -36,20 +37,21 @@ def main(argv):
         print(f"ok {what}: kernel={sim.info()['kernel']} ring={sim.info()['ring_layout']} "
               f"launches={sim.info()['kernel_launches']}", flush=True)
 
-    def run(net, inp, T, kernel, stream, ring=0, what="", trace=0):
+    def run(net, inp, T, kernel, stream, ring=0, what="", trace=0, operand=0):
         sim = r.Simulator(net)
         sim.set_option(r.OPT_KERNEL, kernel)
         sim.set_option(r.OPT_STREAM, stream)
         if kernel == 2:
             sim.set_option(r.OPT_RING_LAYOUT, ring)
+            sim.set_option(r.OPT_OPERAND, operand)
         if trace:
             sim.set_trace(trace)
         sim.load_inputs(inp).run(T)
         check(sim, net, inp, T, what)
         sim.close()
 
-    variants = argv or ["popc", "popc_stream", "tc", "tc_wm", "tc_multi", "tc_wide", "tc_pull", "tc_grp",
-                        "loopback", "digest"]
+    variants = argv or ["popc", "popc_stream", "tc", "tc_wm", "tc_multi", "tc_wide", "tc_pull", "tc_pull_fold",
+                        "tc_comp", "tc_grp", "loopback", "digest"]
     net2, inp2 = config2(S=70)
     T2 = net2.meta["T"]
     mesh, mesh_in = config5(S=3, T=6, grid=6)
@@ -73,7 +75,11 @@ def main(argv):
                 setattr(w, f, getattr(w, f) + 7)
             run(w, mesh_in, 6, 2, 1, ring=2, what=v)
         elif v == "tc_pull":
-            run(mesh, mesh_in, 6, 2, 1, ring=3, what=v)
+            run(mesh, mesh_in, 6, 2, 1, ring=3, what=v, operand=2)
+        elif v == "tc_pull_fold":
+            run(mesh, mesh_in, 6, 2, 1, ring=3, what=v, operand=1)
+        elif v == "tc_comp":
+            run(net2, inp2, 6, 2, 1, ring=1, what=v, operand=2)
         elif v == "tc_grp":
             from workloads.gen import bigcore
             for A, N in ((512, 1024), (256, 512)):

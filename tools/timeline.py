@@ -1,6 +1,6 @@
 """Print the TC kernel's per-tile pipeline timeline of CTA 0 (debug aid).
 
-  python tools/timeline.py [config3|config5|config5g] [S] [ticks] [ring layout 0-3]
+  python tools/timeline.py [config3|config5|config5g] [S] [ticks] [ring layout 0-3] [operand 0-2]
 """
 import os
 import sys
@@ -20,5 +20,7 @@ sim = Simulator(net)
 sim.set_option(3, 2)
 if len(sys.argv) > 4:
     sim.set_option(5, int(sys.argv[4]))
+if len(sys.argv) > 5:
+    sim.set_option(7, int(sys.argv[5]))   # RANC_OPT_OPERAND
 sim.load_inputs(inp)
 sim.run(int(sys.argv[3]) if len(sys.argv) > 3 else 3)
