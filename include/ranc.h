@@ -211,11 +211,11 @@ ranc_status ranc_set_allocator(ranc_ctx* ctx, void* (*alloc)(size_t, void*),
 #define RANC_OPT_KERNEL 3
 /* RANC_OPT_RING_LAYOUT (tensor-core kernel only; device memory layout of the
  * scheduler rings, Alg. 1 l.3-5 and l.15-20, P:79-82 / P:102-110): 0 (default)
- * automatic -- when more than 2/3 of all neurons route to their own
- * destination word (e.g. the random mesh of config 5): the history scheduler
- * (3) if a tick has more than two 64-sample tiles per SM (per-tick
- * launches), else word-major; otherwise sample-major (layered MNIST nets
- * deposit whole words together); 1 sample-major
+ * automatic -- the history scheduler (3) when more than 1/3 of all neurons
+ * route to their own destination word (the random mesh of config 5, VMM)
+ * and a tick has more than two 64-sample tiles per SM (per-tick launches);
+ * else word-major when more than 2/3 do; otherwise sample-major (layered
+ * MNIST nets deposit whole words together); 1 sample-major
  * [Rp][G][S][W]; 2 word-major [Rp][G][W][S] (a warp's deposits for 32 samples
  * of one route hit one 128-byte line); 3 history scheduler: no ring -- every
  * routing neuron owns a position in its destination core's list and each

@@ -355,14 +355,15 @@ ranc_status ranc_reset_state(ranc_ctx* ctx) {
                         tc_smem_bytes(ctx->net) > 227 * 1024)
                            ? RANC_KERNEL_POPC
                            : RANC_KERNEL_TC;
-  // the history scheduler (layout 3) replaces the word-major ring on request,
-  // and automatically for networks of per-neuron routes whose ticks run as
+  // the history scheduler (layout 3) replaces the ring on request, and
+  // automatically for networks with many per-neuron routes whose ticks run as
   // per-tick launches anyway (more than two 64-sample tiles per SM: no
-  // cooperative multi-tick launch), e.g. config 5: 126 -> 97 us per tick
+  // cooperative multi-tick launch), e.g. config 5 (126 -> 97 us per tick)
+  // and VMM-1024
   const int64_t tc_items = (int64_t)ctx->G_loc * ((ctx->S + tc_tile() - 1) / tc_tile());
   const bool pull = ctx->kernel_active == RANC_KERNEL_TC && pull_eligible(ctx) &&
                     (ctx->ring_layout == 3 ||
-                     (ctx->ring_layout == 0 && ctx->net.tc_wmajor && tc_items > 2 * (int64_t)ctx->num_sms));
+                     (ctx->ring_layout == 0 && ctx->net.tc_hist && tc_items > 2 * (int64_t)ctx->num_sms));
   const bool wmajor = ctx->kernel_active == RANC_KERNEL_TC &&
                       (pull || ctx->ring_layout == 2 || (ctx->ring_layout == 0 && ctx->net.tc_wmajor));
   if (wmajor != ctx->ring_wmajor) ctx->inw_valid = false;   // decoded inputs follow the ring layout

@@ -393,6 +393,9 @@ ranc_status validate_and_compile(const ranc_network_desc* d, Compiled* out, std:
           if (route_kind(o.route_tc[(size_t)c * Np + n].x) == RK_ROUTE && !o.wflags_tc[(size_t)c * (Np / 32) + n / 32])
             ++scattered;
       o.tc_wmajor = 3 * scattered > 2 * (int64_t)G * N;
+      // the history scheduler pays off from a third of scattered routers on
+      // (VMM-1024: 743 -> 711 ms per step, config 5: 126 -> 97 us per tick)
+      o.tc_hist = 3 * scattered > (int64_t)G * N;
     }
     // History scheduler (RANC_OPT_RING_LAYOUT 3): every routing neuron owns
     // one POSITION in a destination-ordered list; each tick it stores its

@@ -70,7 +70,6 @@ struct TickParams {
   int32_t grp_rows;         // tensor-core path: rows per neuron group (Compiled::grp_rows)
   int32_t grp_ns;           // neuron-group launch: spike stages (2, or 1 beyond 512 axons)
   int32_t serp;             // tensor-core per-tick launches: odd ticks walk each CTA's items backwards
-  uint32_t epi_wait, epi_backoff;   // tensor-core per-tick launches: epilogue accumulator wait (suspend hint / back-off ns)
   int32_t fault;            // RANC_OPT_DEBUG_FAULT (mutation tests): 1 = skip the grid barrier of
                             // cooperative multi-tick launches
   int64_t t;                // tick being executed
@@ -116,8 +115,6 @@ struct TickParams {
   const uint32_t* xbits;
   const uint32_t* wq;
   const uint32_t* tsel;
-  int32_t comp_epi;         // compact operand expanded by the epilogue warps (else the spike warps)
-  int32_t comp_nc;          // type-selector slots in shared memory (cores of one CTA, at most)
 };
 
 // Host copy of the compiled network.
@@ -132,6 +129,8 @@ struct Compiled {
   bool any_route = false;       // some neuron has dest_kind ROUTE
   bool any_output = false;      // some neuron has dest_kind OUTPUT
   bool tc_wide = false;         // some weight outside [-128,127]: Wfold split w = 256*hi + lo, [G][2][Npad*Kp] (u8 lo, s8 hi)
+  bool tc_hist = false;         // automatic ring layout: the history scheduler when a third of all neurons
+                                // are such routers (and a tick runs as per-tick launches)
   bool tc_wmajor = false;       // automatic ring layout: word-major when most routing neurons sit in
                                 // warps without a shared destination word (per-neuron routes)
   std::vector<int8_t> wfold;    // [G][Npad*Kp] canonical operand layout, tensor-core axon order
@@ -283,7 +282,7 @@ int pieces_template(int E);
 int tc_tile();
 size_t tc_smem_bytes(const Compiled& n);
 size_t tc_smem_bytes_pull(const Compiled& n);
-size_t tc_smem_bytes_comp(const Compiled& n, bool pull, int nc = 1);
+size_t tc_smem_bytes_comp(const Compiled& n, bool pull);
 cudaError_t launch_tick_tc(ranc_ctx* ctx, TickParams p);
 cudaError_t decode_inputs_tc(ranc_ctx* ctx);
 bool stream_eligible(ranc_ctx* ctx, int64_t num_ticks);

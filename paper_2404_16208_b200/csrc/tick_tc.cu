@@ -102,7 +102,7 @@ constexpr int kCntPlanes = 8;   // counts < 256 between flushes
 // neuron-group launch, grp)
 __host__ __device__ inline TcLayout tc_layout(int wrows, int Kp, int W, int WIp, int rmax, bool wide, int pot_items = 1,
                                               bool cnt_planes = false, bool multi = false, int grp = 0,
-                                              int pull_emax = -1, bool comp = false, int comp_nc = 1) {
+                                              int pull_emax = -1, bool comp = false) {
   // grp: spike stages of a neuron-group launch (0: not grouped); its operand
   // buffer holds one K chunk of at most kKChunk axons
   TcLayout L;
@@ -113,8 +113,8 @@ __host__ __device__ inline TcLayout tc_layout(int wrows, int Kp, int W, int WIp,
   o = (o + 15) & ~15u;
   L.lut = o;                                  // u32 [16]: nibble -> four 0/1 bytes
   o += 256 * 8;
-  L.tsel = o;                                 // compact operand: u32 [comp_nc][Kp/4] prmt type selectors
-  if (comp) o += (uint32_t)Kp * (uint32_t)comp_nc;
+  L.tsel = o;                                 // compact operand: u32 [Kp/4] the core's prmt type selectors
+  if (comp) o += (uint32_t)Kp;
   o = (o + 127) & ~127u;
   L.potbuf = o;                               // uint4 [NT/8][epilogue threads]: next tile's potentials
   o += (NT / 8) * (32 * 8) * 16 * (uint32_t)pot_items;   // = 4 chunks x 512 epilogue threads per item
@@ -270,7 +270,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
   const int GS = kGrp ? p.grp_rows : Np;
   const int nGrp = kGrp ? Np / GS : 1;
   const TcLayout L = tc_layout(GS, Kp, W, WIp, p.rmax, kWide, kMulti ? p.pot_items : 1, kMulti && p.out_planes,
-                               kMulti, kGrp ? p.grp_ns : 0, kPull ? p.hist_emax : -1, kComp, kComp ? p.comp_nc : 1);
+                               kMulti, kGrp ? p.grp_ns : 0, kPull ? p.hist_emax : -1, kComp);
   constexpr int NS = kGrp ? NS_GRP : kWide ? NS_WIDE : kMulti ? NS_MULTI : kComp ? NS_COMP : ranc::NS;   // spike stages (at most)
   const int nsr = kGrp ? p.grp_ns : NS;   // spike stages in use
   const int nK = kGrp ? (Kp + kKChunk - 1) / kKChunk : 1;   // K chunks of a group's operand
@@ -337,9 +337,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       ptx::mbar_init(&bars[ACCEMPTY0 + i], kEpiWarps);
     }
     // (compact operand expanded by the epilogue: one arrival per epilogue warp)
-    ptx::mbar_init(&bars[WFULL], kComp && p.comp_epi ? kEpiWarps : 1);
+    ptx::mbar_init(&bars[WFULL], 1);
     ptx::mbar_init(&bars[WFREE], 1);
-    ptx::mbar_init(&bars[WFULL1], kComp && p.comp_epi ? kEpiWarps : 1);
+    ptx::mbar_init(&bars[WFULL1], 1);
     ptx::mbar_init(&bars[WFREE1], 1);
     ptx::fence_mbar_init();
   }
@@ -548,7 +548,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
     const uint64_t pol_keep = kComp ? ptx::policy_evict_last() : 0ull;
     int ncores = 0, jcore = 0;
     const int core0 = first_idx / nT, core_dir = rev ? -1 : 1;
-    if (kComp && !p.comp_epi && nwork > 0) ncores = abs((rev ? lo : hi - 1) / nT - core0) + 1;
+    if (kComp && nwork > 0) ncores = abs((rev ? lo : hi - 1) / nT - core0) + 1;
     auto comp_load = [&](int j) {   // registers <- the compact operand of the CTA's j-th core
       if (j >= ncores) return;
       const int cg = p.c_lo + core0 + core_dir * j;
@@ -840,7 +840,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
         ptx::mbar_arrive(&bars[BFULL0 + s]);
         ptx::mbar_arrive(&bars[SEMPTY0 + s]);   // raw/lines of this stage are consumed
       }
-      if (kComp && !p.comp_epi && k0 + 1 < nwork && next_cl_of(cl, tile) != cl) {   // the next item starts a new core
+      if (kComp && k0 + 1 < nwork && next_cl_of(cl, tile) != cl) {   // the next item starts a new core
         comp_expand(++jcore);
         comp_load(jcore + 1);
       }
@@ -904,65 +904,6 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
           ptx::cp_async16(pbuf + (kCh * sb + i) * PB, dst + (size_t)(kCh * sb + i) * Np);
         ptx::cp_async_commit();
       }
-    }
-    // kComp && p.comp_epi: the epilogue warps expand the compact operands
-    // (see the spike stage for the bit layout): the CTA's cores'
-    // type selectors are staged once; core j is expanded into buffer j & 1
-    // as soon as the last accumulator of core j - 2 (whose MMAs read that
-    // buffer) has been taken, from registers prefetched a core earlier (the
-    // epilogue waits for accumulators anyway: the work leaves the spike
-    // warps' per-item chain).  Thread -> (neuron xn, words xq + tpn * i).
-    const bool cepi = kComp && p.comp_epi;
-    const int et512 = threadIdx.x - 32 * kFirstEpi;
-    const int xcore0 = first_idx / nT, xdir = rev ? -1 : 1;
-    const int xnc = cepi && nwork > 0 ? abs((rev ? lo : hi - 1) / nT - xcore0) + 1 : 0;
-    const int tpn = 512 / Np, xn = et512 & (Np - 1), xq = et512 / Np;   // (Np = 128 or 256)
-    uint32_t ex[4] = {0u, 0u, 0u, 0u}, ewq = 0u;
-    int xj = 0;   // the next core to expand
-    const uint64_t xpol = cepi ? ptx::policy_evict_last() : 0ull;
-    auto xload = [&](int j) {   // registers <- the compact operand of the CTA's j-th core
-      if (j >= xnc) return;
-      const int cg = p.c_lo + xcore0 + xdir * j;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int w = xq + tpn * i;
-        ex[i] = w < W ? ptx::ldg_hint(p.xbits + ((size_t)cg * W + w) * Np + xn, xpol) : 0u;
-      }
-      ewq = ptx::ldg_hint(p.wq + (size_t)cg * Np + xn, xpol);
-    };
-    auto xexpand = [&](int j) {   // operand buffer j & 1 <- this thread's part of core j
-      const int b = j & 1;
-      const uint4* ts = reinterpret_cast<const uint4*>(smem + L.tsel + (uint32_t)j * Kp);
-      uint4* const abuf = reinterpret_cast<uint4*>(w_s + b * (uint32_t)(Np * Kp));
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int w = xq + tpn * i;
-        if (w < W) {
-          const uint4 s0 = ts[2 * w], s1 = ts[2 * w + 1];
-          const uint32_t sel[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
-          uint32_t o[8];
-#pragma unroll
-          for (int m = 0; m < 8; ++m) o[m] = ptx::prmt(ex[i] << m, 0u, 0xBA98u) & ptx::prmt(ewq, 0u, sel[m]);
-          abuf[(2 * w) * Np + xn] = make_uint4(o[0], o[1], o[2], o[3]);
-          abuf[(2 * w + 1) * Np + xn] = make_uint4(o[4], o[5], o[6], o[7]);
-        }
-      }
-      ptx::fence_proxy_async_smem();   // generic writes -> the tensor core's (async proxy) reads
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&bars[b ? WFULL1 : WFULL]);
-    };
-    if (cepi && xnc > 0) {
-      uint32_t* ts = reinterpret_cast<uint32_t*>(smem + L.tsel);
-      const int kq = Kp >> 2;
-      for (int i = et512; i < xnc * kq; i += 32 * kEpiWarps)
-        ts[i] = __ldg(p.tsel + (size_t)(p.c_lo + xcore0 + xdir * (i / kq)) * kq + i % kq);
-      named_sync(3, 32 * kEpiWarps);
-      xload(0);
-      xexpand(0);
-      xload(1);
-      xexpand(1);
-      xload(2);
-      xj = 2;
     }
     long long dbg_wait = 0;
     const long long dbg_t0 = dbg_on ? clock64() : 0;
@@ -1042,8 +983,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       // back-off polling (measured best against the suspend-hint wait, a plain
       // spin and a per-quarter named barrier)
       if (spin) ptx::mbar_wait(&bars[ACCFULL0 + a], ua & 1);
-      else if (p.epi_wait) ptx::mbar_wait_sleep(&bars[ACCFULL0 + a], ua & 1, p.epi_wait);
-      else ptx::mbar_wait_backoff(&bars[ACCFULL0 + a], ua & 1, p.epi_backoff);
+      else ptx::mbar_wait_backoff(&bars[ACCFULL0 + a], ua & 1, 128);
       if (dbg_on && blockIdx.x == 0) dbg_wait += clock64() - tw0;
       if (lane == 0 && ew == 0) stamp_k(k, 8);
       tc::fence_after();
@@ -1266,11 +1206,6 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       __syncwarp();
       if (lane == 0 && ew == 0) stamp_k(k, 11);
       if (lane == 0) ptx::mbar_arrive(&bars[ACCEMPTY0 + a]);
-      // the last item of core xj - 2: its buffer is free for core xj
-      if (cepi && xj < xnc && (k0 + 1 == nwork || ncl != cl)) {
-        xexpand(xj);
-        xload(++xj);
-      }
       }
       adv(cl, tile);
     }
@@ -1374,10 +1309,9 @@ size_t tc_smem_bytes_pull(const Compiled& n) {
   return tc_layout(n.grp_rows, n.Kp, n.W, n.WIp, n.rmax, n.tc_wide, 1, false, false, 0, n.hist_emax).total;
 }
 
-// shared memory of the compact-operand launch (two expanded operand buffers;
-// the type selectors of `nc` cores)
-size_t tc_smem_bytes_comp(const Compiled& n, bool pull, int nc) {
-  return tc_layout(n.grp_rows, n.Kp, n.W, n.WIp, n.rmax, false, 1, false, false, 0, pull ? n.hist_emax : -1, true, nc)
+// shared memory of the compact-operand launch (two expanded operand buffers)
+size_t tc_smem_bytes_comp(const Compiled& n, bool pull) {
+  return tc_layout(n.grp_rows, n.Kp, n.W, n.WIp, n.rmax, false, 1, false, false, 0, pull ? n.hist_emax : -1, true)
       .total;
 }
 
@@ -1499,24 +1433,13 @@ cudaError_t launch_tick_tc(ranc_ctx* ctx, TickParams p) {
   // the expansion runs in the epilogue warps when the type selectors of a
   // CTA's cores fit the shared memory (else in the spike warps);
   // RANC_DEBUG_COMP_SPIKE=1 forces the spike warps (timing comparisons)
-  static const bool comp_spike = getenv("RANC_DEBUG_COMP_SPIKE") != nullptr;
-  const int comp_nc = (int)((total + grid - 1) / grid / nT) + 2;   // cores of one CTA, at most
-  p.comp_epi = !comp_spike && tc_smem_bytes_comp(n, ctx->ring_pull, comp_nc) <= 227 * 1024 &&
-               (n.Npad == 128 || n.Npad == 256);
-  p.comp_nc = p.comp_epi ? comp_nc : 1;
   const bool comp = n.tc_comp_ok && (ctx->operand == 2 || (ctx->operand == 0 && nT <= 2 && ctx->ring_pull)) &&
-                    tc_smem_bytes_comp(n, ctx->ring_pull, p.comp_nc) <= 227 * 1024;
+                    tc_smem_bytes_comp(n, ctx->ring_pull) <= 227 * 1024;
   ctx->operand_used = comp ? 2 : 1;
-  const size_t smem = comp ? tc_smem_bytes_comp(n, ctx->ring_pull, p.comp_nc)
+  const size_t smem = comp ? tc_smem_bytes_comp(n, ctx->ring_pull)
                            : ctx->ring_pull ? tc_smem_bytes_pull(n) : tc_smem_bytes(n);
   static const bool no_serp = getenv("RANC_DEBUG_NO_SERP") != nullptr;   // (timing comparisons)
   p.serp = no_serp ? 0 : 1;
-  // epilogue accumulator wait (timing experiments): RANC_DEBUG_EPI_WAIT = suspend-hint ns
-  // (0: polling with back-off), RANC_DEBUG_EPI_BACKOFF = back-off ns
-  static const char* ew = getenv("RANC_DEBUG_EPI_WAIT");
-  static const char* eb = getenv("RANC_DEBUG_EPI_BACKOFF");
-  p.epi_wait = ew ? (uint32_t)atoi(ew) : 0u;
-  p.epi_backoff = eb ? (uint32_t)atoi(eb) : 128u;
   static std::atomic<uint64_t> configured{0};
   if (first_use_on_device(configured)) {
     const void* fns[] = {(const void*)tick_tc_kernel<false, false, false, false>,

@@ -82,15 +82,19 @@ def test_config5_full_mesh_every_tick(ranc, variant, ring):
     assert np.array_equal(cnt[idx], ref_c)
 
 
-def test_vmm1024_closed_form_full_batch(ranc):
-    """VMM-1024 as benchmarked (256 cores on a 16x16 grid, S = 1000, drained):
+@pytest.mark.parametrize("ring", [0, 1])
+def test_vmm1024_closed_form_full_batch(ranc, ring):
+    """VMM-1024 as benchmarked (256 cores on a 16x16 grid, S = 1000, drained;
+    the automatic layout -- the history scheduler -- and sample-major rings):
     the class counts of every sample equal M+ x and M- x (P6, numpy)."""
     net, inp = vmm(S=1000, seed=1004, **VMM_VARIANTS["vmm1024"])
     M, X = net.meta["M"], net.meta["X"]
     sim = ranc.Simulator(net)
+    sim.set_option(ranc.OPT_RING_LAYOUT, ring)
     sim.load_inputs(inp).run(net.meta["T"])
     cnt = sim.outputs()
     assert sim.info()["kernel"] == 2
+    assert sim.info()["ring_layout"] == (3 if ring == 0 else 1)
     sim.close()
     assert np.array_equal(cnt[:, 0::2], X @ np.maximum(M, 0).T)
     assert np.array_equal(cnt[:, 1::2], X @ np.maximum(-M, 0).T)
