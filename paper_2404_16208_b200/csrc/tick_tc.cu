@@ -909,13 +909,16 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
     const long long dbg_t0 = dbg_on ? clock64() : 0;
     const int cl0 = cl, tile0 = tile;
     // neuron parameters of the next work item's core (prefetched one item ahead)
-    short4 nprm = make_short4(0, 0, 0, 0);
+    // (kept as the raw 8 bytes until use: unpacked right after the load, a
+    // short4 made every prefetch wait for its own load -- 13 % of the stall
+    // samples at config 5)
+    uint2 nprm = make_uint2(0u, 0u);
     uint2 nrt = make_uint2(0u, 0u);
     int nini = 0;
     uint32_t nhp = 0u, hpos = 0u;   // history scheduler: this neuron's position
     if (!kMulti && active && nwork > 0) {
       const size_t nc = (size_t)(p.c_lo + cl0) * Np + n;
-      nprm = p.prm[nc];
+      nprm = *reinterpret_cast<const uint2*>(p.prm + nc);
       nrt = p.route[nc];
       nini = p.init[nc];
       if (kPull) nhp = p.hpos[nc];
@@ -957,13 +960,13 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       // ahead (one tile per core at config 5: the loads would otherwise stall
       // the epilogue at every item); prefetch the next item's now
       // (the multi-tick launch, at most two items per CTA, loads them in place)
-      short4 prm = nprm;
+      uint2 prm = nprm;
       uint2 rt = nrt;
       int ini = nini;
       const uint32_t hp = nhp;
       if (kMulti && active && key != prev_core) {
         const size_t nc = (size_t)c * Np + n;
-        prm = p.prm[nc];
+        prm = *reinterpret_cast<const uint2*>(p.prm + nc);
         rt = p.route[nc];
         ini = p.init[nc];
       }
@@ -972,7 +975,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
         const int nkn = g + 1 < nGrp ? n + GS : n0;
         if (nkc != cl || nkn != n) {
           const size_t nc = (size_t)(p.c_lo + nkc) * Np + nkn;
-          nprm = p.prm[nc];
+          nprm = *reinterpret_cast<const uint2*>(p.prm + nc);
           nrt = p.route[nc];
           nini = p.init[nc];
           if (kPull) nhp = p.hpos[nc];
@@ -989,7 +992,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       tc::fence_after();
       if (active) {
         if (key != prev_core) {
-          leak = prm.x; pth = prm.y; nth = prm.z; rst = prm.w;
+          leak = (int)(int16_t)(prm.x & 0xFFFFu); pth = (int)prm.x >> 16;   // short4 {leak, th+, th-, R}
+          nth = (int)(int16_t)(prm.y & 0xFFFFu); rst = (int)prm.y >> 16;
           init = ini;
           hpos = hp;
           if (p.fresh && first) {
