@@ -60,10 +60,16 @@ constexpr int kEpiWarps = 16;
 // Warp ids (SMSP = warp % 4): 0..15 epilogue (TMEM lane quarter = warp % 4,
 // so every SMSP holds four epilogue warps to hide the LIF's dependency
 // latencies); 16..19 spike stage; 20 producer; 21 MMA issuer.
-constexpr int kFirstEpi = 0, kProdWarp = kEpiWarps + 4, kMmaWarp = kEpiWarps + 5;
-__device__ __forceinline__ bool is_spike_warp(int w) { return w >= kEpiWarps && w < kEpiWarps + 4; }
-__device__ __forceinline__ int spike_thread(int w, int lane) { return 32 * (w - kEpiWarps) + lane; }
+constexpr int kFirstEpi = 0;
 constexpr int kThreadsTC = 32 * (2 + kExpWarps + kEpiWarps);  // 704
+// history-scheduler launches with the compact operand: 8 spike warps (two
+// per SMSP: their per-item chain -- position ORs, B operand, operand
+// expansion -- is the longest one; 832 threads keep 72 registers per thread;
+// config 5 95.7 -> 90 us per tick; the folded VMM-1024 launch was 2 % slower
+// with them, so it keeps 4)
+constexpr int kExpWarpsHist = 8;
+constexpr int kThreadsHist = 32 * (2 + kExpWarpsHist + kEpiWarps);  // 832
+__host__ __device__ constexpr int tc_threads(bool hist) { return hist ? kThreadsHist : kThreadsTC; }
 constexpr int kExpThreads = 32 * kExpWarps;
 constexpr int kSub = 16;               // samples per TMEM load / LIF pass of an epilogue warp
 static_assert(kExpThreads == 2 * NT, "spike stage maps thread -> (sample, 16-bit half)");
@@ -251,7 +257,7 @@ __device__ __forceinline__ uint32_t lif(const uint4 (&cur)[NE / 8], const uint32
 // the masks into the staged ring-word layout.  No atomics in global memory,
 // no clears: position i of slot t was written at tick t - d_i.
 template <bool kMulti, bool kDebug, bool kWm, bool kWide, bool kGrp = false, bool kPull = false, bool kComp = false>
-__global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams p, const int nticks_arg) {
+__global__ void __launch_bounds__(tc_threads(kPull && kComp), 1) tick_tc_kernel(const TickParams p, const int nticks_arg) {
   static_assert(!kGrp || !kMulti, "neuron groups are a per-tick launch");
   static_assert(!kComp || (!kMulti && !kWide && !kGrp), "the compact operand is a per-tick int8 launch");
   static_assert(!kPull || (!kMulti && kWm && !kGrp), "the pull scheduler is a per-tick word-major launch");
@@ -323,7 +329,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
   };
 
   // role warps
-  const int prod_warp = kProdWarp, mma_warp = kMmaWarp;
+  // spike warps: 4 (8 with the history scheduler), then the producer and MMA warps
+  constexpr int kEW = kPull && kComp ? kExpWarpsHist : kExpWarps;
+  constexpr int SET = 32 * kEW;   // spike threads
+  const int prod_warp = kEpiWarps + kEW, mma_warp = kEpiWarps + kEW + 1;
   if (warp == mma_warp) tc::alloc(tmem_holder, tcols < 32 ? 32 : tcols);
   if (threadIdx.x == 0) {
     for (int i = 0; i < NS; ++i) {
@@ -527,24 +536,27 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
     }
     tick_barrier();
     }
-  } else if (is_spike_warp(warp)) {
+  } else if (warp >= kEpiWarps && warp < kEpiWarps + kEW) {
     // ------------------------------------------------------------ spike stage
-    const int et = spike_thread(warp, lane);
+    const int et = 32 * (warp - kEpiWarps) + lane;
     int runs_core = -1;
     // nibble -> four 0/1 bytes; a 16-entry u32 table spans 16 distinct banks,
     // so the lookups never conflict
     uint32_t* lut = reinterpret_cast<uint32_t*>(smem + L.lut);
-    for (int b = et; b < 16; b += kExpThreads) lut[b] = tc::nib2bytes((uint32_t)b);
+    for (int b = et; b < 16; b += SET) lut[b] = tc::nib2bytes((uint32_t)b);
     if (kPull)   // the per-axon masks start (and stay between items) zero
-      for (int i = et; i < 2 * Kp; i += kExpThreads) reinterpret_cast<uint32_t*>(smem + L.pmask)[i] = 0u;
-    named_sync(2, kExpThreads);
+      for (int i = et; i < 2 * Kp; i += SET) reinterpret_cast<uint32_t*>(smem + L.pmask)[i] = 0u;
+    named_sync(2, SET);
     // kComp: the spike warps expand each core's compact operand (crossbar
     // bits, type weights, axon types) into Wfold[n][a'] = conn * w[n][type(a')]
     // in the canonical layout, into operand buffer j & 1 for the
     // CTA's j-th core, one core ahead of the MMAs; the compact operand of the
     // core after that is prefetched into registers meanwhile (L2 evict_last:
     // every core's operand is read again next tick).
-    uint32_t cx[2][8], cw[2] = {0u, 0u}, cts = 0u;
+    constexpr int kNH = SET >= 256 ? 1 : 2;   // neurons per thread (Np <= 256)
+    uint32_t cx[kNH][8], cw[kNH], cts = 0u;
+#pragma unroll
+    for (int h = 0; h < kNH; ++h) cw[h] = 0u;
     const uint64_t pol_keep = kComp ? ptx::policy_evict_last() : 0ull;
     int ncores = 0, jcore = 0;
     const int core0 = first_idx / nT, core_dir = rev ? -1 : 1;
@@ -553,8 +565,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       if (j >= ncores) return;
       const int cg = p.c_lo + core0 + core_dir * j;
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int nn = et + 128 * h;
+      for (int h = 0; h < kNH; ++h) {
+        const int nn = et + SET * h;
 #pragma unroll
         for (int w = 0; w < 8; ++w)
           cx[h][w] = (nn < Np && w < W) ? ptx::ldg_hint(p.xbits + ((size_t)cg * W + w) * Np + nn, pol_keep) : 0u;
@@ -568,11 +580,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       if (et == 0 && j > 0) stamp_k(j - 1, 12);   // (timeline: slots 12 / 13 = expansion start / end)
       uint32_t* ts = reinterpret_cast<uint32_t*>(smem + L.tsel);
       if (et < (Kp >> 2)) ts[et] = cts;
-      named_sync(2, kExpThreads);
+      named_sync(2, SET);
       uint4* const abuf = reinterpret_cast<uint4*>(w_s + b * (uint32_t)(Np * Kp));
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int nn = et + 128 * h;
+      for (int h = 0; h < kNH; ++h) {
+        const int nn = et + SET * h;
         if (nn >= Np) break;   // Np = 128 or 256: warp-uniform
         const uint32_t wv = cw[h];
 #pragma unroll
@@ -593,7 +605,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
         }
       }
       ptx::fence_proxy_async_smem();   // generic writes -> the tensor core's (async proxy) reads
-      named_sync(2, kExpThreads);
+      named_sync(2, SET);
       if (et == 0) {
         ptx::mbar_arrive(&bars[b ? WFULL1 : WFULL]);
         if (j > 0) stamp_k(j - 1, 13);
@@ -634,7 +646,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
         const uint16_t* hax = reinterpret_cast<const uint16_t*>(st + L.paoff);
         uint32_t* msk = reinterpret_cast<uint32_t*>(smem + L.pmask);
         const int hcnt = (int)*reinterpret_cast<const uint32_t*>(st + L.hcnt);
-        for (int e = et; e < hcnt; e += kExpThreads) {
+        for (int e = et; e < hcnt; e += SET) {
           const uint2 v = gat[e];
           if (v.x | v.y) {
             const int ap = hax[e];
@@ -647,18 +659,18 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
         const bool inj = t < p.T_in && p.nruns[c] > 0;
         if (inj) {
           if (p.inw) {
-            for (int i = et; i < NT * W; i += kExpThreads) raw[i] = lines[i];
+            for (int i = et; i < NT * W; i += SET) raw[i] = lines[i];
           } else {
             int2* runs = reinterpret_cast<int2*>(smem + L.runs);
             int32_t* wr = reinterpret_cast<int32_t*>(smem + L.runs + (uint32_t)p.rmax * 8);
             if (c != runs_core) {
-              named_sync(2, kExpThreads);
-              for (int i = et; i < p.nruns[c]; i += kExpThreads) runs[i] = p.runs[(size_t)c * p.rmax + i];
-              for (int i = et; i < W; i += kExpThreads) wr[i] = p.word_runs[(size_t)c * W + i];
-              named_sync(2, kExpThreads);
+              named_sync(2, SET);
+              for (int i = et; i < p.nruns[c]; i += SET) runs[i] = p.runs[(size_t)c * p.rmax + i];
+              for (int i = et; i < W; i += SET) wr[i] = p.word_runs[(size_t)c * W + i];
+              named_sync(2, SET);
               runs_core = c;
             }
-            for (int i = et; i < NT * W; i += kExpThreads) {
+            for (int i = et; i < NT * W; i += SET) {
               const int w = i / NT, sm = i % NT;
               uint32_t acc = 0u;
               const int32_t fr = wr[w];
@@ -676,16 +688,16 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
               raw[i] = acc;
             }
           }
-          named_sync(2, kExpThreads);
-          for (int b = et >> 5; b < 2 * W; b += kExpWarps) {
+          named_sync(2, SET);
+          for (int b = et >> 5; b < 2 * W; b += kEW) {
             const int w = b >> 1, hf = b & 1;
             const uint32_t x = transpose32(raw[w * NT + 32 * hf + lane], lane);
             if (x) atomicOr(msk + 2 * (32 * w + lane) + hf, x);
           }
         }
-        named_sync(2, kExpThreads);
+        named_sync(2, SET);
         if (p.spkin)   // RANC_TRACE_STATE_DIGEST: the axon spikes integrated this tick
-          for (int b = et >> 5; b < 2 * W; b += kExpWarps) {
+          for (int b = et >> 5; b < 2 * W; b += kEW) {
             const int w = b >> 1, hf = b & 1, sm = 32 * hf + lane;
             const uint32_t y = transpose32(msk[2 * (32 * w + lane) + hf], lane);
             if (sm < ns) p.spkin[((size_t)(s0 + sm) * p.G_loc + cl) * W + w] = y;
@@ -697,7 +709,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
         // SBO = 128 between 16-sample groups); samples >= ns get no spikes
         uint8_t* b_s = st + L.b;
         const uint64_t keep = ns >= 64 ? ~0ull : ((1ull << ns) - 1ull);
-        for (int ap = et; ap < Kp; ap += kExpThreads) {
+        for (int ap = et; ap < Kp; ap += SET) {
           uint2* mp = reinterpret_cast<uint2*>(msk) + ap;
           const uint2 mv = *mp;
           *mp = make_uint2(0u, 0u);
@@ -834,7 +846,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tick_tc_kernel(const TickParams
       }   // !kPull
       if (et == 0) stamp_k(k, 15);
       ptx::fence_proxy_async_smem();
-      named_sync(2, kExpThreads);
+      named_sync(2, SET);
       if (et == 0) {
         stamp_k(k, 4);
         ptx::mbar_arrive(&bars[BFULL0 + s]);
@@ -1492,7 +1504,7 @@ cudaError_t launch_tick_tc(ranc_ctx* ctx, TickParams p) {
   // next grid's start-up with this one's tail (griddepcontrol in the kernel)
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kThreadsTC);
+  cfg.blockDim = dim3(tc_threads(pull && comp));
   cfg.dynamicSmemBytes = smem;
   cfg.stream = ctx->stream;
   cudaLaunchAttribute attr[1];
