@@ -454,10 +454,12 @@ ranc_status validate_and_compile(const ranc_network_desc* d, Compiled* out, std:
     // tiles per core): instead of the 64 KB folded Wfold, the crossbar bits,
     // the neuron's K type weights and the axon types (9.3 KB per core at
     // A = N = 256); the spike warps expand it on chip, one core
-    // ahead.  Bit layout for the expansion (tick_tc.cu): in word w of neuron
-    // n, axon a' = 32w + 4m + j (m = 0..7, j = 0..3) is bit 8j + 7 - m, so
-    // that (word << m) holds the connections of the m-th 4-axon group in the
-    // sign bits of its four bytes (one prmt turns them into byte masks).
+    // ahead.  Bit layout for the expansion (tick_tc.cu): word w of neuron n
+    // holds the ABSENT connections (1 = no synapse; padding axons and rows
+    // are all ones) of axons a' = 32w + 4m + j (m = 0..7, j = 0..3) at bit
+    // 16 * (m / 4) + 4j + m % 4, so that one shift puts the four of group m
+    // at bits 2, 6, 10, 14 -- bit 2 of each byte selector of a prmt, which
+    // then picks a zero byte instead of the axon type's weight.
     //   xbits u32 [G][W][Npad]   wq u32 [G][Npad] (byte k = int8 w[n][k])
     //   tsel  u32 [G][Kp/4]      prmt selector: nibble j = type of axon 4g + j
     o.tc_comp_ok = o.tc_ok && !o.tc_wide && !o.tc_grp && o.Npad <= 256 && W <= 8;
@@ -465,7 +467,7 @@ ranc_status validate_and_compile(const ranc_network_desc* d, Compiled* out, std:
     o.wq.clear();
     o.tsel.clear();
     if (o.tc_comp_ok) {
-      o.xbits.assign((size_t)G * W * Np, 0u);
+      o.xbits.assign((size_t)G * W * Np, ~0u);
       o.wq.assign((size_t)G * Np, 0u);
       o.tsel.assign((size_t)G * (o.Kp / 4), 0u);
       for (int c = 0; c < G; ++c) {
@@ -482,7 +484,7 @@ ranc_status validate_and_compile(const ranc_network_desc* d, Compiled* out, std:
           for (int a = 0; a < A; ++a)
             if ((src[a >> 5] >> (a & 31)) & 1u) {
               const int ap = inv[a], w = ap >> 5, m = (ap >> 2) & 7, j = ap & 3;
-              o.xbits[((size_t)c * W + w) * Np + n] |= 1u << (8 * j + 7 - m);
+              o.xbits[((size_t)c * W + w) * Np + n] &= ~(1u << (16 * (m >> 2) + 4 * j + (m & 3)));
             }
         }
       }

@@ -591,15 +591,20 @@ __global__ void __launch_bounds__(tc_threads(kPull && kComp), 1) tick_tc_kernel(
         for (int w = 0; w < 8; ++w) {
           if (w >= W) break;
           // chunk kc = 2w + (m >> 2) (16 axons) of row nn sits at (kc * Np + nn) * 16
-          // bytes (tc.h); byte j of word m: axon 32w + 4m + j, its connection bit
-          // is the sign of byte j of (x << m), its weight byte selected by type
+          // bytes (tc.h); byte j of word m: axon 32w + 4m + j, its weight byte
+          // selected by type (selector nibble j = type) unless the synapse is
+          // absent (nibble bit 2 set: a byte of the zero operand) -- one shift,
+          // one lop3 and one prmt per four synapses
           const uint32_t x = cx[h][w];
           const uint4 s0 = reinterpret_cast<const uint4*>(ts)[2 * w];
           const uint4 s1 = reinterpret_cast<const uint4*>(ts)[2 * w + 1];
           const uint32_t sel[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
           uint32_t o[8];
 #pragma unroll
-          for (int m = 0; m < 8; ++m) o[m] = ptx::prmt(x << m, 0u, 0xBA98u) & ptx::prmt(wv, 0u, sel[m]);
+          for (int m = 0; m < 8; ++m) {
+            const uint32_t z = m < 2 ? x << (2 - m) : m < 4 ? x >> (m - 2) : x >> (14 + (m & 3));
+            o[m] = ptx::prmt(wv, 0u, (z & 0x4444u) | sel[m]);
+          }
           abuf[(2 * w) * Np + nn] = make_uint4(o[0], o[1], o[2], o[3]);
           abuf[(2 * w + 1) * Np + nn] = make_uint4(o[4], o[5], o[6], o[7]);
         }
