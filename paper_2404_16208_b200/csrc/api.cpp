@@ -111,7 +111,8 @@ void free_all(ranc_ctx* ctx) {
                     &ctx->d_stage, &ctx->d_stage2, &ctx->d_raster, &ctx->d_fired, &ctx->d_exports, &ctx->d_send, &ctx->d_recv,
                     &ctx->d_send_list, &ctx->d_recv_list, &ctx->d_dbg, &ctx->d_inw, &ctx->d_inslot,
                     &ctx->d_slot_core, &ctx->d_spkin, &ctx->d_digest, &ctx->d_perm_dig, &ctx->d_gsend, &ctx->d_grecv,
-                    &ctx->d_hist, &ctx->d_hpos, &ctx->d_hbase, &ctx->d_hax, &ctx->d_xbits, &ctx->d_wq, &ctx->d_tsel};
+                    &ctx->d_hist, &ctx->d_hpos, &ctx->d_hbase, &ctx->d_hax, &ctx->d_xbits, &ctx->d_wq, &ctx->d_tsel,
+                    &ctx->d_part, &ctx->d_cta_ns};
   for (DevBuf* b : bufs) dev_free(ctx, b);
 }
 

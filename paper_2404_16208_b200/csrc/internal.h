@@ -115,6 +115,11 @@ struct TickParams {
   const uint32_t* xbits;
   const uint32_t* wq;
   const uint32_t* tsel;
+  // cost-balanced partition of per-tick launches: CTA b takes items
+  // [part[b], part[b+1]) (nullptr: equal shares) and, when cta_ns is set,
+  // stores its busy time in ns
+  const int32_t* part;
+  uint32_t* cta_ns;
 };
 
 // Host copy of the compiled network.
@@ -240,6 +245,11 @@ struct ranc_ctx {
   ranc::DevBuf d_xbits, d_wq, d_tsel;
   int32_t operand = 0;           // RANC_OPT_OPERAND request: 0 auto, 1 folded, 2 compact
   int32_t operand_used = 0;      // operand of the last tensor-core launch (1 folded, 2 compact)
+  // cost-balanced work partition of the per-tick tensor-core launches
+  ranc::DevBuf d_part, d_cta_ns;
+  int64_t part_key = -1;         // (items, grid) the partition was made for
+  int64_t part_ticks = 0;        // ticks run with it
+  bool part_fresh = false;       // a rebalance kernel was queued after the last tick (no PDL for the next)
   // RANC_TRACE_STATE_DIGEST
   ranc::DevBuf d_spkin, d_digest, d_perm_dig;
   int32_t perm_dig_kernel = 0;   // kernel whose axon order d_perm_dig holds

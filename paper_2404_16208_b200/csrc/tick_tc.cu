@@ -284,8 +284,12 @@ __global__ void __launch_bounds__(tc_threads(kPull && kComp), 1) tick_tc_kernel(
   const int Mh = GS >> 7;
   const int nT = (p.S + NT - 1) / NT;
   const int total = p.G_loc * nT;
-  const int lo = (int)((int64_t)blockIdx.x * total / gridDim.x);
-  const int hi = (int)((int64_t)(blockIdx.x + 1) * total / gridDim.x);
+  // this CTA's contiguous range of (core, tile) work items: equal shares, or
+  // (per-tick launches, p.part) the cost-balanced partition of the previous
+  // ticks -- written only by the rebalance kernel, after which the next tick
+  // is launched without programmatic dependency (so it is complete here)
+  const int lo = (!kMulti && p.part) ? p.part[blockIdx.x] : (int)((int64_t)blockIdx.x * total / gridDim.x);
+  const int hi = (!kMulti && p.part) ? p.part[blockIdx.x + 1] : (int)((int64_t)(blockIdx.x + 1) * total / gridDim.x);
   const int nwork = hi - lo;
   // Serpentine order (per-tick launches, p.serp): odd ticks walk the CTA's
   // items backwards, so a tick starts on the items whose potentials, ring
@@ -366,7 +370,7 @@ __global__ void __launch_bounds__(tc_threads(kPull && kComp), 1) tick_tc_kernel(
   tc::fence_after();
   const uint32_t tmem = *tmem_holder;
   unsigned long long gt_start = 0;
-  if (dbg_on && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt_start));
+  if ((dbg_on || p.cta_ns) && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt_start));
 
   if (warp == prod_warp) {
     // ------------------------------------------------------------ producer (TMA)
@@ -1240,6 +1244,11 @@ __global__ void __launch_bounds__(tc_threads(kPull && kComp), 1) tick_tc_kernel(
   tc::fence_before();
   __syncthreads();
   if (warp == mma_warp) tc::dealloc(tmem, tcols < 32 ? 32 : tcols);
+  if (p.cta_ns && threadIdx.x == 0) {   // this CTA's busy time, for the partition
+    unsigned long long gt_end;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt_end));
+    p.cta_ns[blockIdx.x] = (uint32_t)min(gt_end - gt_start, 0xFFFFFFFFull);
+  }
   if (dbg_on && threadIdx.x == 0 && blockIdx.x < 256) {
     unsigned long long gt_end;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt_end));
@@ -1288,6 +1297,46 @@ __global__ void decode_inputs_kernel(const uint32_t* __restrict__ lines, uint32_
     const size_t row = (size_t)t * n_slots + slot;   // same layout as the ring
     inw[wmajor ? (row * W + w) * Sr + s : (row * Sr + s) * W + w] = acc;
   }
+}
+
+// Cost-balanced work partition of the per-tick launches (load balance only:
+// the items of one tick are independent, so results do not depend on it).
+// From the CTAs' measured busy times over their current ranges (a piecewise
+// constant cost per item), the item sequence is cut into g pieces of equal
+// estimated cost; the new bounds are averaged with the old ones (damping).
+__global__ void rebalance_kernel(int32_t* part, const uint32_t* cta_ns, int g) {
+  __shared__ int32_t nb[1025];
+  if (threadIdx.x != 0 || g > 1024) return;
+  double tot = 0.0, mx = 0.0;
+  for (int b = 0; b < g; ++b) {
+    tot += (double)cta_ns[b];
+    mx = fmax(mx, (double)cta_ns[b]);
+  }
+  if (tot <= 0.0 || mx <= 1.03 * tot / g) return;   // balanced within 3 %: keep (uniform meshes: moving
+                                                      // items only costs L2 locality)
+  nb[0] = part[0];
+  nb[g] = part[g];
+  double cum = 0.0;
+  int b = 0;
+  for (int k = 1; k < g; ++k) {
+    const double target = tot * k / g;
+    while (b < g - 1 && cum + (double)cta_ns[b] < target) cum += (double)cta_ns[b++];
+    const int items = part[b + 1] - part[b];
+    const double f = cta_ns[b] > 0 ? (target - cum) / (double)cta_ns[b] : 0.0;
+    int cut = part[b] + (int)(f * items + 0.5);
+    nb[k] = cut;
+  }
+  for (int k = 1; k < g; ++k) {
+    int v = (part[k] + nb[k] + 1) / 2;
+    v = max(v, part[0] + k);                 // at least one item per CTA
+    v = min(v, part[g] - (g - k));
+    nb[k] = v;
+  }
+  for (int k = 1; k < g; ++k) part[k] = max(nb[k], part[k - 1] + 1);
+}
+
+__global__ void part_init_kernel(int32_t* part, int g, int total) {
+  for (int b = threadIdx.x; b <= g; b += blockDim.x) part[b] = (int)((int64_t)b * total / g);
 }
 
 }  // namespace
@@ -1407,7 +1456,10 @@ void dump_timeline(ranc_ctx* ctx, int64_t t, int grid) {
       e_min = std::min(e_min, h[64 * 16 + 64 + 2 * b + 1]);
       e_max = std::max(e_max, h[64 * 16 + 64 + 2 * b + 1]);
     }
-    fprintf(stderr, "CTA end times (ns after first start): min %llu max %llu; slowest CTAs:", e_min - s_min,
+    fprintf(stderr, "CTA end times (ns after first start), by CTA:");
+    for (int b = 0; b < std::min(grid, 256); ++b)
+      fprintf(stderr, "%s%llu", b % 16 ? " " : "\n  ", h[64 * 16 + 64 + 2 * b + 1] - s_min);
+    fprintf(stderr, "\nCTA end times (ns after first start): min %llu max %llu; slowest CTAs:", e_min - s_min,
             e_max - s_min);
     for (int b = 0; b < std::min(grid, 256); ++b)
       if (h[64 * 16 + 64 + 2 * b + 1] + 20000 > e_max) fprintf(stderr, " %d", b);
@@ -1487,6 +1539,27 @@ cudaError_t launch_tick_tc(ranc_ctx* ctx, TickParams p) {
   if (dbg && !ctx->d_dbg.p) dev_alloc(ctx, &ctx->d_dbg, kDbg * 8);
   p.dbg = dbg ? (unsigned long long*)ctx->d_dbg.p : nullptr;
   if (dbg) cudaMemsetAsync(ctx->d_dbg.p, 0, kDbg * 8, ctx->stream);
+  // cost-balanced partition: measured on the first ticks and every 64th,
+  // rebalanced by a one-thread kernel after the measured tick
+  static const bool no_bal = getenv("RANC_DEBUG_NO_BALANCE") != nullptr;
+  bool measure = false;
+  if (!no_bal && grid > 1 && grid <= 1024 && total >= 2 * (int64_t)grid) {
+    const int64_t key = total * 4096 + grid;
+    if (ctx->part_key != key) {
+      if (dev_alloc(ctx, &ctx->d_part, (size_t)(grid + 1) * 4) != RANC_OK ||
+          dev_alloc(ctx, &ctx->d_cta_ns, (size_t)grid * 4) != RANC_OK)
+        return cudaErrorMemoryAllocation;
+      part_init_kernel<<<1, 256, 0, ctx->stream>>>((int32_t*)ctx->d_part.p, grid, (int)total);
+      ctx->launches++;
+      ctx->part_key = key;
+      ctx->part_ticks = 0;
+      ctx->part_fresh = true;
+    }
+    p.part = (const int32_t*)ctx->d_part.p;
+    measure = ctx->part_ticks < 6 || (ctx->part_ticks & 63) == 0;
+    p.cta_ns = measure ? (uint32_t*)ctx->d_cta_ns.p : nullptr;
+    ++ctx->part_ticks;
+  }
   const bool pull = ctx->ring_pull;
   const void* fn = comp ? (pull ? (dbg ? (const void*)tick_tc_kernel<false, true, true, false, false, true, true>
                                        : (const void*)tick_tc_kernel<false, false, true, false, false, true, true>)
@@ -1515,13 +1588,19 @@ cudaError_t launch_tick_tc(ranc_ctx* ctx, TickParams p) {
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   static const bool no_pdl = getenv("RANC_DEBUG_NO_PDL") != nullptr;
-  attr[0].val.programmaticStreamSerializationAllowed = (ctx->pdl && !no_pdl) ? 1 : 0;
+  // (not right after a rebalance: the kernel reads the partition at its start)
+  attr[0].val.programmaticStreamSerializationAllowed = (ctx->pdl && !no_pdl && !ctx->part_fresh) ? 1 : 0;
+  ctx->part_fresh = measure;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   int one = 1;
   void* args[] = {&p, &one};
   const cudaError_t e = cudaLaunchKernelExC(&cfg, fn, args);
   if (e != cudaSuccess) return e;
+  if (measure) {
+    rebalance_kernel<<<1, 32, 0, ctx->stream>>>((int32_t*)ctx->d_part.p, (const uint32_t*)ctx->d_cta_ns.p, grid);
+    ctx->launches++;
+  }
   if (dbg) dump_timeline(ctx, p.t, grid);
   return cudaGetLastError();
 }
