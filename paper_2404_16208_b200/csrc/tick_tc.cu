@@ -62,11 +62,11 @@ constexpr int kEpiWarps = 16;
 // latencies); 16..19 spike stage; 20 producer; 21 MMA issuer.
 constexpr int kFirstEpi = 0;
 constexpr int kThreadsTC = 32 * (2 + kExpWarps + kEpiWarps);  // 704
-// history-scheduler launches with the compact operand: 8 spike warps (two
-// per SMSP: their per-item chain -- position ORs, B operand, operand
-// expansion -- is the longest one; 832 threads keep 72 registers per thread;
-// config 5 95.7 -> 90 us per tick; the folded VMM-1024 launch was 2 % slower
-// with them, so it keeps 4)
+// history-scheduler launches with the compact operand: 8 spike warps in two
+// groups of 4 that take alternate work items (their per-item chain --
+// position ORs, B operand, operand expansion -- is the longest one; 832
+// threads keep 72 registers per thread; config 5 95.7 -> 84 us per tick; the
+// folded VMM-1024 launch was 1-2 % slower with them, so it keeps 4)
 constexpr int kExpWarpsHist = 8;
 constexpr int kThreadsHist = 32 * (2 + kExpWarpsHist + kEpiWarps);  // 832
 __host__ __device__ constexpr int tc_threads(bool hist) { return hist ? kThreadsHist : kThreadsTC; }
@@ -110,17 +110,23 @@ __host__ __device__ inline TcLayout tc_layout(int wrows, int Kp, int W, int WIp,
                                               bool cnt_planes = false, bool multi = false, int grp = 0,
                                               int pull_emax = -1, bool comp = false) {
   // grp: spike stages of a neuron-group launch (0: not grouped); its operand
-  // buffer holds one K chunk of at most kKChunk axons
+  // buffer holds one K chunk of at most kKChunk axons.  History launches
+  // (pull_emax >= 0) with the compact operand run two spike groups: their
+  // runs, type selectors and per-axon masks are per group; history launches
+  // without input lines stage no ring rows or input words.
+  const bool pull = pull_emax >= 0;
+  const uint32_t ng = pull && comp ? 2u : 1u;
+  const bool stage_rows = !pull || WIp > 0;
   TcLayout L;
   L.w = 1024;
   uint32_t o = L.w + (uint32_t)wrows * (grp ? (Kp < kKChunk ? Kp : kKChunk) : Kp) * (wide || comp ? 2u : 1u);
   L.runs = o;                                 // int2 [rmax] + int32 [W] of the current core
-  o += (uint32_t)rmax * 8 + (uint32_t)W * 4;
+  o += ((uint32_t)rmax * 8 + (uint32_t)W * 4) * ng;
   o = (o + 15) & ~15u;
   L.lut = o;                                  // u32 [16]: nibble -> four 0/1 bytes
   o += 256 * 8;
   L.tsel = o;                                 // compact operand: u32 [Kp/4] the core's prmt type selectors
-  if (comp) o += (uint32_t)Kp;
+  if (comp) o += (uint32_t)Kp * ng;
   o = (o + 127) & ~127u;
   L.potbuf = o;                               // uint4 [NT/8][epilogue threads]: next tile's potentials
   o += (NT / 8) * (32 * 8) * 16 * (uint32_t)pot_items;   // = 4 chunks x 512 epilogue threads per item
@@ -128,14 +134,14 @@ __host__ __device__ inline TcLayout tc_layout(int wrows, int Kp, int W, int WIp,
   if (cnt_planes) o += (uint32_t)pot_items * kCntPlanes * 512 * 4;
   o = (o + 15) & ~15u;
   L.pmask = o;                                // history scheduler: u64 [Kp] spike masks per axon (64 samples)
-  if (pull_emax >= 0) o += (uint32_t)Kp * 8;
+  if (pull) o += (uint32_t)Kp * 8 * ng;
   L.stage = (o + 1023) & ~1023u;
   uint32_t q = 0;
   L.b = q;     q += (uint32_t)NT * Kp;       // spikes as 0/1 bytes, canonical layout
   q = (q + 15) & ~15u;
-  L.raw = q;   q += (uint32_t)NT * W * 4;    // scheduler rows due now (TMA)
+  L.raw = q;   if (stage_rows) q += (uint32_t)NT * W * 4;    // scheduler rows due now (TMA)
   q = (q + 15) & ~15u;
-  L.lines = q; q += (uint32_t)NT * (WIp > W ? WIp : W) * 4;  // input line rows or decoded words (TMA)
+  L.lines = q; if (stage_rows) q += (uint32_t)NT * (WIp > W ? WIp : W) * 4;  // input line rows or decoded words (TMA)
   q = (q + 15) & ~15u;
   L.paoff = q;                                // history: u16 [emax] destination axon per position (TMA)
   if (pull_emax >= 0) q += (uint32_t)pull_emax * 2;
@@ -542,22 +548,32 @@ __global__ void __launch_bounds__(tc_threads(kPull && kComp), 1) tick_tc_kernel(
     }
   } else if (warp >= kEpiWarps && warp < kEpiWarps + kEW) {
     // ------------------------------------------------------------ spike stage
-    const int et = 32 * (warp - kEpiWarps) + lane;
+    // history launches: two independent spike groups of 4 warps take
+    // alternate work items (their own spike stages, per-axon masks, type
+    // selectors and named barrier), so that two items' chains overlap
+    constexpr int kSG = kPull && kComp ? 2 : 1;             // spike groups
+    constexpr int GT = 128;                                 // threads per group
+    const int gi = (warp - kEpiWarps) >> 2;                 // this warp's group
+    const int et = 32 * ((warp - kEpiWarps) & 3) + lane;    // thread within the group
+    const int gbar = 2 + gi;                                // the group's named barrier
     int runs_core = -1;
+    const uint32_t runs_off = (uint32_t)gi * ((uint32_t)p.rmax * 8 + (uint32_t)W * 4);
+    uint32_t* const gmsk = reinterpret_cast<uint32_t*>(smem + L.pmask) + (size_t)gi * 2 * Kp;
     // nibble -> four 0/1 bytes; a 16-entry u32 table spans 16 distinct banks,
     // so the lookups never conflict
     uint32_t* lut = reinterpret_cast<uint32_t*>(smem + L.lut);
-    for (int b = et; b < 16; b += SET) lut[b] = tc::nib2bytes((uint32_t)b);
+    if (gi == 0)
+      for (int b = et; b < 16; b += GT) lut[b] = tc::nib2bytes((uint32_t)b);
     if (kPull)   // the per-axon masks start (and stay between items) zero
-      for (int i = et; i < 2 * Kp; i += SET) reinterpret_cast<uint32_t*>(smem + L.pmask)[i] = 0u;
-    named_sync(2, SET);
+      for (int i = et; i < 2 * Kp; i += GT) gmsk[i] = 0u;
+    named_sync(4, SET);
     // kComp: the spike warps expand each core's compact operand (crossbar
     // bits, type weights, axon types) into Wfold[n][a'] = conn * w[n][type(a')]
     // in the canonical layout, into operand buffer j & 1 for the
     // CTA's j-th core, one core ahead of the MMAs; the compact operand of the
     // core after that is prefetched into registers meanwhile (L2 evict_last:
     // every core's operand is read again next tick).
-    constexpr int kNH = SET >= 256 ? 1 : 2;   // neurons per thread (Np <= 256)
+    constexpr int kNH = 2;   // neurons per thread (Np <= 256)
     uint32_t cx[kNH][8], cw[kNH], cts = 0u;
 #pragma unroll
     for (int h = 0; h < kNH; ++h) cw[h] = 0u;
@@ -570,7 +586,7 @@ __global__ void __launch_bounds__(tc_threads(kPull && kComp), 1) tick_tc_kernel(
       const int cg = p.c_lo + core0 + core_dir * j;
 #pragma unroll
       for (int h = 0; h < kNH; ++h) {
-        const int nn = et + SET * h;
+        const int nn = et + GT * h;
 #pragma unroll
         for (int w = 0; w < 8; ++w)
           cx[h][w] = (nn < Np && w < W) ? ptx::ldg_hint(p.xbits + ((size_t)cg * W + w) * Np + nn, pol_keep) : 0u;
@@ -582,13 +598,13 @@ __global__ void __launch_bounds__(tc_threads(kPull && kComp), 1) tick_tc_kernel(
       const int b = j & 1;
       if (j >= 2) wait(&bars[b ? WFREE1 : WFREE], ((j >> 1) - 1) & 1);   // core j - 2's MMAs are done
       if (et == 0 && j > 0) stamp_k(j - 1, 12);   // (timeline: slots 12 / 13 = expansion start / end)
-      uint32_t* ts = reinterpret_cast<uint32_t*>(smem + L.tsel);
+      uint32_t* ts = reinterpret_cast<uint32_t*>(smem + L.tsel + (uint32_t)gi * Kp);
       if (et < (Kp >> 2)) ts[et] = cts;
-      named_sync(2, SET);
+      named_sync(gbar, GT);
       uint4* const abuf = reinterpret_cast<uint4*>(w_s + b * (uint32_t)(Np * Kp));
 #pragma unroll
       for (int h = 0; h < kNH; ++h) {
-        const int nn = et + SET * h;
+        const int nn = et + GT * h;
         if (nn >= Np) break;   // Np = 128 or 256: warp-uniform
         const uint32_t wv = cw[h];
 #pragma unroll
@@ -614,22 +630,39 @@ __global__ void __launch_bounds__(tc_threads(kPull && kComp), 1) tick_tc_kernel(
         }
       }
       ptx::fence_proxy_async_smem();   // generic writes -> the tensor core's (async proxy) reads
-      named_sync(2, SET);
+      named_sync(gbar, GT);
       if (et == 0) {
         ptx::mbar_arrive(&bars[b ? WFULL1 : WFULL]);
         if (j > 0) stamp_k(j - 1, 13);
       }
     };
+    // one group: core j + 1 is expanded after the last item of core j (one
+    // core ahead).  Two groups: the group of a core's first item expands
+    // it after that item's B operand (the other group's item overlaps), the
+    // compact operand of the group's next core prefetched meanwhile.
+    // (walking order: a core starts at tile 0, or at tile nT - 1 reversed)
+    int cx_j = -1;   // the core whose compact operand is in cx
+    auto core_start = [&](int k0_, int tile_) { return k0_ == 0 || (rev ? tile_ == nT - 1 : tile_ == 0); };
     if (kComp && ncores > 0) {
-      comp_load(0);
-      comp_expand(0);
-      comp_load(1);
+      if (kSG == 1) {
+        comp_load(0);
+        comp_expand(0);
+        comp_load(1);
+      } else {
+        int ccl = first_idx / nT, ctile = first_idx - (first_idx / nT) * nT;
+        for (int i = 0; i < gi; ++i) adv(ccl, ctile);
+        if (gi < nwork && core_start(gi, ctile)) {
+          cx_j = abs(ccl - core0);
+          comp_load(cx_j);
+        }
+      }
     }
     for (int it = 0; it < nticks; ++it) {
     const int64_t t = p.t + it;
     const int cur = (int)(t & p.rp_mask);
     int cl = first_idx / nT, tile = first_idx - (first_idx / nT) * nT;
-    for (int k0 = 0; k0 < nwork; ++k0, adv(cl, tile)) {
+    for (int i = 0; i < gi; ++i) adv(cl, tile);
+    for (int k0 = gi; k0 < nwork; k0 += kSG) {
       const int k = it * nwork + k0;
       const int c = p.c_lo + cl;
       const int s = k % nsr, u = k / nsr;
@@ -653,9 +686,9 @@ __global__ void __launch_bounds__(tc_threads(kPull && kComp), 1) tick_tc_kernel(
         // become operand bytes without a bit transpose.
         const uint2* gat = reinterpret_cast<const uint2*>(st + L.pull);
         const uint16_t* hax = reinterpret_cast<const uint16_t*>(st + L.paoff);
-        uint32_t* msk = reinterpret_cast<uint32_t*>(smem + L.pmask);
+        uint32_t* msk = gmsk;
         const int hcnt = (int)*reinterpret_cast<const uint32_t*>(st + L.hcnt);
-        for (int e = et; e < hcnt; e += SET) {
+        for (int e = et; e < hcnt; e += GT) {
           const uint2 v = gat[e];
           if (v.x | v.y) {
             const int ap = hax[e];
@@ -668,18 +701,18 @@ __global__ void __launch_bounds__(tc_threads(kPull && kComp), 1) tick_tc_kernel(
         const bool inj = t < p.T_in && p.nruns[c] > 0;
         if (inj) {
           if (p.inw) {
-            for (int i = et; i < NT * W; i += SET) raw[i] = lines[i];
+            for (int i = et; i < NT * W; i += GT) raw[i] = lines[i];
           } else {
-            int2* runs = reinterpret_cast<int2*>(smem + L.runs);
-            int32_t* wr = reinterpret_cast<int32_t*>(smem + L.runs + (uint32_t)p.rmax * 8);
+            int2* runs = reinterpret_cast<int2*>(smem + L.runs + runs_off);
+            int32_t* wr = reinterpret_cast<int32_t*>(smem + L.runs + runs_off + (uint32_t)p.rmax * 8);
             if (c != runs_core) {
-              named_sync(2, SET);
-              for (int i = et; i < p.nruns[c]; i += SET) runs[i] = p.runs[(size_t)c * p.rmax + i];
-              for (int i = et; i < W; i += SET) wr[i] = p.word_runs[(size_t)c * W + i];
-              named_sync(2, SET);
+              named_sync(gbar, GT);
+              for (int i = et; i < p.nruns[c]; i += GT) runs[i] = p.runs[(size_t)c * p.rmax + i];
+              for (int i = et; i < W; i += GT) wr[i] = p.word_runs[(size_t)c * W + i];
+              named_sync(gbar, GT);
               runs_core = c;
             }
-            for (int i = et; i < NT * W; i += SET) {
+            for (int i = et; i < NT * W; i += GT) {
               const int w = i / NT, sm = i % NT;
               uint32_t acc = 0u;
               const int32_t fr = wr[w];
@@ -697,16 +730,16 @@ __global__ void __launch_bounds__(tc_threads(kPull && kComp), 1) tick_tc_kernel(
               raw[i] = acc;
             }
           }
-          named_sync(2, SET);
-          for (int b = et >> 5; b < 2 * W; b += kEW) {
+          named_sync(gbar, GT);
+          for (int b = et >> 5; b < 2 * W; b += 4) {
             const int w = b >> 1, hf = b & 1;
             const uint32_t x = transpose32(raw[w * NT + 32 * hf + lane], lane);
             if (x) atomicOr(msk + 2 * (32 * w + lane) + hf, x);
           }
         }
-        named_sync(2, SET);
+        named_sync(gbar, GT);
         if (p.spkin)   // RANC_TRACE_STATE_DIGEST: the axon spikes integrated this tick
-          for (int b = et >> 5; b < 2 * W; b += kEW) {
+          for (int b = et >> 5; b < 2 * W; b += 4) {
             const int w = b >> 1, hf = b & 1, sm = 32 * hf + lane;
             const uint32_t y = transpose32(msk[2 * (32 * w + lane) + hf], lane);
             if (sm < ns) p.spkin[((size_t)(s0 + sm) * p.G_loc + cl) * W + w] = y;
@@ -718,7 +751,7 @@ __global__ void __launch_bounds__(tc_threads(kPull && kComp), 1) tick_tc_kernel(
         // SBO = 128 between 16-sample groups); samples >= ns get no spikes
         uint8_t* b_s = st + L.b;
         const uint64_t keep = ns >= 64 ? ~0ull : ((1ull << ns) - 1ull);
-        for (int ap = et; ap < Kp; ap += SET) {
+        for (int ap = et; ap < Kp; ap += GT) {
           uint2* mp = reinterpret_cast<uint2*>(msk) + ap;
           const uint2 mv = *mp;
           *mp = make_uint2(0u, 0u);
@@ -855,16 +888,31 @@ __global__ void __launch_bounds__(tc_threads(kPull && kComp), 1) tick_tc_kernel(
       }   // !kPull
       if (et == 0) stamp_k(k, 15);
       ptx::fence_proxy_async_smem();
-      named_sync(2, SET);
+      named_sync(gbar, GT);
       if (et == 0) {
         stamp_k(k, 4);
         ptx::mbar_arrive(&bars[BFULL0 + s]);
         ptx::mbar_arrive(&bars[SEMPTY0 + s]);   // raw/lines of this stage are consumed
       }
-      if (kComp && k0 + 1 < nwork && next_cl_of(cl, tile) != cl) {   // the next item starts a new core
+      if (kComp && kSG == 1 && k0 + 1 < nwork && next_cl_of(cl, tile) != cl) {   // the next item starts a new core
         comp_expand(++jcore);
         comp_load(jcore + 1);
       }
+      // the group's next item
+      int ncl = cl, ntile = tile;
+      for (int i = 0; i < kSG; ++i) adv(ncl, ntile);
+      if (kComp && kSG > 1 && core_start(k0, tile)) {   // this item starts its core: expand it
+        const int j = abs(cl - core0);
+        if (cx_j != j) comp_load(j);
+        comp_expand(j);
+        cx_j = -1;
+        if (k0 + kSG < nwork && core_start(k0 + kSG, ntile)) {
+          cx_j = abs(ncl - core0);
+          comp_load(cx_j);
+        }
+      }
+      cl = ncl;
+      tile = ntile;
     }
     tick_barrier();
     }
