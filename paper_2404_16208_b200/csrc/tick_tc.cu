@@ -1090,18 +1090,20 @@ __global__ void __launch_bounds__(tc_threads(kPull && kComp), 1) tick_tc_kernel(
           // a route to a core of another rank is delivered by the exchange step
           const uint32_t dloc = rt.y - (uint32_t)p.c_lo;
           route_here = kind == RK_ROUTE && dloc < (uint32_t)p.G_loc;
-          ring_base = wm ? ((size_t)dloc * W + (ax >> 5)) * p.Sr : (size_t)dloc * p.Sr * W + (ax >> 5);
           exporting = p.fired && p.exports[c];
-          const uint32_t wf = p.wflags ? p.wflags[(size_t)c * (Np >> 5) + (n >> 5)] : 0u;
-          block_route = wf & 1u;
-          block_identity = (wf & 3u) == 3u;
-          const uint32_t rmask = __ballot_sync(0xFFFFFFFFu, route_here);
-          // block routes: all routing lanes share the destination word and delay
-          warp_ring_base = rmask ? __shfl_sync(0xFFFFFFFFu, ring_base, __ffs(rmask) - 1) : 0;
-          warp_rdelay = rmask ? __shfl_sync(0xFFFFFFFFu, rdelay, __ffs(rmask) - 1) : 0;
-          if (!kMulti) {   // one tick: the slots are fixed for the launch
-            ring_off = ring_base + (size_t)((p.t + rdelay) & p.rp_mask) * slot_stride;
-            warp_ring_off = warp_ring_base + (size_t)((p.t + warp_rdelay) & p.rp_mask) * slot_stride;
+          if (!kPull) {   // ring deposits (the history scheduler stores at positions instead)
+            ring_base = wm ? ((size_t)dloc * W + (ax >> 5)) * p.Sr : (size_t)dloc * p.Sr * W + (ax >> 5);
+            const uint32_t wf = p.wflags ? p.wflags[(size_t)c * (Np >> 5) + (n >> 5)] : 0u;
+            block_route = wf & 1u;
+            block_identity = (wf & 3u) == 3u;
+            const uint32_t rmask = __ballot_sync(0xFFFFFFFFu, route_here);
+            // block routes: all routing lanes share the destination word and delay
+            warp_ring_base = rmask ? __shfl_sync(0xFFFFFFFFu, ring_base, __ffs(rmask) - 1) : 0;
+            warp_rdelay = rmask ? __shfl_sync(0xFFFFFFFFu, rdelay, __ffs(rmask) - 1) : 0;
+            if (!kMulti) {   // one tick: the slots are fixed for the launch
+              ring_off = ring_base + (size_t)((p.t + rdelay) & p.rp_mask) * slot_stride;
+              warp_ring_off = warp_ring_base + (size_t)((p.t + warp_rdelay) & p.rp_mask) * slot_stride;
+            }
           }
           out_lanes = __ballot_sync(0xFFFFFFFFu, kind == RK_OUTPUT);
           has_output = out_lanes != 0u;
