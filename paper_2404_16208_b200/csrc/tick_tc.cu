@@ -1107,10 +1107,14 @@ __global__ void __launch_bounds__(tc_threads(kPull && kComp), 1) tick_tc_kernel(
           }
           out_lanes = __ballot_sync(0xFFFFFFFFu, kind == RK_OUTPUT);
           has_output = out_lanes != 0u;
-          // lanes of the same output class (classes are < C, never ~0u)
-          out_peers = __match_any_sync(0xFFFFFFFFu, kind == RK_OUTPUT ? cls : 0xFFFFFFFFu);
-          // more than 8 class groups: per-lane adds (see the output bus below)
-          out_scatter = __popc(__ballot_sync(0xFFFFFFFFu, kind == RK_OUTPUT && __ffs(out_peers) - 1 == lane)) > 8;
+          out_peers = 0u;
+          out_scatter = false;
+          if (has_output) {   // (warp-uniform)
+            // lanes of the same output class (classes are < C, never ~0u)
+            out_peers = __match_any_sync(0xFFFFFFFFu, kind == RK_OUTPUT ? cls : 0xFFFFFFFFu);
+            // more than 8 class groups: per-lane adds (see the output bus below)
+            out_scatter = __popc(__ballot_sync(0xFFFFFFFFu, kind == RK_OUTPUT && __ffs(out_peers) - 1 == lane)) > 8;
+          }
           prev_core = key;
         }
         // this item's potential region: the multi-tick launch keeps one per
