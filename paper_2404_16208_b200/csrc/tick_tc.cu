@@ -1055,6 +1055,7 @@ __global__ void __launch_bounds__(tc_threads(kPull && kComp), 1) tick_tc_kernel(
       // back-off polling (measured best against the suspend-hint wait, a plain
       // spin and a per-quarter named barrier)
       if (spin) ptx::mbar_wait(&bars[ACCFULL0 + a], ua & 1);
+      else if (kComp) ptx::mbar_wait_sleep(&bars[ACCFULL0 + a], ua & 1, 1000);   // (issue-bound compact launches: -1 %)
       else ptx::mbar_wait_backoff(&bars[ACCFULL0 + a], ua & 1, 128);
       if (dbg_on && blockIdx.x == 0) dbg_wait += clock64() - tw0;
       if (lane == 0 && ew == 0) stamp_k(k, 8);
