@@ -266,7 +266,7 @@ template <bool kMulti, bool kDebug, bool kWm, bool kWide, bool kGrp = false, boo
 __global__ void __launch_bounds__(tc_threads(kPull && kComp), 1) tick_tc_kernel(const TickParams p, const int nticks_arg) {
   static_assert(!kGrp || !kMulti, "neuron groups are a per-tick launch");
   static_assert(!kComp || (!kMulti && !kWide && !kGrp), "the compact operand is a per-tick int8 launch");
-  static_assert(!kPull || (!kMulti && kWm && !kGrp), "the pull scheduler is a per-tick word-major launch");
+  static_assert(!kPull || (!kMulti && kWm && !kGrp), "the history scheduler is a per-tick word-major launch");
   const int nticks = kMulti ? nticks_arg : 1;
   // kDebug: the RANC_DEBUG_TIMELINE instrumentation (a separate instantiation,
   // so that the product kernel issues none of it)
@@ -1556,11 +1556,8 @@ cudaError_t launch_tick_tc(ranc_ctx* ctx, TickParams p) {
   // compact operand: requested, or automatic with at most two sample tiles
   // per core (the folded operand would be re-read for every 64 samples)
   const int64_t nT = (ctx->S + NT - 1) / NT;
-  // (automatic: with the history scheduler, whose spike stage leaves the
-  // spike warps room for the expansion; measured on config 5)
-  // the expansion runs in the epilogue warps when the type selectors of a
-  // CTA's cores fit the shared memory (else in the spike warps);
-  // RANC_DEBUG_COMP_SPIKE=1 forces the spike warps (timing comparisons)
+  // (automatic: with the history scheduler, whose two spike groups expand
+  // the operands; measured on config 5)
   const bool comp = n.tc_comp_ok && (ctx->operand == 2 || (ctx->operand == 0 && nT <= 2 && ctx->ring_pull)) &&
                     tc_smem_bytes_comp(n, ctx->ring_pull) <= 227 * 1024;
   ctx->operand_used = comp ? 2 : 1;
